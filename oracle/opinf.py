@@ -1,0 +1,151 @@
+"""Oracle: offline stage -- POD, boundary POD, ridge OpInf, training runs (Algorithm 2).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py). The operators this module writes
+are inputs shared by both online paths (the CUDA library reads them through the C-ABI).
+
+  * POD: thin SVD U = Phi Sigma Psi^T, Phi_r = first r columns (eq:pod_cutoff);
+    Euclidean, uncentred; column signs fixed so the largest-|entry| is positive (R17).
+  * Energy rule E_r = sum_{i<=r} s_i^2 / sum_i s_i^2 (P:L788-792 eq:pod_energy); the smallest r
+    with E_r >= delta_E = 0.999999 (reading R16).
+  * OpInf (P:L263-272 eq:quadratic_opinf, linear form; L609-614 eq:opinf_schwarz_inference):
+        argmin_O || O [U^; G^] - D_t^2(U^) ||_F^2 + lambda ||O||_F^2 ,  O = [-Kbar, Bbar]
+    with U^ = Phi^T U, G^ = Phi_dS^T S and D_t^2 the central second difference on interior
+    columns (reading R18), one lambda in SI units (R20), solved as augmented least squares.
+  * Training recipes per reading R25.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import fem, schwarz
+
+
+def pod(U, r):
+    """First r left singular vectors (sign-fixed) and all singular values of U."""
+    Phi, sigma, _ = np.linalg.svd(U, full_matrices=False)
+    Phi = Phi[:, :r].copy()
+    idx = np.argmax(np.abs(Phi), axis=0)
+    sgn = np.sign(Phi[idx, np.arange(Phi.shape[1])])
+    sgn[sgn == 0] = 1.0
+    return Phi * sgn[None, :], sigma
+
+
+def energy(sigma):
+    """E_r for r = 1..len(sigma) (eq:pod_energy)."""
+    s2 = np.asarray(sigma, dtype=np.float64) ** 2
+    return np.cumsum(s2) / s2.sum()
+
+
+def energy_rank(sigma, delta=0.999999):
+    """Smallest r with E_r >= delta (reading R16)."""
+    E = energy(sigma)
+    return int(np.searchsorted(E, delta, side="left") + 1)
+
+
+def second_difference(Ubar, dt):
+    """D_t^2 on interior columns k = 1..K-2: (U_{k+1} - 2 U_k + U_{k-1}) / dt^2."""
+    return (Ubar[:, 2:] - 2.0 * Ubar[:, 1:-1] + Ubar[:, :-2]) / (dt * dt)
+
+
+def opinf_fit(Ubar, Ghat, dt, lam):
+    """Ridge OpInf for  u^'' + Kbar u^ = Bbar g^  from projected snapshots (columns = time)."""
+    Y = second_difference(Ubar, dt)                      # (r, K-2)
+    D = np.vstack([Ubar[:, 1:-1], Ghat[:, 1:-1]])        # (r + r_b, K-2)
+    n = D.shape[0]
+    A = np.vstack([D.T, np.sqrt(lam) * np.eye(n)])
+    b = np.vstack([Y.T, np.zeros((n, Y.shape[0]))])
+    Ot, *_ = np.linalg.lstsq(A, b, rcond=None)
+    O = Ot.T                                             # (r, r + r_b)
+    r = Ubar.shape[0]
+    return -O[:, :r], O[:, r:]
+
+
+def build_rom_operators(U, S, dt, r, lam, delta=0.999999, r_b=None):
+    """Phi, Phi_dS, Kbar, Bbar from snapshot matrices U (n_free x K) and S (n_s x K)."""
+    Phi, sigma = pod(U, r)
+    Phi_s_full, sigma_s = pod(S, min(S.shape))
+    if r_b is None:
+        r_b = energy_rank(sigma_s, delta)
+    Phi_s = Phi_s_full[:, :r_b]
+    Kbar, Bbar = opinf_fit(Phi.T @ U, Phi_s.T @ S, dt, lam)
+    return dict(Phi=Phi, Phi_s=Phi_s, Kbar=Kbar, Bbar=Bbar, sigma=sigma, sigma_s=sigma_s,
+                r=r, r_b=r_b, lam=lam, dt=dt)
+
+
+# ---------------------------------------------------------------------------------------
+# training runs (reading R25)
+# ---------------------------------------------------------------------------------------
+
+def _online_models_codes(cfg):
+    boxes = [fem.Box(s["lo"], s["hi"], s["nel"]) for s in cfg["subdomains"]]
+    faces = schwarz.detect_schwarz_faces(boxes)
+    return boxes, faces
+
+
+def train_single_domain(cfg, inputs):
+    """c2: single-domain FOM on the training box, snapshots at steps 0..n-1 restricted to the
+    ROM sub-block (nodes with x >= lo of the ROM box; conformal)."""
+    tr = cfg["rom"]["training"]
+    dom = tr["domain"]
+    train_cfg = dict(cfg, subdomains=[dom])
+    m = schwarz.build_models(train_cfg)[0]
+    u0 = inputs.initial_displacements(cfg, dom)
+    state = m.init_state(u0)
+    snaps = [state["u"][0].copy()]
+    for _ in range(tr["n_snapshots"] - 1):
+        state = m.advance(state, np.zeros((1, 0)))
+        snaps.append(state["u"][0].copy())
+    boxes, faces = _online_models_codes(cfg)
+    ops = {}
+    for i, s in enumerate(cfg["subdomains"]):
+        if s["kind"] != "rom":
+            continue
+        rb = boxes[i]
+        tb = m.box
+        off = np.rint((rb.lo - tb.lo) / tb.h).astype(int)
+        assert np.allclose(rb.h, tb.h), "c2 training restriction assumes a conformal sub-block"
+        I, J, K = rb.ijk(np.arange(rb.n_nodes))
+        tnodes = tb.node_id(I + off[0], J + off[1], K + off[2])
+        codes = fem.dof_codes(rb, s["dirichlet"], faces[i].keys()).reshape(-1)
+        free = np.nonzero(codes == fem.FREE)[0]
+        sd = np.nonzero(codes == fem.SCHWARZ)[0]
+        X = np.stack([u[tnodes].reshape(-1) for u in snaps], axis=1)      # (3 n_rom, K)
+        ops[i] = build_rom_operators(X[free], X[sd], cfg["dt"], cfg["rom"]["r"], cfg["rom"]["lam"],
+                                     cfg["rom"]["energy"])
+    return ops
+
+
+def train_coupled(cfg, inputs):
+    """c4/c5: FOM-FOM(-FOM) O-SAM on the training meshes, all snapshots 0..n_steps (top-down
+    training, Algorithm 2 steps 1-2)."""
+    tr = cfg["rom"]["training"]
+    train_cfg = dict(cfg, subdomains=tr["subdomains"], batch=1)
+    models = schwarz.build_models(train_cfg)
+    u0s = [inputs.initial_displacement(train_cfg, s)[None] for s in tr["subdomains"]]
+    snaps = [[] for _ in models]
+
+    def record(states):
+        for i, st in enumerate(states):
+            snaps[i].append(st["u"][0].reshape(-1).copy())
+
+    states = [m.init_state(u0) for m, u0 in zip(models, u0s)]
+    record(states)
+    for _ in range(tr["n_steps"]):
+        states, _ = schwarz.controller_step(models, states, cfg["tol"], cfg["max_iters"], cfg["min_iters"])
+        record(states)
+    ops = {}
+    for i, s in enumerate(cfg["subdomains"]):
+        if s["kind"] != "rom":
+            continue
+        m = models[i]
+        X = np.stack(snaps[i], axis=1)
+        ops[i] = build_rom_operators(X[m.free_dofs], X[m.schwarz_dofs], cfg["dt"], cfg["rom"]["r"],
+                                     cfg["rom"]["lam"], cfg["rom"]["energy"])
+    return ops
+
+
+def train(cfg, inputs):
+    kind = cfg["rom"]["training"]["kind"]
+    if kind == "single_domain":
+        return train_single_domain(cfg, inputs)
+    return train_coupled(cfg, inputs)

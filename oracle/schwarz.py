@@ -1,0 +1,272 @@
+"""Oracle: subdomain models (FOM, OpInf ROM) and the O-SAM controller (Algorithm 1).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+  * Schwarz boundary  d_S Omega_i = d Omega_i  cap  Omega_j: a face of box i
+    that lies strictly inside box j (normal direction) and is covered by it laterally; all
+    components of its closed-face nodes, Dirichlet taking precedence (readings R12, R13).
+  * FOM step: explicit Newmark with Schwarz values s = Pi u_j (fem.py).
+  * ROM step (SURVEY c.1 step 10, readings R8, R19, R22):
+        u^* = u^ + dt v^ + dt^2/2 a^ ;  g^ = Phi_dS^T s ;  a^' = e_b (-Kbar u^* + Bbar g^) ;
+        v^' = v^ + dt/2 (a^ + a^')
+  * Source field for the transfer: FOM -> its iterate; ROM -> Phi u^ on free DOFs, 0 on
+    Dirichlet DOFs and its own current s on its Schwarz DOFs; Phi "restricted to the
+    relevant boundary DoFs".
+  * Controller (P:L370-404 algo:sam-fom, L443-467 eq:conv_criterion, readings R5-R9, R26, R29):
+    multiplicative sweep in the given order; a source that precedes the destination in the
+    sweep supplies iterate n, otherwise iterate n-1 (iterate 0 = its checkpoint, constant
+    extension); convergence tested from n >= min_iters on
+        num = sum_i ||(u_i^n - u_i^{n-1}) + dt (v_i^n - v_i^{n-1})||^2 ,
+        den = sum_i ||u_i^n + dt v_i^n||^2   over unconstrained DOFs (ROM: reduced coords),
+    converged iff num == 0 or num < tol_rel^2 den (or num < tol_abs^2 if tol_abs > 0).
+    Per sample when batched; converged samples are frozen; max_iters -> keep last iterate.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import fem, transfer
+
+GEOM_TOL = 1e-12
+
+
+def detect_schwarz_faces(boxes):
+    """For each box i: {face: source j} following d_S Omega_i = d Omega_i cap Omega_j."""
+    out = []
+    for i, bi in enumerate(boxes):
+        faces = {}
+        size = float(np.max(bi.hi - bi.lo))
+        for f in range(6):
+            ax, side = f // 2, f % 2
+            x = bi.hi[ax] if side else bi.lo[ax]
+            for j, bj in enumerate(boxes):
+                if j == i:
+                    continue
+                inside = bj.lo[ax] + GEOM_TOL * size < x < bj.hi[ax] - GEOM_TOL * size
+                lateral = all(bj.lo[d] <= bi.lo[d] + GEOM_TOL * size and bi.hi[d] <= bj.hi[d] + GEOM_TOL * size
+                              for d in range(3) if d != ax)
+                if inside and lateral:
+                    faces[f] = j
+                    break
+        out.append(faces)
+    return out
+
+
+class _Base:
+    def __init__(self, sub, schwarz_faces, E, nu, rho):
+        self.box = fem.Box(sub["lo"], sub["hi"], sub["nel"])
+        self.spec = sub
+        self.schwarz_faces = dict(schwarz_faces)
+        self.codes = fem.dof_codes(self.box, sub["dirichlet"], self.schwarz_faces.keys())
+        flat = self.codes.reshape(-1)
+        self.schwarz_dofs = np.nonzero(flat == fem.SCHWARZ)[0]
+        self.free_dofs = np.nonzero(flat == fem.FREE)[0]
+        # source of each Schwarz node: the first Schwarz face (in face order) holding it
+        self.schwarz_nodes = np.unique(self.schwarz_dofs // 3)
+        src = np.full(self.box.n_nodes, -1, dtype=np.int64)
+        for f in sorted(self.schwarz_faces, reverse=True):
+            src[self.box.face_nodes(f)] = self.schwarz_faces[f]
+        self.node_src = src[self.schwarz_nodes]
+        self.E, self.nu, self.rho = E, nu, rho
+        self._proj = None
+
+    # transfer ---------------------------------------------------------------
+    def build_projectors(self, models):
+        """Donor maps of Pi for every source feeding this subdomain (host setup)."""
+        self._proj = []
+        X = self.box.coords(self.schwarz_nodes)
+        for j in np.unique(self.node_src):
+            sel = np.nonzero(self.node_src == j)[0]
+            nodes, w = transfer.projector(models[j].box, X[sel])
+            self._proj.append((int(j), sel, nodes, w))
+
+    def gather_s(self, source_states, models):
+        """s at this subdomain's Schwarz DOFs (B, n_sdofs) from the sources' current fields."""
+        vals = None
+        for j, sel, nodes, w in self._proj:
+            v = transfer.apply(nodes, w, lambda ids: models[j].values_at(source_states[j], ids))
+            if vals is None:
+                vals = np.zeros((v.shape[0], len(self.schwarz_nodes), 3))
+            vals[:, sel, :] = v
+        pos = np.searchsorted(self.schwarz_nodes, self.schwarz_dofs // 3)
+        return vals[:, pos, self.schwarz_dofs % 3]
+
+
+class FOM(_Base):
+    """Full-order model: matrix-free hex8 linear elastic FE + explicit Newmark."""
+
+    kind = "fom"
+    batch = 1
+
+    def __init__(self, sub, schwarz_faces, E, nu, rho, dt):
+        super().__init__(sub, schwarz_faces, E, nu, rho)
+        self.Ke = fem.hex8_stiffness(self.box.h, E, nu)
+        self.m = fem.lumped_mass(self.box, rho)
+        self.dt = dt
+
+    def force(self, u):
+        return fem.internal_force(self.box, self.Ke, u)
+
+    def init_state(self, u0):
+        """c.1 step 8: Dirichlet DOFs := 0, Schwarz DOFs keep the IC; v0 = 0; a0 = -f(u0)/m (free)."""
+        u0 = np.array(u0[0], dtype=np.float64)
+        u0[self.codes == fem.DIRICHLET] = 0.0
+        free = self.codes == fem.FREE
+        a0 = np.where(free, -self.force(u0) / self.m[:, None], 0.0)
+        return dict(u=u0[None], v=np.zeros_like(u0)[None], a=a0[None])
+
+    def advance(self, ckpt, s):
+        u, v, a = fem.explicit_newmark_step(ckpt["u"][0], ckpt["v"][0], ckpt["a"][0], s[0], self.codes,
+                                            self.schwarz_dofs, self.force, self.m, self.dt)
+        return dict(u=u[None], v=v[None], a=a[None])
+
+    def values_at(self, state, nodes):
+        return state["u"][:, nodes, :]
+
+    def norm_terms(self, new, prev):
+        free = (self.codes == fem.FREE)[None]
+        d = (new["u"] - prev["u"]) + self.dt * (new["v"] - prev["v"])
+        w = new["u"] + self.dt * new["v"]
+        return (np.where(free, d * d, 0.0).sum(axis=(1, 2)), np.where(free, w * w, 0.0).sum(axis=(1, 2)))
+
+
+class ROM(_Base):
+    """Linear OpInf ROM  a^ + Kbar u^ = Bbar g^ ,  g^ = Phi_dS^T s  (eq:opinf_model_schwarz)."""
+
+    kind = "rom"
+
+    def __init__(self, sub, schwarz_faces, E, nu, rho, dt, ops, e_scale=None):
+        super().__init__(sub, schwarz_faces, E, nu, rho)
+        self.dt = dt
+        self.Phi = np.asarray(ops["Phi"], dtype=np.float64)       # (n_free, r)
+        self.Phi_s = np.asarray(ops["Phi_s"], dtype=np.float64)   # (n_sdofs, r_b)
+        self.Kbar = np.asarray(ops["Kbar"], dtype=np.float64)     # (r, r)
+        self.Bbar = np.asarray(ops["Bbar"], dtype=np.float64)     # (r, r_b)
+        if self.Phi.shape[0] != len(self.free_dofs) or self.Phi_s.shape[0] != len(self.schwarz_dofs):
+            raise ValueError("ROM operator shapes do not match the subdomain DOF sets")
+        self.e = np.ones(1) if e_scale is None else np.asarray(e_scale, dtype=np.float64)
+        self.batch = len(self.e)
+        self.free_row = np.full(3 * self.box.n_nodes, -1, dtype=np.int64)
+        self.free_row[self.free_dofs] = np.arange(len(self.free_dofs))
+        self.sdof_idx = np.full(3 * self.box.n_nodes, -1, dtype=np.int64)
+        self.sdof_idx[self.schwarz_dofs] = np.arange(len(self.schwarz_dofs))
+
+    def accel(self, uh, s):
+        gh = s @ self.Phi_s                                          # (B, r_b) = (Phi_s^T s)^T
+        return self.e[:, None] * (-uh @ self.Kbar.T + gh @ self.Bbar.T)
+
+    def init_state(self, u0):
+        """u^0 = Phi^T u0[free], v^0 = 0, s0 = u0 at the Schwarz DOFs, a^0 = e(-Kbar u^0 + Bbar Phi_s^T s0)
+        (SURVEY c.1 step 10)."""
+        u0 = np.asarray(u0, dtype=np.float64).reshape(u0.shape[0], -1)
+        if u0.shape[0] == 1 and self.batch > 1:
+            u0 = np.repeat(u0, self.batch, axis=0)
+        uh = u0[:, self.free_dofs] @ self.Phi
+        s0 = u0[:, self.schwarz_dofs]
+        return dict(uh=uh, vh=np.zeros_like(uh), ah=self.accel(uh, s0), s=s0)
+
+    def advance(self, ckpt, s):
+        dt = self.dt
+        uh = ckpt["uh"] + dt * ckpt["vh"] + 0.5 * dt * dt * ckpt["ah"]
+        ah = self.accel(uh, s)
+        vh = ckpt["vh"] + 0.5 * dt * (ckpt["ah"] + ah)
+        return dict(uh=uh, vh=vh, ah=ah, s=np.array(s))
+
+    def values_at(self, state, nodes):
+        """Phi u^ on free DOFs, 0 on Dirichlet, own s on Schwarz DOFs, at the given nodes."""
+        shape = nodes.shape
+        dofs = (3 * nodes.reshape(-1)[:, None] + np.arange(3)[None, :]).reshape(-1)
+        out = np.zeros((state["uh"].shape[0], dofs.size))
+        rows = self.free_row[dofs]
+        f = rows >= 0
+        out[:, f] = state["uh"] @ self.Phi[rows[f]].T
+        sidx = self.sdof_idx[dofs]
+        g = sidx >= 0
+        out[:, g] = state["s"][:, sidx[g]]
+        return out.reshape(state["uh"].shape[0], *shape, 3)
+
+    def full_field(self, state):
+        out = np.zeros((state["uh"].shape[0], 3 * self.box.n_nodes))
+        out[:, self.free_dofs] = state["uh"] @ self.Phi.T
+        out[:, self.schwarz_dofs] = state["s"]
+        return out.reshape(out.shape[0], -1, 3)
+
+    def norm_terms(self, new, prev):
+        d = (new["uh"] - prev["uh"]) + self.dt * (new["vh"] - prev["vh"])
+        w = new["uh"] + self.dt * new["vh"]
+        return (d * d).sum(axis=1), (w * w).sum(axis=1)
+
+
+def _select(new, old, active):
+    """Per-sample freeze: keep `old` for inactive samples."""
+    out = {}
+    for k in new:
+        a = active.reshape((-1,) + (1,) * (new[k].ndim - 1)) if new[k].shape[0] == active.shape[0] else None
+        out[k] = new[k] if a is None else np.where(a, new[k], old[k])
+    return out
+
+
+def controller_step(models, states, tol_rel, max_iters=50, min_iters=2, tol_abs=0.0, trace=None):
+    """One controller step of Algorithm 1. Returns (new states, iterations per sample)."""
+    B = max(m.batch for m in models)
+    ckpt = states
+    prev = None
+    active = np.ones(B, dtype=bool)
+    iters = np.zeros(B, dtype=np.int64)
+    for n in range(1, max_iters + 1):
+        new = []
+        for i, mi in enumerate(models):
+            src_states = [new[j] if j < i else (prev[j] if prev is not None else ckpt[j])
+                          for j in range(len(models))]
+            s = mi.gather_s(src_states, models) if len(mi.schwarz_dofs) else np.zeros((mi.batch, 0))
+            if s.shape[0] != mi.batch:
+                s = s[:1] if mi.batch == 1 else np.repeat(s, mi.batch, axis=0)
+            out = mi.advance(ckpt[i], s)
+            if prev is not None and mi.batch > 1:
+                out = _select(out, prev[i], active)
+            new.append(out)
+        iters[active] = n
+        if n >= min_iters:
+            num = np.zeros(B)
+            den = np.zeros(B)
+            for mi, a, b in zip(models, new, prev):
+                nu_, de_ = mi.norm_terms(a, b)
+                num += nu_
+                den += de_
+            conv = (num == 0) | (num < tol_rel * tol_rel * den)
+            if tol_abs > 0:
+                conv |= num < tol_abs * tol_abs
+            if trace is not None:
+                trace.append((n, num.copy(), den.copy()))
+            active &= ~conv
+        prev = new
+        if not active.any():
+            break
+    return new, iters
+
+
+def build_models(cfg, rom_ops=None, e_scale=None):
+    """Instantiate oracle models for a workload description from osam_inputs.config()."""
+    boxes = [fem.Box(s["lo"], s["hi"], s["nel"]) for s in cfg["subdomains"]]
+    faces = detect_schwarz_faces(boxes)
+    models = []
+    for i, s in enumerate(cfg["subdomains"]):
+        if s["kind"] == "fom":
+            models.append(FOM(s, faces[i], cfg["E"], cfg["nu"], cfg["rho"], cfg["dt"]))
+        else:
+            models.append(ROM(s, faces[i], cfg["E"], cfg["nu"], cfg["rho"], cfg["dt"], rom_ops[i], e_scale))
+    for mdl in models:
+        mdl.build_projectors(models)
+    return models
+
+
+def run(models, u0s, dt, n_steps, tol_rel, max_iters=50, min_iters=2, tol_abs=0.0, callback=None):
+    """Run n_steps controller steps from the ICs u0s[i] (batch, n_nodes, 3)."""
+    states = [m.init_state(u0) for m, u0 in zip(models, u0s)]
+    all_iters = []
+    for k in range(n_steps):
+        states, it = controller_step(models, states, tol_rel, max_iters, min_iters, tol_abs)
+        all_iters.append(it)
+        if callback is not None:
+            callback(k, states)
+    return states, np.array(all_iters).reshape(n_steps, -1)
