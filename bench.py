@@ -1,0 +1,310 @@
+#!/usr/bin/env python
+"""Benchmark of the O-SAM FOM/OpInf coupled time loop on B200 (one JSON line on rank 0).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--workload c3]
+
+A "step" is one controller step of Algorithm 1 (all Schwarz sweeps until convergence,
+every row of SURVEY 8(a)) over the workload.  Default workload: BASELINE config c3
+(large FOM-FOM, 41,590,407 DOFs; the largest single-GPU pure-FOM config, on which the
+north_star's HBM-roofline target is stated).  `value` = FOM DOF-updates/s summed over all
+ranks (every FOM DOF counts once per Schwarz sweep).  N > 1 runs independent
+replicas (weak scaling, no data-path collective).
+--impl reference times the CPU oracle (oracle/) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import osam_inputs as I  # noqa: E402
+
+METRIC = "FOM DOF-updates/s"
+UNIT = "DOF-updates/s"
+SAMPLE_LATERAL = 32
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--workload", default="c3")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload_desc(cfg):
+    parts = []
+    dofs = 0
+    for s in cfg["subdomains"]:
+        n = (s["nel"][0] + 1) * (s["nel"][1] + 1) * (s["nel"][2] + 1)
+        if s["kind"] == "fom":
+            dofs += 3 * n
+        parts.append(f"{s['kind'].upper()} {s['nel'][0]}x{s['nel'][1]}x{s['nel'][2]}")
+    return " | ".join(parts), dofs
+
+
+def sample_cfg(cfg, lateral=SAMPLE_LATERAL):
+    """Bounded CPU sample of a FOM workload: same x-structure (meshes, overlap, Schwarz faces,
+    BCs, IC, dt), lateral extent cut to `lateral` elements of the first subdomain."""
+    out = dict(cfg)
+    subs = []
+    ref = cfg["subdomains"][0]
+    for s in cfg["subdomains"]:
+        ny = max(1, round(lateral * s["nel"][1] / ref["nel"][1]))
+        nz = max(1, round(lateral * s["nel"][2] / ref["nel"][2]))
+        hy = s["hi"][1] * lateral / ref["nel"][1]
+        hz = s["hi"][2] * lateral / ref["nel"][2]
+        subs.append(dict(s, hi=(s["hi"][0], hy, hz), nel=(s["nel"][0], ny, nz)))
+    out["subdomains"] = subs
+    return out
+
+
+def oracle_rate(cfg, warmup, steps=None, seconds=None):
+    """Oracle DOF-updates/s on cfg: `warmup` untimed controller steps then `steps` timed (or
+    as many as fit in `seconds`). Returns (rate, steps_timed, wall, threads)."""
+    from oracle import schwarz
+    models = schwarz.build_models(cfg)
+    u0s = [I.initial_displacements(cfg, s) for s in cfg["subdomains"]]
+    st = [m.init_state(u) for m, u in zip(models, u0s)]
+    dofs = sum(3 * m.box.n_nodes for m in models if m.kind == "fom")
+    for _ in range(warmup):
+        st, _ = schwarz.controller_step(models, st, cfg["tol"], cfg["max_iters"], cfg["min_iters"])
+    t0 = time.perf_counter()
+    n = 0
+    sweeps = 0
+    while True:
+        st, it = schwarz.controller_step(models, st, cfg["tol"], cfg["max_iters"], cfg["min_iters"])
+        n += 1
+        sweeps += int(it.max())
+        el = time.perf_counter() - t0
+        if (steps is not None and n >= steps) or (seconds is not None and el >= seconds and n >= 3):
+            break
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
+    except Exception:
+        threads = 1
+    return sweeps * dofs / el, n, el, threads
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md, MEASURED_PEAKS.json absent)"
+
+
+def ncu_traffic():
+    """dram bytes per K1 launch from the committed ncu --set full summary, if present."""
+    path = os.path.join(ROOT, "profiles", "k1_ncu_summary.json")
+    try:
+        return float(json.load(open(path))["dram_bytes_per_k1_launch"])
+    except Exception:
+        return None
+
+
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.06)
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        rows = [r.split(",") for r in out.strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for nm, v in zip(names, r[3:7]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                pass
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = I.config(args.workload)
+    sample = sample_cfg(cfg)
+    desc, _ = workload_desc(cfg)
+    sdesc, _ = workload_desc(sample)
+    rate, n, el, threads = oracle_rate(sample, args.warmup, steps=args.steps)
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / n, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {desc}", "sample": sdesc, "parallelism": "rank 0 only"},
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": f"{args.workload} with lateral extent cut to {SAMPLE_LATERAL} elements: {sdesc}; "
+                                       f"{n} controller steps after {args.warmup} warm-up"},
+            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py --impl ours needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2511_20687_b200 import osam, problem
+
+    cfg = I.config(args.workload)
+    desc, fom_dofs = workload_desc(cfg)
+    stream = torch.cuda.current_stream(dev)
+    subs = problem.build(cfg, stream=stream.cuda_stream)
+    fields = problem.initial_fields(cfg)
+    gpu_fields = [torch.from_numpy(f).to(dev) for f in fields]
+    for sub, f in zip(subs, gpu_fields):
+        sub.set_ic(f)
+    # warm-up (first call binds the Schwarz maps)
+    problem.run(cfg, subs, n_steps=args.warmup)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    clocks = Clocks(local)
+    osam.set_profiling(True)
+    osam.reset_profile()
+    barrier()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    _, iters = problem.run(cfg, subs, n_steps=args.steps)
+    e1.record(stream)
+    barrier()
+    ck = clocks.stop()
+    osam.set_profiling(False)
+    prof = osam.get_profile()
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    sweeps = int(iters.max(axis=1).sum())
+    value = world * sweeps * fom_dofs / (ms / 1e3)
+    steps_per_s = args.steps / (ms / 1e3)
+
+    # end to end through the C ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        host_in = [torch.from_numpy(f).pin_memory() for f in fields]
+        host_out = [torch.empty(2 * f.size, dtype=torch.float64).pin_memory() for f in fields]
+        barrier()
+        t0 = time.perf_counter()
+        for sub, h in zip(subs, host_in):
+            sub.set_ic(h)
+        _, it2 = problem.run(cfg, subs, n_steps=args.steps)
+        for sub, h in zip(subs, host_out):
+            n = h.numel() // 2
+            sub.get_state(h[:n], h[n:])
+        barrier()
+        el = time.perf_counter() - t0
+        if dist is not None:
+            t = torch.tensor([el], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        h2d = sum(f.nbytes for f in fields)
+        d2h = sum(2 * f.nbytes for f in fields) + 4 * (2 + 2) * int(it2.sum())
+        e2e = {"value": world * int(it2.max(axis=1).sum()) * fom_dofs / el, "unit": UNIT,
+               "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+               "note": "set_ic(pinned host IC) + osam_step(K) + get_state(pinned host u,v) per run; bytes / K"}
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    peak, peak_src = measured_peak()
+    k1_ms_per_launch = prof["k1_ms"] / max(1, prof["k1_launches"])
+    bytes_per_launch = prof["k1_bytes"] / max(1, prof["k1_launches"])
+    achieved = bytes_per_launch / (k1_ms_per_launch / 1e3) / 1e9
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {desc} ({fom_dofs} FOM DOFs)",
+                       "l2": "inputs larger than L2 (checkpoint+working state 2 x 3 x 8 B x DOFs = 2.0 GB)",
+                       "parallelism": "replicas" if world > 1 else "1 GPU"},
+            "schwarz_steps_per_s": world * steps_per_s,
+            "schwarz_iters_per_step": float(iters.max(axis=1).mean()),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(), "kernel": "K1 fom_advance",
+                         "bytes_model": "48 B/DOF/sweep + 16 B/DOF from sweep 2 (SURVEY 8(d))",
+                         "k1_ms_per_launch": k1_ms_per_launch, "k1_share_of_step":
+                             prof["k1_ms"] / ms, "peak_source": peak_src},
+            "gpu_launches": int(prof["kernel_launches"]),
+            "clocks": ck, "e2e": e2e}
+    if world == 1 and not args.no_cpu_baseline:
+        sample = sample_cfg(cfg)
+        sdesc, _ = workload_desc(sample)
+        rate, n, el, threads = oracle_rate(sample, 1, seconds=10.0)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
+                                "sample": f"{args.workload} with lateral extent cut to {SAMPLE_LATERAL} elements "
+                                          f"({sdesc}); {n} controller steps, {el:.1f} s"}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,132 @@
+/*
+ * osam.h -- C ABI of the B200 (sm_100a) O-SAM FOM/OpInf coupled time loop.
+ *
+ * Implements the online stage of arXiv 2511.20687 ("Hybrid coupling with operator
+ * inference and the overlapping Schwarz alternating method"): Algorithm 1
+ * with subdomain-local full-order models (hex8 linear-elastic FE, explicit Newmark
+ * beta=0/gamma=1/2 with lumped mass, A.1 P:L1934-1947) and linear
+ * OpInf ROMs (eq:opinf_model_schwarz P:L550-583, online coupling P:L617-722), coupled by
+ * pointwise (trilinear) Schwarz transfer and stopped by the relative
+ * convergence test eq:conv_criterion.  P:L### = /root/reference/PAPER.md line.
+ *
+ * All arithmetic is IEEE fp64.  Every step of the time loop runs in CUDA kernels of
+ * libosam.so; there is no CPU fallback (a missing GPU makes every call return OSAM_ECUDA).
+ *
+ * Conventions
+ *   - Box mesh [lo,hi] with nel[d] hex8 elements per axis; node id p = i + (nx+1)(j + (ny+1)k).
+ *   - Physical fields exchanged through this ABI are SoA per sample: u[c*n + p], c in {x,y,z},
+ *     n = number of nodes; batched fields are sample-major: u[b*3n + c*n + p].
+ *   - Faces are numbered 0:x-, 1:x+, 2:y-, 3:y+, 4:z-, 5:z+.
+ *   - A face of subdomain i that lies strictly inside another subdomain's box (normal
+ *     direction) and is laterally covered by it is a Schwarz face fed by the first such
+ *     subdomain in the osam_step list (d_S Omega_i = d Omega_i cap Omega_j).
+ *     All three components of its closed-face nodes are Schwarz DOFs, except components held
+ *     by a Dirichlet face (Dirichlet > Schwarz > free).  A node on two Schwarz faces takes its
+ *     value from the lower-numbered face.
+ *   - Free DOFs are ordered by ascending canonical DOF id 3p+c; Schwarz DOFs likewise.
+ *
+ * Ownership: the caller owns every pointer it passes.  Host arrays in the descriptor are
+ * copied by osam_create_subdomain.  Field pointers (osam_set_ic / osam_get_state /
+ * osam_get_accel) may be host or device pointers (detected with cudaPointerGetAttributes);
+ * device pointers are accessed only on the subdomain's stream and only during the call.
+ * The library owns its device buffers and frees them in osam_destroy.  Handles are not
+ * thread-safe.  Functions never abort and never print; on error they return a negative
+ * code and osam_last_error() describes it (thread-local string, valid until the next call).
+ */
+#ifndef OSAM_H
+#define OSAM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct osam_subdomain osam_subdomain; /* opaque handle */
+
+enum { OSAM_FOM = 0, OSAM_ROM = 1 };
+
+enum {
+  OSAM_OK = 0,
+  OSAM_WNOTCONVERGED = 1, /* some controller step hit max_iters; last iterate kept */
+  OSAM_EINVAL = -1,       /* bad sizes/pointers, hi <= lo, nel < 1, r > n_free, dt <= 0 ...   */
+  OSAM_ENOMEM = -2,       /* device allocation failed                                           */
+  OSAM_ECUDA = -3,        /* a CUDA runtime call failed (message names it)                      */
+  OSAM_EOVERLAP = -4,     /* a Schwarz node lies outside its source box by > 1e-8 h             */
+  OSAM_EUNSTABLE = -5     /* non-finite convergence norm (state blew up)                       */
+};
+
+typedef struct {
+  int32_t kind;         /* OSAM_FOM | OSAM_ROM                                                  */
+  double lo[3], hi[3];  /* box [lo,hi] in metres                                                */
+  int32_t nel[3];       /* hex8 elements per axis (>= 1)                                        */
+  double E, nu, rho;    /* Pa, -, kg/m^3 (ROM: E0 the operators were trained at)                */
+  uint8_t dirichlet[6]; /* per face, bitmask of displacement components held at 0 (1:x 2:y 4:z) */
+  /* ROM only (ignored for a FOM).  Host pointers, column-major, copied at create.            */
+  int32_t r, r_b, batch;  /* POD rank, Schwarz-boundary POD rank, samples (FOM: must be 1)      */
+  int64_t n_free, n_s;    /* rows of Phi and Phi_s; checked against the geometric DOF split at the
+                             first osam_step (OSAM_EINVAL on mismatch)                            */
+  const double *Phi;      /* n_free x r   POD basis Phi (rows = free DOFs)  */
+  const double *Phi_s;    /* n_s x r_b    Schwarz boundary basis Phi_dS (rows = Schwarz DOFs)   */
+  const double *Kbar;     /* r x r        inferred linear operator      */
+  const double *Bbar;     /* r x r_b      inferred boundary operator  */
+  const double *e_scale;  /* batch factors e_b = E_b/E0 applied to Kbar, Bbar (NULL -> 1)       */
+} osam_subdomain_desc;
+
+typedef struct {
+  double dt;         /* common time step = controller step (> 0)                                */
+  double tol_rel;    /* delta_rel of eq:conv_criterion                                          */
+  double tol_abs;    /* delta_abs; <= 0 disables the absolute test                              */
+  int32_t max_iters; /* Schwarz iteration cap (>= 1)                                             */
+  int32_t min_iters; /* first iteration at which convergence is tested (2)                      */
+} osam_schwarz_cfg;
+
+/* Create a subdomain on `cuda_stream` (a cudaStream_t; NULL = legacy default stream).
+ * Validates the descriptor, uploads ROM operators, allocates the double-buffered state.
+ * Returns OSAM_OK and *out, or a negative code (then *out = NULL). */
+int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_subdomain** out);
+
+/* Initial condition from full-mesh physical fields (batch x 3n doubles each; v0 may be NULL = 0).
+ * FOM: Dirichlet DOFs := 0, Schwarz DOFs keep u0, v := 0 on constrained DOFs, a0 = -f(u0)/m.
+ * ROM: u^0 = Phi^T u0[free], v^0 = Phi^T v0[free], s0 = u0[Schwarz DOFs],
+ *      a^0 = e_b (-Kbar u^0 + Bbar Phi_dS^T s0)  (SURVEY c.1 step 10). */
+int osam_set_ic(osam_subdomain* s, const double* u0, const double* v0);
+
+/* Advance `n_steps` controller steps of Algorithm 1 over the subdomains `sds` (sweep order =
+ * array order).  Schwarz maps are built on the first call (n_steps = 0 only builds them).
+ * iters_out (host, may be NULL): n_steps x max(batch) Schwarz iteration counts, step-major.
+ * Synchronises the stream once at the end. Returns OSAM_OK, OSAM_WNOTCONVERGED or an error. */
+int osam_step(osam_subdomain* const* sds, int32_t n_sd, const osam_schwarz_cfg* cfg, int32_t n_steps,
+              int32_t* iters_out);
+
+/* Current converged state.  FOM: u (all DOFs) and v as physical fields, 3n doubles each.
+ * ROM: u^ and v^ as r x batch column-major (u_out[b*r + i]).  Either pointer may be NULL. */
+int osam_get_state(const osam_subdomain* s, double* u_out, double* v_out);
+
+/* Diagnostic: acceleration (FOM: 3n physical field; ROM: a^, r x batch). */
+int osam_get_accel(const osam_subdomain* s, double* a_out);
+
+/* Counts: nodes, free DOFs, Schwarz DOFs, batch (any pointer may be NULL). */
+int osam_get_sizes(const osam_subdomain* s, int64_t* n_nodes, int64_t* n_free, int64_t* n_schwarz,
+                   int32_t* batch);
+
+void osam_destroy(osam_subdomain* s);
+
+const char* osam_last_error(void);
+
+/* ---- measurement helpers (not part of the method) --------------------------------------
+ * When profiling is on, osam_step records a CUDA event pair around every FOM-advance
+ * launch (kernel K1) on the subdomain's stream and accumulates their durations; the
+ * convergence check then synchronises once per iteration.  osam_get_profile returns the
+ * accumulated K1 milliseconds, the number of K1 launches, the algorithmic bytes those
+ * launches moved (48 B per FOM DOF per sweep + 16 B per DOF from sweep 2 on),
+ * and the total number of kernels this library launched since the last reset. */
+void osam_set_profiling(int32_t on);
+void osam_reset_profile(void);
+void osam_get_profile(double* k1_ms, int64_t* k1_launches, double* k1_bytes, int64_t* kernel_launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OSAM_H */

@@ -1,0 +1,295 @@
+// K2 Schwarz transfer, K3 convergence finalisation, and the OpInf ROM kernels (K4-K6).
+//
+// K2  s[p, c] = sum_{b<8} w_pb U_src[idx_pb, c],  w_pb = prod_d (xi_d or 1 - xi_d)
+//     pointwise (trilinear) projection Pi of the source's current field onto the
+//     destination's Schwarz nodes (reading R11).
+// K3  num = sum_slots num_slot, den = sum_slots den_slot in a fixed order; converged iff
+//     n >= min_iters and (num == 0 or num < tol_rel^2 den or num < tol_abs^2)
+//     (eq:conv_criterion P:L443-467; readings R6, R7, R29).
+// K4  g^ = Phi_dS^T s
+// K5  u^* = u^ + dt v^ + dt^2/2 a^ ; a^' = e_b(-Kbar u^* + Bbar g^) ; v^' = v^ + dt/2 (a^ + a^')
+//     plus reduced-coordinate norm partials (reading R8)  (P:L617-722 eq:schwarz_opinf_discrete)
+// K6  lift at donor nodes: Phi[donor rows] u^* (free), 0 (Dirichlet), own s (Schwarz)
+#include "osam_internal.h"
+
+namespace osam {
+
+namespace {
+
+inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+__global__ void transfer_kernel(int n, const int* __restrict__ idx, const double* __restrict__ xi,
+                                const int* __restrict__ out, const double* __restrict__ src, long long cs,
+                                long long bs_src, double* __restrict__ dst, long long bs_dst,
+                                const int* __restrict__ active) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (p >= n || (active != nullptr && !active[b])) return;
+  const double x = xi[3 * p], y = xi[3 * p + 1], z = xi[3 * p + 2];
+  double w[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    w[q] = ((q & 1) ? x : 1.0 - x) * ((q & 2) ? y : 1.0 - y) * ((q & 4) ? z : 1.0 - z);
+  const double* sb = src + b * bs_src;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const int o = out[3 * p + c];
+    if (o < 0) continue;
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc = fma(w[q], sb[c * cs + idx[8 * p + q]], acc);
+    dst[b * bs_dst + o] = acc;
+  }
+}
+
+__global__ void step_begin_kernel(Ctl c, int B) {
+  const int b = threadIdx.x;
+  if (b < B) {
+    c.active[b] = 1;
+    c.iters[b] = 0;
+  }
+  if (b == 0) {
+    c.flags[0] = 1;
+    c.flags[1] = 0;
+  }
+}
+
+// one block of 256 threads per sample
+__global__ void finalize_kernel(Ctl c, const double2* __restrict__ part, int n_slots, int B, int n, int min_iters,
+                                double tol_rel, double tol_abs) {
+  __shared__ double red[2][8];
+  const int b = blockIdx.x;
+  const int t = threadIdx.x;
+  double num = 0.0, den = 0.0;
+  if (n >= min_iters) {
+    for (int s = t; s < n_slots; s += blockDim.x) {
+      const double2 v = part[(long long)s * B + b];
+      num += v.x;
+      den += v.y;
+    }
+  }
+  num = warp_sum(num);
+  den = warp_sum(den);
+  if ((t & 31) == 0) {
+    red[0][t >> 5] = num;
+    red[1][t >> 5] = den;
+  }
+  __syncthreads();
+  if (t == 0) {
+    num = 0.0;
+    den = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      num += red[0][w];
+      den += red[1][w];
+    }
+    if (c.active[b]) {
+      c.iters[b] = n;
+      if (n >= min_iters) {
+        c.numden[2 * b] = num;
+        c.numden[2 * b + 1] = den;
+        if (!isfinite(num) || !isfinite(den)) c.flags[1] = 1;
+        bool conv = (num == 0.0) || (num < tol_rel * tol_rel * den);
+        if (tol_abs > 0.0) conv = conv || (num < tol_abs * tol_abs);
+        if (conv) c.active[b] = 0;
+      }
+    }
+  }
+}
+
+// flags[0] = any sample still active (single block, after finalize)
+__global__ void any_active_kernel(Ctl c, int B) {
+  int a = 0;
+  for (int b = 0; b < B; ++b) a |= c.active[b];
+  c.flags[0] = a;
+}
+
+// g^[k, b] = sum_q Phi_s[q, k] s[q, b]  (warp per output; fixed lane-strided order + xor tree)
+__global__ void rom_project_bnd_kernel(int r_b, int B, long long ns, const double* __restrict__ Phi_s,
+                                       const double* __restrict__ s, double* __restrict__ gh) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= r_b * B) return;
+  const int k = w % r_b, b = w / r_b;
+  const double* col = Phi_s + (long long)k * ns;
+  const double* sb = s + (long long)b * ns;
+  double acc = 0.0;
+  for (long long q = lane; q < ns; q += 32) acc = fma(col[q], sb[q], acc);
+  acc = warp_sum(acc);
+  if (lane == 0) gh[k + (long long)r_b * b] = acc;
+}
+
+__global__ void rom_predict_kernel(int r, int B, const double* __restrict__ uh, const double* __restrict__ vh,
+                                   const double* __restrict__ ah, double dt, double* __restrict__ us) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= r * B) return;
+  us[t] = fma(0.5 * dt * dt, ah[t], fma(dt, vh[t], uh[t]));
+}
+
+// a^'[i,b] = e_b (-sum_j Kbar[i,j] u^*[j,b] + sum_k Bbar[i,k] g^[k,b]); v^', norm partials.
+// grid (ceil(r/256), B); slot = blockIdx.x; partial layout [slot][B].
+__global__ void __launch_bounds__(256) rom_update_kernel(const RomLaunch L, int mode) {
+  __shared__ double red[2][8];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  const int r = L.r;
+  const bool on = i < r && (mode == 1 || L.active[b]);
+  double num = 0.0, den = 0.0;
+  if (on) {
+    const double* us = L.ustar + (long long)r * b;
+    const double* gh = L.gh + (long long)L.r_b * b;
+    double acc = 0.0;
+    for (int j = 0; j < r; ++j) acc = fma(L.Kbar[i + (long long)r * j], us[j], acc);
+    double accb = 0.0;
+    for (int k = 0; k < L.r_b; ++k) accb = fma(L.Bbar[i + (long long)r * k], gh[k], accb);
+    const double an = L.e[b] * (accb - acc);
+    const long long id = i + (long long)r * b;
+    if (mode == 1) {  // acceleration only (initial condition)
+      L.ah1[id] = an;
+    } else {
+      const double vn = fma(0.5 * L.dt, L.ah0[id] + an, L.vh0[id]);
+      const double un = us[i];
+      if (L.with_norm) {
+        const double d = (un - L.uh1[id]) + L.dt * (vn - L.vh1[id]);
+        const double w = un + L.dt * vn;
+        num = d * d;
+        den = w * w;
+      }
+      L.uh1[id] = un;
+      L.vh1[id] = vn;
+      L.ah1[id] = an;
+    }
+  }
+  if (mode == 1) return;
+  num = warp_sum(num);
+  den = warp_sum(den);
+  const int t = threadIdx.x;
+  if ((t & 31) == 0) {
+    red[0][t >> 5] = num;
+    red[1][t >> 5] = den;
+  }
+  __syncthreads();
+  if (t == 0) {
+    double a = 0.0, c = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      a += red[0][w];
+      c += red[1][w];
+    }
+    L.partial[(long long)blockIdx.x * L.B + b] = make_double2(a, c);
+  }
+}
+
+// out[b][ld] = code>=0 ? sum_j Phi_lift[ld, j] uh[j, b] : (code == -1 ? 0 : s[b][-2-code])
+__global__ void rom_lift_kernel(int r, int B, long long nl, const double* __restrict__ Phi_lift,
+                                const int* __restrict__ code, const double* __restrict__ uh,
+                                const double* __restrict__ s, long long ns, double* __restrict__ out) {
+  const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nl * B) return;
+  const long long ld = w % nl;
+  const int b = (int)(w / nl);
+  const int cd = code[ld];
+  double v = 0.0;
+  if (cd >= 0) {
+    const double* row = Phi_lift + (long long)cd * r;
+    const double* u = uh + (long long)r * b;
+    double acc = 0.0;
+    for (int j = lane; j < r; j += 32) acc = fma(row[j], u[j], acc);
+    v = warp_sum(acc);
+  } else if (cd <= -2) {
+    v = s[(long long)b * ns + (-2 - cd)];
+  }
+  if (lane == 0) out[(long long)b * nl + ld] = v;
+}
+
+// out[i, b] = sum_q Phi[q, i] field_b[dof(ids[q])]  (projection onto the POD basis, IC only)
+__global__ void rom_project_kernel(long long nrows, int r, int B, const double* __restrict__ Phi,
+                                   const int* __restrict__ ids, const double* __restrict__ field, long long fbs,
+                                   long long n_nodes, double* __restrict__ out) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= r * B) return;
+  const int i = w % r, b = w / r;
+  const double* col = Phi + (long long)i * nrows;
+  const double* f = field + (long long)b * fbs;
+  double acc = 0.0;
+  for (long long q = lane; q < nrows; q += 32) {
+    const long long dof = ids[q];
+    acc = fma(col[q], f[(dof % 3) * n_nodes + dof / 3], acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) out[i + (long long)r * b] = acc;
+}
+
+__global__ void gather_dofs_kernel(long long n, int B, const int* __restrict__ ids, const double* __restrict__ field,
+                                   long long fbs, long long n_nodes, double* __restrict__ out) {
+  const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (q >= n) return;
+  const long long dof = ids[q];
+  out[(long long)b * n + q] = field[(long long)b * fbs + (dof % 3) * n_nodes + dof / 3];
+}
+
+}  // namespace
+
+void launch_transfer(const XferMap& m, const double* src, long long cs, long long bs_src, double* dst,
+                     long long bs_dst, int batch, const int* active, cudaStream_t s) {
+  if (m.n == 0) return;
+  transfer_kernel<<<dim3(cdiv(m.n, 128), batch), 128, 0, s>>>(m.n, m.idx, m.xi, m.out, src, cs, bs_src, dst,
+                                                                bs_dst, active);
+}
+
+void launch_step_begin(Ctl c, int B, cudaStream_t s) { step_begin_kernel<<<1, 256, 0, s>>>(c, B); }
+
+void launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int n, int min_iters, double tol_rel,
+                     double tol_abs, cudaStream_t s) {
+  finalize_kernel<<<B, 256, 0, s>>>(c, partial, n_slots, B, n, min_iters, tol_rel, tol_abs);
+  any_active_kernel<<<1, 1, 0, s>>>(c, B);
+}
+
+int rom_partial_slots(int r) { return (int)cdiv(r, 256); }
+
+void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches) {
+  if (L.r_b > 0)
+    rom_project_bnd_kernel<<<cdiv((long long)L.r_b * L.B * 32, 256), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
+                                                                                 L.s, L.gh);
+  rom_predict_kernel<<<cdiv((long long)L.r * L.B, 256), 256, 0, s>>>(L.r, L.B, L.uh0, L.vh0, L.ah0, L.dt, L.ustar);
+  rom_update_kernel<<<dim3(cdiv(L.r, 256), L.B), 256, 0, s>>>(L, 0);
+  *launches += (L.r_b > 0) + 2;
+}
+
+void launch_rom_accel(const RomLaunch& L, const double* uh, double* ah, cudaStream_t s, int* launches) {
+  RomLaunch A = L;
+  A.ustar = const_cast<double*>(uh);
+  A.ah1 = ah;
+  if (L.r_b > 0)
+    rom_project_bnd_kernel<<<cdiv((long long)L.r_b * L.B * 32, 256), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
+                                                                                 L.s, L.gh);
+  rom_update_kernel<<<dim3(cdiv(L.r, 256), L.B), 256, 0, s>>>(A, 1);
+  *launches += (L.r_b > 0) + 1;
+}
+
+void launch_rom_lift(int r, int B, long long nl, const double* Phi_lift, const int* code, const double* uh,
+                     const double* sv, long long ns, double* out, cudaStream_t st) {
+  if (nl == 0) return;
+  rom_lift_kernel<<<cdiv(nl * B * 32, 256), 256, 0, st>>>(r, B, nl, Phi_lift, code, uh, sv, ns, out);
+}
+
+void launch_rom_project(long long nrows, int r, int B, const double* Phi, const int* ids, const double* field,
+                        long long fbs, long long n_nodes, double* out, cudaStream_t s) {
+  rom_project_kernel<<<cdiv((long long)r * B * 32, 256), 256, 0, s>>>(nrows, r, B, Phi, ids, field, fbs, n_nodes,
+                                                                     out);
+}
+
+void launch_gather_dofs(long long n, int B, const int* ids, const double* field, long long fbs, long long n_nodes,
+                        double* out, cudaStream_t s) {
+  if (n == 0) return;
+  gather_dofs_kernel<<<dim3(cdiv(n, 256), B), 256, 0, s>>>(n, B, ids, field, fbs, n_nodes, out);
+}
+
+}  // namespace osam

@@ -1,0 +1,929 @@
+// Host runtime of libosam.so: the C ABI of include/osam.h, subdomain binding (Schwarz-face
+// detection and transfer maps), initial conditions, and the Schwarz controller that drives
+// the kernels of kernels_fom.cu / kernels_xfer_rom.cu.
+//
+// Controller (Algorithm 1): for each controller step, sweep the subdomains in
+// array order; a source that precedes the destination supplies iterate n, otherwise iterate
+// n-1 (iterate 0 = its checkpoint: constant extension, reading R5); test convergence from
+// n >= min_iters with eq:conv_criterion; commit by swapping the checkpoint and
+// working buffers (no copy).  Hitting max_iters keeps the last iterate (reading R9).
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "osam_internal.h"
+
+struct osam_subdomain {
+  osam::Sub s;
+};
+
+namespace osam {
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                            \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) return fail(OSAM_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class T>
+int dalloc(T** p, size_t n) {
+  *p = nullptr;
+  if (n == 0) return OSAM_OK;
+  cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    return fail(e == cudaErrorMemoryAllocation ? OSAM_ENOMEM : OSAM_ECUDA, "cudaMalloc(%zu bytes): %s",
+                n * sizeof(T), cudaGetErrorString(e));
+  }
+  return OSAM_OK;
+}
+#define TRY(x)                 \
+  do {                         \
+    int rc_ = (x);             \
+    if (rc_ != OSAM_OK) return rc_; \
+  } while (0)
+
+template <class T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+// ---- profiling / launch accounting --------------------------------------------------------
+bool g_prof = false;
+double g_k1_ms = 0.0;
+long long g_k1_launches = 0;
+double g_k1_bytes = 0.0;
+long long g_launches = 0;
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// ---- stencil coefficients (independent 1D tensor-product derivation) ---------------------
+// Per axis and node class (0 low end, 1 interior, 2 high end) the assembled 1D rows of
+//   M = int phi_p phi_q,  S = int phi_p' phi_q',  G = int phi_p' phi_q,  Gt = int phi_p phi_q'
+// are the sums of the left- and right-element contributions that exist.  For a box mesh
+// the 3D operator D_jl[p,q] = int d_j N_p d_l N_q factorises into per-axis rows (S on axis
+// j = l; G on j and Gt on l for j != l; M elsewhere), and for isotropic elasticity
+//   K_cd = lambda D_cd + mu delta_cd sum_l D_ll + mu D_dc      (A.1 P:L1939-1947).
+void stencil_table(const double h[3], double lam, double mu, std::vector<double>& out) {
+  double X[3][3][4][3];  // [axis][class][op M,S,G,Gt][offset+1]
+  for (int ax = 0; ax < 3; ++ax) {
+    const double hh = h[ax];
+    const double L[4][3] = {{hh / 6, hh / 3, 0}, {-1 / hh, 1 / hh, 0}, {0.5, 0.5, 0}, {-0.5, 0.5, 0}};
+    const double R[4][3] = {{0, hh / 3, hh / 6}, {0, 1 / hh, -1 / hh}, {0, -0.5, -0.5}, {0, -0.5, 0.5}};
+    for (int cl = 0; cl < 3; ++cl) {
+      const double eL = cl != 0 ? 1.0 : 0.0, eR = cl != 2 ? 1.0 : 0.0;
+      for (int op = 0; op < 4; ++op)
+        for (int o = 0; o < 3; ++o) X[ax][cl][op][o] = eL * L[op][o] + eR * R[op][o];
+    }
+  }
+  out.assign((size_t)NCLASS * 27 * 9, 0.0);
+  for (int cls = 0; cls < NCLASS; ++cls) {
+    const int cl[3] = {cls % 3, (cls / 3) % 3, cls / 9};
+    for (int off = 0; off < 27; ++off) {
+      const int o[3] = {off % 3, (off / 3) % 3, off / 9};
+      double D[3][3];
+      for (int j = 0; j < 3; ++j)
+        for (int l = 0; l < 3; ++l) {
+          double v = 1.0;
+          for (int ax = 0; ax < 3; ++ax) {
+            const int op = (ax == j && ax == l) ? 1 : (ax == j ? 2 : (ax == l ? 3 : 0));
+            v *= X[ax][cl[ax]][op][o[ax]];
+          }
+          D[j][l] = v;
+        }
+      const double tr = D[0][0] + D[1][1] + D[2][2];
+      for (int c = 0; c < 3; ++c)
+        for (int d = 0; d < 3; ++d)
+          out[((size_t)cls * 27 + off) * 9 + c * 3 + d] = lam * D[c][d] + mu * (c == d ? tr : 0.0) + mu * D[d][c];
+    }
+  }
+}
+
+long long face_count(const Geom& g, int f) {
+  const int ax = f >> 1;
+  const int o0 = ax == 0 ? 1 : 0, o1 = ax == 2 ? 1 : 2;
+  return (long long)g.nn[o0] * g.nn[o1];
+}
+
+// ---- binding ------------------------------------------------------------------------------
+void release_maps(Sub& s) {
+  for (auto& m : s.maps) {
+    dfree(m.idx);
+    dfree(m.xi);
+    dfree(m.out);
+  }
+  s.maps.clear();
+}
+
+void release_binding(Sub& s) {
+  release_maps(s);
+  for (int f = 0; f < 6; ++f) dfree(s.faces.s[f]);
+  dfree(s.Phi);
+  dfree(s.Phi_s);
+  dfree(s.Kbar);
+  dfree(s.Bbar);
+  dfree(s.e);
+  for (int b = 0; b < 2; ++b) {
+    for (int q = 0; q < 4; ++q) dfree(s.rst[b][q]);
+    dfree(s.lift[b]);
+  }
+  dfree(s.ustar);
+  dfree(s.gh);
+  dfree(s.free_ids);
+  dfree(s.sdof_ids);
+  dfree(s.Phi_lift);
+  dfree(s.lift_code);
+  s.bound = false;
+  s.group.clear();
+}
+
+struct Group {
+  std::vector<osam_subdomain*> sds;
+  int B = 1;
+  int n_slots = 0;
+  double2* partial = nullptr;
+  int* ctl_i = nullptr;  // [flags0, flags1, active[B], iters[B]]
+  double* numden = nullptr;
+  int* h_ctl = nullptr;  // pinned copy
+  std::vector<cudaEvent_t> ev;
+  ~Group() {
+    dfree(partial);
+    dfree(ctl_i);
+    dfree(numden);
+    if (h_ctl) cudaFreeHost(h_ctl);
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+  Ctl ctl() const { return Ctl{ctl_i + 2, ctl_i + 2 + B, numden, ctl_i}; }
+};
+std::map<std::vector<osam_subdomain*>, std::unique_ptr<Group>> g_groups;
+
+void forget_groups_with(osam_subdomain* h) {
+  for (auto it = g_groups.begin(); it != g_groups.end();) {
+    if (std::find(it->first.begin(), it->first.end(), h) != it->first.end())
+      it = g_groups.erase(it);
+    else
+      ++it;
+  }
+}
+
+// Schwarz faces: d_S Omega_i = d Omega_i cap Omega_j
+void detect_faces(const std::vector<Sub*>& subs, int i, int face_src[6]) {
+  const Sub& a = *subs[i];
+  double size = 0;
+  for (int d = 0; d < 3; ++d) size = std::max(size, a.hi[d] - a.lo[d]);
+  const double tol = 1e-12 * size;
+  for (int f = 0; f < 6; ++f) {
+    face_src[f] = -1;
+    const int ax = f / 2;
+    const double x = (f & 1) ? a.hi[ax] : a.lo[ax];
+    for (int j = 0; j < (int)subs.size(); ++j) {
+      if (j == i) continue;
+      const Sub& b = *subs[j];
+      bool ok = b.lo[ax] + tol < x && x < b.hi[ax] - tol;
+      for (int d = 0; d < 3 && ok; ++d)
+        if (d != ax) ok = b.lo[d] <= a.lo[d] + tol && a.hi[d] <= b.hi[d] + tol;
+      if (ok) {
+        face_src[f] = j;
+        break;
+      }
+    }
+  }
+}
+
+void build_codes(Sub& s) {
+  const Geom& g = s.g;
+  s.codes.assign((size_t)3 * s.n_nodes, DOF_FREE);
+  for (long long p = 0; p < s.n_nodes; ++p) {
+    const int idx[3] = {(int)(p % g.nn[0]), (int)((p / g.nn[0]) % g.nn[1]), (int)(p / ((long long)g.nn[0] * g.nn[1]))};
+    bool onf[6];
+    for (int f = 0; f < 6; ++f) onf[f] = idx[f / 2] == ((f & 1) ? g.nn[f / 2] - 1 : 0);
+    bool sw = false;
+    for (int f = 0; f < 6; ++f) sw = sw || (onf[f] && s.face_src[f] >= 0);
+    for (int c = 0; c < 3; ++c) {
+      bool dir = false;
+      for (int f = 0; f < 6; ++f) dir = dir || (onf[f] && ((s.dirichlet[f] >> c) & 1));
+      s.codes[3 * p + c] = dir ? DOF_DIRICHLET : (sw ? DOF_SCHWARZ : DOF_FREE);
+    }
+  }
+  s.n_free = s.n_sdof = 0;
+  for (auto c : s.codes) {
+    s.n_free += c == DOF_FREE;
+    s.n_sdof += c == DOF_SCHWARZ;
+  }
+}
+
+// owner Schwarz face of a node (lowest face index), -1 if none
+int owner_face(const Sub& s, long long p) {
+  const Geom& g = s.g;
+  const int idx[3] = {(int)(p % g.nn[0]), (int)((p / g.nn[0]) % g.nn[1]), (int)(p / ((long long)g.nn[0] * g.nn[1]))};
+  for (int f = 0; f < 6; ++f)
+    if (s.face_src[f] >= 0 && idx[f / 2] == ((f & 1) ? g.nn[f / 2] - 1 : 0)) return f;
+  return -1;
+}
+
+template <class T>
+int upload(T** d, const std::vector<T>& h, cudaStream_t st) {
+  TRY(dalloc(d, h.size()));
+  if (!h.empty()) CK(cudaMemcpyAsync(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+  return OSAM_OK;
+}
+
+int process_ic(Sub& s, int* launches);
+
+int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>& handles) {
+  const int n = (int)subs.size();
+  for (int i = 0; i < n; ++i) {
+    release_binding(*subs[i]);
+    detect_faces(subs, i, subs[i]->face_src);
+    build_codes(*subs[i]);
+  }
+  // ROM shape checks and uploads
+  for (int i = 0; i < n; ++i) {
+    Sub& s = *subs[i];
+    s.group = handles;
+    if (s.kind != OSAM_ROM) {
+      for (int f = 0; f < 6; ++f) {
+        s.faces.dir[f] = s.dirichlet[f];
+        s.faces.sw[f] = s.face_src[f] >= 0;
+        s.faces.nface[f] = (int)face_count(s.g, f);
+        s.faces.s[f] = nullptr;
+        if (s.faces.sw[f]) TRY(dalloc(&s.faces.s[f], 3 * (size_t)s.faces.nface[f]));
+      }
+      continue;
+    }
+    const long long rows_phi = (long long)(s.h_Phi.size() / std::max(1, s.r));
+    const long long rows_phis = s.r_b > 0 ? (long long)(s.h_Phi_s.size() / s.r_b) : s.n_sdof;
+    if (rows_phi != s.n_free || rows_phis != s.n_sdof)
+      return fail(OSAM_EINVAL, "ROM subdomain %d: Phi has %lld rows, Phi_s %lld, but the geometric split gives "
+                  "n_free=%lld, n_s=%lld", i, rows_phi, rows_phis, s.n_free, s.n_sdof);
+    if (s.r > s.n_free) return fail(OSAM_EINVAL, "ROM subdomain %d: r > n_free", i);
+    std::vector<int> fid, sid;
+    for (long long q = 0; q < 3 * s.n_nodes; ++q) {
+      if (s.codes[q] == DOF_FREE) fid.push_back((int)q);
+      if (s.codes[q] == DOF_SCHWARZ) sid.push_back((int)q);
+    }
+    TRY(upload(&s.Phi, s.h_Phi, s.stream));
+    TRY(upload(&s.Phi_s, s.h_Phi_s, s.stream));
+    TRY(upload(&s.Kbar, s.h_Kbar, s.stream));
+    TRY(upload(&s.Bbar, s.h_Bbar, s.stream));
+    TRY(upload(&s.e, s.h_e, s.stream));
+    TRY(upload(&s.free_ids, fid, s.stream));
+    TRY(upload(&s.sdof_ids, sid, s.stream));
+    for (int b = 0; b < 2; ++b) {
+      for (int q = 0; q < 3; ++q) TRY(dalloc(&s.rst[b][q], (size_t)s.r * s.batch));
+      TRY(dalloc(&s.rst[b][3], (size_t)std::max<long long>(1, s.n_sdof) * s.batch));
+    }
+    TRY(dalloc(&s.ustar, (size_t)s.r * s.batch));
+    TRY(dalloc(&s.gh, (size_t)std::max(1, s.r_b) * s.batch));
+  }
+  // donor maps: collect, per source, the nodes it must provide (ROM sources: compact lists)
+  struct Pending {
+    int dst, face, src;
+    std::vector<long long> corner;  // [n][8] source node ids
+    std::vector<double> xi;         // [n][3]
+    std::vector<int> out;           // [n][3]
+  };
+  std::vector<Pending> pend;
+  for (int i = 0; i < n; ++i) {
+    Sub& d = *subs[i];
+    for (int f = 0; f < 6; ++f) {
+      const int j = d.face_src[f];
+      if (j < 0) continue;
+      const Sub& src = *subs[j];
+      Pending P;
+      P.dst = i;
+      P.face = f;
+      P.src = j;
+      const int ax = f >> 1;
+      const int o0 = ax == 0 ? 1 : 0, o1 = ax == 2 ? 1 : 2;
+      const long long nf = face_count(d.g, f);
+      P.corner.resize(nf * 8);
+      P.xi.resize(nf * 3);
+      P.out.resize(nf * 3);
+      std::vector<long long> sdof_index;
+      if (d.kind == OSAM_ROM) {
+        sdof_index.assign((size_t)3 * d.n_nodes, -1);
+        long long q = 0;
+        for (long long t = 0; t < 3 * d.n_nodes; ++t)
+          if (d.codes[t] == DOF_SCHWARZ) sdof_index[t] = q++;
+      }
+      for (long long t = 0; t < nf; ++t) {
+        int idx[3];
+        idx[ax] = (f & 1) ? d.g.nn[ax] - 1 : 0;
+        idx[o0] = (int)(t % d.g.nn[o0]);
+        idx[o1] = (int)(t / d.g.nn[o0]);
+        const long long p = idx[0] + (long long)d.g.nn[0] * (idx[1] + (long long)d.g.nn[1] * idx[2]);
+        int cell[3];
+        for (int a = 0; a < 3; ++a) {
+          const double X = d.lo[a] + idx[a] * d.g.h[a];
+          const double tt = (X - src.lo[a]) / src.g.h[a];
+          int ci = (int)std::floor(tt);
+          ci = std::min(std::max(ci, 0), src.nel[a] - 1);
+          const double x = tt - ci;
+          if (!(x >= -1e-8 && x <= 1.0 + 1e-8))
+            return fail(OSAM_EOVERLAP, "Schwarz node %lld of subdomain %d (face %d) lies outside source %d", p, i, f,
+                        j);
+          cell[a] = ci;
+          P.xi[3 * t + a] = x;
+        }
+        for (int q = 0; q < 8; ++q) {
+          const long long ci = cell[0] + (q & 1), cj = cell[1] + ((q >> 1) & 1), ck = cell[2] + ((q >> 2) & 1);
+          P.corner[8 * t + q] = ci + (long long)src.g.nn[0] * (cj + (long long)src.g.nn[1] * ck);
+        }
+        for (int c = 0; c < 3; ++c) {
+          if (d.kind == OSAM_ROM) {
+            const bool mine = d.codes[3 * p + c] == DOF_SCHWARZ && owner_face(d, p) == f;
+            P.out[3 * t + c] = mine ? (int)sdof_index[3 * p + c] : -1;
+          } else {
+            P.out[3 * t + c] = (int)(c * nf + t);
+          }
+        }
+      }
+      pend.push_back(std::move(P));
+    }
+  }
+  for (int j = 0; j < n; ++j) {
+    Sub& s = *subs[j];
+    if (s.kind != OSAM_ROM) continue;
+    std::vector<long long> nodes;
+    for (auto& P : pend)
+      if (P.src == j) nodes.insert(nodes.end(), P.corner.begin(), P.corner.end());
+    std::sort(nodes.begin(), nodes.end());
+    nodes.erase(std::unique(nodes.begin(), nodes.end()), nodes.end());
+    s.lift_nodes = nodes;
+    s.n_lift = (long long)nodes.size();
+    const long long nl = 3 * s.n_lift;
+    std::vector<long long> free_row((size_t)3 * s.n_nodes, -1), sidx((size_t)3 * s.n_nodes, -1);
+    long long fr = 0, sr = 0;
+    for (long long t = 0; t < 3 * s.n_nodes; ++t) {
+      if (s.codes[t] == DOF_FREE) free_row[t] = fr++;
+      if (s.codes[t] == DOF_SCHWARZ) sidx[t] = sr++;
+    }
+    std::vector<double> phil((size_t)std::max<long long>(nl, 1) * s.r, 0.0);
+    std::vector<int> code((size_t)std::max<long long>(nl, 1), -1);
+    for (int c = 0; c < 3; ++c)
+      for (long long qi = 0; qi < s.n_lift; ++qi) {
+        const long long ld = c * s.n_lift + qi;
+        const long long dof = 3 * nodes[qi] + c;
+        if (s.codes[dof] == DOF_FREE) {
+          code[ld] = (int)ld;
+          for (int k = 0; k < s.r; ++k) phil[ld * s.r + k] = s.h_Phi[free_row[dof] + (size_t)s.n_free * k];
+        } else if (s.codes[dof] == DOF_SCHWARZ) {
+          code[ld] = -2 - (int)sidx[dof];
+        }
+      }
+    TRY(upload(&s.Phi_lift, phil, s.stream));
+    TRY(upload(&s.lift_code, code, s.stream));
+    for (int b = 0; b < 2; ++b) TRY(dalloc(&s.lift[b], (size_t)std::max<long long>(nl, 1) * s.batch));
+  }
+  for (auto& P : pend) {
+    Sub& d = *subs[P.dst];
+    const Sub& src = *subs[P.src];
+    XferMap m;
+    m.src = P.src;
+    m.face = P.face;
+    m.n = (int)(P.corner.size() / 8);
+    std::vector<int> idx(P.corner.size());
+    for (size_t q = 0; q < P.corner.size(); ++q) {
+      const long long node = P.corner[q];
+      if (src.kind == OSAM_ROM) {
+        idx[q] = (int)(std::lower_bound(src.lift_nodes.begin(), src.lift_nodes.end(), node) - src.lift_nodes.begin());
+      } else {
+        const long long i0 = node % src.g.nn[0], j0 = (node / src.g.nn[0]) % src.g.nn[1],
+                        k0 = node / ((long long)src.g.nn[0] * src.g.nn[1]);
+        idx[q] = (int)(i0 + src.g.px * (j0 + (long long)src.g.nn[1] * k0));
+      }
+    }
+    TRY(upload(&m.idx, idx, d.stream));
+    TRY(upload(&m.xi, P.xi, d.stream));
+    TRY(upload(&m.out, P.out, d.stream));
+    d.maps.push_back(m);
+  }
+  for (int i = 0; i < n; ++i) subs[i]->bound = true;
+  int launches = 0;
+  for (int i = 0; i < n; ++i)
+    if (subs[i]->ic_pending) TRY(process_ic(*subs[i], &launches));
+  g_launches += launches;
+  return OSAM_OK;
+}
+
+// Initial condition once the Schwarz split is known (c.1 steps 8 and 10).
+int process_ic(Sub& s, int* launches) {
+  cudaStream_t st = s.stream;
+  if (s.kind == OSAM_FOM) {
+    const int c = s.cur;
+    launch_fom_zero_constrained(s.g, s.faces, s.st[c][0], s.st[c][1], s.st[c][2], 1, st);
+    launch_fom_face_gather(s.g, s.faces, s.st[c][0], st);
+    FomLaunch L{};
+    L.g = s.g;
+    L.f = s.faces;
+    L.u0 = s.st[c][0];
+    L.v0 = s.st[c][1];
+    L.a0 = s.st[c][2];
+    L.u1 = s.st[1 - c][0];
+    L.v1 = s.st[1 - c][1];
+    L.a1 = s.st[1 - c][2];
+    L.dt = 0.0;
+    L.mass_e = s.mass_e;
+    L.coef = s.coef;
+    L.with_norm = 0;
+    double2* scratch = nullptr;
+    TRY(dalloc(&scratch, (size_t)fom_partial_slots(s.g)));
+    L.partial = scratch;
+    *launches += 2;
+    launch_fom_advance(L, s.stencil, st, launches);
+    CK(cudaStreamSynchronize(st));
+    dfree(scratch);
+    s.cur = 1 - c;
+  } else {
+    const int c = s.cur;
+    const long long fbs = 3 * s.n_nodes;
+    launch_rom_project(s.n_free, s.r, s.batch, s.Phi, s.free_ids, s.ic_u, fbs, s.n_nodes, s.rst[c][0], st);
+    launch_rom_project(s.n_free, s.r, s.batch, s.Phi, s.free_ids, s.ic_v, fbs, s.n_nodes, s.rst[c][1], st);
+    launch_gather_dofs(s.n_sdof, s.batch, s.sdof_ids, s.ic_u, fbs, s.n_nodes, s.rst[c][3], st);
+    RomLaunch L{};
+    L.r = s.r;
+    L.r_b = s.r_b;
+    L.B = s.batch;
+    L.n_sdof = s.n_sdof;
+    L.Phi_s = s.Phi_s;
+    L.Kbar = s.Kbar;
+    L.Bbar = s.Bbar;
+    L.e = s.e;
+    L.s = s.rst[c][3];
+    L.gh = s.gh;
+    launch_rom_accel(L, s.rst[c][0], s.rst[c][2], st, launches);
+    launch_rom_lift(s.r, s.batch, 3 * s.n_lift, s.Phi_lift, s.lift_code, s.rst[c][0], s.rst[c][3], s.n_sdof,
+                    s.lift[c], st);
+    *launches += 4;
+    CK(cudaStreamSynchronize(st));
+  }
+  CK(cudaGetLastError());
+  dfree(s.ic_u);
+  dfree(s.ic_v);
+  s.ic_pending = false;
+  return OSAM_OK;
+}
+
+int get_group(osam_subdomain* const* sds, int n_sd, Group** out) {
+  std::vector<osam_subdomain*> key(sds, sds + n_sd);
+  auto it = g_groups.find(key);
+  std::vector<Sub*> subs;
+  for (auto h : key) subs.push_back(&h->s);
+  bool need_bind = it == g_groups.end();
+  for (auto s : subs) need_bind = need_bind || !s->bound || s->group != key;
+  if (need_bind) {
+    TRY(bind_group(subs, key));
+    auto G = std::make_unique<Group>();
+    G->sds = key;
+    G->B = 1;
+    for (auto s : subs) G->B = std::max(G->B, s->batch);
+    G->n_slots = 0;
+    for (auto s : subs) G->n_slots += s->kind == OSAM_FOM ? fom_partial_slots(s->g) : rom_partial_slots(s->r);
+    TRY(dalloc(&G->partial, (size_t)std::max(1, G->n_slots) * G->B));
+    TRY(dalloc(&G->ctl_i, (size_t)2 + 2 * G->B));
+    TRY(dalloc(&G->numden, (size_t)2 * G->B));
+    CK(cudaMallocHost((void**)&G->h_ctl, sizeof(int) * (2 + 2 * G->B)));
+    g_groups[key] = std::move(G);
+    it = g_groups.find(key);
+  }
+  *out = it->second.get();
+  return OSAM_OK;
+}
+
+// one controller step; returns OSAM_OK / OSAM_WNOTCONVERGED / error; iters (host) [B]
+int controller_step(Group& G, const osam_schwarz_cfg& cfg, int32_t* iters) {
+  std::vector<Sub*> subs;
+  for (auto h : G.sds) subs.push_back(&h->s);
+  const int n_sd = (int)subs.size();
+  cudaStream_t st = subs[0]->stream;
+  const int B = G.B;
+  const Ctl ctl = G.ctl();
+  int launches = 0;
+  launch_step_begin(ctl, B, st);
+  ++launches;
+  int n = 1;
+  bool done = false, hit_max = false;
+  int n_fom = 0;
+  for (auto s : subs) n_fom += s->kind == OSAM_FOM;
+  if (g_prof && (int)G.ev.size() < 2 * n_fom) {
+    while ((int)G.ev.size() < 2 * n_fom) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      G.ev.push_back(e);
+    }
+  }
+  for (n = 1; n <= cfg.max_iters; ++n) {
+    int slot = 0;
+    int fom_k = 0;
+    for (int i = 0; i < n_sd; ++i) {
+      Sub& d = *subs[i];
+      // K2: Schwarz transfer from each source's current field
+      for (const XferMap& m : d.maps) {
+        const Sub& src = *subs[m.src];
+        const bool newest = (m.src < i) || (n > 1);
+        const int sb = newest ? 1 - src.cur : src.cur;
+        const double* field;
+        long long cs, bs;
+        if (src.kind == OSAM_FOM) {
+          field = src.st[sb][0];
+          cs = src.g.npad;
+          bs = 0;
+        } else {
+          field = src.lift[sb];
+          cs = src.n_lift;
+          bs = 3 * src.n_lift;
+        }
+        double* dst;
+        long long dbs;
+        if (d.kind == OSAM_FOM) {
+          dst = d.faces.s[m.face];
+          dbs = 0;
+        } else {
+          dst = d.rst[1 - d.cur][3];
+          dbs = d.n_sdof;
+        }
+        launch_transfer(m, field, cs, bs, dst, dbs, B, B > 1 ? ctl.active : nullptr, st);
+        ++launches;
+      }
+      const int with_norm = n >= 2 ? 1 : 0;
+      if (d.kind == OSAM_FOM) {
+        const int c = d.cur;
+        FomLaunch L{};
+        L.g = d.g;
+        L.f = d.faces;
+        L.u0 = d.st[c][0];
+        L.v0 = d.st[c][1];
+        L.a0 = d.st[c][2];
+        L.u1 = d.st[1 - c][0];
+        L.v1 = d.st[1 - c][1];
+        L.a1 = d.st[1 - c][2];
+        L.dt = cfg.dt;
+        L.mass_e = d.mass_e;
+        L.coef = d.coef;
+        L.with_norm = with_norm;
+        L.partial = G.partial + (size_t)slot * B;
+        if (g_prof) CK(cudaEventRecord(G.ev[2 * fom_k], st));
+        launch_fom_advance(L, d.stencil, st, &launches);
+        if (g_prof) CK(cudaEventRecord(G.ev[2 * fom_k + 1], st));
+        g_k1_bytes += (48.0 + (with_norm ? 16.0 : 0.0)) * 3.0 * (double)d.n_nodes;
+        ++g_k1_launches;
+        ++fom_k;
+        slot += fom_partial_slots(d.g);
+      } else {
+        const int c = d.cur;
+        RomLaunch L{};
+        L.r = d.r;
+        L.r_b = d.r_b;
+        L.B = d.batch;
+        L.n_sdof = d.n_sdof;
+        L.Phi_s = d.Phi_s;
+        L.Kbar = d.Kbar;
+        L.Bbar = d.Bbar;
+        L.e = d.e;
+        L.uh0 = d.rst[c][0];
+        L.vh0 = d.rst[c][1];
+        L.ah0 = d.rst[c][2];
+        L.uh1 = d.rst[1 - c][0];
+        L.vh1 = d.rst[1 - c][1];
+        L.ah1 = d.rst[1 - c][2];
+        L.s = d.rst[1 - c][3];
+        L.ustar = d.ustar;
+        L.gh = d.gh;
+        L.active = ctl.active;
+        L.dt = cfg.dt;
+        L.with_norm = with_norm;
+        L.partial = G.partial + (size_t)slot * B;
+        launch_rom_advance(L, st, &launches);
+        launch_rom_lift(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, d.rst[1 - c][0], d.rst[1 - c][3],
+                        d.n_sdof, d.lift[1 - c], st);
+        launches += d.n_lift > 0;
+        slot += rom_partial_slots(d.r);
+      }
+    }
+    launch_finalize(ctl, G.partial, G.n_slots, B, n, cfg.min_iters, cfg.tol_rel, cfg.tol_abs, st);
+    launches += 2;
+    if (n >= cfg.min_iters || g_prof) {
+      CK(cudaMemcpyAsync(G.h_ctl, G.ctl_i, sizeof(int) * (2 + 2 * B), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (g_prof) {
+        for (int k = 0; k < fom_k; ++k) {
+          float ms = 0.f;
+          CK(cudaEventElapsedTime(&ms, G.ev[2 * k], G.ev[2 * k + 1]));
+          g_k1_ms += ms;
+        }
+      }
+      if (G.h_ctl[1]) {
+        g_launches += launches;
+        return fail(OSAM_EUNSTABLE, "non-finite Schwarz convergence norm at iteration %d", n);
+      }
+      if (n >= cfg.min_iters && !G.h_ctl[0]) {
+        done = true;
+        break;
+      }
+    }
+  }
+  if (!done) {
+    hit_max = true;
+    n = cfg.max_iters;
+    CK(cudaMemcpyAsync(G.h_ctl, G.ctl_i, sizeof(int) * (2 + 2 * B), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  CK(cudaGetLastError());
+  for (int b = 0; b < B; ++b) iters[b] = G.h_ctl[2 + B + b];
+  for (auto s : subs) s->cur = 1 - s->cur;  // commit: working iterate becomes the checkpoint
+  g_launches += launches;
+  return hit_max ? OSAM_WNOTCONVERGED : OSAM_OK;
+}
+
+}  // namespace
+}  // namespace osam
+
+using namespace osam;
+
+extern "C" {
+
+const char* osam_last_error(void) { return g_err.c_str(); }
+
+int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_subdomain** out) {
+  if (!out) return fail(OSAM_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!d) return fail(OSAM_EINVAL, "descriptor is NULL");
+  if (d->kind != OSAM_FOM && d->kind != OSAM_ROM) return fail(OSAM_EINVAL, "kind must be OSAM_FOM or OSAM_ROM");
+  for (int a = 0; a < 3; ++a) {
+    if (!(d->hi[a] > d->lo[a])) return fail(OSAM_EINVAL, "hi <= lo on axis %d", a);
+    if (d->nel[a] < 1) return fail(OSAM_EINVAL, "nel[%d] < 1", a);
+  }
+  if (!(d->E > 0) || !(d->rho > 0) || !(d->nu > -1.0 && d->nu < 0.5)) return fail(OSAM_EINVAL, "bad material");
+  for (int f = 0; f < 6; ++f)
+    if (d->dirichlet[f] > 7) return fail(OSAM_EINVAL, "dirichlet[%d] > 7", f);
+  const long long nn0 = d->nel[0] + 1LL, nn1 = d->nel[1] + 1LL, nn2 = d->nel[2] + 1LL;
+  if (nn0 * nn1 * nn2 > (1LL << 30)) return fail(OSAM_EINVAL, "mesh too large (> 2^30 nodes)");
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(OSAM_ECUDA, "cudaGetDevice: %s (no usable GPU)", cudaGetErrorString(e));
+
+  auto h = std::make_unique<osam_subdomain>();
+  Sub& s = h->s;
+  s.kind = d->kind;
+  for (int a = 0; a < 3; ++a) {
+    s.lo[a] = d->lo[a];
+    s.hi[a] = d->hi[a];
+    s.nel[a] = d->nel[a];
+  }
+  s.E = d->E;
+  s.nu = d->nu;
+  s.rho = d->rho;
+  s.lam = d->E * d->nu / ((1 + d->nu) * (1 - 2 * d->nu));
+  s.mu = d->E / (2 * (1 + d->nu));
+  std::memcpy(s.dirichlet, d->dirichlet, 6);
+  s.stream = (cudaStream_t)cuda_stream;
+  Geom& g = s.g;
+  g.nn[0] = (int)nn0;
+  g.nn[1] = (int)nn1;
+  g.nn[2] = (int)nn2;
+  g.px = (int)((nn0 + 3) / 4 * 4);
+  g.plane = (long long)g.px * nn1;
+  g.npad = (g.plane * nn2 + 31) / 32 * 32;
+  for (int a = 0; a < 3; ++a) g.h[a] = (d->hi[a] - d->lo[a]) / d->nel[a];
+  s.n_nodes = nn0 * nn1 * nn2;
+  s.mass_e = d->rho * g.h[0] * g.h[1] * g.h[2] / 8.0;
+  for (int f = 0; f < 6; ++f) s.faces.s[f] = nullptr;
+  if (s.kind == OSAM_FOM) {
+    if (d->batch > 1) return fail(OSAM_EINVAL, "a FOM subdomain has batch 1");
+    s.batch = 1;
+    std::vector<double> tab;
+    stencil_table(g.h, s.lam, s.mu, tab);
+    // the interior kernel skips the structural zeros of the interior class: check them
+    for (int off = 0; off < 27; ++off) {
+      const int o[3] = {off % 3 - 1, (off / 3) % 3 - 1, off / 9 - 1};
+      for (int c = 0; c < 3; ++c)
+        for (int dd = 0; dd < 3; ++dd) {
+          const double v = tab[((size_t)13 * 27 + off) * 9 + c * 3 + dd];
+          s.stencil.c[off * 9 + c * 3 + dd] = v;
+          if (c != dd && (o[c] == 0 || o[dd] == 0) && v != 0.0)
+            return fail(OSAM_EINVAL, "internal: interior stencil zero pattern violated");
+        }
+    }
+    int rc = upload(&s.coef, tab, s.stream);
+    if (rc != OSAM_OK) return rc;
+    for (int b = 0; b < 2; ++b)
+      for (int q = 0; q < 3; ++q) {
+        rc = dalloc(&s.st[b][q], (size_t)3 * g.npad);
+        if (rc != OSAM_OK) {
+          osam_destroy(h.release());
+          return rc;
+        }
+        CK(cudaMemsetAsync(s.st[b][q], 0, sizeof(double) * 3 * g.npad, s.stream));
+      }
+  } else {
+    if (d->r < 1 || d->r_b < 0 || d->batch < 1) return fail(OSAM_EINVAL, "ROM needs r >= 1, r_b >= 0, batch >= 1");
+    if (!d->Phi || !d->Kbar || (d->r_b > 0 && (!d->Phi_s || !d->Bbar)))
+      return fail(OSAM_EINVAL, "ROM operator pointer is NULL");
+    if (d->n_free < d->r || d->n_s < 0) return fail(OSAM_EINVAL, "ROM: n_free < r or n_s < 0");
+    s.r = d->r;
+    s.r_b = d->r_b;
+    s.batch = d->batch;
+    s.h_Phi.assign(d->Phi, d->Phi + (size_t)d->n_free * d->r);
+    if (d->r_b > 0) {
+      s.h_Phi_s.assign(d->Phi_s, d->Phi_s + (size_t)d->n_s * d->r_b);
+      s.h_Bbar.assign(d->Bbar, d->Bbar + (size_t)d->r * d->r_b);
+    }
+    s.h_Kbar.assign(d->Kbar, d->Kbar + (size_t)d->r * d->r);
+    s.h_e.assign((size_t)d->batch, 1.0);
+    if (d->e_scale)
+      for (int b = 0; b < d->batch; ++b) s.h_e[b] = d->e_scale[b];
+    if (d->r_b == 0) s.h_Phi_s.clear();
+  }
+  CK(cudaStreamSynchronize(s.stream));
+  *out = h.release();
+  return OSAM_OK;
+}
+
+int osam_set_ic(osam_subdomain* h, const double* u0, const double* v0) {
+  if (!h || !u0) return fail(OSAM_EINVAL, "NULL handle or u0");
+  Sub& s = h->s;
+  cudaStream_t st = s.stream;
+  const size_t nf = (size_t)s.batch * 3 * s.n_nodes;
+  double *du = nullptr, *dv = nullptr;
+  TRY(dalloc(&du, nf));
+  TRY(dalloc(&dv, nf));
+  if (is_device_ptr(u0))
+    CK(cudaMemcpyAsync(du, u0, nf * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  else
+    CK(cudaMemcpyAsync(du, u0, nf * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (v0 == nullptr)
+    CK(cudaMemsetAsync(dv, 0, nf * sizeof(double), st));
+  else if (is_device_ptr(v0))
+    CK(cudaMemcpyAsync(dv, v0, nf * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  else
+    CK(cudaMemcpyAsync(dv, v0, nf * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (s.kind == OSAM_FOM) {
+    const int c = s.cur;
+    launch_fom_pack(s.g, du, s.st[c][0], s.n_nodes, st);
+    launch_fom_pack(s.g, dv, s.st[c][1], s.n_nodes, st);
+    CK(cudaMemsetAsync(s.st[c][2], 0, sizeof(double) * 3 * s.g.npad, st));
+    CK(cudaStreamSynchronize(st));
+    dfree(du);
+    dfree(dv);
+    g_launches += 2;
+  } else {
+    dfree(s.ic_u);
+    dfree(s.ic_v);
+    s.ic_u = du;
+    s.ic_v = dv;
+  }
+  s.ic_pending = true;
+  if (s.bound) {
+    int launches = 0;
+    TRY(process_ic(s, &launches));
+    g_launches += launches;
+  }
+  return OSAM_OK;
+}
+
+int osam_step(osam_subdomain* const* sds, int32_t n_sd, const osam_schwarz_cfg* cfg, int32_t n_steps,
+              int32_t* iters_out) {
+  if (!sds || n_sd < 1 || !cfg || n_steps < 0) return fail(OSAM_EINVAL, "bad osam_step arguments");
+  if (!(cfg->dt > 0) || cfg->max_iters < 1 || cfg->min_iters < 2 || !(cfg->tol_rel >= 0))
+    return fail(OSAM_EINVAL, "bad Schwarz configuration (dt > 0, max_iters >= 1, min_iters >= 2)");
+  int B = 1;
+  for (int i = 0; i < n_sd; ++i) {
+    if (!sds[i]) return fail(OSAM_EINVAL, "NULL handle %d", i);
+    for (int j = 0; j < i; ++j)
+      if (sds[j] == sds[i]) return fail(OSAM_EINVAL, "handle listed twice");
+    if (sds[i]->s.stream != sds[0]->s.stream) return fail(OSAM_EINVAL, "all subdomains must share one stream");
+    B = std::max(B, sds[i]->s.batch);
+  }
+  for (int i = 0; i < n_sd; ++i) {
+    if (sds[i]->s.batch != B && !(B > 1 && sds[i]->s.batch == B))
+      return fail(OSAM_EINVAL, "all subdomains of a batched step must have batch %d (FOMs have batch 1)", B);
+  }
+  Group* G = nullptr;
+  TRY(get_group(sds, n_sd, &G));
+  for (int i = 0; i < n_sd; ++i)
+    if (sds[i]->s.ic_pending) {
+      int launches = 0;
+      TRY(process_ic(sds[i]->s, &launches));
+      g_launches += launches;
+    }
+  int status = OSAM_OK;
+  std::vector<int32_t> it(B);
+  for (int k = 0; k < n_steps; ++k) {
+    const int rc = controller_step(*G, *cfg, it.data());
+    if (rc < 0) return rc;
+    if (rc == OSAM_WNOTCONVERGED) status = OSAM_WNOTCONVERGED;
+    if (iters_out)
+      for (int b = 0; b < B; ++b) iters_out[(size_t)k * B + b] = it[b];
+  }
+  CK(cudaStreamSynchronize(sds[0]->s.stream));
+  return status;
+}
+
+static int copy_out(const double* src, double* dst, size_t n, cudaStream_t st) {
+  if (is_device_ptr(dst))
+    CK(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  else
+    CK(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  return OSAM_OK;
+}
+
+static int get_field(const osam_subdomain* h, int which, double* out) {
+  const Sub& s = h->s;
+  if (s.ic_pending) return fail(OSAM_EINVAL, "initial condition not processed yet: call osam_step first");
+  cudaStream_t st = s.stream;
+  if (s.kind == OSAM_FOM) {
+    double* tmp = nullptr;
+    TRY(dalloc(&tmp, (size_t)3 * s.n_nodes));
+    launch_fom_unpack(s.g, s.st[s.cur][which], tmp, s.n_nodes, st);
+    ++g_launches;
+    const int rc = copy_out(tmp, out, (size_t)3 * s.n_nodes, st);
+    CK(cudaStreamSynchronize(st));
+    dfree(tmp);
+    return rc;
+  }
+  if (!s.bound) return fail(OSAM_EINVAL, "ROM state not initialised: call osam_step first");
+  TRY(copy_out(s.rst[s.cur][which], out, (size_t)s.r * s.batch, st));
+  CK(cudaStreamSynchronize(st));
+  return OSAM_OK;
+}
+
+int osam_get_state(const osam_subdomain* h, double* u_out, double* v_out) {
+  if (!h) return fail(OSAM_EINVAL, "NULL handle");
+  if (u_out) TRY(get_field(h, 0, u_out));
+  if (v_out) TRY(get_field(h, 1, v_out));
+  return OSAM_OK;
+}
+
+int osam_get_accel(const osam_subdomain* h, double* a_out) {
+  if (!h || !a_out) return fail(OSAM_EINVAL, "NULL argument");
+  return get_field(h, 2, a_out);
+}
+
+int osam_get_sizes(const osam_subdomain* h, int64_t* n_nodes, int64_t* n_free, int64_t* n_schwarz, int32_t* batch) {
+  if (!h) return fail(OSAM_EINVAL, "NULL handle");
+  if (n_nodes) *n_nodes = h->s.n_nodes;
+  if (n_free) *n_free = h->s.bound ? h->s.n_free : -1;
+  if (n_schwarz) *n_schwarz = h->s.bound ? h->s.n_sdof : -1;
+  if (batch) *batch = h->s.batch;
+  return OSAM_OK;
+}
+
+void osam_destroy(osam_subdomain* h) {
+  if (!h) return;
+  forget_groups_with(h);
+  Sub& s = h->s;
+  if (s.stream) cudaStreamSynchronize(s.stream);
+  release_binding(s);
+  for (int b = 0; b < 2; ++b)
+    for (int q = 0; q < 3; ++q) dfree(s.st[b][q]);
+  dfree(s.coef);
+  dfree(s.ic_u);
+  dfree(s.ic_v);
+  delete h;
+}
+
+void osam_set_profiling(int32_t on) { g_prof = on != 0; }
+
+void osam_reset_profile(void) {
+  g_k1_ms = 0.0;
+  g_k1_launches = 0;
+  g_k1_bytes = 0.0;
+  g_launches = 0;
+}
+
+void osam_get_profile(double* k1_ms, int64_t* k1_launches, double* k1_bytes, int64_t* kernel_launches) {
+  if (k1_ms) *k1_ms = g_k1_ms;
+  if (k1_launches) *k1_launches = g_k1_launches;
+  if (k1_bytes) *k1_bytes = g_k1_bytes;
+  if (kernel_launches) *kernel_launches = g_launches;
+}
+
+}  // extern "C"

@@ -1,0 +1,163 @@
+// Internal types shared by the libosam.so translation units (host runtime + kernels).
+// See include/osam.h for the public contract and DESIGN.md for the data layout.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/osam.h"
+
+namespace osam {
+
+enum DofCode { DOF_FREE = 0, DOF_DIRICHLET = 1, DOF_SCHWARZ = 2 };
+
+// Structured box geometry in the padded SoA layout used on the device:
+//   field[c * npad + i + px * (j + nn[1] * k)],  px = nn[0] rounded up to a multiple of 4.
+struct Geom {
+  int nn[3];
+  int px;
+  long long plane;  // px * nn[1]
+  long long npad;   // component stride (multiple of 32 doubles)
+  double h[3];
+};
+
+// Per-subdomain boundary description passed to kernels by value.
+struct Faces {
+  unsigned char dir[6];  // Dirichlet component bitmask per face
+  unsigned char sw[6];   // 1 if the face is a Schwarz face
+  int nface[6];          // nodes on the face
+  double* s[6];          // Schwarz values of the face, SoA [3][nface], in-face id a + nn[o0]*b
+};
+
+// 27 boundary classes x 27 neighbour offsets x 3x3 blocks of the merged hex8 stencil.
+// class = cx + 3 (cy + 3 cz), c_d = 0 low face, 1 interior, 2 high face (per axis);
+// offset = (ox+1) + 3((oy+1) + 3(oz+1)).
+constexpr int NCLASS = 27;
+constexpr int STENCIL_BLOCK = 27 * 9;
+struct InteriorStencil {
+  double c[STENCIL_BLOCK];  // class 13 (interior), [offset][c][d]
+};
+
+// Transfer map of one Schwarz face (destination) from one source.
+struct XferMap {
+  int src = -1;          // index of the source subdomain in the step group
+  int face = -1;         // destination face
+  int n = 0;             // destination nodes
+  int* idx = nullptr;    // [n][8] source field indices (FOM: padded node id; ROM: compact lift id)
+  double* xi = nullptr;  // [n][3] local coordinates in [0,1]
+  int* out = nullptr;    // [n][3] destination index (FOM: c*nface+f; ROM: Schwarz DOF id; -1 skip)
+};
+
+struct Sub {
+  // descriptor
+  int kind = OSAM_FOM;
+  double lo[3], hi[3];
+  int nel[3];
+  double E, nu, rho, lam, mu;
+  unsigned char dirichlet[6];
+  int batch = 1;
+  int r = 0, r_b = 0;
+  cudaStream_t stream = nullptr;
+  Geom g;
+  long long n_nodes = 0;
+
+  // binding (first osam_step): Schwarz faces and DOF sets
+  bool bound = false;
+  std::vector<osam_subdomain*> group;
+  int face_src[6] = {-1, -1, -1, -1, -1, -1};
+  long long n_free = 0, n_sdof = 0;
+  std::vector<int8_t> codes;  // host DOF codes (canonical DOF id 3p + c)
+  std::vector<XferMap> maps;  // one per Schwarz face of this (destination) subdomain
+
+  // FOM device state: buffers [2] x {u, v, a}, each 3 * npad doubles
+  int cur = 0;
+  double* st[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  Faces faces;
+  double* coef = nullptr;  // device [NCLASS][27][9]
+  InteriorStencil stencil;
+  double mass_e = 0.0;  // rho * V_e / 8
+
+  // ROM device data
+  double *Phi = nullptr, *Phi_s = nullptr, *Kbar = nullptr, *Bbar = nullptr, *e = nullptr;
+  std::vector<double> h_Phi, h_Phi_s, h_Kbar, h_Bbar, h_e;  // host copies (create)
+  double* rst[2][4] = {{nullptr}};  // [buf] uh, vh, ah, s   (r x B, r x B, r x B, n_sdof x B)
+  double* ustar = nullptr;          // r x B scratch
+  double* gh = nullptr;             // r_b x B scratch
+  int* free_ids = nullptr;          // n_free canonical DOF ids (device)
+  int* sdof_ids = nullptr;          // n_sdof canonical DOF ids (device)
+  // ROM as a transfer source: compact donor nodes and their lifted field [2][B][3][n_lift]
+  std::vector<long long> lift_nodes;  // host, sorted node ids
+  long long n_lift = 0;
+  double* Phi_lift = nullptr;  // [3 n_lift][r] row-major
+  int* lift_code = nullptr;    // [3 n_lift]: >= 0 Phi_lift row, -1 Dirichlet, -2-q Schwarz DOF q
+  double* lift[2] = {nullptr, nullptr};
+
+  // pending IC (raw full fields, batch x 3 n)
+  bool ic_pending = false;
+  double* ic_u = nullptr;
+  double* ic_v = nullptr;
+};
+
+// ---- kernel launchers (defined in the .cu files) ---------------------------------------
+struct FomLaunch {
+  Geom g;
+  Faces f;
+  const double *u0, *v0, *a0;  // checkpoint
+  double *u1, *v1, *a1;        // working iterate (also previous iterate for the norm)
+  double dt;
+  double mass_e;
+  const double* coef;  // [NCLASS][27][9]
+  int with_norm;       // 1 from Schwarz iteration 2 on
+  double2* partial;    // per-block (num, den)
+};
+// Returns the number of partial slots written (interior blocks + surface blocks).
+int fom_partial_slots(const Geom& g);
+void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, cudaStream_t s, int* launches);
+
+void launch_transfer(const XferMap& m, const double* src, long long src_cstride, long long src_bstride,
+                     double* dst, long long dst_bstride, int batch, const int* active, cudaStream_t s);
+void launch_fom_face_gather(const Geom& g, const Faces& f, const double* u, cudaStream_t s);
+void launch_fom_pack(const Geom& g, const double* src_unpadded, double* dst_padded, long long n_nodes,
+                     cudaStream_t s);
+void launch_fom_unpack(const Geom& g, const double* src_padded, double* dst_unpadded, long long n_nodes,
+                       cudaStream_t s);
+void launch_fom_zero_constrained(const Geom& g, const Faces& f, double* u, double* v, double* a,
+                                 int zero_u_dirichlet, cudaStream_t s);
+
+struct RomLaunch {
+  int r, r_b, B;
+  long long n_sdof;
+  const double *Phi_s, *Kbar, *Bbar, *e;
+  const double *uh0, *vh0, *ah0;  // checkpoint
+  double *uh1, *vh1, *ah1;        // working
+  const double* s;                // working Schwarz values (n_sdof x B)
+  double *ustar, *gh;
+  const int* active;
+  double dt;
+  int with_norm;
+  double2* partial;
+};
+int rom_partial_slots(int r);
+void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches);
+void launch_rom_lift(int r, int B, long long n_lift, const double* Phi_lift, const int* code, const double* uh,
+                     const double* s, long long n_sdof, double* out, cudaStream_t st);
+void launch_rom_project(long long n_rows, int r, int B, const double* Phi, const int* ids, const double* field,
+                        long long field_bstride, long long n_nodes, double* out, cudaStream_t s);
+void launch_gather_dofs(long long n, int B, const int* ids, const double* field, long long field_bstride,
+                        long long n_nodes, double* out, cudaStream_t s);
+void launch_rom_accel(const RomLaunch& L, const double* uh, double* ah, cudaStream_t s, int* launches);
+
+struct Ctl {
+  int* active;       // [B]
+  int* iters;        // [B] of the current step
+  double* numden;    // [B][2] last check
+  int* flags;        // [0] any active, [1] unstable
+};
+void launch_step_begin(Ctl c, int B, cudaStream_t s);
+void launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int n, int min_iters, double tol_rel,
+                     double tol_abs, cudaStream_t s);
+
+}  // namespace osam

@@ -1,0 +1,194 @@
+"""Thin Python binding of libosam.so (include/osam.h): argument marshalling only.
+
+Every step of the O-SAM time loop runs in the CUDA kernels of libosam.so; this module
+only builds the C structs, passes pointers (torch CUDA tensors -> device pointers,
+NumPy arrays -> host pointers) and converts error codes to exceptions.  There is no CPU
+fallback: if the shared library is missing or no GPU is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libosam.so")
+
+OSAM_FOM, OSAM_ROM = 0, 1
+OSAM_OK, OSAM_WNOTCONVERGED = 0, 1
+ERRORS = {-1: "OSAM_EINVAL", -2: "OSAM_ENOMEM", -3: "OSAM_ECUDA", -4: "OSAM_EOVERLAP", -5: "OSAM_EUNSTABLE"}
+
+# C entry points declared in include/osam.h
+EXPORTS = ("osam_create_subdomain", "osam_set_ic", "osam_step", "osam_get_state", "osam_get_accel",
+           "osam_get_sizes", "osam_destroy", "osam_last_error", "osam_set_profiling", "osam_reset_profile",
+           "osam_get_profile")
+
+
+class osam_subdomain_desc(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("lo", C.c_double * 3), ("hi", C.c_double * 3), ("nel", C.c_int32 * 3),
+                ("E", C.c_double), ("nu", C.c_double), ("rho", C.c_double), ("dirichlet", C.c_uint8 * 6),
+                ("r", C.c_int32), ("r_b", C.c_int32), ("batch", C.c_int32),
+                ("n_free", C.c_int64), ("n_s", C.c_int64),
+                ("Phi", C.POINTER(C.c_double)), ("Phi_s", C.POINTER(C.c_double)),
+                ("Kbar", C.POINTER(C.c_double)), ("Bbar", C.POINTER(C.c_double)),
+                ("e_scale", C.POINTER(C.c_double))]
+
+
+class osam_schwarz_cfg(C.Structure):
+    _fields_ = [("dt", C.c_double), ("tol_rel", C.c_double), ("tol_abs", C.c_double),
+                ("max_iters", C.c_int32), ("min_iters", C.c_int32)]
+
+
+class OsamError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib():
+    """Load libosam.so (built in-tree by __graft_entry__.build()); raise if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise OSError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        vp = C.c_void_p
+        L.osam_create_subdomain.argtypes = [C.POINTER(osam_subdomain_desc), vp, C.POINTER(vp)]
+        L.osam_set_ic.argtypes = [vp, vp, vp]
+        L.osam_step.argtypes = [C.POINTER(vp), C.c_int32, C.POINTER(osam_schwarz_cfg), C.c_int32,
+                                C.POINTER(C.c_int32)]
+        L.osam_get_state.argtypes = [vp, vp, vp]
+        L.osam_get_accel.argtypes = [vp, vp]
+        L.osam_get_sizes.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                     C.POINTER(C.c_int32)]
+        L.osam_destroy.argtypes = [vp]
+        L.osam_destroy.restype = None
+        L.osam_last_error.restype = C.c_char_p
+        L.osam_set_profiling.argtypes = [C.c_int32]
+        L.osam_set_profiling.restype = None
+        L.osam_reset_profile.restype = None
+        L.osam_get_profile.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_int64)]
+        L.osam_get_profile.restype = None
+        for name in ("osam_create_subdomain", "osam_set_ic", "osam_step", "osam_get_state", "osam_get_accel",
+                     "osam_get_sizes"):
+            getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc < 0:
+        raise OsamError(rc, lib().osam_last_error().decode())
+    return rc
+
+
+def _ptr(x):
+    """Device pointer of a torch CUDA tensor, host pointer of a C-contiguous float64 ndarray."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return C.c_void_p(x.data_ptr())
+    if not (isinstance(x, np.ndarray) and x.dtype == np.float64 and x.flags.c_contiguous):
+        raise ValueError("expected a contiguous float64 ndarray or torch tensor")
+    return C.c_void_p(x.ctypes.data)
+
+
+def _dptr(a):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class Subdomain:
+    """Owning wrapper of an osam_subdomain handle (osam_create_subdomain / osam_destroy)."""
+
+    def __init__(self, kind, lo, hi, nel, E, nu, rho, dirichlet=(0,) * 6, stream=None, rom=None, e_scale=None):
+        d = osam_subdomain_desc()
+        d.kind = kind
+        d.lo[:] = [float(x) for x in lo]
+        d.hi[:] = [float(x) for x in hi]
+        d.nel[:] = [int(x) for x in nel]
+        d.E, d.nu, d.rho = float(E), float(nu), float(rho)
+        d.dirichlet[:] = [int(x) for x in dirichlet]
+        self._keep = []
+        d.batch = 1
+        if kind == OSAM_ROM:
+            Phi = np.asfortranarray(rom["Phi"], dtype=np.float64)
+            Phi_s = np.asfortranarray(rom["Phi_s"], dtype=np.float64)
+            Kbar = np.asfortranarray(rom["Kbar"], dtype=np.float64)
+            Bbar = np.asfortranarray(rom["Bbar"], dtype=np.float64)
+            d.r, d.r_b = Phi.shape[1], Phi_s.shape[1]
+            d.n_free, d.n_s = Phi.shape[0], Phi_s.shape[0]
+            d.Phi, d.Phi_s, d.Kbar, d.Bbar = _dptr(Phi), _dptr(Phi_s), _dptr(Kbar), _dptr(Bbar)
+            self._keep += [Phi, Phi_s, Kbar, Bbar]
+            if e_scale is not None:
+                e = np.ascontiguousarray(e_scale, dtype=np.float64)
+                d.batch = len(e)
+                d.e_scale = _dptr(e)
+                self._keep.append(e)
+            self.r = d.r
+        self.kind = kind
+        self.batch = d.batch
+        self.nn = tuple(int(n) + 1 for n in nel)
+        self.n_nodes = self.nn[0] * self.nn[1] * self.nn[2]
+        h = C.c_void_p()
+        _check(lib().osam_create_subdomain(C.byref(d), C.c_void_p(stream or 0), C.byref(h)))
+        self.handle = h
+        self._keep = []  # the library copied the host arrays
+
+    def set_ic(self, u0, v0=None):
+        _check(lib().osam_set_ic(self.handle, _ptr(u0), _ptr(v0)))
+
+    def get_state(self, u_out=None, v_out=None):
+        _check(lib().osam_get_state(self.handle, _ptr(u_out), _ptr(v_out)))
+
+    def get_accel(self, a_out):
+        _check(lib().osam_get_accel(self.handle, _ptr(a_out)))
+
+    def sizes(self):
+        n, f, s = C.c_int64(), C.c_int64(), C.c_int64()
+        b = C.c_int32()
+        _check(lib().osam_get_sizes(self.handle, C.byref(n), C.byref(f), C.byref(s), C.byref(b)))
+        return n.value, f.value, s.value, b.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().osam_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def osam_step(subdomains, dt, tol_rel, n_steps, max_iters=50, min_iters=2, tol_abs=0.0, iters_out=None):
+    """osam_step over `subdomains` (sweep order); returns (status, iters [n_steps, batch])."""
+    cfg = osam_schwarz_cfg(float(dt), float(tol_rel), float(tol_abs), int(max_iters), int(min_iters))
+    arr = (C.c_void_p * len(subdomains))(*[s.handle for s in subdomains])
+    B = max(s.batch for s in subdomains)
+    if iters_out is None:
+        iters_out = np.zeros((max(n_steps, 1), B), dtype=np.int32)
+    ip = iters_out.ctypes.data_as(C.POINTER(C.c_int32)) if n_steps > 0 else None
+    rc = _check(lib().osam_step(arr, len(subdomains), C.byref(cfg), int(n_steps), ip))
+    return rc, iters_out[:n_steps]
+
+
+def set_profiling(on):
+    lib().osam_set_profiling(1 if on else 0)
+
+
+def reset_profile():
+    lib().osam_reset_profile()
+
+
+def get_profile():
+    ms, n, b, k = C.c_double(), C.c_int64(), C.c_double(), C.c_int64()
+    lib().osam_get_profile(C.byref(ms), C.byref(n), C.byref(b), C.byref(k))
+    return dict(k1_ms=ms.value, k1_launches=n.value, k1_bytes=b.value, kernel_launches=k.value)

@@ -1,0 +1,52 @@
+"""CPU checks of the C-ABI boundary: libosam.so loads and exports every symbol include/osam.h declares."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "osam.h")
+LIB = os.path.join(ROOT, "paper_2511_20687_b200", "libosam.so")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(osam_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_five_calls():
+    names = declared_functions()
+    for required in ("osam_create_subdomain", "osam_set_ic", "osam_step", "osam_get_state", "osam_destroy"):
+        assert required in names
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="libosam.so not built (run __graft_entry__.build())")
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(LIB)
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    from paper_2511_20687_b200 import osam
+    assert set(osam.EXPORTS) >= set(declared_functions())
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="libosam.so not built")
+def test_no_gpu_fails_loudly_not_silently():
+    """Without a GPU the library must refuse (OSAM_ECUDA), never fall back to a CPU path."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2511_20687_b200 import osam
+    with pytest.raises(osam.OsamError) as e:
+        osam.Subdomain(osam.OSAM_FOM, (0, 0, 0), (1, 1, 1), (2, 2, 2), 1e9, 0.25, 1000.0)
+    assert e.value.code == -3
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2511_20687_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".h", ".cpp")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in text and "from oracle" not in text, f

@@ -1,0 +1,187 @@
+"""GPU parity: libosam.so (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE north_star): relative L2 <= 1e-10 per subdomain and field after
+the last step, and identical per-step Schwarz iteration counts.
+"""
+import numpy as np
+import pytest
+
+import osam_inputs as I
+from oracle import fem, opinf, schwarz
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2511_20687_b200 import osam, problem
+    osam.lib()
+    return problem
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def oracle_run(cfg, n_steps, rom_ops=None, e=None, every=None):
+    models = schwarz.build_models(cfg, rom_ops=rom_ops, e_scale=e)
+    u0s = [I.initial_displacements(cfg, s) for s in cfg["subdomains"]]
+    snaps = {}
+
+    def cb(k, st):
+        if every and (k + 1) in every:
+            snaps[k + 1] = [dict((kk, vv.copy()) for kk, vv in s.items()) for s in st]
+    states, iters = schwarz.run(models, u0s, cfg["dt"], n_steps, cfg["tol"], cfg["max_iters"], cfg["min_iters"],
+                                callback=cb)
+    return models, states, iters, snaps
+
+
+def compare(problem, subs, models, states, tol=TOL):
+    worst = 0.0
+    for sub, m, st in zip(subs, models, states):
+        if m.kind == "fom":
+            u, v, a = problem.fom_state(sub, accel=True)
+            for got, ref in ((u, st["u"][0]), (v, st["v"][0]), (a, st["a"][0])):
+                e = rel(got, ref)
+                worst = max(worst, e)
+                assert e <= tol, (m.spec["name"], e)
+        else:
+            uh, vh, ah = problem.rom_state(sub, accel=True)
+            for got, ref in ((uh, st["uh"]), (vh, st["vh"]), (ah, st["ah"])):
+                for b in range(ref.shape[0]):
+                    e = rel(got[b], ref[b])
+                    worst = max(worst, e)
+                    assert e <= tol, (m.spec["name"], b, e)
+    return worst
+
+
+def run_both(problem, cfg, n_steps, rom_ops=None, checkpoints=()):
+    e = problem.e_scale(cfg)
+    subs = problem.build(cfg, rom_ops)
+    problem.set_ics(cfg, subs, device="cuda:0")
+    models, states, it_ref, snaps = oracle_run(cfg, n_steps, rom_ops, e, every=set(checkpoints))
+    done = 0
+    iters = []
+    for cp in sorted(set(checkpoints) | {n_steps}):
+        _, it = problem.run(cfg, subs, n_steps=cp - done)
+        iters.append(it)
+        done = cp
+        if cp in snaps:
+            compare(problem, subs, models, snaps[cp])
+    iters = np.concatenate(iters)
+    assert np.array_equal(iters, it_ref.reshape(iters.shape)), "Schwarz iteration counts differ"
+    worst = compare(problem, subs, models, states)
+    return subs, iters, worst
+
+
+def test_c1_full_horizon(gpu):
+    cfg = I.config("c1")
+    _, iters, worst = run_both(gpu, cfg, cfg["n_steps"], checkpoints=(1, 10, 100))
+    assert (iters == 3).all()
+    print("c1 worst rel L2", worst)
+
+
+@pytest.fixture(scope="module")
+def c2_ops():
+    return opinf.train(I.config("c2"), I)
+
+
+def test_c2_fom_rom_full_horizon(gpu, c2_ops):
+    cfg = I.config("c2")
+    _, iters, worst = run_both(gpu, cfg, cfg["n_steps"], rom_ops=c2_ops, checkpoints=(1, 100))
+    assert (iters == 3).all()
+    print("c2 worst rel L2", worst)
+
+
+def test_c5_batched_rom_rom(gpu):
+    cfg = I.config("c5")
+    ops = opinf.train(cfg, I)
+    _, iters, worst = run_both(gpu, cfg, cfg["n_steps"], rom_ops=ops, checkpoints=(1, 200))
+    assert iters.shape == (cfg["n_steps"], 64) and (iters == 3).all()
+    print("c5 worst rel L2", worst)
+
+
+@pytest.mark.parametrize("factor,steps", [(8.0, 25), (5.3, 12)])
+def test_scaled_c3_several_tiles_ragged(gpu, factor, steps):
+    """Non-matching meshes spanning several 32x8x16 interior tiles with ragged tails."""
+    cfg = I.scaled(I.config("c3"), factor)
+    _, iters, worst = run_both(gpu, cfg, steps, checkpoints=(1,))
+    assert (iters == 3).all()
+
+
+def test_scaled_c4_fom_between_two_roms(gpu):
+    """Three subdomains: ROM | FOM | ROM, the FOM with two Schwarz faces (c4 topology)."""
+    cfg = I.scaled(I.config("c4"), 10.0)
+    cfg["rom"] = dict(cfg["rom"], r=40)
+    cfg["rom"]["training"] = dict(cfg["rom"]["training"], n_steps=120,
+                                  subdomains=[dict(s, kind="fom", nel=(8, 8, 8)) for s in cfg["subdomains"]])
+    for s in cfg["subdomains"]:
+        if s["kind"] == "rom":
+            s["nel"] = (8, 8, 8)
+    ops = opinf.train(cfg, I)
+    run_both(gpu, cfg, 40, rom_ops=ops, checkpoints=(1,))
+
+
+@pytest.mark.parametrize("nel", [(1, 1, 1), (3, 2, 5), (40, 9, 3)])
+def test_single_fom_degenerate_and_ragged(gpu, nel):
+    sub = I._sub("one", "fom", (0, 0, 0), (0.3, 0.2, 0.1), nel, (I.CLAMP, 0, 2, 0, 0, 4))
+    cfg = dict(I.config("c1"), subdomains=[sub])
+    cfg["ic"] = dict(kind="gauss3d", A=1e-3, sigma=0.05, center=(0.1, 0.1, 0.05), direction=(0.6, 0.0, 0.8))
+    cfg["dt"] = 0.5 * min(0.3 / nel[0], 0.2 / nel[1], 0.1 / nel[2]) / fem.p_wave_speed(1e9, 0.25, 1000.0)
+    _, iters, _ = run_both(gpu, cfg, 15)
+    assert (iters == 2).all()      # no Schwarz data: iterate 2 reproduces iterate 1
+
+
+def test_zero_steps_and_restart(gpu):
+    cfg = I.config("c1")
+    subs = gpu.build(cfg)
+    gpu.set_ics(cfg, subs)                      # host pointers
+    st, it = gpu.run(cfg, subs, n_steps=0)
+    assert it.shape[0] == 0
+    u_a, _ = gpu.fom_state(subs[0])
+    gpu.run(cfg, subs, n_steps=5)
+    gpu.set_ics(cfg, subs, device="cuda:0")     # restart from the IC via device pointers
+    u_b, _ = gpu.fom_state(subs[0])
+    assert np.array_equal(u_a, u_b)
+
+
+def test_bitwise_repeatable(gpu):
+    cfg = I.scaled(I.config("c3"), 8.0)
+    outs = []
+    for _ in range(2):
+        subs = gpu.build(cfg)
+        gpu.set_ics(cfg, subs, device="cuda:0")
+        gpu.run(cfg, subs, n_steps=6)
+        outs.append([gpu.fom_state(s) for s in subs])
+    for a, b in zip(*outs):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_invalid_arguments(gpu, c2_ops):
+    from paper_2511_20687_b200 import osam
+    with pytest.raises(osam.OsamError) as e:
+        osam.Subdomain(osam.OSAM_FOM, (0, 0, 0), (1, 1, 1), (0, 2, 2), 1e9, 0.25, 1000.0)
+    assert e.value.code == -1
+    with pytest.raises(osam.OsamError):
+        osam.Subdomain(osam.OSAM_FOM, (0, 0, 0), (-1, 1, 1), (2, 2, 2), 1e9, 0.25, 1000.0)
+    cfg = I.config("c2")
+    bad = dict(c2_ops[1])
+    bad["Phi"] = bad["Phi"][:-3]
+    subs = gpu.build(cfg, {1: bad})
+    gpu.set_ics(cfg, subs)
+    with pytest.raises(osam.OsamError) as e:
+        gpu.run(cfg, subs, n_steps=1)
+    assert e.value.code == -1
+    cfg1 = I.config("c1")
+    subs = gpu.build(cfg1)
+    gpu.set_ics(cfg1, subs)
+    with pytest.raises(osam.OsamError):
+        osam.osam_step(subs, -1.0, 1e-10, 1)
+    with pytest.raises(osam.OsamError):
+        osam.osam_step(subs, cfg1["dt"], 1e-10, 1, min_iters=1)
