@@ -458,7 +458,7 @@ int process_ic(Sub& s, int* launches) {
     TRY(dalloc(&scratch, (size_t)fom_partial_slots(s.g)));
     L.partial = scratch;
     *launches += 2;
-    launch_fom_advance(L, s.stencil, st, launches);
+    launch_fom_advance(L, s.stencil, s.tmap[c], st, launches);
     CK(cudaStreamSynchronize(st));
     dfree(scratch);
     s.cur = 1 - c;
@@ -591,7 +591,7 @@ int controller_step(Group& G, const osam_schwarz_cfg& cfg, int32_t* iters) {
         L.with_norm = with_norm;
         L.partial = G.partial + (size_t)slot * B;
         if (g_prof) CK(cudaEventRecord(G.ev[2 * fom_k], st));
-        launch_fom_advance(L, d.stencil, st, &launches);
+        launch_fom_advance(L, d.stencil, d.tmap[c], st, &launches);
         if (g_prof) CK(cudaEventRecord(G.ev[2 * fom_k + 1], st));
         g_k1_bytes += (48.0 + (with_norm ? 16.0 : 0.0)) * 3.0 * (double)d.n_nodes;
         ++g_k1_launches;
@@ -743,6 +743,13 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
         }
         CK(cudaMemsetAsync(s.st[b][q], 0, sizeof(double) * 3 * g.npad, s.stream));
       }
+    for (int b = 0; b < 2; ++b) {
+      const int r = make_state_tmaps(g, s.st[b], s.tmap[b]);
+      if (r != 0) {
+        osam_destroy(h.release());
+        return fail(OSAM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", r);
+      }
+    }
   } else {
     if (d->r < 1 || d->r_b < 0 || d->batch < 1) return fail(OSAM_EINVAL, "ROM needs r >= 1, r_b >= 0, batch >= 1");
     if (!d->Phi || !d->Kbar || (d->r_b > 0 && (!d->Phi_s || !d->Bbar)))

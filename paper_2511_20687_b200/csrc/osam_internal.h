@@ -2,6 +2,8 @@
 // See include/osam.h for the public contract and DESIGN.md for the data layout.
 #pragma once
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -78,6 +80,7 @@ struct Sub {
   Faces faces;
   double* coef = nullptr;  // device [NCLASS][27][9]
   InteriorStencil stencil;
+  CUtensorMap tmap[2][3];  // TMA descriptors of st[b][0..2] (4D: x, y, z, component)
   double mass_e = 0.0;  // rho * V_e / 8
 
   // ROM device data
@@ -115,7 +118,9 @@ struct FomLaunch {
 };
 // Returns the number of partial slots written (interior blocks + surface blocks).
 int fom_partial_slots(const Geom& g);
-void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, cudaStream_t s, int* launches);
+void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUtensorMap* tm, cudaStream_t s,
+                        int* launches);
+int make_state_tmaps(const Geom& g, double* const arrays[3], CUtensorMap out[3]);
 
 void launch_transfer(const XferMap& m, const double* src, long long src_cstride, long long src_bstride,
                      double* dst, long long dst_bstride, int batch, const int* active, cudaStream_t s);
