@@ -2,9 +2,12 @@
 # one GPU round: tests, bench, ncu launch list, ncu full capture of the FOM kernels
 set -x
 TAG=${1:-r}
+mkdir -p gpurun_out
 B="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e"
-timeout 1500 python -m pytest tests -m gpu -q -rA --timeout 900 > gpurun_out/pytest_gpu_$TAG.log 2>&1
+nvidia-smi > gpurun_out/smi_$TAG.txt 2>&1
+timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > gpurun_out/smoke_$TAG.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -rA --timeout 900 -x > gpurun_out/pytest_gpu_$TAG.log 2>&1
 timeout 600 python bench.py > gpurun_out/bench_$TAG.log 2>&1
-$B > gpurun_out/plain_$TAG.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $B > gpurun_out/ncu1_$TAG.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:fom_ -s 8 -c 4 -o gpurun_out/prof_$TAG $B > gpurun_out/ncu2_$TAG.log 2>&1
+timeout 300 $B > gpurun_out/plain_$TAG.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $B > gpurun_out/ncu1_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fom_ -s 8 -c 4 -o gpurun_out/prof_$TAG $B > gpurun_out/ncu2_$TAG.log 2>&1
 echo done
