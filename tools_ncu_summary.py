@@ -38,7 +38,12 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio",
-        "smsp__average_warp_latency_per_inst_issued.ratio"]
+        "smsp__average_warp_latency_per_inst_issued.ratio",
+        "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+        "smsp__inst_executed.sum", "smsp__sass_inst_executed_op_shared_ld.sum", "smsp__inst_executed_op_branch.sum",
+        "smsp__sass_inst_executed_op_local_st.sum", "sm__inst_executed.avg.per_cycle_active",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "lts__t_sector_hit_rate.pct", "sm__cycles_elapsed.avg.per_second"]
 
 
 def raw(rep):
