@@ -249,7 +249,9 @@ void launch_step_begin(Ctl c, int B, cudaStream_t s) { step_begin_kernel<<<1, 25
 void launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int n, int min_iters, double tol_rel,
                      double tol_abs, cudaStream_t s) {
   finalize_kernel<<<B, 256, 0, s>>>(c, partial, n_slots, B, n, min_iters, tol_rel, tol_abs);
+  debug_check("finalize_kernel", s);
   any_active_kernel<<<1, 1, 0, s>>>(c, B);
+  debug_check("any_active_kernel", s);
 }
 
 int rom_partial_slots(int r) { return (int)cdiv(r, 256); }
@@ -259,7 +261,9 @@ void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches) {
     rom_project_bnd_kernel<<<cdiv((long long)L.r_b * L.B * 32, 256), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
                                                                                  L.s, L.gh);
   rom_predict_kernel<<<cdiv((long long)L.r * L.B, 256), 256, 0, s>>>(L.r, L.B, L.uh0, L.vh0, L.ah0, L.dt, L.ustar);
+  debug_check("rom_predict_kernel", s);
   rom_update_kernel<<<dim3(cdiv(L.r, 256), L.B), 256, 0, s>>>(L, 0);
+  debug_check("rom_update_kernel", s);
   *launches += (L.r_b > 0) + 2;
 }
 
@@ -271,6 +275,7 @@ void launch_rom_accel(const RomLaunch& L, const double* uh, double* ah, cudaStre
     rom_project_bnd_kernel<<<cdiv((long long)L.r_b * L.B * 32, 256), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
                                                                                  L.s, L.gh);
   rom_update_kernel<<<dim3(cdiv(L.r, 256), L.B), 256, 0, s>>>(A, 1);
+  debug_check("rom_update_kernel", s);
   *launches += (L.r_b > 0) + 1;
 }
 
@@ -278,6 +283,7 @@ void launch_rom_lift(int r, int B, long long nl, const double* Phi_lift, const i
                      const double* sv, long long ns, double* out, cudaStream_t st) {
   if (nl == 0) return;
   rom_lift_kernel<<<cdiv(nl * B * 32, 256), 256, 0, st>>>(r, B, nl, Phi_lift, code, uh, sv, ns, out);
+  debug_check("rom_lift_kernel", st);
 }
 
 void launch_rom_project(long long nrows, int r, int B, const double* Phi, const int* ids, const double* field,
@@ -290,6 +296,7 @@ void launch_gather_dofs(long long n, int B, const int* ids, const double* field,
                         double* out, cudaStream_t s) {
   if (n == 0) return;
   gather_dofs_kernel<<<dim3(cdiv(n, 256), B), 256, 0, s>>>(n, B, ids, field, fbs, n_nodes, out);
+  debug_check("gather_dofs_kernel", s);
 }
 
 }  // namespace osam

@@ -68,6 +68,17 @@ void dfree(T*& p) {
   p = nullptr;
 }
 
+}  // namespace
+
+void debug_check(const char* kernel, cudaStream_t s) {
+  static const bool on = getenv("OSAM_DEBUG_SYNC") != nullptr;
+  if (!on) return;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) fprintf(stderr, "[osam debug] kernel %s failed: %s\n", kernel, cudaGetErrorString(e));
+}
+
+namespace {
 // ---- profiling / launch accounting --------------------------------------------------------
 bool g_prof = false;
 double g_k1_ms = 0.0;
@@ -145,6 +156,7 @@ void release_maps(Sub& s) {
 void release_binding(Sub& s) {
   release_maps(s);
   for (int f = 0; f < 6; ++f) dfree(s.faces.s[f]);
+  dfree(s.scratch_partial);
   dfree(s.Phi);
   dfree(s.Phi_s);
   dfree(s.Kbar);
@@ -276,6 +288,7 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
         s.faces.s[f] = nullptr;
         if (s.faces.sw[f]) TRY(dalloc(&s.faces.s[f], 3 * (size_t)s.faces.nface[f]));
       }
+      TRY(dalloc(&s.scratch_partial, (size_t)fom_partial_slots(s.g, s.faces)));
       continue;
     }
     const long long rows_phi = (long long)(s.h_Phi.size() / std::max(1, s.r));
@@ -438,30 +451,13 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
 int process_ic(Sub& s, int* launches) {
   cudaStream_t st = s.stream;
   if (s.kind == OSAM_FOM) {
+    // Dirichlet DOFs := 0, constrained w := 0; Schwarz DOFs keep u0 and seed the face arrays.
+    // a0 = -f(u0)/m enters w at the first osam_step (fom_set_step), once dt is known.
     const int c = s.cur;
-    launch_fom_zero_constrained(s.g, s.faces, s.st[c][0], s.st[c][1], s.st[c][2], 1, st);
+    launch_fom_zero_constrained(s.g, s.faces, s.st[c][0], s.st[c][1], 1, st);
     launch_fom_face_gather(s.g, s.faces, s.st[c][0], st);
-    FomLaunch L{};
-    L.g = s.g;
-    L.f = s.faces;
-    L.u0 = s.st[c][0];
-    L.v0 = s.st[c][1];
-    L.a0 = s.st[c][2];
-    L.u1 = s.st[1 - c][0];
-    L.v1 = s.st[1 - c][1];
-    L.a1 = s.st[1 - c][2];
-    L.dt = 0.0;
-    L.mass_e = s.mass_e;
-    L.coef = s.coef;
-    L.with_norm = 0;
-    double2* scratch = nullptr;
-    TRY(dalloc(&scratch, (size_t)fom_partial_slots(s.g)));
-    L.partial = scratch;
     *launches += 2;
-    launch_fom_advance(L, s.stencil, s.tmap[c], st, launches);
     CK(cudaStreamSynchronize(st));
-    dfree(scratch);
-    s.cur = 1 - c;
   } else {
     const int c = s.cur;
     const long long fbs = 3 * s.n_nodes;
@@ -506,7 +502,7 @@ int get_group(osam_subdomain* const* sds, int n_sd, Group** out) {
     G->B = 1;
     for (auto s : subs) G->B = std::max(G->B, s->batch);
     G->n_slots = 0;
-    for (auto s : subs) G->n_slots += s->kind == OSAM_FOM ? fom_partial_slots(s->g) : rom_partial_slots(s->r);
+    for (auto s : subs) G->n_slots += s->kind == OSAM_FOM ? fom_partial_slots(s->g, s->faces) : rom_partial_slots(s->r);
     TRY(dalloc(&G->partial, (size_t)std::max(1, G->n_slots) * G->B));
     TRY(dalloc(&G->ctl_i, (size_t)2 + 2 * G->B));
     TRY(dalloc(&G->numden, (size_t)2 * G->B));
@@ -515,6 +511,40 @@ int get_group(osam_subdomain* const* sds, int n_sd, Group** out) {
     it = g_groups.find(key);
   }
   *out = it->second.get();
+  return OSAM_OK;
+}
+
+// K1 launch description reading buffer `from` and writing buffer 1 - from.
+FomLaunch fom_launch(const Sub& d, int from, double dtp, double cw, double cv, double dt, int with_norm,
+                     double2* partial, double* a_out) {
+  FomLaunch L{};
+  L.g = d.g;
+  L.f = d.faces;
+  L.u0 = d.st[from][0];
+  L.w0 = d.st[from][1];
+  L.u1 = d.st[1 - from][0];
+  L.w1 = d.st[1 - from][1];
+  L.a_out = a_out;
+  L.dtp = dtp;
+  L.cw = cw;
+  L.cv = cv;
+  L.dt = dt;
+  for (int q = 0; q < 8; ++q) L.inv_mass[q] = d.inv_mass[q];
+  L.coef = d.coef;
+  L.with_norm = with_norm;
+  L.partial = partial;
+  return L;
+}
+
+// Make the stored w refer to step dt: w <- w + (dt - w_dt)/2 a with a = -K u / m (one force
+// pass, u unchanged; Schwarz DOFs read the face arrays, which hold the stored Schwarz values).
+int fom_set_step(Sub& d, double dt, int* launches) {
+  if (d.w_dt == dt) return OSAM_OK;
+  const int c = d.cur;
+  const FomLaunch L = fom_launch(d, c, 0.0, 0.5 * (dt - d.w_dt), 0.0, dt, 0, d.scratch_partial, nullptr);
+  launch_fom_advance(L, d.stencil, d.tmap[c], d.stream, launches);
+  d.cur = 1 - c;
+  d.w_dt = dt;
   return OSAM_OK;
 }
 
@@ -576,27 +606,15 @@ int controller_step(Group& G, const osam_schwarz_cfg& cfg, int32_t* iters) {
       const int with_norm = n >= 2 ? 1 : 0;
       if (d.kind == OSAM_FOM) {
         const int c = d.cur;
-        FomLaunch L{};
-        L.g = d.g;
-        L.f = d.faces;
-        L.u0 = d.st[c][0];
-        L.v0 = d.st[c][1];
-        L.a0 = d.st[c][2];
-        L.u1 = d.st[1 - c][0];
-        L.v1 = d.st[1 - c][1];
-        L.a1 = d.st[1 - c][2];
-        L.dt = cfg.dt;
-        L.mass_e = d.mass_e;
-        L.coef = d.coef;
-        L.with_norm = with_norm;
-        L.partial = G.partial + (size_t)slot * B;
+        const FomLaunch L = fom_launch(d, c, cfg.dt, cfg.dt, 0.5 * cfg.dt, cfg.dt, with_norm,
+                                       G.partial + (size_t)slot * B, nullptr);
         if (g_prof) CK(cudaEventRecord(G.ev[2 * fom_k], st));
         launch_fom_advance(L, d.stencil, d.tmap[c], st, &launches);
         if (g_prof) CK(cudaEventRecord(G.ev[2 * fom_k + 1], st));
-        g_k1_bytes += (48.0 + (with_norm ? 16.0 : 0.0)) * 3.0 * (double)d.n_nodes;
+        g_k1_bytes += (32.0 + (with_norm ? 8.0 : 0.0)) * 3.0 * (double)d.n_nodes;
         ++g_k1_launches;
         ++fom_k;
-        slot += fom_partial_slots(d.g);
+        slot += fom_partial_slots(d.g, d.faces);
       } else {
         const int c = d.cur;
         RomLaunch L{};
@@ -715,27 +733,50 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
   for (int a = 0; a < 3; ++a) g.h[a] = (d->hi[a] - d->lo[a]) / d->nel[a];
   s.n_nodes = nn0 * nn1 * nn2;
   s.mass_e = d->rho * g.h[0] * g.h[1] * g.h[2] / 8.0;
+  for (int q = 0; q < 8; ++q)
+    s.inv_mass[q] = 1.0 / (s.mass_e * ((q & 1) ? 2.0 : 1.0) * ((q & 2) ? 2.0 : 1.0) * ((q & 4) ? 2.0 : 1.0));
   for (int f = 0; f < 6; ++f) s.faces.s[f] = nullptr;
   if (s.kind == OSAM_FOM) {
     if (d->batch > 1) return fail(OSAM_EINVAL, "a FOM subdomain has batch 1");
     s.batch = 1;
     std::vector<double> tab;
     stencil_table(g.h, s.lam, s.mu, tab);
-    // the interior kernel skips the structural zeros of the interior class: check them
+    // parity-reduced interior stencil (kernels_fom.cu): K_cd(ox, oy, oz) = sx sy k[oz+1][c][d][|ox| + 2|oy|]
+    // with sx = sign(ox) for blocks odd in x (exactly one of c, d is x), sy likewise in y, and the
+    // oz = +1 slice equal to the oz = -1 slice times -1 for blocks odd in z.  Verified exactly.
+    for (int sl = 0; sl < 3; ++sl)
+      for (int c = 0; c < 3; ++c)
+        for (int dd = 0; dd < 3; ++dd)
+          for (int q = 0; q < 4; ++q) {
+            const int off = (1 + (q & 1)) + 3 * ((1 + (q >> 1)) + 3 * sl);
+            s.stencil.k[sl][c][dd][q] = tab[((size_t)13 * 27 + off) * 9 + c * 3 + dd];
+          }
     for (int off = 0; off < 27; ++off) {
       const int o[3] = {off % 3 - 1, (off / 3) % 3 - 1, off / 9 - 1};
       for (int c = 0; c < 3; ++c)
         for (int dd = 0; dd < 3; ++dd) {
-          const double v = tab[((size_t)13 * 27 + off) * 9 + c * 3 + dd];
-          s.stencil.c[off * 9 + c * 3 + dd] = v;
-          if (c != dd && (o[c] == 0 || o[dd] == 0) && v != 0.0)
-            return fail(OSAM_EINVAL, "internal: interior stencil zero pattern violated");
+          const bool xodd = (c == 0) != (dd == 0), yodd = (c == 1) != (dd == 1), zodd = (c == 2) != (dd == 2);
+          const int sl = o[2] == 1 ? 0 : o[2] + 1;
+          double v = s.stencil.k[sl][c][dd][std::abs(o[0]) + 2 * std::abs(o[1])];
+          if (xodd && o[0] == 0) v = 0.0;
+          if (yodd && o[1] == 0) v = 0.0;
+          if (xodd && o[0] < 0) v = -v;
+          if (yodd && o[1] < 0) v = -v;
+          if (zodd && o[2] == 0) v = 0.0;
+          if (zodd && o[2] == 1) v = -v;
+          if (v != tab[((size_t)13 * 27 + off) * 9 + c * 3 + dd])
+            return fail(OSAM_EINVAL, "internal: interior stencil parity structure violated");
         }
     }
     int rc = upload(&s.coef, tab, s.stream);
     if (rc != OSAM_OK) return rc;
+    rc = dalloc(&s.scratch_a, (size_t)3 * g.npad);
+    if (rc != OSAM_OK) {
+      osam_destroy(h.release());
+      return rc;
+    }
     for (int b = 0; b < 2; ++b)
-      for (int q = 0; q < 3; ++q) {
+      for (int q = 0; q < 2; ++q) {
         rc = dalloc(&s.st[b][q], (size_t)3 * g.npad);
         if (rc != OSAM_OK) {
           osam_destroy(h.release());
@@ -795,8 +836,8 @@ int osam_set_ic(osam_subdomain* h, const double* u0, const double* v0) {
   if (s.kind == OSAM_FOM) {
     const int c = s.cur;
     launch_fom_pack(s.g, du, s.st[c][0], s.n_nodes, st);
-    launch_fom_pack(s.g, dv, s.st[c][1], s.n_nodes, st);
-    CK(cudaMemsetAsync(s.st[c][2], 0, sizeof(double) * 3 * s.g.npad, st));
+    launch_fom_pack(s.g, dv, s.st[c][1], s.n_nodes, st);  // w holds v until the first osam_step
+    s.w_dt = 0.0;
     CK(cudaStreamSynchronize(st));
     dfree(du);
     dfree(dv);
@@ -841,6 +882,12 @@ int osam_step(osam_subdomain* const* sds, int32_t n_sd, const osam_schwarz_cfg* 
       TRY(process_ic(sds[i]->s, &launches));
       g_launches += launches;
     }
+  if (n_steps > 0) {
+    int launches = 0;
+    for (int i = 0; i < n_sd; ++i)
+      if (sds[i]->s.kind == OSAM_FOM) TRY(fom_set_step(sds[i]->s, cfg->dt, &launches));
+    g_launches += launches;
+  }
   int status = OSAM_OK;
   std::vector<int32_t> it(B);
   for (int k = 0; k < n_steps; ++k) {
@@ -867,9 +914,20 @@ static int get_field(const osam_subdomain* h, int which, double* out) {
   if (s.ic_pending) return fail(OSAM_EINVAL, "initial condition not processed yet: call osam_step first");
   cudaStream_t st = s.stream;
   if (s.kind == OSAM_FOM) {
+    const double* field = s.st[s.cur][0];
+    if (which != 0) {
+      // a = -K u / m and v = w - w_dt/2 a by one force pass into the spare buffer (the committed
+      // state is not modified).
+      if (!s.bound) return fail(OSAM_EINVAL, "FOM state not bound: call osam_step first");
+      int launches = 0;
+      const FomLaunch L = fom_launch(s, s.cur, 0.0, -0.5 * s.w_dt, 0.0, 0.0, 0, s.scratch_partial, s.scratch_a);
+      launch_fom_advance(L, s.stencil, s.tmap[s.cur], st, &launches);
+      g_launches += launches;
+      field = which == 1 ? s.st[1 - s.cur][1] : s.scratch_a;
+    }
     double* tmp = nullptr;
     TRY(dalloc(&tmp, (size_t)3 * s.n_nodes));
-    launch_fom_unpack(s.g, s.st[s.cur][which], tmp, s.n_nodes, st);
+    launch_fom_unpack(s.g, field, tmp, s.n_nodes, st);
     ++g_launches;
     const int rc = copy_out(tmp, out, (size_t)3 * s.n_nodes, st);
     CK(cudaStreamSynchronize(st));
@@ -910,7 +968,8 @@ void osam_destroy(osam_subdomain* h) {
   if (s.stream) cudaStreamSynchronize(s.stream);
   release_binding(s);
   for (int b = 0; b < 2; ++b)
-    for (int q = 0; q < 3; ++q) dfree(s.st[b][q]);
+    for (int q = 0; q < 2; ++q) dfree(s.st[b][q]);
+  dfree(s.scratch_a);
   dfree(s.coef);
   dfree(s.ic_u);
   dfree(s.ic_v);

@@ -39,8 +39,10 @@ struct Faces {
 // offset = (ox+1) + 3((oy+1) + 3(oz+1)).
 constexpr int NCLASS = 27;
 constexpr int STENCIL_BLOCK = 27 * 9;
+// Interior-class stencil in parity-reduced form: k[slice][c][d] = {K(0,0), K(1,0), K(0,1), K(1,1)}
+// at in-plane offsets (ox, oy), slice = oz + 1 (see kernels_fom.cu "parity-reduced stencil").
 struct InteriorStencil {
-  double c[STENCIL_BLOCK];  // class 13 (interior), [offset][c][d]
+  double k[3][3][3][4];
 };
 
 // Transfer map of one Schwarz face (destination) from one source.
@@ -74,14 +76,18 @@ struct Sub {
   std::vector<int8_t> codes;  // host DOF codes (canonical DOF id 3p + c)
   std::vector<XferMap> maps;  // one per Schwarz face of this (destination) subdomain
 
-  // FOM device state: buffers [2] x {u, v, a}, each 3 * npad doubles
+  // FOM device state: buffers [2] x {u, w}, each 3 * npad doubles; w = v + w_dt/2 a (DESIGN R30)
   int cur = 0;
-  double* st[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  double* st[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  double w_dt = 0.0;  // the step the stored w refers to (0: w holds v)
   Faces faces;
   double* coef = nullptr;  // device [NCLASS][27][9]
   InteriorStencil stencil;
-  CUtensorMap tmap[2][3];  // TMA descriptors of st[b][0..2] (4D: x, y, z, component)
-  double mass_e = 0.0;  // rho * V_e / 8
+  CUtensorMap tmap[2][2];  // TMA descriptors of st[b][0..1] (4D: x, y, z, component)
+  double mass_e = 0.0;     // rho * V_e / 8
+  double inv_mass[8];      // 1 / (mass_e * prod_d (2 if interior on axis d else 1)), index cx + 2 cy + 4 cz (1 = interior)
+  double* scratch_a = nullptr;        // 3 * npad: acceleration for osam_get_accel
+  double2* scratch_partial = nullptr; // partial slots of non-sweep K1 launches
 
   // ROM device data
   double *Phi = nullptr, *Phi_s = nullptr, *Kbar = nullptr, *Bbar = nullptr, *e = nullptr;
@@ -108,19 +114,23 @@ struct Sub {
 struct FomLaunch {
   Geom g;
   Faces f;
-  const double *u0, *v0, *a0;  // checkpoint
-  double *u1, *v1, *a1;        // working iterate (also previous iterate for the norm)
-  double dt;
-  double mass_e;
+  const double *u0, *w0;  // checkpoint (u, w)
+  double *u1, *w1;        // working iterate (w1 is also the previous iterate for the norm)
+  double* a_out;          // optional acceleration output (diagnostics), may be null
+  double dtp;             // predictor: u* = u0 + dtp w0
+  double cw;              // w1 = w0 + cw a
+  double cv;              // v = w0 + cv a (norm denominator)
+  double dt;              // step in the convergence norm
+  double inv_mass[8];
   const double* coef;  // [NCLASS][27][9]
   int with_norm;       // 1 from Schwarz iteration 2 on
   double2* partial;    // per-block (num, den)
 };
-// Returns the number of partial slots written (interior blocks + surface blocks).
-int fom_partial_slots(const Geom& g);
+// Number of partial slots a K1 launch writes (tiled blocks + x-face blocks).
+int fom_partial_slots(const Geom& g, const Faces& f);
 void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUtensorMap* tm, cudaStream_t s,
                         int* launches);
-int make_state_tmaps(const Geom& g, double* const arrays[3], CUtensorMap out[3]);
+int make_state_tmaps(const Geom& g, double* const arrays[2], CUtensorMap out[2]);
 
 void launch_transfer(const XferMap& m, const double* src, long long src_cstride, long long src_bstride,
                      double* dst, long long dst_bstride, int batch, const int* active, cudaStream_t s);
@@ -129,8 +139,8 @@ void launch_fom_pack(const Geom& g, const double* src_unpadded, double* dst_padd
                      cudaStream_t s);
 void launch_fom_unpack(const Geom& g, const double* src_padded, double* dst_unpadded, long long n_nodes,
                        cudaStream_t s);
-void launch_fom_zero_constrained(const Geom& g, const Faces& f, double* u, double* v, double* a,
-                                 int zero_u_dirichlet, cudaStream_t s);
+void launch_fom_zero_constrained(const Geom& g, const Faces& f, double* u, double* w, int zero_u_dirichlet,
+                                 cudaStream_t s);
 
 struct RomLaunch {
   int r, r_b, B;
@@ -154,6 +164,10 @@ void launch_rom_project(long long n_rows, int r, int B, const double* Phi, const
 void launch_gather_dofs(long long n, int B, const int* ids, const double* field, long long field_bstride,
                         long long n_nodes, double* out, cudaStream_t s);
 void launch_rom_accel(const RomLaunch& L, const double* uh, double* ah, cudaStream_t s, int* launches);
+
+// OSAM_DEBUG_SYNC=1: synchronise after every launch and report the first failing kernel on
+// stderr (development aid only; off by default).
+void debug_check(const char* kernel, cudaStream_t s);
 
 struct Ctl {
   int* active;       // [B]

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libosam.so")
+LIB_PATH = os.environ.get("OSAM_LIB") or os.path.join(_HERE, "libosam.so")
 
 OSAM_FOM, OSAM_ROM = 0, 1
 OSAM_OK, OSAM_WNOTCONVERGED = 0, 1
