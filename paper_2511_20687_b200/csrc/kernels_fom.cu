@@ -1,27 +1,34 @@
 // K1: fused FOM advance -- explicit Newmark (beta = 0, gamma = 1/2) step of a hex8
-// linear-elastic box subdomain with lumped mass (A.1 P:L1934-1947),
-// in the two-vector (u, w) form, w = v + dt/2 a (SURVEY 8(d) "leapfrog"; R30):
+// linear-elastic box subdomain with lumped mass (A.1 P:L1934-1947).
 //
-//   u* = u + dtp w            on free DOFs; 0 on Dirichlet DOFs; s on Schwarz DOFs
-//   f  = K u*                 (matrix-free 27-point merged hex8 stencil, 153 nonzeros/node)
-//   a' = -f / m_L ,  w' = w + cw a'  on free DOFs (w' = a' = 0 on constrained DOFs)
-//   partial sums of  num = ||dt (w' - w_prev)/2||^2  and  den = ||u* + dt (w + cv a')||^2
+// State (R30): q = u + dt w (the next step's predictor) and w = v + dt/2 a, with the
+// boundary values stored in q (0 on Dirichlet DOFs, the current Schwarz values s on Schwarz DOFs,
+// written there by the transfer K2).  One launch computes, from the staged field X and the
+// per-node field W:
 //
-// A Schwarz sweep uses dtp = cw = dt, cv = dt/2: then u* is the Newmark predictor
-// u + dt v + dt^2/2 a, v' = w + dt/2 a' = v + dt/2 (a + a') and w' = v' + dt/2 a', and
-// (u* - u*_prev) + dt (v' - v'_prev) = dt (w' - w'_prev)/2 on free DOFs because u* depends only
-// on the checkpoint (eq:conv_criterion P:L443-467).  dtp = 0 with cw = (dt_new - dt_old)/2 changes
-// the step a stored w refers to; cw = -dt/2 recovers v = w - dt/2 a for osam_get_state.
+//   f  = K X                   (matrix-free 27-point merged hex8 stencil, 153 nonzeros/node)
+//   a  = -f / m_L ,  W' = W + cw a ,  Q' = X + cq W'      on free DOFs
+//   W' = a = 0 ,  Q' = X                                   on constrained DOFs
+//   partial sums  num = ||dt (W' - W'_prev)/2||^2 ,  den = ||X + dt (W + cv a)||^2   (free DOFs)
+//
+// A Schwarz sweep (X = q, W = w of the checkpoint; cw = cq = dt, cv = dt/2) is exactly
+//   u* = u + dt v + dt^2/2 a (the Newmark predictor, = q),  a' = -K u*/m,
+//   v' = v + dt/2 (a + a') = w + dt/2 a',  w' = w + dt a',  q' = u* + dt w',
+// and the convergence change (u* - u*_prev) + dt (v' - v'_prev) = dt (w' - w'_prev)/2 on free DOFs
+// because u* depends on the checkpoint only (eq:conv_criterion P:L443-467).  Other coefficient
+// choices convert the state (initial condition: X = u0, W = v0, cw = dt/2; a new dt; v for output).
 //
 // Two kernels make one K1:
 //   * the tiled kernel covers every node.  A block owns a TX x TY tile in (x, y) and a balanced
-//     chunk of node planes in z; one thread streams the checkpoint planes (u, w; tile + one-node
-//     halo) with 4D TMA loads into a 3-deep mbarrier ring.  Each staged plane is converted once to
-//     u* in shared memory; each thread then loads its 3x3 in-plane neighbourhood once (27 shared
-//     loads) and applies it to the forces of node planes m+1, m, m-1 held in registers (2.5D
-//     streaming).  A warp is one x-row, so the (y, z) boundary class is warp-uniform: interior rows
-//     use the 153-coefficient stencil from the kernel-parameter constant bank, face rows their class
-//     table.  Lanes on an x-face write it only when the face is fully constrained (no force needed).
+//     chunk of node planes in z.  One thread streams X planes (tile + halo) with 4D TMA loads into
+//     a 4-deep ring guarded by full/empty mbarriers (no block-wide barrier in the loop: warps only
+//     wait for data, the producer waits for the slowest warp to release a stage).  Each thread
+//     forms, per staged plane and component, the 9 parity combinations of its 3x3 in-plane
+//     neighbourhood and applies them to the forces of node planes m+1, m, m-1 held in registers
+//     (2.5D streaming; accumulator roles rotate with period 3, unrolled).  A warp is one x-row, so
+//     the (y, z) boundary class is warp-uniform: interior rows use the parity-reduced interior
+//     stencil, face rows their class table (out of line).  Lanes on an x-face write it only when
+//     the face is fully constrained (no force needed).
 //   * the x-face kernel covers x-faces with free DOFs (a node per thread, class table).
 // No atomics; every sum has a fixed order, so results are bitwise repeatable.
 #include "osam_internal.h"
@@ -33,6 +40,7 @@ namespace {
 constexpr int TX = 32;
 constexpr int TY = 8;
 constexpr int NT = TX * TY;
+constexpr int NWARP = NT / 32;
 constexpr int ZC = 16;  // target z-planes per block (balanced split)
 constexpr int XF_BLOCK = 128;
 
@@ -42,92 +50,21 @@ __device__ __forceinline__ long long gidx(const Geom& g, int i, int j, int k) {
 
 __device__ __forceinline__ int axis_class(int idx, int nn) { return idx == 0 ? 0 : (idx == nn - 1 ? 2 : 1); }
 
-// Boundary data of a node on the surface: Dirichlet component mask and the Schwarz value
-// (first Schwarz face, in face order, holding the node).  Dirichlet > Schwarz > free.
-struct NodeBC {
-  unsigned dmask;
-  bool sw;
-  double s[3];
-};
-
-__device__ __forceinline__ NodeBC node_bc(const Geom& g, const Faces& F, int i, int j, int k) {
-  NodeBC b;
-  b.dmask = 0;
-  b.sw = false;
-  b.s[0] = b.s[1] = b.s[2] = 0.0;
+// free-DOF mask (bit c) of a node: Dirichlet > Schwarz > free (readings R12, R13)
+__device__ __forceinline__ unsigned free_mask(const Geom& g, const Faces& F, int i, int j, int k) {
+  unsigned dm = 0;
+  bool sw = false;
 #pragma unroll
   for (int f = 0; f < 6; ++f) {
     const int ax = f >> 1;
     const int v = ax == 0 ? i : (ax == 1 ? j : k);
     const bool on = v == ((f & 1) ? g.nn[ax] - 1 : 0);
     if (on) {
-      b.dmask |= F.dir[f];
-      if (F.sw[f] && !b.sw) {
-        b.sw = true;
-        // in-face index a + nn[o0] * b with (o0, o1) the two other axes in ascending order
-        const long long fi = ax == 0 ? (j + (long long)g.nn[1] * k)
-                                     : (ax == 1 ? (i + (long long)g.nn[0] * k) : (i + (long long)g.nn[0] * j));
-        const long long nf = F.nface[f];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) b.s[c] = F.s[f][c * nf + fi];
-      }
-    }
-  }
-  return b;
-}
-
-// Boundary info of a staged (x, y) position, fixed across z-planes: bits 0-2 Dirichlet mask of
-// the x/y faces holding it, bits 3-5 the first Schwarz face among faces 0-3 (7: none), bit 6 set
-// iff the position lies in the box.  PINFO_FREE = in the box and on no x/y face.
-constexpr int PINFO_FREE = 64 | (7 << 3);
-
-__device__ __forceinline__ int pos_info(const Geom& g, const Faces& F, int ii, int jj) {
-  if (ii < 0 || ii > g.nn[0] - 1 || jj < 0 || jj > g.nn[1] - 1) return 0;
-  unsigned dm = 0;
-  int sf = 7;
-#pragma unroll
-  for (int f = 0; f < 4; ++f) {
-    const int v = f < 2 ? ii : jj;
-    const bool on = v == ((f & 1) ? g.nn[f >> 1] - 1 : 0);
-    if (on) {
       dm |= F.dir[f];
-      if (F.sw[f] && sf == 7) sf = f;
+      sw = sw || F.sw[f];
     }
   }
-  return (int)dm | (sf << 3) | 64;
-}
-
-// Boundary overwrite of the predictor at a staged position off the z-faces, from its pos_info.
-__device__ __forceinline__ void apply_bc_xy(const Geom& g, const Faces& F, int info, int ii, int jj, int m,
-                                            double p[3]) {
-  const int sf = (info >> 3) & 7;
-  double sv[3] = {0.0, 0.0, 0.0};
-  if (sf != 7) {
-    const long long fi = sf < 2 ? (jj + (long long)g.nn[1] * m) : (ii + (long long)g.nn[0] * m);
-    const double* sp = sf == 0 ? F.s[0] : (sf == 1 ? F.s[1] : (sf == 2 ? F.s[2] : F.s[3]));
-    const long long nf = sf == 0 ? F.nface[0] : (sf == 1 ? F.nface[1] : (sf == 2 ? F.nface[2] : F.nface[3]));
-#pragma unroll
-    for (int c = 0; c < 3; ++c) sv[c] = sp[c * nf + fi];
-  }
-#pragma unroll
-  for (int c = 0; c < 3; ++c) p[c] = ((info >> c) & 1) ? 0.0 : (sf != 7 ? sv[c] : p[c]);
-}
-
-__device__ __forceinline__ bool is_boundary(const Geom& g, int i, int j, int k) {
-  return i == 0 || j == 0 || k == 0 || i == g.nn[0] - 1 || j == g.nn[1] - 1 || k == g.nn[2] - 1;
-}
-
-// predictor with the boundary overwrite of a surface position
-__device__ __forceinline__ void apply_bc(const Geom& g, const Faces& F, int i, int j, int k, double p[3]) {
-  const NodeBC b = node_bc(g, F, i, j, k);
-#pragma unroll
-  for (int c = 0; c < 3; ++c) p[c] = ((b.dmask >> c) & 1) ? 0.0 : (b.sw ? b.s[c] : p[c]);
-}
-
-// free-DOF mask (bit c) of a surface node
-__device__ __forceinline__ unsigned free_mask(const Geom& g, const Faces& F, int i, int j, int k) {
-  const NodeBC b = node_bc(g, F, i, j, k);
-  return b.sw ? 0u : (~b.dmask) & 7u;
+  return sw ? 0u : (~dm) & 7u;
 }
 
 __device__ __forceinline__ double warp_sum(double x) {
@@ -172,6 +109,10 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
   asm volatile(
       "{\n"
@@ -201,12 +142,10 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
 constexpr int PX = TX + 4;
 constexpr int PY = TY + 2;
 constexpr int PLANE = PX * PY;                             // positions per staged plane
-constexpr int NSTAGE = 4;  // TMA ring: 2 planes in flight, the current one, the previous one (own w)
-constexpr int NUST = 3;    // u* buffers: previous plane (own u* at finish), current, next
-constexpr int ARR_BYTES = 3 * PLANE * 8;                   // one array (x,y,z comps) of one plane
+constexpr int NSTAGE = 4;                                  // ring: 2 planes in flight, current, previous
+constexpr int ARR_BYTES = 3 * PLANE * 8;                   // X (x,y,z comps) of one plane
 constexpr int ARR_STRIDE = (ARR_BYTES + 127) / 128 * 128;  // 128-B aligned TMA destinations
-constexpr int STAGE_BYTES = 2 * ARR_STRIDE;                // u, w
-constexpr int SMEM_TILED = NSTAGE * STAGE_BYTES + NUST * ARR_STRIDE + 64;
+constexpr int SMEM_TILED = NSTAGE * ARR_STRIDE + 2 * NSTAGE * 8;
 
 // ---- interior rows: parity-reduced stencil ---------------------------------------------
 // On a uniform box every interior block K_cd(ox, oy, oz) is even or odd in ox and in oy (the 1D
@@ -265,10 +204,10 @@ __device__ __forceinline__ void contrib(double& acc, const double P[9], const In
 }
 
 template <int d, bool DA, bool DB, bool DC>
-__device__ __forceinline__ void fast_comp(double A[3], double B[3], double C[3], const double* us, int base,
+__device__ __forceinline__ void fast_comp(double A[3], double B[3], double C[3], const double* xs, int base,
                                           const InteriorStencil& S) {
   double P[9];
-  combos(us + d * PLANE + base, P);
+  combos(xs + d * PLANE + base, P);
   if (DA) {
     contrib<0, false, 0, d>(A[0], P, S);
     contrib<0, false, 1, d>(A[1], P, S);
@@ -286,26 +225,26 @@ __device__ __forceinline__ void fast_comp(double A[3], double B[3], double C[3],
   }
 }
 
-// interior rows: the staged plane's contributions to the targets that are needed
+// interior rows: the staged plane's contributions to the targets
 // (A: node plane m+1 sees plane m at oz = -1; B: plane m, oz = 0; C: plane m-1, oz = +1)
 template <bool DA, bool DB, bool DC>
-__device__ __forceinline__ void plane_fast(double A[3], double B[3], double C[3], const double* us, int base,
+__device__ __forceinline__ void plane_fast(double A[3], double B[3], double C[3], const double* xs, int base,
                                            const InteriorStencil& S) {
-  fast_comp<0, DA, DB, DC>(A, B, C, us, base, S);
-  fast_comp<1, DA, DB, DC>(A, B, C, us, base, S);
-  fast_comp<2, DA, DB, DC>(A, B, C, us, base, S);
+  fast_comp<0, DA, DB, DC>(A, B, C, xs, base, S);
+  fast_comp<1, DA, DB, DC>(A, B, C, xs, base, S);
+  fast_comp<2, DA, DB, DC>(A, B, C, xs, base, S);
 }
 
 // Face rows / face planes: full 3x3 blocks from the class table (L1 broadcast).
 template <int OZ>
-__device__ __forceinline__ void plane_class(double acc[3], const double* us, int base,
+__device__ __forceinline__ void plane_class(double acc[3], const double* xs, int base,
                                             const double* __restrict__ cls_coef) {
 #pragma unroll
   for (int oy = 0; oy < 3; ++oy) {
 #pragma unroll
     for (int ox = 0; ox < 3; ++ox) {
       const int q = base + oy * PX + ox;
-      const double w[3] = {us[q], us[PLANE + q], us[2 * PLANE + q]};
+      const double w[3] = {xs[q], xs[PLANE + q], xs[2 * PLANE + q]};
       const double* cb = cls_coef + (ox + 3 * (oy + 3 * OZ)) * 9;
 #pragma unroll
       for (int c = 0; c < 3; ++c)
@@ -316,31 +255,31 @@ __device__ __forceinline__ void plane_class(double acc[3], const double* us, int
 }
 
 template <int OZ>
-__device__ __forceinline__ void target_any(double acc[3], const double* us, int base, int cy, int cz,
+__device__ __forceinline__ void target_any(double acc[3], const double* xs, int base, int cy, int cz,
                                            const InteriorStencil& S, const double* coef) {
   if (cy == 1 && cz == 1) {
     double d0[3] = {0.0, 0.0, 0.0}, d1[3] = {0.0, 0.0, 0.0};
-    if (OZ == 0) plane_fast<true, false, false>(acc, d0, d1, us, base, S);
-    if (OZ == 1) plane_fast<false, true, false>(d0, acc, d1, us, base, S);
-    if (OZ == 2) plane_fast<false, false, true>(d0, d1, acc, us, base, S);
+    if (OZ == 0) plane_fast<true, false, false>(acc, d0, d1, xs, base, S);
+    if (OZ == 1) plane_fast<false, true, false>(d0, acc, d1, xs, base, S);
+    if (OZ == 2) plane_fast<false, false, true>(d0, d1, acc, xs, base, S);
   } else {
-    plane_class<OZ>(acc, us, base, coef + (size_t)(1 + 3 * (cy + 3 * cz)) * 27 * 9);
+    plane_class<OZ>(acc, xs, base, coef + (size_t)(1 + 3 * (cy + 3 * cz)) * 27 * 9);
   }
 }
 
-// Face rows / face planes (rare): the three targets' contributions of one staged plane from the
-// class tables, out of line to keep the hot loop small.
+// Face rows / face planes (rare): the three targets' contributions of one staged plane, out of
+// line to keep the hot loop small.
 struct Contrib3 {
   double v[9];
 };
 
-__device__ __noinline__ Contrib3 plane_slow(const double* us, int base, int cy, int czA, int czB, int czC,
+__device__ __noinline__ Contrib3 plane_slow(const double* xs, int base, int cy, int czA, int czB, int czC,
                                              const InteriorStencil& S, const double* coef) {
   Contrib3 r;
   double A[3] = {0.0, 0.0, 0.0}, B[3] = {0.0, 0.0, 0.0}, C[3] = {0.0, 0.0, 0.0};
-  target_any<0>(A, us, base, cy, czA, S, coef);
-  target_any<1>(B, us, base, cy, czB, S, coef);
-  target_any<2>(C, us, base, cy, czC, S, coef);
+  target_any<0>(A, xs, base, cy, czA, S, coef);
+  target_any<1>(B, xs, base, cy, czB, S, coef);
+  target_any<2>(C, xs, base, cy, czC, S, coef);
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     r.v[c] = A[c];
@@ -350,25 +289,21 @@ __device__ __noinline__ Contrib3 plane_slow(const double* us, int base, int cy, 
   return r;
 }
 
-__device__ __noinline__ void apply_bc_full(const Geom& g, const Faces& F, int i, int j, int k, double& p0, double& p1,
-                                           double& p2) {
-  double p[3] = {p0, p1, p2};
-  apply_bc(g, F, i, j, k, p);
-  p0 = p[0];
-  p1 = p[1];
-  p2 = p[2];
-}
-
 // Per-thread constants of the tiled kernel.
 struct Tile {
-  int t, qo, base, q1;
-  bool has1;
-  int info0, info1;
+  int qo, base;
   int x0, y0, i, j;
-  bool active, xface, writer;
+  bool active, xface, writer, lead;
   int cy, kbeg, kend, nplanes;
   long long id0;
 };
+
+__device__ __forceinline__ void issue_plane(const Tile& T, int it, double* ring, unsigned long long* full,
+                                            const CUtensorMap* tx) {
+  const int s = it & (NSTAGE - 1);
+  mbar_expect_tx(&full[s], ARR_BYTES);
+  tma_load_4d(ring + (size_t)s * (ARR_STRIDE / 8), tx, T.x0, T.y0, T.kbeg - 1 + it, 0, &full[s]);
+}
 
 // One staged plane (iteration it, staged plane m = kbeg - 1 + it).  Accumulator slots rotate by
 // role: A = acc[SA] (node plane m+1), B = acc[SB] (plane m), C = acc[SC] (plane m-1, finished
@@ -376,9 +311,8 @@ struct Tile {
 // are accumulated too (and never used): that keeps every iteration identical.
 template <int SA, int SB, int SC>
 __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStencil& S, const Tile& T, int it,
-                                        double (&acc)[3][3], double& num, double& den, double* raw, double* ust,
-                                        unsigned long long* bar, const CUtensorMap* tu, const CUtensorMap* tw) {
-  constexpr int U3 = (3 - SA) % 3;  // == it % 3
+                                        double (&acc)[3][3], double& num, double& den, double* ring,
+                                        unsigned long long* full, unsigned long long* empty, const CUtensorMap* tx) {
   const Geom& g = L.g;
   const int nz = g.nn[2] - 1;
   const long long np = g.npad;
@@ -386,66 +320,32 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
   const int kf = m - 1;
   const bool fin = T.writer && kf >= T.kbeg && kf <= T.kend;
   const long long id = T.id0 + (long long)kf * g.plane;
-  double qw[3] = {0.0, 0.0, 0.0};
-  if (fin && L.with_norm && !T.xface) {  // previous Schwarz iterate (norm), issued before the wait
+  // own W and the previous iterate's W' of node plane kf: issued before the wait
+  double wo[3] = {0.0, 0.0, 0.0}, qw[3] = {0.0, 0.0, 0.0};
+  if (fin && !T.xface) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) qw[c] = L.w1[c * np + id];
+    for (int c = 0; c < 3; ++c) wo[c] = L.w0[c * np + id];
+    if (L.with_norm) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) qw[c] = L.w_out[c * np + id];
+    }
+  }
+  // producer: refill the stage of plane it+2 once every warp has released its previous plane it-2
+  if (T.lead && it + 2 < T.nplanes) {
+    if (it >= 2) mbar_wait(&empty[(it + 2) & (NSTAGE - 1)], (unsigned)(((it - 2) >> 2) & 1));
+    issue_plane(T, it + 2, ring, full, tx);
   }
   const int s = it & (NSTAGE - 1);
-  mbar_wait(&bar[s], (unsigned)((it / NSTAGE) & 1));
-  const double* ru = raw + (size_t)s * (STAGE_BYTES / 8);
-  const double* rw = ru + ARR_STRIDE / 8;
-  double* us = ust + U3 * (ARR_STRIDE / 8);
-  // predictor u* = u + dtp w (TMA zero-fills out-of-box positions; the padding columns hold 0)
-  {
-    const bool mval = m >= 0 && m <= nz;
-    const bool bplane = (m == 0) || (m == nz);
-    const double dtp = L.dtp;
-    double p[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) p[c] = fma(dtp, rw[c * PLANE + T.t], ru[c * PLANE + T.t]);
-    if (mval && T.info0 != PINFO_FREE && T.info0 != 0) {
-      if (bplane)
-        apply_bc_full(g, L.f, T.x0 + T.t % PX, T.y0 + T.t / PX, m, p[0], p[1], p[2]);
-      else
-        apply_bc_xy(g, L.f, T.info0, T.x0 + T.t % PX, T.y0 + T.t / PX, m, p);
-    } else if (bplane && T.info0 == PINFO_FREE) {
-      apply_bc(g, L.f, T.x0 + T.t % PX, T.y0 + T.t / PX, m, p);
-    }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) us[c * PLANE + T.t] = p[c];
-    if (T.has1) {
-      const int q1 = T.q1;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) p[c] = fma(dtp, rw[c * PLANE + q1], ru[c * PLANE + q1]);
-      if (mval && T.info1 != PINFO_FREE && T.info1 != 0) {
-        if (bplane)
-          apply_bc_full(g, L.f, T.x0 + q1 % PX, T.y0 + q1 / PX, m, p[0], p[1], p[2]);
-        else
-          apply_bc_xy(g, L.f, T.info1, T.x0 + q1 % PX, T.y0 + q1 / PX, m, p);
-      } else if (bplane && T.info1 == PINFO_FREE) {
-        apply_bc_full(g, L.f, T.x0 + q1 % PX, T.y0 + q1 / PX, m, p[0], p[1], p[2]);
-      }
-#pragma unroll
-      for (int c = 0; c < 3; ++c) us[c * PLANE + q1] = p[c];
-    }
-  }
-  __syncthreads();
-  if (T.t == 0 && it + 2 < T.nplanes) {  // refill: stage (it+2) % 4 was last read in iteration it-1
-    const int s2 = (it + 2) & (NSTAGE - 1);
-    double* dst = raw + (size_t)s2 * (STAGE_BYTES / 8);
-    mbar_expect_tx(&bar[s2], 2 * ARR_BYTES);
-    tma_load_4d(dst, tu, T.x0, T.y0, m + 2, 0, &bar[s2]);
-    tma_load_4d(dst + ARR_STRIDE / 8, tw, T.x0, T.y0, m + 2, 0, &bar[s2]);
-  }
+  mbar_wait(&full[s], (unsigned)((it >> 2) & 1));
+  const double* xs = ring + (size_t)s * (ARR_STRIDE / 8);
   if (T.active) {
     double* A = acc[SA];
     double* B = acc[SB];
     double* C = acc[SC];
     if (T.cy == 1 && m >= 2 && m <= nz - 2) {
-      plane_fast<true, true, true>(A, B, C, us, T.base, S);
+      plane_fast<true, true, true>(A, B, C, xs, T.base, S);
     } else {
-      const Contrib3 r = plane_slow(us, T.base, T.cy, axis_class(m + 1, g.nn[2]), axis_class(m, g.nn[2]),
+      const Contrib3 r = plane_slow(xs, T.base, T.cy, axis_class(m + 1, g.nn[2]), axis_class(m, g.nn[2]),
                                     axis_class(kf, g.nn[2]), S, L.coef);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -455,37 +355,35 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
       }
     }
     if (fin) {
-      // own u* and checkpoint w of plane kf = m-1, kept in shared memory since iteration it-1
-      const double* pus = ust + ((U3 + 2) % 3) * (ARR_STRIDE / 8) + T.qo;
-      const double* pws = raw + (size_t)((it - 1) & (NSTAGE - 1)) * (STAGE_BYTES / 8) + ARR_STRIDE / 8 + T.qo;
-      double* u1 = L.u1 + id;
-      double* w1 = L.w1 + id;
+      // own X of plane kf, staged in iteration it-1 (stage released at the end of this iteration)
+      const double* xo = ring + (size_t)((it - 1) & (NSTAGE - 1)) * (ARR_STRIDE / 8) + T.qo;
       const int cz = axis_class(kf, g.nn[2]);
-      if (T.xface) {  // fully constrained x-face node: prescribed u, w = a = 0
+      if (T.xface) {  // fully constrained x-face node: Q' = X (prescribed), W' = a = 0
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          u1[c * np] = pus[c * PLANE];
-          w1[c * np] = 0.0;
+          if (L.q_out) L.q_out[c * np + id] = xo[c * PLANE];
+          L.w_out[c * np + id] = 0.0;
           if (L.a_out) L.a_out[c * np + id] = 0.0;
         }
-      } else if (T.cy == 1 && cz == 1 && L.a_out == nullptr) {  // interior node, all DOFs free
+      } else if (T.cy == 1 && cz == 1 && L.a_out == nullptr && L.q_out != nullptr) {  // interior node
         const double inv_m = L.inv_mass[7];
-        double pu[3], an[3], wn[3], pw[3];
+        double* qo = L.q_out + id;
+        double* wp = L.w_out + id;
+        double an[3], wn[3], x[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          pu[c] = pus[c * PLANE];
-          pw[c] = pws[c * PLANE];
+          x[c] = xo[c * PLANE];
           an[c] = -C[c] * inv_m;
-          wn[c] = fma(L.cw, an[c], pw[c]);
-          u1[c * np] = pu[c];
-          w1[c * np] = wn[c];
+          wn[c] = fma(L.cw, an[c], wo[c]);
+          qo[c * np] = fma(L.cq, wn[c], x[c]);
+          wp[c * np] = wn[c];
         }
         if (L.with_norm) {
           const double hdt = 0.5 * L.dt;
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             const double d = hdt * (wn[c] - qw[c]);
-            const double w = fma(L.dt, fma(L.cv, an[c], pw[c]), pu[c]);
+            const double w = fma(L.dt, fma(L.cv, an[c], wo[c]), x[c]);
             num = fma(d, d, num);
             den = fma(w, w, den);
           }
@@ -495,49 +393,54 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
         const double inv_m = L.inv_mass[1 + 2 * (T.cy == 1) + 4 * (cz == 1)];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const double pu = pus[c * PLANE], pw = pws[c * PLANE];
-          double an = 0.0, wn = 0.0;
+          const double x = xo[c * PLANE];
+          double an = 0.0, wn = 0.0, qn = x;
           if ((fm >> c) & 1) {
             an = -C[c] * inv_m;
-            wn = fma(L.cw, an, pw);
+            wn = fma(L.cw, an, wo[c]);
+            qn = fma(L.cq, wn, x);
             if (L.with_norm) {
               const double d = 0.5 * L.dt * (wn - qw[c]);
-              const double w = fma(L.dt, fma(L.cv, an, pw), pu);
+              const double w = fma(L.dt, fma(L.cv, an, wo[c]), x);
               num = fma(d, d, num);
               den = fma(w, w, den);
             }
           }
-          u1[c * np] = pu;
-          w1[c * np] = wn;
+          if (L.q_out) L.q_out[c * np + id] = qn;
+          L.w_out[c * np + id] = wn;
           if (L.a_out) L.a_out[c * np + id] = an;
         }
       }
     }
   }
+  // this warp is done with plane it-1 (own values above; stencil in the previous iteration)
+  __syncwarp();
+  if (it >= 1 && (threadIdx.x & 31) == 0) mbar_arrive(&empty[(it - 1) & (NSTAGE - 1)]);
 #pragma unroll
   for (int c = 0; c < 3; ++c) acc[SC][c] = 0.0;
 }
 
 __global__ void __launch_bounds__(NT, 2)
     fom_tiled_kernel(const __grid_constant__ FomLaunch L, const __grid_constant__ InteriorStencil S,
-                     const __grid_constant__ CUtensorMap tu, const __grid_constant__ CUtensorMap tw) {
+                     const __grid_constant__ CUtensorMap tmx) {
   extern __shared__ __align__(128) unsigned char smem[];
-  double* raw = reinterpret_cast<double*>(smem);
-  double* ust = reinterpret_cast<double*>(smem + NSTAGE * STAGE_BYTES);
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(smem + NSTAGE * STAGE_BYTES + NUST * ARR_STRIDE);
+  double* ring = reinterpret_cast<double*>(smem);
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + NSTAGE * ARR_STRIDE);
+  unsigned long long* empty = full + NSTAGE;
   const Geom& g = L.g;
   const int nx = g.nn[0] - 1, ny = g.nn[1] - 1;
   Tile T;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  T.t = ty * TX + tx;
+  const int t = ty * TX + tx;
+  T.lead = t == 0;
   T.x0 = blockIdx.x * TX - 2;  // node coordinates of staged position (0,0)
   T.y0 = blockIdx.y * TY - 1;
   T.i = T.x0 + 2 + tx;
   T.j = T.y0 + 1 + ty;
   T.active = (T.i <= nx) && (T.j <= ny);
   T.xface = (T.i == 0) || (T.i == nx);
-  const int xs = T.i == 0 ? 0 : 1;
-  const bool xf_full = T.xface && (L.f.dir[xs] == 7 || L.f.sw[xs]);
+  const int xsd = T.i == 0 ? 0 : 1;
+  const bool xf_full = T.xface && (L.f.dir[xsd] == 7 || L.f.sw[xsd]);
   T.writer = T.active && (!T.xface || xf_full);
   T.cy = axis_class(T.j, g.nn[1]);  // warp-uniform (a warp is one x-row)
   T.kbeg = (int)((long long)blockIdx.z * g.nn[2] / gridDim.z);
@@ -545,49 +448,43 @@ __global__ void __launch_bounds__(NT, 2)
   T.nplanes = T.kend - T.kbeg + 3;
   T.qo = (ty + 1) * PX + (tx + 2);
   T.base = ty * PX + tx + 1;
-  T.q1 = T.t + NT;
-  T.has1 = T.q1 < PLANE;
-  T.info0 = pos_info(g, L.f, T.x0 + T.t % PX, T.y0 + T.t / PX);
-  T.info1 = T.has1 ? pos_info(g, L.f, T.x0 + T.q1 % PX, T.y0 + T.q1 / PX) : 0;
   T.id0 = T.i + (long long)g.px * T.j;
 
-  if (T.t == 0) {
-    for (int s = 0; s < NSTAGE; ++s) mbar_init(&bar[s], 1);
+  if (t == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWARP);
+    }
     mbar_fence_init();
   }
   __syncthreads();
-  if (T.t == 0) {
-    for (int it = 0; it < 2 && it < T.nplanes; ++it) {
-      double* dst = raw + (size_t)it * (STAGE_BYTES / 8);
-      mbar_expect_tx(&bar[it], 2 * ARR_BYTES);
-      tma_load_4d(dst, &tu, T.x0, T.y0, T.kbeg - 1 + it, 0, &bar[it]);
-      tma_load_4d(dst + ARR_STRIDE / 8, &tw, T.x0, T.y0, T.kbeg - 1 + it, 0, &bar[it]);
-    }
+  if (T.lead) {
+    issue_plane(T, 0, ring, full, &tmx);
+    if (T.nplanes > 1) issue_plane(T, 1, ring, full, &tmx);
   }
 
   double acc[3][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
   double num = 0.0, den = 0.0;
   for (int it = 0; it < T.nplanes;) {  // unrolled by the period 3 of the slot rotation
-    k1_iter<0, 1, 2>(L, S, T, it, acc, num, den, raw, ust, bar, &tu, &tw);
+    k1_iter<0, 1, 2>(L, S, T, it, acc, num, den, ring, full, empty, &tmx);
     if (++it >= T.nplanes) break;
-    k1_iter<2, 0, 1>(L, S, T, it, acc, num, den, raw, ust, bar, &tu, &tw);
+    k1_iter<2, 0, 1>(L, S, T, it, acc, num, den, ring, full, empty, &tmx);
     if (++it >= T.nplanes) break;
-    k1_iter<1, 2, 0>(L, S, T, it, acc, num, den, raw, ust, bar, &tu, &tw);
+    k1_iter<1, 2, 0>(L, S, T, it, acc, num, den, ring, full, empty, &tmx);
     ++it;
   }
   const int slot = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
   block_partial<NT>(num, den, L.partial, slot);
 }
 
-// Nodes on an x-face with free DOFs (one per thread): gather over the 18 neighbours inside the
-// box, class-table stencil.  side_mask bit 0: face x = 0, bit 1: face x = nx.
+// Nodes on an x-face with free DOFs (one per thread): gather X over the 18 neighbours inside
+// the box, class-table stencil.  side_mask bit 0: face x = 0, bit 1: face x = nx.
 __global__ void __launch_bounds__(XF_BLOCK) fom_xface_kernel(const FomLaunch L, int slot0, int side_mask) {
   const Geom& g = L.g;
   const long long np = g.npad;
   const long long nf = (long long)g.nn[1] * g.nn[2];
   const int nsides = (side_mask & 1) + ((side_mask >> 1) & 1);
   const long long t = blockIdx.x * (long long)XF_BLOCK + threadIdx.x;
-  const double dtp = L.dtp;
   const int nx = g.nn[0] - 1;
   double num = 0.0, den = 0.0;
   if (t < nsides * nf) {
@@ -598,56 +495,46 @@ __global__ void __launch_bounds__(XF_BLOCK) fom_xface_kernel(const FomLaunch L, 
     const int k = (int)(r / g.nn[1]);
     const long long id = gidx(g, i, j, k);
     const unsigned fm = free_mask(g, L.f, i, j, k);
-    double own[3] = {0.0, 0.0, 0.0};
-    double f[3] = {0.0, 0.0, 0.0};
-    const int cl = (side ? 2 : 0) + 3 * (axis_class(j, g.nn[1]) + 3 * axis_class(k, g.nn[2]));
-    const double* coef = L.coef + (size_t)cl * 27 * 9;
+    const int cyj = axis_class(j, g.nn[1]), czk = axis_class(k, g.nn[2]);
+    const double* coef = L.coef + (size_t)((side ? 2 : 0) + 3 * (cyj + 3 * czk)) * 27 * 9;
     const int oxlo = side ? -1 : 0;
-    for (int oz = -1; oz <= 1; ++oz) {
-      const int kk = k + oz;
-      if (kk < 0 || kk > g.nn[2] - 1) continue;
-      for (int oy = -1; oy <= 1; ++oy) {
-        const int jj = j + oy;
-        if (jj < 0 || jj > g.nn[1] - 1) continue;
+    const int kl = k > 0 ? -1 : 0, kh = k < g.nn[2] - 1 ? 1 : 0;
+    const int jl = j > 0 ? -1 : 0, jh = j < g.nn[1] - 1 ? 1 : 0;
+    double f[3] = {0.0, 0.0, 0.0};
+    for (int oz = kl; oz <= kh; ++oz) {
+      for (int oy = jl; oy <= jh; ++oy) {
 #pragma unroll
         for (int dx = 0; dx < 2; ++dx) {
           const int ox = oxlo + dx;
-          const int ii = i + ox;
-          const long long q = gidx(g, ii, jj, kk);
-          double p[3];
-#pragma unroll
-          for (int c = 0; c < 3; ++c) p[c] = fma(dtp, __ldg(L.w0 + c * np + q), __ldg(L.u0 + c * np + q));
-          if (is_boundary(g, ii, jj, kk)) apply_bc(g, L.f, ii, jj, kk, p);
-          if (ox == 0 && oy == 0 && oz == 0) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) own[c] = p[c];
-          }
+          const long long q = gidx(g, i + ox, j + oy, k + oz);
+          const double x[3] = {__ldg(L.x + q), __ldg(L.x + np + q), __ldg(L.x + 2 * np + q)};
           const double* cb = coef + ((ox + 1) + 3 * ((oy + 1) + 3 * (oz + 1))) * 9;
 #pragma unroll
           for (int c = 0; c < 3; ++c)
 #pragma unroll
-            for (int d = 0; d < 3; ++d) f[c] = fma(__ldg(cb + c * 3 + d), p[d], f[c]);
+            for (int d = 0; d < 3; ++d) f[c] = fma(__ldg(cb + c * 3 + d), x[d], f[c]);
         }
       }
     }
-    const double inv_m = L.inv_mass[(axis_class(j, g.nn[1]) == 1 ? 2 : 0) + (axis_class(k, g.nn[2]) == 1 ? 4 : 0)];
+    const double inv_m = L.inv_mass[(cyj == 1 ? 2 : 0) + (czk == 1 ? 4 : 0)];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      double an = 0.0, wn = 0.0;
+      const double x = __ldg(L.x + c * np + id);
+      double an = 0.0, wn = 0.0, qn = x;
       if ((fm >> c) & 1) {
-        const double w0 = __ldg(L.w0 + c * np + id);
+        const double w0 = L.w0[c * np + id];
         an = -f[c] * inv_m;
         wn = fma(L.cw, an, w0);
+        qn = fma(L.cq, wn, x);
         if (L.with_norm) {
-          const double d = 0.5 * L.dt * (wn - L.w1[c * np + id]);
-          const double v = fma(L.cv, an, w0);
-          const double w = fma(L.dt, v, own[c]);
+          const double d = 0.5 * L.dt * (wn - L.w_out[c * np + id]);
+          const double w = fma(L.dt, fma(L.cv, an, w0), x);
           num = fma(d, d, num);
           den = fma(w, w, den);
         }
       }
-      L.u1[c * np + id] = own[c];
-      L.w1[c * np + id] = wn;
+      if (L.q_out) L.q_out[c * np + id] = qn;
+      L.w_out[c * np + id] = wn;
       if (L.a_out) L.a_out[c * np + id] = an;
     }
   }
@@ -703,46 +590,28 @@ __global__ void unpack_kernel(Geom g, const double* __restrict__ src, double* __
   for (int c = 0; c < 3; ++c) dst[c * n + p] = src[c * g.npad + q];
 }
 
-__global__ void face_gather_kernel(Geom g, Faces F, const double* __restrict__ u) {
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-#pragma unroll
-  for (int f = 0; f < 6; ++f) {
-    if (!F.sw[f] || t >= F.nface[f]) continue;
-    const int ax = f >> 1;
-    const int side = (f & 1) ? g.nn[ax] - 1 : 0;
-    int i, j, k;
-    if (ax == 0) {
-      i = side;
-      j = (int)(t % g.nn[1]);
-      k = (int)(t / g.nn[1]);
-    } else if (ax == 1) {
-      j = side;
-      i = (int)(t % g.nn[0]);
-      k = (int)(t / g.nn[0]);
-    } else {
-      k = side;
-      i = (int)(t % g.nn[0]);
-      j = (int)(t / g.nn[0]);
-    }
-    const long long q = gidx(g, i, j, k);
-    for (int c = 0; c < 3; ++c) F.s[f][c * (long long)F.nface[f] + t] = u[c * g.npad + q];
-  }
-}
-
-// Dirichlet u := 0 (if zero_u), constrained w := 0 on every surface node.
-__global__ void zero_constrained_kernel(Geom g, Faces F, double* u, double* w, int zero_u) {
+// Dirichlet u := 0, constrained w := 0 on every surface node (initial condition).
+__global__ void zero_constrained_kernel(Geom g, Faces F, double* u, double* w) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= surface_count(g)) return;
   int i, j, k;
   surface_node(g, t, &i, &j, &k);
   const long long q = gidx(g, i, j, k);
-  const NodeBC b = node_bc(g, F, i, j, k);
-  for (int c = 0; c < 3; ++c) {
-    const bool dir = (b.dmask >> c) & 1;
-    if (dir || b.sw) {
-      w[c * g.npad + q] = 0.0;
-      if (zero_u && dir) u[c * g.npad + q] = 0.0;
+  unsigned dm = 0;
+  bool sw = false;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    const int ax = f >> 1;
+    const int v = ax == 0 ? i : (ax == 1 ? j : k);
+    if (v == ((f & 1) ? g.nn[ax] - 1 : 0)) {
+      dm |= F.dir[f];
+      sw = sw || F.sw[f];
     }
+  }
+  for (int c = 0; c < 3; ++c) {
+    const bool dir = (dm >> c) & 1;
+    if (dir || sw) w[c * g.npad + q] = 0.0;
+    if (dir) u[c * g.npad + q] = 0.0;
   }
 }
 
@@ -779,7 +648,7 @@ void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUt
     cudaFuncSetAttribute(fom_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TILED);
     attr_set = true;
   }
-  fom_tiled_kernel<<<gi, dim3(TX, TY), SMEM_TILED, s>>>(L, st, tm[0], tm[1]);
+  fom_tiled_kernel<<<gi, dim3(TX, TY), SMEM_TILED, s>>>(L, st, *tm);
   debug_check("fom_tiled_kernel", s);
   ++*launches;
   const unsigned xb = xface_blocks(L.g, L.f);
@@ -790,7 +659,7 @@ void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUt
   }
 }
 
-int make_state_tmaps(const Geom& g, double* const arrays[2], CUtensorMap out[2]) {
+int make_field_tmap(const Geom& g, double* array, CUtensorMap* out) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -803,20 +672,10 @@ int make_state_tmaps(const Geom& g, double* const arrays[2], CUtensorMap out[2])
   const cuuint64_t strides[3] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.plane * 8, (cuuint64_t)g.npad * 8};
   const cuuint32_t box[4] = {PX, PY, 1, 3};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
-  for (int q = 0; q < 2; ++q) {
-    CUresult r = encode(&out[q], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, arrays[q], dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return (int)r;
-  }
-  return 0;
-}
-
-void launch_fom_face_gather(const Geom& g, const Faces& f, const double* u, cudaStream_t s) {
-  int nmax = 1;
-  for (int q = 0; q < 6; ++q) nmax = f.nface[q] > nmax ? f.nface[q] : nmax;
-  face_gather_kernel<<<cdiv(nmax, 256), 256, 0, s>>>(g, f, u);
-  debug_check("face_gather_kernel", s);
+  const CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, array, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : (int)r;
 }
 
 void launch_fom_pack(const Geom& g, const double* src, double* dst, long long n, cudaStream_t s) {
@@ -829,8 +688,8 @@ void launch_fom_unpack(const Geom& g, const double* src, double* dst, long long 
   debug_check("unpack_kernel", s);
 }
 
-void launch_fom_zero_constrained(const Geom& g, const Faces& f, double* u, double* w, int zero_u, cudaStream_t s) {
-  zero_constrained_kernel<<<cdiv(surface_count(g), 256), 256, 0, s>>>(g, f, u, w, zero_u);
+void launch_fom_zero_constrained(const Geom& g, const Faces& f, double* u, double* w, cudaStream_t s) {
+  zero_constrained_kernel<<<cdiv(surface_count(g), 256), 256, 0, s>>>(g, f, u, w);
   debug_check("zero_constrained_kernel", s);
 }
 

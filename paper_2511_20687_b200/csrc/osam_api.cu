@@ -155,7 +155,6 @@ void release_maps(Sub& s) {
 
 void release_binding(Sub& s) {
   release_maps(s);
-  for (int f = 0; f < 6; ++f) dfree(s.faces.s[f]);
   dfree(s.scratch_partial);
   dfree(s.Phi);
   dfree(s.Phi_s);
@@ -284,9 +283,6 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
       for (int f = 0; f < 6; ++f) {
         s.faces.dir[f] = s.dirichlet[f];
         s.faces.sw[f] = s.face_src[f] >= 0;
-        s.faces.nface[f] = (int)face_count(s.g, f);
-        s.faces.s[f] = nullptr;
-        if (s.faces.sw[f]) TRY(dalloc(&s.faces.s[f], 3 * (size_t)s.faces.nface[f]));
       }
       TRY(dalloc(&s.scratch_partial, (size_t)fom_partial_slots(s.g, s.faces)));
       continue;
@@ -371,12 +367,14 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
           P.corner[8 * t + q] = ci + (long long)src.g.nn[0] * (cj + (long long)src.g.nn[1] * ck);
         }
         for (int c = 0; c < 3; ++c) {
-          if (d.kind == OSAM_ROM) {
-            const bool mine = d.codes[3 * p + c] == DOF_SCHWARZ && owner_face(d, p) == f;
-            P.out[3 * t + c] = mine ? (int)sdof_index[3 * p + c] : -1;
-          } else {
-            P.out[3 * t + c] = (int)(c * nf + t);
-          }
+          // each Schwarz DOF is written by the map of its lowest Schwarz face; Dirichlet wins
+          const bool mine = d.codes[3 * p + c] == DOF_SCHWARZ && owner_face(d, p) == f;
+          if (!mine)
+            P.out[3 * t + c] = -1;
+          else if (d.kind == OSAM_ROM)
+            P.out[3 * t + c] = (int)sdof_index[3 * p + c];
+          else  // FOM: straight into the checkpoint's q (R30)
+            P.out[3 * t + c] = (int)(c * d.g.npad + idx[0] + (long long)d.g.px * (idx[1] + (long long)d.g.nn[1] * idx[2]));
         }
       }
       pend.push_back(std::move(P));
@@ -451,12 +449,10 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
 int process_ic(Sub& s, int* launches) {
   cudaStream_t st = s.stream;
   if (s.kind == OSAM_FOM) {
-    // Dirichlet DOFs := 0, constrained w := 0; Schwarz DOFs keep u0 and seed the face arrays.
-    // a0 = -f(u0)/m enters w at the first osam_step (fom_set_step), once dt is known.
-    const int c = s.cur;
-    launch_fom_zero_constrained(s.g, s.faces, s.st[c][0], s.st[c][1], 1, st);
-    launch_fom_face_gather(s.g, s.faces, s.st[c][0], st);
-    *launches += 2;
+    // RAW state (u, v): Dirichlet u := 0, constrained v := 0; Schwarz DOFs keep u0.  a0 = -f(u0)/m
+    // enters at the first osam_step (fom_set_step), once dt is known.
+    launch_fom_zero_constrained(s.g, s.faces, s.st[s.cur][0], s.st[s.cur][1], st);
+    *launches += 1;
     CK(cudaStreamSynchronize(st));
   } else {
     const int c = s.cur;
@@ -514,19 +510,19 @@ int get_group(osam_subdomain* const* sds, int n_sd, Group** out) {
   return OSAM_OK;
 }
 
-// K1 launch description reading buffer `from` and writing buffer 1 - from.
-FomLaunch fom_launch(const Sub& d, int from, double dtp, double cw, double cv, double dt, int with_norm,
-                     double2* partial, double* a_out) {
+// K1 launch description (kernels_fom.cu): stencil input X, per-node W, outputs Q', W' (, a).
+FomLaunch fom_launch(const Sub& d, const double* x, const double* w0, double* q_out, double* w_out, double cw,
+                     double cq, double cv, double dt, int with_norm, double2* partial, double* a_out) {
   FomLaunch L{};
   L.g = d.g;
   L.f = d.faces;
-  L.u0 = d.st[from][0];
-  L.w0 = d.st[from][1];
-  L.u1 = d.st[1 - from][0];
-  L.w1 = d.st[1 - from][1];
+  L.x = x;
+  L.w0 = w0;
+  L.q_out = q_out;
+  L.w_out = w_out;
   L.a_out = a_out;
-  L.dtp = dtp;
   L.cw = cw;
+  L.cq = cq;
   L.cv = cv;
   L.dt = dt;
   for (int q = 0; q < 8; ++q) L.inv_mass[q] = d.inv_mass[q];
@@ -536,14 +532,22 @@ FomLaunch fom_launch(const Sub& d, int from, double dtp, double cw, double cv, d
   return L;
 }
 
-// Make the stored w refer to step dt: w <- w + (dt - w_dt)/2 a with a = -K u / m (one force
-// pass, u unchanged; Schwarz DOFs read the face arrays, which hold the stored Schwarz values).
+// Bring the state to STEP(dt) (R30), with a = -K u / m from one force pass:
+//   RAW (u, v) in st[c]:    w = v + dt/2 a, q = u + dt w  -> st[1-c]; st[c][0] keeps u
+//   STEP(dt0) in st[c]:     u = st[1-c][0] exactly; w <- w + (dt - dt0)/2 a, q = u + dt w in place
 int fom_set_step(Sub& d, double dt, int* launches) {
   if (d.w_dt == dt) return OSAM_OK;
   const int c = d.cur;
-  const FomLaunch L = fom_launch(d, c, 0.0, 0.5 * (dt - d.w_dt), 0.0, dt, 0, d.scratch_partial, nullptr);
-  launch_fom_advance(L, d.stencil, d.tmap[c], d.stream, launches);
-  d.cur = 1 - c;
+  if (d.w_dt == 0.0) {
+    const FomLaunch L = fom_launch(d, d.st[c][0], d.st[c][1], d.st[1 - c][0], d.st[1 - c][1], 0.5 * dt, dt, 0.0,
+                                   dt, 0, d.scratch_partial, nullptr);
+    launch_fom_advance(L, d.stencil, &d.tmap[c], d.stream, launches);
+    d.cur = 1 - c;
+  } else {
+    const FomLaunch L = fom_launch(d, d.st[1 - c][0], d.st[c][1], d.st[c][0], d.st[c][1], 0.5 * (dt - d.w_dt), dt,
+                                   0.0, dt, 0, d.scratch_partial, nullptr);
+    launch_fom_advance(L, d.stencil, &d.tmap[1 - c], d.stream, launches);
+  }
   d.w_dt = dt;
   return OSAM_OK;
 }
@@ -583,7 +587,9 @@ int controller_step(Group& G, const osam_schwarz_cfg& cfg, int32_t* iters) {
         const double* field;
         long long cs, bs;
         if (src.kind == OSAM_FOM) {
-          field = src.st[sb][0];
+          // a FOM iterate's displacement is its checkpoint q (predictor + current Schwarz values);
+          // iterate 0 (constant extension) is the checkpoint u, kept in st[1-cur][0]
+          field = newest ? src.st[src.cur][0] : src.st[1 - src.cur][0];
           cs = src.g.npad;
           bs = 0;
         } else {
@@ -594,7 +600,7 @@ int controller_step(Group& G, const osam_schwarz_cfg& cfg, int32_t* iters) {
         double* dst;
         long long dbs;
         if (d.kind == OSAM_FOM) {
-          dst = d.faces.s[m.face];
+          dst = d.st[d.cur][0];
           dbs = 0;
         } else {
           dst = d.rst[1 - d.cur][3];
@@ -606,10 +612,10 @@ int controller_step(Group& G, const osam_schwarz_cfg& cfg, int32_t* iters) {
       const int with_norm = n >= 2 ? 1 : 0;
       if (d.kind == OSAM_FOM) {
         const int c = d.cur;
-        const FomLaunch L = fom_launch(d, c, cfg.dt, cfg.dt, 0.5 * cfg.dt, cfg.dt, with_norm,
-                                       G.partial + (size_t)slot * B, nullptr);
+        const FomLaunch L = fom_launch(d, d.st[c][0], d.st[c][1], d.st[1 - c][0], d.st[1 - c][1], cfg.dt, cfg.dt,
+                                       0.5 * cfg.dt, cfg.dt, with_norm, G.partial + (size_t)slot * B, nullptr);
         if (g_prof) CK(cudaEventRecord(G.ev[2 * fom_k], st));
-        launch_fom_advance(L, d.stencil, d.tmap[c], st, &launches);
+        launch_fom_advance(L, d.stencil, &d.tmap[c], st, &launches);
         if (g_prof) CK(cudaEventRecord(G.ev[2 * fom_k + 1], st));
         g_k1_bytes += (32.0 + (with_norm ? 8.0 : 0.0)) * 3.0 * (double)d.n_nodes;
         ++g_k1_launches;
@@ -735,7 +741,7 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
   s.mass_e = d->rho * g.h[0] * g.h[1] * g.h[2] / 8.0;
   for (int q = 0; q < 8; ++q)
     s.inv_mass[q] = 1.0 / (s.mass_e * ((q & 1) ? 2.0 : 1.0) * ((q & 2) ? 2.0 : 1.0) * ((q & 4) ? 2.0 : 1.0));
-  for (int f = 0; f < 6; ++f) s.faces.s[f] = nullptr;
+  std::memset(&s.faces, 0, sizeof s.faces);
   if (s.kind == OSAM_FOM) {
     if (d->batch > 1) return fail(OSAM_EINVAL, "a FOM subdomain has batch 1");
     s.batch = 1;
@@ -771,6 +777,7 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
     int rc = upload(&s.coef, tab, s.stream);
     if (rc != OSAM_OK) return rc;
     rc = dalloc(&s.scratch_a, (size_t)3 * g.npad);
+    if (rc == OSAM_OK) rc = dalloc(&s.scratch_v, (size_t)3 * g.npad);
     if (rc != OSAM_OK) {
       osam_destroy(h.release());
       return rc;
@@ -785,7 +792,7 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
         CK(cudaMemsetAsync(s.st[b][q], 0, sizeof(double) * 3 * g.npad, s.stream));
       }
     for (int b = 0; b < 2; ++b) {
-      const int r = make_state_tmaps(g, s.st[b], s.tmap[b]);
+      const int r = make_field_tmap(g, s.st[b][0], &s.tmap[b]);
       if (r != 0) {
         osam_destroy(h.release());
         return fail(OSAM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", r);
@@ -836,7 +843,7 @@ int osam_set_ic(osam_subdomain* h, const double* u0, const double* v0) {
   if (s.kind == OSAM_FOM) {
     const int c = s.cur;
     launch_fom_pack(s.g, du, s.st[c][0], s.n_nodes, st);
-    launch_fom_pack(s.g, dv, s.st[c][1], s.n_nodes, st);  // w holds v until the first osam_step
+    launch_fom_pack(s.g, dv, s.st[c][1], s.n_nodes, st);  // RAW state (u, v) until the first osam_step
     s.w_dt = 0.0;
     CK(cudaStreamSynchronize(st));
     dfree(du);
@@ -914,16 +921,18 @@ static int get_field(const osam_subdomain* h, int which, double* out) {
   if (s.ic_pending) return fail(OSAM_EINVAL, "initial condition not processed yet: call osam_step first");
   cudaStream_t st = s.stream;
   if (s.kind == OSAM_FOM) {
-    const double* field = s.st[s.cur][0];
+    const double* field = s.st[s.w_dt == 0.0 ? s.cur : 1 - s.cur][0];  // u (R30)
     if (which != 0) {
       // a = -K u / m and v = w - w_dt/2 a by one force pass into the spare buffer (the committed
       // state is not modified).
       if (!s.bound) return fail(OSAM_EINVAL, "FOM state not bound: call osam_step first");
       int launches = 0;
-      const FomLaunch L = fom_launch(s, s.cur, 0.0, -0.5 * s.w_dt, 0.0, 0.0, 0, s.scratch_partial, s.scratch_a);
-      launch_fom_advance(L, s.stencil, s.tmap[s.cur], st, &launches);
+      const int xb = s.w_dt == 0.0 ? s.cur : 1 - s.cur;  // buffer holding u
+      const FomLaunch L = fom_launch(s, s.st[xb][0], s.st[s.cur][1], nullptr, s.scratch_v, -0.5 * s.w_dt, 0.0, 0.0,
+                                     0.0, 0, s.scratch_partial, s.scratch_a);
+      launch_fom_advance(L, s.stencil, &s.tmap[xb], st, &launches);
       g_launches += launches;
-      field = which == 1 ? s.st[1 - s.cur][1] : s.scratch_a;
+      field = which == 1 ? s.scratch_v : s.scratch_a;
     }
     double* tmp = nullptr;
     TRY(dalloc(&tmp, (size_t)3 * s.n_nodes));
@@ -970,6 +979,7 @@ void osam_destroy(osam_subdomain* h) {
   for (int b = 0; b < 2; ++b)
     for (int q = 0; q < 2; ++q) dfree(s.st[b][q]);
   dfree(s.scratch_a);
+  dfree(s.scratch_v);
   dfree(s.coef);
   dfree(s.ic_u);
   dfree(s.ic_v);

@@ -30,8 +30,6 @@ struct Geom {
 struct Faces {
   unsigned char dir[6];  // Dirichlet component bitmask per face
   unsigned char sw[6];   // 1 if the face is a Schwarz face
-  int nface[6];          // nodes on the face
-  double* s[6];          // Schwarz values of the face, SoA [3][nface], in-face id a + nn[o0]*b
 };
 
 // 27 boundary classes x 27 neighbour offsets x 3x3 blocks of the merged hex8 stencil.
@@ -52,7 +50,8 @@ struct XferMap {
   int n = 0;             // destination nodes
   int* idx = nullptr;    // [n][8] source field indices (FOM: padded node id; ROM: compact lift id)
   double* xi = nullptr;  // [n][3] local coordinates in [0,1]
-  int* out = nullptr;    // [n][3] destination index (FOM: c*nface+f; ROM: Schwarz DOF id; -1 skip)
+  int* out = nullptr;    // [n][3] destination index (FOM: c*npad + padded node id in q; ROM: Schwarz DOF
+                         // id; -1 skip: Dirichlet component or a node owned by a lower Schwarz face)
 };
 
 struct Sub {
@@ -76,18 +75,22 @@ struct Sub {
   std::vector<int8_t> codes;  // host DOF codes (canonical DOF id 3p + c)
   std::vector<XferMap> maps;  // one per Schwarz face of this (destination) subdomain
 
-  // FOM device state: buffers [2] x {u, w}, each 3 * npad doubles; w = v + w_dt/2 a (DESIGN R30)
+  // FOM device state: buffers [2] x {q, w}, each 3 * npad doubles (R30).
+  //   STEP state (w_dt > 0): st[cur] = (q, w) with q = u + w_dt w (boundary values in q) and
+  //   w = v + w_dt/2 a; st[1-cur][0] = u of the checkpoint (exactly).
+  //   RAW state (w_dt == 0, after osam_set_ic): st[cur] = (u, v).
   int cur = 0;
   double* st[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-  double w_dt = 0.0;  // the step the stored w refers to (0: w holds v)
+  double w_dt = 0.0;
   Faces faces;
   double* coef = nullptr;  // device [NCLASS][27][9]
   InteriorStencil stencil;
-  CUtensorMap tmap[2][2];  // TMA descriptors of st[b][0..1] (4D: x, y, z, component)
-  double mass_e = 0.0;     // rho * V_e / 8
-  double inv_mass[8];      // 1 / (mass_e * prod_d (2 if interior on axis d else 1)), index cx + 2 cy + 4 cz (1 = interior)
-  double* scratch_a = nullptr;        // 3 * npad: acceleration for osam_get_accel
-  double2* scratch_partial = nullptr; // partial slots of non-sweep K1 launches
+  CUtensorMap tmap[2];  // TMA descriptors of st[b][0] (4D: x, y, z, component)
+  double mass_e = 0.0;  // rho * V_e / 8
+  double inv_mass[8];   // 1 / (mass_e * prod_d (2 if interior on axis d else 1)), index cx + 2 cy + 4 cz
+  double* scratch_v = nullptr;         // 3 * npad: v for osam_get_state
+  double* scratch_a = nullptr;         // 3 * npad: acceleration for osam_get_accel
+  double2* scratch_partial = nullptr;  // partial slots of non-sweep K1 launches
 
   // ROM device data
   double *Phi = nullptr, *Phi_s = nullptr, *Kbar = nullptr, *Bbar = nullptr, *e = nullptr;
@@ -114,13 +117,14 @@ struct Sub {
 struct FomLaunch {
   Geom g;
   Faces f;
-  const double *u0, *w0;  // checkpoint (u, w)
-  double *u1, *w1;        // working iterate (w1 is also the previous iterate for the norm)
-  double* a_out;          // optional acceleration output (diagnostics), may be null
-  double dtp;             // predictor: u* = u0 + dtp w0
-  double cw;              // w1 = w0 + cw a
-  double cv;              // v = w0 + cv a (norm denominator)
-  double dt;              // step in the convergence norm
+  const double* x;   // staged field X (stencil input; TMA descriptor passed separately)
+  const double* w0;  // per-node field W
+  double* q_out;     // Q' = X + cq W' (may be null: not written)
+  double* w_out;     // W' = W + cw a (also read first: previous iterate for the norm)
+  double* a_out;     // optional acceleration output (diagnostics), may be null
+  double cw, cq;
+  double cv;  // v = W + cv a (norm denominator)
+  double dt;  // step in the convergence norm
   double inv_mass[8];
   const double* coef;  // [NCLASS][27][9]
   int with_norm;       // 1 from Schwarz iteration 2 on
@@ -130,17 +134,15 @@ struct FomLaunch {
 int fom_partial_slots(const Geom& g, const Faces& f);
 void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUtensorMap* tm, cudaStream_t s,
                         int* launches);
-int make_state_tmaps(const Geom& g, double* const arrays[2], CUtensorMap out[2]);
+int make_field_tmap(const Geom& g, double* array, CUtensorMap* out);
 
 void launch_transfer(const XferMap& m, const double* src, long long src_cstride, long long src_bstride,
                      double* dst, long long dst_bstride, int batch, const int* active, cudaStream_t s);
-void launch_fom_face_gather(const Geom& g, const Faces& f, const double* u, cudaStream_t s);
 void launch_fom_pack(const Geom& g, const double* src_unpadded, double* dst_padded, long long n_nodes,
                      cudaStream_t s);
 void launch_fom_unpack(const Geom& g, const double* src_padded, double* dst_unpadded, long long n_nodes,
                        cudaStream_t s);
-void launch_fom_zero_constrained(const Geom& g, const Faces& f, double* u, double* w, int zero_u_dirichlet,
-                                 cudaStream_t s);
+void launch_fom_zero_constrained(const Geom& g, const Faces& f, double* u, double* w, cudaStream_t s);
 
 struct RomLaunch {
   int r, r_b, B;
