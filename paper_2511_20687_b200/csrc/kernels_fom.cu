@@ -41,7 +41,10 @@ constexpr int TX = 32;
 constexpr int TY = 8;
 constexpr int NT = TX * TY;
 constexpr int NWARP = NT / 32;
-constexpr int ZC = 16;  // target z-planes per block (balanced split)
+#ifndef OSAM_ZC
+#define OSAM_ZC 16
+#endif
+constexpr int ZC = OSAM_ZC;  // target z-planes per block (balanced split)
 constexpr int XF_BLOCK = 128;
 
 __device__ __forceinline__ long long gidx(const Geom& g, int i, int j, int k) {
@@ -142,10 +145,13 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
 constexpr int PX = TX + 4;
 constexpr int PY = TY + 2;
 constexpr int PLANE = PX * PY;                             // positions per staged plane
-constexpr int NSTAGE = 4;                                  // ring: 2 planes in flight, current, previous
-constexpr int ARR_BYTES = 3 * PLANE * 8;                   // X (x,y,z comps) of one plane
+constexpr int NSTAGE = 5;                                  // ring: 3 planes in flight, current, previous
+constexpr int ARR_BYTES = 3 * PLANE * 8;                   // X (x,y,z comps) of one plane, with halo
 constexpr int ARR_STRIDE = (ARR_BYTES + 127) / 128 * 128;  // 128-B aligned TMA destinations
-constexpr int SMEM_TILED = NSTAGE * ARR_STRIDE + 2 * NSTAGE * 8;
+constexpr int WPL = TX * TY;                               // tile positions of W (no halo)
+constexpr int W_BYTES = 3 * WPL * 8;
+constexpr int STAGE_BYTES = ARR_STRIDE + 2 * W_BYTES;      // X, W, W'_prev
+constexpr int SMEM_TILED = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8;
 
 // ---- interior rows: parity-reduced stencil ---------------------------------------------
 // On a uniform box every interior block K_cd(ox, oy, oz) is even or odd in ox and in oy (the 1D
@@ -291,19 +297,36 @@ __device__ __noinline__ Contrib3 plane_slow(const double* xs, int base, int cy, 
 
 // Per-thread constants of the tiled kernel.
 struct Tile {
-  int qo, base;
+  int qo, base, wo;
   int x0, y0, i, j;
   bool active, xface, writer, lead;
   int cy, kbeg, kend, nplanes;
   long long id0;
 };
 
-__device__ __forceinline__ void issue_plane(const Tile& T, int it, double* ring, unsigned long long* full,
-                                            const CUtensorMap* tx) {
-  const int s = it & (NSTAGE - 1);
-  mbar_expect_tx(&full[s], ARR_BYTES);
-  tma_load_4d(ring + (size_t)s * (ARR_STRIDE / 8), tx, T.x0, T.y0, T.kbeg - 1 + it, 0, &full[s]);
+struct Maps {
+  const CUtensorMap *x, *w, *wp;
+};
+
+// stage layout: X plane (halo box) | W plane (tile box) | W'_prev plane (tile box)
+__device__ __forceinline__ void issue_plane(const FomLaunch& L, const Tile& T, int it, int s, unsigned char* ring,
+                                            unsigned long long* full, const Maps& M) {
+  unsigned char* st = ring + (size_t)s * STAGE_BYTES;
+  const int m = T.kbeg - 1 + it;
+  mbar_expect_tx(&full[s], ARR_BYTES + (L.with_norm ? 2 : 1) * W_BYTES);
+  tma_load_4d(st, M.x, T.x0, T.y0, m, 0, &full[s]);
+  tma_load_4d(st + ARR_STRIDE, M.w, T.x0 + 2, T.y0 + 1, m, 0, &full[s]);
+  if (L.with_norm) tma_load_4d(st + ARR_STRIDE + W_BYTES, M.wp, T.x0 + 2, T.y0 + 1, m, 0, &full[s]);
 }
+
+// Ring bookkeeping (stage index of plane it, and the phase parity of its use).
+struct Ring {
+  int s;          // stage of the current plane
+  int sp;         // stage of the previous plane
+  int sn;         // stage the producer fills next (plane it + NSTAGE - 2)
+  unsigned fph;   // bit s: parity of the next completion of full[s]
+  unsigned eph;   // bit s: parity of the next completion of empty[s]
+};
 
 // One staged plane (iteration it, staged plane m = kbeg - 1 + it).  Accumulator slots rotate by
 // role: A = acc[SA] (node plane m+1), B = acc[SB] (plane m), C = acc[SC] (plane m-1, finished
@@ -311,33 +334,25 @@ __device__ __forceinline__ void issue_plane(const Tile& T, int it, double* ring,
 // are accumulated too (and never used): that keeps every iteration identical.
 template <int SA, int SB, int SC>
 __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStencil& S, const Tile& T, int it,
-                                        double (&acc)[3][3], double& num, double& den, double* ring,
-                                        unsigned long long* full, unsigned long long* empty, const CUtensorMap* tx) {
+                                        double (&acc)[3][3], double& num, double& den, unsigned char* ring,
+                                        unsigned long long* full, unsigned long long* empty, const Maps& M, Ring& R) {
   const Geom& g = L.g;
   const int nz = g.nn[2] - 1;
   const long long np = g.npad;
   const int m = T.kbeg - 1 + it;
   const int kf = m - 1;
   const bool fin = T.writer && kf >= T.kbeg && kf <= T.kend;
-  const long long id = T.id0 + (long long)kf * g.plane;
-  // own W and the previous iterate's W' of node plane kf: issued before the wait
-  double wo[3] = {0.0, 0.0, 0.0}, qw[3] = {0.0, 0.0, 0.0};
-  if (fin && !T.xface) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) wo[c] = L.w0[c * np + id];
-    if (L.with_norm) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) qw[c] = L.w_out[c * np + id];
+  // producer: fill plane it + NSTAGE - 2 into the stage released by plane it - 2
+  if (T.lead && it + NSTAGE - 2 < T.nplanes) {
+    if (it >= 2) {
+      mbar_wait(&empty[R.sn], (R.eph >> R.sn) & 1u);
+      R.eph ^= 1u << R.sn;
     }
+    issue_plane(L, T, it + NSTAGE - 2, R.sn, ring, full, M);
   }
-  // producer: refill the stage of plane it+2 once every warp has released its previous plane it-2
-  if (T.lead && it + 2 < T.nplanes) {
-    if (it >= 2) mbar_wait(&empty[(it + 2) & (NSTAGE - 1)], (unsigned)(((it - 2) >> 2) & 1));
-    issue_plane(T, it + 2, ring, full, tx);
-  }
-  const int s = it & (NSTAGE - 1);
-  mbar_wait(&full[s], (unsigned)((it >> 2) & 1));
-  const double* xs = ring + (size_t)s * (ARR_STRIDE / 8);
+  mbar_wait(&full[R.s], (R.fph >> R.s) & 1u);
+  R.fph ^= 1u << R.s;
+  const double* xs = reinterpret_cast<const double*>(ring + (size_t)R.s * STAGE_BYTES);
   if (T.active) {
     double* A = acc[SA];
     double* B = acc[SB];
@@ -355,8 +370,12 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
       }
     }
     if (fin) {
-      // own X of plane kf, staged in iteration it-1 (stage released at the end of this iteration)
-      const double* xo = ring + (size_t)((it - 1) & (NSTAGE - 1)) * (ARR_STRIDE / 8) + T.qo;
+      // own X, W, W'_prev of plane kf, staged in iteration it-1 (released at the end of this one)
+      const unsigned char* sp = ring + (size_t)R.sp * STAGE_BYTES;
+      const double* xo = reinterpret_cast<const double*>(sp) + T.qo;
+      const double* wo = reinterpret_cast<const double*>(sp + ARR_STRIDE) + T.wo;
+      const double* qw = reinterpret_cast<const double*>(sp + ARR_STRIDE + W_BYTES) + T.wo;
+      const long long id = T.id0 + (long long)kf * g.plane;
       const int cz = axis_class(kf, g.nn[2]);
       if (T.xface) {  // fully constrained x-face node: Q' = X (prescribed), W' = a = 0
 #pragma unroll
@@ -369,12 +388,13 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
         const double inv_m = L.inv_mass[7];
         double* qo = L.q_out + id;
         double* wp = L.w_out + id;
-        double an[3], wn[3], x[3];
+        double an[3], wn[3], x[3], w0[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           x[c] = xo[c * PLANE];
+          w0[c] = wo[c * WPL];
           an[c] = -C[c] * inv_m;
-          wn[c] = fma(L.cw, an[c], wo[c]);
+          wn[c] = fma(L.cw, an[c], w0[c]);
           qo[c * np] = fma(L.cq, wn[c], x[c]);
           wp[c * np] = wn[c];
         }
@@ -382,8 +402,8 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
           const double hdt = 0.5 * L.dt;
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            const double d = hdt * (wn[c] - qw[c]);
-            const double w = fma(L.dt, fma(L.cv, an[c], wo[c]), x[c]);
+            const double d = hdt * (wn[c] - qw[c * WPL]);
+            const double w = fma(L.dt, fma(L.cv, an[c], w0[c]), x[c]);
             num = fma(d, d, num);
             den = fma(w, w, den);
           }
@@ -396,12 +416,13 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
           const double x = xo[c * PLANE];
           double an = 0.0, wn = 0.0, qn = x;
           if ((fm >> c) & 1) {
+            const double w0 = wo[c * WPL];
             an = -C[c] * inv_m;
-            wn = fma(L.cw, an, wo[c]);
+            wn = fma(L.cw, an, w0);
             qn = fma(L.cq, wn, x);
             if (L.with_norm) {
-              const double d = 0.5 * L.dt * (wn - qw[c]);
-              const double w = fma(L.dt, fma(L.cv, an, wo[c]), x);
+              const double d = 0.5 * L.dt * (wn - qw[c * WPL]);
+              const double w = fma(L.dt, fma(L.cv, an, w0), x);
               num = fma(d, d, num);
               den = fma(w, w, den);
             }
@@ -415,20 +436,25 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
   }
   // this warp is done with plane it-1 (own values above; stencil in the previous iteration)
   __syncwarp();
-  if (it >= 1 && (threadIdx.x & 31) == 0) mbar_arrive(&empty[(it - 1) & (NSTAGE - 1)]);
+  if (it >= 1 && (threadIdx.x & 31) == 0) mbar_arrive(&empty[R.sp]);
 #pragma unroll
   for (int c = 0; c < 3; ++c) acc[SC][c] = 0.0;
+  R.sp = R.s;
+  R.s = R.s + 1 == NSTAGE ? 0 : R.s + 1;
+  R.sn = R.sn + 1 == NSTAGE ? 0 : R.sn + 1;
 }
 
 __global__ void __launch_bounds__(NT, 2)
     fom_tiled_kernel(const __grid_constant__ FomLaunch L, const __grid_constant__ InteriorStencil S,
-                     const __grid_constant__ CUtensorMap tmx) {
+                     const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
+                     const __grid_constant__ CUtensorMap tmwp) {
   extern __shared__ __align__(128) unsigned char smem[];
-  double* ring = reinterpret_cast<double*>(smem);
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + NSTAGE * ARR_STRIDE);
+  unsigned char* ring = smem;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + NSTAGE * STAGE_BYTES);
   unsigned long long* empty = full + NSTAGE;
   const Geom& g = L.g;
   const int nx = g.nn[0] - 1, ny = g.nn[1] - 1;
+  const Maps M{&tmx, &tmw, &tmwp};
   Tile T;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int t = ty * TX + tx;
@@ -448,6 +474,7 @@ __global__ void __launch_bounds__(NT, 2)
   T.nplanes = T.kend - T.kbeg + 3;
   T.qo = (ty + 1) * PX + (tx + 2);
   T.base = ty * PX + tx + 1;
+  T.wo = t;
   T.id0 = T.i + (long long)g.px * T.j;
 
   if (t == 0) {
@@ -458,19 +485,19 @@ __global__ void __launch_bounds__(NT, 2)
     mbar_fence_init();
   }
   __syncthreads();
+  Ring R{0, NSTAGE - 1, NSTAGE - 2, 0u, 0u};
   if (T.lead) {
-    issue_plane(T, 0, ring, full, &tmx);
-    if (T.nplanes > 1) issue_plane(T, 1, ring, full, &tmx);
+    for (int p = 0; p < NSTAGE - 2 && p < T.nplanes; ++p) issue_plane(L, T, p, p, ring, full, M);
   }
 
   double acc[3][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
   double num = 0.0, den = 0.0;
   for (int it = 0; it < T.nplanes;) {  // unrolled by the period 3 of the slot rotation
-    k1_iter<0, 1, 2>(L, S, T, it, acc, num, den, ring, full, empty, &tmx);
+    k1_iter<0, 1, 2>(L, S, T, it, acc, num, den, ring, full, empty, M, R);
     if (++it >= T.nplanes) break;
-    k1_iter<2, 0, 1>(L, S, T, it, acc, num, den, ring, full, empty, &tmx);
+    k1_iter<2, 0, 1>(L, S, T, it, acc, num, den, ring, full, empty, M, R);
     if (++it >= T.nplanes) break;
-    k1_iter<1, 2, 0>(L, S, T, it, acc, num, den, ring, full, empty, &tmx);
+    k1_iter<1, 2, 0>(L, S, T, it, acc, num, den, ring, full, empty, M, R);
     ++it;
   }
   const int slot = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
@@ -639,8 +666,8 @@ int fom_partial_slots(const Geom& g, const Faces& f) {
   return (int)((long long)gi.x * gi.y * gi.z + xface_blocks(g, f));
 }
 
-void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUtensorMap* tm, cudaStream_t s,
-                        int* launches) {
+void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUtensorMap* tmx,
+                        const CUtensorMap* tmw, const CUtensorMap* tmwp, cudaStream_t s, int* launches) {
   const dim3 gi = tiled_grid(L.g);
   const int n_int = gi.x * gi.y * gi.z;
   static bool attr_set = false;
@@ -648,7 +675,7 @@ void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUt
     cudaFuncSetAttribute(fom_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TILED);
     attr_set = true;
   }
-  fom_tiled_kernel<<<gi, dim3(TX, TY), SMEM_TILED, s>>>(L, st, *tm);
+  fom_tiled_kernel<<<gi, dim3(TX, TY), SMEM_TILED, s>>>(L, st, *tmx, *tmw, *tmwp);
   debug_check("fom_tiled_kernel", s);
   ++*launches;
   const unsigned xb = xface_blocks(L.g, L.f);
@@ -659,7 +686,9 @@ void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUt
   }
 }
 
-int make_field_tmap(const Geom& g, double* array, CUtensorMap* out) {
+// 4D (x, y, z, component) descriptor of a padded SoA field; halo = true: the X box (tile plus a
+// 2/1-node halo in x/y), false: the W box (tile only).
+int make_field_tmap(const Geom& g, double* array, bool halo, CUtensorMap* out) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -670,7 +699,7 @@ int make_field_tmap(const Geom& g, double* array, CUtensorMap* out) {
   }
   const cuuint64_t dims[4] = {(cuuint64_t)g.px, (cuuint64_t)g.nn[1], (cuuint64_t)g.nn[2], 3};
   const cuuint64_t strides[3] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.plane * 8, (cuuint64_t)g.npad * 8};
-  const cuuint32_t box[4] = {PX, PY, 1, 3};
+  const cuuint32_t box[4] = {halo ? (cuuint32_t)PX : (cuuint32_t)TX, halo ? (cuuint32_t)PY : (cuuint32_t)TY, 1, 3};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   const CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, array, dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

@@ -541,12 +541,12 @@ int fom_set_step(Sub& d, double dt, int* launches) {
   if (d.w_dt == 0.0) {
     const FomLaunch L = fom_launch(d, d.st[c][0], d.st[c][1], d.st[1 - c][0], d.st[1 - c][1], 0.5 * dt, dt, 0.0,
                                    dt, 0, d.scratch_partial, nullptr);
-    launch_fom_advance(L, d.stencil, &d.tmap[c], d.stream, launches);
+    launch_fom_advance(L, d.stencil, &d.tmap[c], &d.tmapw[c], &d.tmapw[1 - c], d.stream, launches);
     d.cur = 1 - c;
   } else {
     const FomLaunch L = fom_launch(d, d.st[1 - c][0], d.st[c][1], d.st[c][0], d.st[c][1], 0.5 * (dt - d.w_dt), dt,
                                    0.0, dt, 0, d.scratch_partial, nullptr);
-    launch_fom_advance(L, d.stencil, &d.tmap[1 - c], d.stream, launches);
+    launch_fom_advance(L, d.stencil, &d.tmap[1 - c], &d.tmapw[c], &d.tmapw[c], d.stream, launches);
   }
   d.w_dt = dt;
   return OSAM_OK;
@@ -615,7 +615,7 @@ int controller_step(Group& G, const osam_schwarz_cfg& cfg, int32_t* iters) {
         const FomLaunch L = fom_launch(d, d.st[c][0], d.st[c][1], d.st[1 - c][0], d.st[1 - c][1], cfg.dt, cfg.dt,
                                        0.5 * cfg.dt, cfg.dt, with_norm, G.partial + (size_t)slot * B, nullptr);
         if (g_prof) CK(cudaEventRecord(G.ev[2 * fom_k], st));
-        launch_fom_advance(L, d.stencil, &d.tmap[c], st, &launches);
+        launch_fom_advance(L, d.stencil, &d.tmap[c], &d.tmapw[c], &d.tmapw[1 - c], st, &launches);
         if (g_prof) CK(cudaEventRecord(G.ev[2 * fom_k + 1], st));
         g_k1_bytes += (32.0 + (with_norm ? 8.0 : 0.0)) * 3.0 * (double)d.n_nodes;
         ++g_k1_launches;
@@ -792,7 +792,8 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
         CK(cudaMemsetAsync(s.st[b][q], 0, sizeof(double) * 3 * g.npad, s.stream));
       }
     for (int b = 0; b < 2; ++b) {
-      const int r = make_field_tmap(g, s.st[b][0], &s.tmap[b]);
+      int r = make_field_tmap(g, s.st[b][0], true, &s.tmap[b]);
+      if (r == 0) r = make_field_tmap(g, s.st[b][1], false, &s.tmapw[b]);
       if (r != 0) {
         osam_destroy(h.release());
         return fail(OSAM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", r);
@@ -930,7 +931,7 @@ static int get_field(const osam_subdomain* h, int which, double* out) {
       const int xb = s.w_dt == 0.0 ? s.cur : 1 - s.cur;  // buffer holding u
       const FomLaunch L = fom_launch(s, s.st[xb][0], s.st[s.cur][1], nullptr, s.scratch_v, -0.5 * s.w_dt, 0.0, 0.0,
                                      0.0, 0, s.scratch_partial, s.scratch_a);
-      launch_fom_advance(L, s.stencil, &s.tmap[xb], st, &launches);
+      launch_fom_advance(L, s.stencil, &s.tmap[xb], &s.tmapw[s.cur], &s.tmapw[s.cur], st, &launches);
       g_launches += launches;
       field = which == 1 ? s.scratch_v : s.scratch_a;
     }

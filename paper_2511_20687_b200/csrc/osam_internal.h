@@ -85,7 +85,8 @@ struct Sub {
   Faces faces;
   double* coef = nullptr;  // device [NCLASS][27][9]
   InteriorStencil stencil;
-  CUtensorMap tmap[2];  // TMA descriptors of st[b][0] (4D: x, y, z, component)
+  CUtensorMap tmap[2];   // TMA descriptors of st[b][0] with the halo box (4D: x, y, z, component)
+  CUtensorMap tmapw[2];  // TMA descriptors of st[b][1] with the tile box
   double mass_e = 0.0;  // rho * V_e / 8
   double inv_mass[8];   // 1 / (mass_e * prod_d (2 if interior on axis d else 1)), index cx + 2 cy + 4 cz
   double* scratch_v = nullptr;         // 3 * npad: v for osam_get_state
@@ -132,9 +133,9 @@ struct FomLaunch {
 };
 // Number of partial slots a K1 launch writes (tiled blocks + x-face blocks).
 int fom_partial_slots(const Geom& g, const Faces& f);
-void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUtensorMap* tm, cudaStream_t s,
-                        int* launches);
-int make_field_tmap(const Geom& g, double* array, CUtensorMap* out);
+void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUtensorMap* tmx,
+                        const CUtensorMap* tmw, const CUtensorMap* tmwp, cudaStream_t s, int* launches);
+int make_field_tmap(const Geom& g, double* array, bool halo, CUtensorMap* out);
 
 void launch_transfer(const XferMap& m, const double* src, long long src_cstride, long long src_bstride,
                      double* dst, long long dst_bstride, int batch, const int* active, cudaStream_t s);

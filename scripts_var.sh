@@ -1,0 +1,3 @@
+#!/bin/bash
+# time variant builds var/*.so with bench.py (no ncu)
+for v in var/*.so; do echo "== $v"; OSAM_LIB=$v timeout 300 python bench.py --steps 30 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1; done > gpurun_out/var.log 2>&1
