@@ -31,6 +31,8 @@
 //     the face is fully constrained (no force needed).
 //   * the x-face kernel covers x-faces with free DOFs (a node per thread, class table).
 // No atomics; every sum has a fixed order, so results are bitwise repeatable.
+#include <algorithm>
+
 #include "osam_internal.h"
 
 namespace osam {
@@ -41,8 +43,11 @@ constexpr int TX = 32;
 constexpr int TY = 8;
 constexpr int NT = TX * TY;
 constexpr int NWARP = NT / 32;
+#ifndef OSAM_EO
+#define OSAM_EO 0
+#endif
 #ifndef OSAM_ZC
-#define OSAM_ZC 16
+#define OSAM_ZC 8
 #endif
 constexpr int ZC = OSAM_ZC;  // target z-planes per block (balanced split)
 constexpr int XF_BLOCK = 128;
@@ -121,7 +126,11 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
       "{\n"
       ".reg .pred P1;\n"
       "LAB_WAIT:\n"
+#ifdef OSAM_HINT
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, " OSAM_HINT ";\n"
+#else
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+#endif
       "@P1 bra DONE;\n"
       "bra LAB_WAIT;\n"
       "DONE:\n"
@@ -139,6 +148,14 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// L2 prefetch of a tensor box (no shared memory, no completion tracking)
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int x, int y, int z, int c) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<unsigned long long>(map)),
+               "r"(x), "r"(y), "r"(z), "r"(c)
+               : "memory");
+}
+
 // Staged x-range [x0, x0 + PX) with x0 = 32 bx - 2: the TMA box must start on a 16-byte
 // boundary in the innermost dimension (an odd fp64 start coordinate raises an illegal
 // instruction on sm_100a), so the left halo is two columns wide (the first is unused).
@@ -152,6 +169,10 @@ constexpr int WPL = TX * TY;                               // tile positions of 
 constexpr int W_BYTES = 3 * WPL * 8;
 constexpr int STAGE_BYTES = ARR_STRIDE + 2 * W_BYTES;      // X, W, W'_prev
 constexpr int SMEM_TILED = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8;
+#ifndef OSAM_PF
+#define OSAM_PF 3
+#endif
+constexpr int PF_AHEAD = OSAM_PF;  // planes beyond the ring that are prefetched into L2
 
 // ---- interior rows: parity-reduced stencil ---------------------------------------------
 // On a uniform box every interior block K_cd(ox, oy, oz) is even or odd in ox and in oy (the 1D
@@ -209,25 +230,48 @@ __device__ __forceinline__ void contrib(double& acc, const double P[9], const In
   }
 }
 
+// z-even / z-odd part of the oz = -1 slice for block (c, d): A (oz = -1) gets even + odd, C (oz = +1)
+// gets even - odd.
+template <int c, int d>
+__device__ __forceinline__ void contrib_eo(double& ev, double& od, const double P[9], const InteriorStencil& S) {
+  constexpr bool zodd = (c == 2) != (d == 2);
+  if (zodd)
+    contrib<0, false, c, d>(od, P, S);
+  else
+    contrib<0, false, c, d>(ev, P, S);
+}
+
 template <int d, bool DA, bool DB, bool DC>
 __device__ __forceinline__ void fast_comp(double A[3], double B[3], double C[3], const double* xs, int base,
                                           const InteriorStencil& S) {
   double P[9];
   combos(xs + d * PLANE + base, P);
-  if (DA) {
-    contrib<0, false, 0, d>(A[0], P, S);
-    contrib<0, false, 1, d>(A[1], P, S);
-    contrib<0, false, 2, d>(A[2], P, S);
+  if (OSAM_EO && DA && DC) {
+    double ev[3] = {0.0, 0.0, 0.0}, od[3] = {0.0, 0.0, 0.0};
+    contrib_eo<0, d>(ev[0], od[0], P, S);
+    contrib_eo<1, d>(ev[1], od[1], P, S);
+    contrib_eo<2, d>(ev[2], od[2], P, S);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      A[c] += ev[c] + od[c];
+      C[c] += ev[c] - od[c];
+    }
+  } else {
+    if (DA) {
+      contrib<0, false, 0, d>(A[0], P, S);
+      contrib<0, false, 1, d>(A[1], P, S);
+      contrib<0, false, 2, d>(A[2], P, S);
+    }
+    if (DC) {
+      contrib<0, true, 0, d>(C[0], P, S);
+      contrib<0, true, 1, d>(C[1], P, S);
+      contrib<0, true, 2, d>(C[2], P, S);
+    }
   }
   if (DB) {
     contrib<1, false, 0, d>(B[0], P, S);
     contrib<1, false, 1, d>(B[1], P, S);
     contrib<1, false, 2, d>(B[2], P, S);
-  }
-  if (DC) {
-    contrib<0, true, 0, d>(C[0], P, S);
-    contrib<0, true, 1, d>(C[1], P, S);
-    contrib<0, true, 2, d>(C[2], P, S);
   }
 }
 
@@ -241,65 +285,91 @@ __device__ __forceinline__ void plane_fast(double A[3], double B[3], double C[3]
   fast_comp<2, DA, DB, DC>(A, B, C, xs, base, S);
 }
 
-// Face rows / face planes: full 3x3 blocks from the class table (L1 broadcast).
-template <int OZ>
-__device__ __forceinline__ void plane_class(double acc[3], const double* xs, int base,
-                                            const double* __restrict__ cls_coef) {
-#pragma unroll
-  for (int oy = 0; oy < 3; ++oy) {
-#pragma unroll
-    for (int ox = 0; ox < 3; ++ox) {
-      const int q = base + oy * PX + ox;
-      const double w[3] = {xs[q], xs[PLANE + q], xs[2 * PLANE + q]};
-      const double* cb = cls_coef + (ox + 3 * (oy + 3 * OZ)) * 9;
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) acc[c] = fma(__ldg(cb + c * 3 + d), w[d], acc[c]);
-    }
-  }
-}
-
-template <int OZ>
-__device__ __forceinline__ void target_any(double acc[3], const double* xs, int base, int cy, int cz,
-                                           const InteriorStencil& S, const double* coef) {
-  if (cy == 1 && cz == 1) {
-    double d0[3] = {0.0, 0.0, 0.0}, d1[3] = {0.0, 0.0, 0.0};
-    if (OZ == 0) plane_fast<true, false, false>(acc, d0, d1, xs, base, S);
-    if (OZ == 1) plane_fast<false, true, false>(d0, acc, d1, xs, base, S);
-    if (OZ == 2) plane_fast<false, false, true>(d0, d1, acc, xs, base, S);
-  } else {
-    plane_class<OZ>(acc, xs, base, coef + (size_t)(1 + 3 * (cy + 3 * cz)) * 27 * 9);
-  }
-}
-
-// Face rows / face planes (rare): the three targets' contributions of one staged plane, out of
-// line to keep the hot loop small.
+// Face rows / face planes (rare): "row form" of the stencil, valid for every (y, z) class because
+// the x-parity of each block holds for all lanes of the tiled kernel (x-face lanes never use the
+// force): sum_ox K(ox, oy) w(ox, oy) = K(0, oy) c_row + K(1, oy) e_row (x-even blocks) or
+// K(1, oy) o_row (x-odd blocks).  rowc holds {K(0, oy), K(1, oy)} per (cy, cz, slice, c, d, oy),
+// built and checked on the host; out of line to keep the hot loop small.
 struct Contrib3 {
   double v[9];
 };
 
 __device__ __noinline__ Contrib3 plane_slow(const double* xs, int base, int cy, int czA, int czB, int czC,
-                                             const InteriorStencil& S, const double* coef) {
-  Contrib3 r;
-  double A[3] = {0.0, 0.0, 0.0}, B[3] = {0.0, 0.0, 0.0}, C[3] = {0.0, 0.0, 0.0};
-  target_any<0>(A, xs, base, cy, czA, S, coef);
-  target_any<1>(B, xs, base, cy, czB, S, coef);
-  target_any<2>(C, xs, base, cy, czC, S, coef);
+                                             const double* __restrict__ rowc) {
+  const double* kt[3] = {rowc + ((cy * 3 + czA) * 3 + 0) * 54, rowc + ((cy * 3 + czB) * 3 + 1) * 54,
+                         rowc + ((cy * 3 + czC) * 3 + 2) * 54};
+  double acc[3][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    r.v[c] = A[c];
-    r.v[3 + c] = B[c];
-    r.v[6 + c] = C[c];
+  for (int d = 0; d < 3; ++d) {
+    const double* a = xs + d * PLANE + base;
+    double cr[3], er[3], orr[3];
+#pragma unroll
+    for (int oy = 0; oy < 3; ++oy) {
+      const double l = a[oy * PX], c = a[oy * PX + 1], r = a[oy * PX + 2];
+      cr[oy] = c;
+      er[oy] = l + r;
+      orr[oy] = r - l;
+    }
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const bool even = (c == 0) == (d == 0);
+#pragma unroll
+        for (int oy = 0; oy < 3; ++oy) {
+          const double* k = kt[t] + ((c * 3 + d) * 3 + oy) * 2;
+          if (even) {
+            acc[t][c] = fma(__ldg(k), cr[oy], acc[t][c]);
+            acc[t][c] = fma(__ldg(k + 1), er[oy], acc[t][c]);
+          } else {
+            acc[t][c] = fma(__ldg(k + 1), orr[oy], acc[t][c]);
+          }
+        }
+      }
+    }
   }
+  Contrib3 r;
+#pragma unroll
+  for (int t = 0; t < 3; ++t)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) r.v[3 * t + c] = acc[t][c];
   return r;
 }
 
-// Per-thread constants of the tiled kernel.
+// Tiles of the persistent tiled kernel: TX x TY nodes in (x, y), a balanced chunk of ~ZC node
+// planes in z; tile t -> (bx, by, bz) with bx fastest.
+struct TileGrid {
+  int tx, ty, tz;
+  __device__ __forceinline__ int count() const { return tx * ty * tz; }
+};
+
+__device__ __forceinline__ TileGrid tile_grid(const Geom& g) {
+  return TileGrid{(g.nn[0] + TX - 1) / TX, (g.nn[1] + TY - 1) / TY, (g.nn[2] + ZC - 1) / ZC};
+}
+
+// Geometry of one tile as the producer and the consumers see it.
+struct TileGeo {
+  int x0, y0;        // node coordinates of staged position (0, 0)
+  int kbeg, kend;    // node planes finished by this tile
+  int nplanes;       // staged planes kbeg-1 .. kend+1
+};
+
+__device__ __forceinline__ TileGeo tile_geo(const Geom& g, const TileGrid& G, int t) {
+  const int bx = t % G.tx, by = (t / G.tx) % G.ty, bz = t / (G.tx * G.ty);
+  TileGeo o;
+  o.x0 = bx * TX - 2;
+  o.y0 = by * TY - 1;
+  o.kbeg = (int)((long long)bz * g.nn[2] / G.tz);
+  o.kend = (int)((long long)(bz + 1) * g.nn[2] / G.tz) - 1;
+  o.nplanes = o.kend - o.kbeg + 3;
+  return o;
+}
+
+// Per-thread constants of the current tile.
 struct Tile {
   int qo, base, wo;
-  int x0, y0, i, j;
-  bool active, xface, writer, lead;
+  int i, j;
+  bool active, xface, writer;
   int cy, kbeg, kend, nplanes;
   long long id0;
 };
@@ -309,46 +379,67 @@ struct Maps {
 };
 
 // stage layout: X plane (halo box) | W plane (tile box) | W'_prev plane (tile box)
-__device__ __forceinline__ void issue_plane(const FomLaunch& L, const Tile& T, int it, int s, unsigned char* ring,
+__device__ __forceinline__ void issue_plane(const FomLaunch& L, const TileGeo& P, int it, int s, unsigned char* ring,
                                             unsigned long long* full, const Maps& M) {
   unsigned char* st = ring + (size_t)s * STAGE_BYTES;
-  const int m = T.kbeg - 1 + it;
+  const int m = P.kbeg - 1 + it;
   mbar_expect_tx(&full[s], ARR_BYTES + (L.with_norm ? 2 : 1) * W_BYTES);
-  tma_load_4d(st, M.x, T.x0, T.y0, m, 0, &full[s]);
-  tma_load_4d(st + ARR_STRIDE, M.w, T.x0 + 2, T.y0 + 1, m, 0, &full[s]);
-  if (L.with_norm) tma_load_4d(st + ARR_STRIDE + W_BYTES, M.wp, T.x0 + 2, T.y0 + 1, m, 0, &full[s]);
+  tma_load_4d(st, M.x, P.x0, P.y0, m, 0, &full[s]);
+  tma_load_4d(st + ARR_STRIDE, M.w, P.x0 + 2, P.y0 + 1, m, 0, &full[s]);
+  if (L.with_norm) tma_load_4d(st + ARR_STRIDE + W_BYTES, M.wp, P.x0 + 2, P.y0 + 1, m, 0, &full[s]);
 }
 
-// Ring bookkeeping (stage index of plane it, and the phase parity of its use).
+// Ring bookkeeping over the CTA's whole plane stream (all its tiles, in order).
 struct Ring {
-  int s;          // stage of the current plane
-  int sp;         // stage of the previous plane
-  int sn;         // stage the producer fills next (plane it + NSTAGE - 2)
-  unsigned fph;   // bit s: parity of the next completion of full[s]
-  unsigned eph;   // bit s: parity of the next completion of empty[s]
+  int s;         // stage of the current plane
+  int sp;        // stage of the previous plane
+  int sn;        // stage the producer fills next
+  int gi;        // planes consumed so far (all tiles)
+  unsigned fph;  // bit s: parity of the next completion of full[s]
+  unsigned eph;  // bit s: parity of the next completion of empty[s]
 };
 
-// One staged plane (iteration it, staged plane m = kbeg - 1 + it).  Accumulator slots rotate by
-// role: A = acc[SA] (node plane m+1), B = acc[SB] (plane m), C = acc[SC] (plane m-1, finished
-// here if it lies in [kbeg, kend], then zeroed to become the next A).  Targets outside the chunk
-// are accumulated too (and never used): that keeps every iteration identical.
+// Producer cursor (thread 0 only): the next plane to load, possibly in a later tile of this CTA.
+struct Prod {
+  int t;      // tile (>= ntiles: done)
+  int it;     // plane within the tile
+  int issued; // planes issued so far (all tiles)
+  TileGeo P;
+};
+
+__device__ __forceinline__ void prod_issue(const FomLaunch& L, const TileGrid& G, Prod& pr, int s, unsigned char* ring,
+                                           unsigned long long* full, const Maps& M) {
+  issue_plane(L, pr.P, pr.it, s, ring, full, M);
+  ++pr.issued;
+  if (++pr.it == pr.P.nplanes) {
+    pr.it = 0;
+    pr.t += gridDim.x;
+    if (pr.t < G.count()) pr.P = tile_geo(L.g, G, pr.t);
+  }
+}
+
+// One staged plane (iteration it of the tile, staged plane m = kbeg - 1 + it).  Accumulator slots
+// rotate by role: A = acc[SA] (node plane m+1), B = acc[SB] (plane m), C = acc[SC] (plane m-1,
+// finished here if it lies in [kbeg, kend], then zeroed to become the next A).  Targets outside the
+// chunk are accumulated too (and never used): that keeps every iteration identical.
 template <int SA, int SB, int SC>
 __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStencil& S, const Tile& T, int it,
                                         double (&acc)[3][3], double& num, double& den, unsigned char* ring,
-                                        unsigned long long* full, unsigned long long* empty, const Maps& M, Ring& R) {
+                                        unsigned long long* full, unsigned long long* empty, const Maps& M, Ring& R,
+                                        Prod& pr, const TileGrid& G, bool lead) {
   const Geom& g = L.g;
   const int nz = g.nn[2] - 1;
   const long long np = g.npad;
   const int m = T.kbeg - 1 + it;
   const int kf = m - 1;
   const bool fin = T.writer && kf >= T.kbeg && kf <= T.kend;
-  // producer: fill plane it + NSTAGE - 2 into the stage released by plane it - 2
-  if (T.lead && it + NSTAGE - 2 < T.nplanes) {
-    if (it >= 2) {
+  // producer: fill the next plane of the stream into the stage released by plane gi - 2
+  if (lead && pr.t < G.count()) {
+    if (R.gi >= 2) {
       mbar_wait(&empty[R.sn], (R.eph >> R.sn) & 1u);
       R.eph ^= 1u << R.sn;
     }
-    issue_plane(L, T, it + NSTAGE - 2, R.sn, ring, full, M);
+    prod_issue(L, G, pr, R.sn, ring, full, M);
   }
   mbar_wait(&full[R.s], (R.fph >> R.s) & 1u);
   R.fph ^= 1u << R.s;
@@ -357,11 +448,15 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
     double* A = acc[SA];
     double* B = acc[SB];
     double* C = acc[SC];
+#ifdef OSAM_NOCOMPUTE
+    if (false) {
+#else
     if (T.cy == 1 && m >= 2 && m <= nz - 2) {
       plane_fast<true, true, true>(A, B, C, xs, T.base, S);
     } else {
+#endif
       const Contrib3 r = plane_slow(xs, T.base, T.cy, axis_class(m + 1, g.nn[2]), axis_class(m, g.nn[2]),
-                                    axis_class(kf, g.nn[2]), S, L.coef);
+                                    axis_class(kf, g.nn[2]), L.rowc);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         A[c] += r.v[c];
@@ -434,16 +529,18 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
       }
     }
   }
-  // this warp is done with plane it-1 (own values above; stencil in the previous iteration)
+  // this warp is done with the previous plane of the stream (own values above, stencil before)
   __syncwarp();
-  if (it >= 1 && (threadIdx.x & 31) == 0) mbar_arrive(&empty[R.sp]);
+  if (R.gi >= 1 && (threadIdx.x & 31) == 0) mbar_arrive(&empty[R.sp]);
 #pragma unroll
   for (int c = 0; c < 3; ++c) acc[SC][c] = 0.0;
+  ++R.gi;
   R.sp = R.s;
   R.s = R.s + 1 == NSTAGE ? 0 : R.s + 1;
-  R.sn = R.sn + 1 == NSTAGE ? 0 : R.sn + 1;
+  if (lead) R.sn = R.sn + 1 == NSTAGE ? 0 : R.sn + 1;
 }
 
+// Persistent: CTA b processes tiles b, b + gridDim.x, ... with one continuous TMA plane stream.
 __global__ void __launch_bounds__(NT, 2)
     fom_tiled_kernel(const __grid_constant__ FomLaunch L, const __grid_constant__ InteriorStencil S,
                      const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
@@ -455,29 +552,12 @@ __global__ void __launch_bounds__(NT, 2)
   const Geom& g = L.g;
   const int nx = g.nn[0] - 1, ny = g.nn[1] - 1;
   const Maps M{&tmx, &tmw, &tmwp};
-  Tile T;
+  const TileGrid G = tile_grid(g);
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int t = ty * TX + tx;
-  T.lead = t == 0;
-  T.x0 = blockIdx.x * TX - 2;  // node coordinates of staged position (0,0)
-  T.y0 = blockIdx.y * TY - 1;
-  T.i = T.x0 + 2 + tx;
-  T.j = T.y0 + 1 + ty;
-  T.active = (T.i <= nx) && (T.j <= ny);
-  T.xface = (T.i == 0) || (T.i == nx);
-  const int xsd = T.i == 0 ? 0 : 1;
-  const bool xf_full = T.xface && (L.f.dir[xsd] == 7 || L.f.sw[xsd]);
-  T.writer = T.active && (!T.xface || xf_full);
-  T.cy = axis_class(T.j, g.nn[1]);  // warp-uniform (a warp is one x-row)
-  T.kbeg = (int)((long long)blockIdx.z * g.nn[2] / gridDim.z);
-  T.kend = (int)((long long)(blockIdx.z + 1) * g.nn[2] / gridDim.z) - 1;
-  T.nplanes = T.kend - T.kbeg + 3;
-  T.qo = (ty + 1) * PX + (tx + 2);
-  T.base = ty * PX + tx + 1;
-  T.wo = t;
-  T.id0 = T.i + (long long)g.px * T.j;
+  const bool lead = t == 0;
 
-  if (t == 0) {
+  if (lead) {
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NWARP);
@@ -485,23 +565,48 @@ __global__ void __launch_bounds__(NT, 2)
     mbar_fence_init();
   }
   __syncthreads();
-  Ring R{0, NSTAGE - 1, NSTAGE - 2, 0u, 0u};
-  if (T.lead) {
-    for (int p = 0; p < NSTAGE - 2 && p < T.nplanes; ++p) issue_plane(L, T, p, p, ring, full, M);
+  Ring R{0, NSTAGE - 1, 0, 0, 0u, 0u};
+  Prod pr{(int)blockIdx.x, 0, 0, TileGeo{}};
+  if (lead) {
+    if (pr.t < G.count()) pr.P = tile_geo(g, G, pr.t);
+    for (int p = 0; p < NSTAGE - 2 && pr.t < G.count(); ++p) prod_issue(L, G, pr, p, ring, full, M);
+    R.sn = pr.issued % NSTAGE;
   }
 
   double acc[3][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
   double num = 0.0, den = 0.0;
-  for (int it = 0; it < T.nplanes;) {  // unrolled by the period 3 of the slot rotation
-    k1_iter<0, 1, 2>(L, S, T, it, acc, num, den, ring, full, empty, M, R);
-    if (++it >= T.nplanes) break;
-    k1_iter<2, 0, 1>(L, S, T, it, acc, num, den, ring, full, empty, M, R);
-    if (++it >= T.nplanes) break;
-    k1_iter<1, 2, 0>(L, S, T, it, acc, num, den, ring, full, empty, M, R);
-    ++it;
+  for (int tile = blockIdx.x; tile < G.count(); tile += gridDim.x) {
+    const TileGeo P = tile_geo(g, G, tile);
+    Tile T;
+    T.i = P.x0 + 2 + tx;
+    T.j = P.y0 + 1 + ty;
+    T.active = (T.i <= nx) && (T.j <= ny);
+    T.xface = (T.i == 0) || (T.i == nx);
+    const int xsd = T.i == 0 ? 0 : 1;
+    const bool xf_full = T.xface && (L.f.dir[xsd] == 7 || L.f.sw[xsd]);
+    T.writer = T.active && (!T.xface || xf_full);
+    T.cy = axis_class(T.j, g.nn[1]);  // warp-uniform (a warp is one x-row)
+    T.kbeg = P.kbeg;
+    T.kend = P.kend;
+    T.nplanes = P.nplanes;
+    T.qo = (ty + 1) * PX + (tx + 2);
+    T.base = ty * PX + tx + 1;
+    T.wo = t;
+    T.id0 = T.i + (long long)g.px * T.j;
+    for (int it = 0; it < T.nplanes;) {  // unrolled by the period 3 of the slot rotation
+      k1_iter<0, 1, 2>(L, S, T, it, acc, num, den, ring, full, empty, M, R, pr, G, lead);
+      if (++it >= T.nplanes) break;
+      k1_iter<2, 0, 1>(L, S, T, it, acc, num, den, ring, full, empty, M, R, pr, G, lead);
+      if (++it >= T.nplanes) break;
+      k1_iter<1, 2, 0>(L, S, T, it, acc, num, den, ring, full, empty, M, R, pr, G, lead);
+      ++it;
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) acc[q][c] = 0.0;
   }
-  const int slot = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  block_partial<NT>(num, den, L.partial, slot);
+  block_partial<NT>(num, den, L.partial, blockIdx.x);
 }
 
 // Nodes on an x-face with free DOFs (one per thread): gather X over the 18 neighbours inside
@@ -644,7 +749,23 @@ __global__ void zero_constrained_kernel(Geom g, Faces F, double* u, double* w) {
 
 inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
-dim3 tiled_grid(const Geom& g) { return dim3(cdiv(g.nn[0], TX), cdiv(g.nn[1], TY), cdiv(g.nn[2], ZC)); }
+long long tile_count(const Geom& g) {
+  return (long long)cdiv(g.nn[0], TX) * cdiv(g.nn[1], TY) * cdiv(g.nn[2], ZC);
+}
+
+// persistent grid: as many CTAs as fit on the device at once (at most one per tile)
+int tiled_ctas(const Geom& g) {
+  static int resident = 0;
+  if (resident == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(fom_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TILED);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fom_tiled_kernel, NT, SMEM_TILED);
+    resident = std::max(1, sms * std::max(1, per_sm));
+  }
+  return (int)std::min<long long>(resident, tile_count(g));
+}
 
 int xface_sides(const Faces& f) {
   int m = 0;
@@ -661,21 +782,12 @@ unsigned xface_blocks(const Geom& g, const Faces& f) {
 
 }  // namespace
 
-int fom_partial_slots(const Geom& g, const Faces& f) {
-  const dim3 gi = tiled_grid(g);
-  return (int)((long long)gi.x * gi.y * gi.z + xface_blocks(g, f));
-}
+int fom_partial_slots(const Geom& g, const Faces& f) { return tiled_ctas(g) + (int)xface_blocks(g, f); }
 
 void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUtensorMap* tmx,
                         const CUtensorMap* tmw, const CUtensorMap* tmwp, cudaStream_t s, int* launches) {
-  const dim3 gi = tiled_grid(L.g);
-  const int n_int = gi.x * gi.y * gi.z;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(fom_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TILED);
-    attr_set = true;
-  }
-  fom_tiled_kernel<<<gi, dim3(TX, TY), SMEM_TILED, s>>>(L, st, *tmx, *tmw, *tmwp);
+  const int n_int = tiled_ctas(L.g);
+  fom_tiled_kernel<<<n_int, dim3(TX, TY), SMEM_TILED, s>>>(L, st, *tmx, *tmw, *tmwp);
   debug_check("fom_tiled_kernel", s);
   ++*launches;
   const unsigned xb = xface_blocks(L.g, L.f);
@@ -723,3 +835,4 @@ void launch_fom_zero_constrained(const Geom& g, const Faces& f, double* u, doubl
 }
 
 }  // namespace osam
+

@@ -527,6 +527,7 @@ FomLaunch fom_launch(const Sub& d, const double* x, const double* w0, double* q_
   L.dt = dt;
   for (int q = 0; q < 8; ++q) L.inv_mass[q] = d.inv_mass[q];
   L.coef = d.coef;
+  L.rowc = d.rowc;
   L.with_norm = with_norm;
   L.partial = partial;
   return L;
@@ -774,7 +775,27 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
             return fail(OSAM_EINVAL, "internal: interior stencil parity structure violated");
         }
     }
-    int rc = upload(&s.coef, tab, s.stream);
+    // row form for face rows / face planes (kernels_fom.cu plane_slow), x-interior classes
+    std::vector<double> rowc((size_t)27 * 54, 0.0);
+    for (int cy = 0; cy < 3; ++cy)
+      for (int cz = 0; cz < 3; ++cz)
+        for (int sl = 0; sl < 3; ++sl) {
+          const size_t cls = 1 + 3 * (cy + 3 * cz);
+          for (int c = 0; c < 3; ++c)
+            for (int dd = 0; dd < 3; ++dd)
+              for (int oy = 0; oy < 3; ++oy) {
+                auto K = [&](int ox) { return tab[(cls * 27 + (ox + 1) + 3 * (oy + 3 * sl)) * 9 + c * 3 + dd]; };
+                const bool even = (c == 0) == (dd == 0);
+                if (even ? K(-1) != K(1) : (K(-1) != -K(1) || K(0) != 0.0))
+                  return fail(OSAM_EINVAL, "internal: face-class stencil x-parity violated");
+                const size_t at = ((((size_t)(cy * 3 + cz) * 3 + sl) * 3 + c) * 3 + dd) * 3 + oy;
+                rowc[2 * at] = even ? K(0) : 0.0;
+                rowc[2 * at + 1] = K(1);
+              }
+        }
+    int rc = upload(&s.rowc, rowc, s.stream);
+    if (rc != OSAM_OK) return rc;
+    rc = upload(&s.coef, tab, s.stream);
     if (rc != OSAM_OK) return rc;
     rc = dalloc(&s.scratch_a, (size_t)3 * g.npad);
     if (rc == OSAM_OK) rc = dalloc(&s.scratch_v, (size_t)3 * g.npad);
@@ -982,6 +1003,7 @@ void osam_destroy(osam_subdomain* h) {
   dfree(s.scratch_a);
   dfree(s.scratch_v);
   dfree(s.coef);
+  dfree(s.rowc);
   dfree(s.ic_u);
   dfree(s.ic_v);
   delete h;

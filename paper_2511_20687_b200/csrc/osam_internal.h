@@ -84,6 +84,7 @@ struct Sub {
   double w_dt = 0.0;
   Faces faces;
   double* coef = nullptr;  // device [NCLASS][27][9]
+  double* rowc = nullptr;  // device row-form coefficients [cy][cz][slice][c][d][oy][2] (kernels_fom.cu)
   InteriorStencil stencil;
   CUtensorMap tmap[2];   // TMA descriptors of st[b][0] with the halo box (4D: x, y, z, component)
   CUtensorMap tmapw[2];  // TMA descriptors of st[b][1] with the tile box
@@ -128,6 +129,7 @@ struct FomLaunch {
   double dt;  // step in the convergence norm
   double inv_mass[8];
   const double* coef;  // [NCLASS][27][9]
+  const double* rowc;  // [3][3][3][3][3][3][2] row-form coefficients
   int with_norm;       // 1 from Schwarz iteration 2 on
   double2* partial;    // per-block (num, den)
 };
