@@ -32,6 +32,7 @@
 //   * the x-face kernel covers x-faces with free DOFs (a node per thread, class table).
 // No atomics; every sum has a fixed order, so results are bitwise repeatable.
 #include <algorithm>
+#include <cstdlib>
 
 #include "osam_internal.h"
 
@@ -53,7 +54,7 @@ constexpr int ZC = OSAM_ZC;  // target z-planes per block (balanced split)
 constexpr int XF_BLOCK = 128;
 
 __device__ __forceinline__ long long gidx(const Geom& g, int i, int j, int k) {
-  return i + (long long)g.px * (j + (long long)g.nn[1] * k);
+  return i + (long long)g.px * j + g.plane * k;
 }
 
 __device__ __forceinline__ int axis_class(int idx, int nn) { return idx == 0 ? 0 : (idx == nn - 1 ? 2 : 1); }
@@ -167,7 +168,11 @@ constexpr int ARR_BYTES = 3 * PLANE * 8;                   // X (x,y,z comps) of
 constexpr int ARR_STRIDE = (ARR_BYTES + 127) / 128 * 128;  // 128-B aligned TMA destinations
 constexpr int WPL = TX * TY;                               // tile positions of W (no halo)
 constexpr int W_BYTES = 3 * WPL * 8;
-constexpr int STAGE_BYTES = ARR_STRIDE + 2 * W_BYTES;      // X, W, W'_prev
+#ifdef OSAM_WP_LDG
+constexpr int STAGE_BYTES = ARR_STRIDE + W_BYTES;  // X, W (W'_prev read from global memory)
+#else
+constexpr int STAGE_BYTES = ARR_STRIDE + 2 * W_BYTES;  // X, W, W'_prev
+#endif
 constexpr int SMEM_TILED = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8;
 #ifndef OSAM_PF
 #define OSAM_PF 3
@@ -383,10 +388,16 @@ __device__ __forceinline__ void issue_plane(const FomLaunch& L, const TileGeo& P
                                             unsigned long long* full, const Maps& M) {
   unsigned char* st = ring + (size_t)s * STAGE_BYTES;
   const int m = P.kbeg - 1 + it;
+#ifdef OSAM_WP_LDG
+  mbar_expect_tx(&full[s], ARR_BYTES + W_BYTES);
+#else
   mbar_expect_tx(&full[s], ARR_BYTES + (L.with_norm ? 2 : 1) * W_BYTES);
+#endif
   tma_load_4d(st, M.x, P.x0, P.y0, m, 0, &full[s]);
   tma_load_4d(st + ARR_STRIDE, M.w, P.x0 + 2, P.y0 + 1, m, 0, &full[s]);
+#ifndef OSAM_WP_LDG
   if (L.with_norm) tma_load_4d(st + ARR_STRIDE + W_BYTES, M.wp, P.x0 + 2, P.y0 + 1, m, 0, &full[s]);
+#endif
 }
 
 // Ring bookkeeping over the CTA's whole plane stream (all its tiles, in order).
@@ -433,6 +444,14 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
   const int m = T.kbeg - 1 + it;
   const int kf = m - 1;
   const bool fin = T.writer && kf >= T.kbeg && kf <= T.kend;
+#ifdef OSAM_WP_LDG
+  double qwr[3] = {0.0, 0.0, 0.0};  // previous iterate's W' (norm), issued before the waits
+  if (fin && L.with_norm && !T.xface) {
+    const long long idp = T.id0 + (long long)kf * g.plane;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) qwr[c] = L.w_out[c * np + idp];
+  }
+#endif
   // producer: fill the next plane of the stream into the stage released by plane gi - 2
   if (lead && pr.t < G.count()) {
     if (R.gi >= 2) {
@@ -469,7 +488,13 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
       const unsigned char* sp = ring + (size_t)R.sp * STAGE_BYTES;
       const double* xo = reinterpret_cast<const double*>(sp) + T.qo;
       const double* wo = reinterpret_cast<const double*>(sp + ARR_STRIDE) + T.wo;
+#ifdef OSAM_WP_LDG
+      const double* qw = qwr;
+      constexpr int QWS = 1;
+#else
       const double* qw = reinterpret_cast<const double*>(sp + ARR_STRIDE + W_BYTES) + T.wo;
+      constexpr int QWS = WPL;
+#endif
       const long long id = T.id0 + (long long)kf * g.plane;
       const int cz = axis_class(kf, g.nn[2]);
       if (T.xface) {  // fully constrained x-face node: Q' = X (prescribed), W' = a = 0
@@ -497,7 +522,7 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
           const double hdt = 0.5 * L.dt;
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            const double d = hdt * (wn[c] - qw[c * WPL]);
+            const double d = hdt * (wn[c] - qw[c * QWS]);
             const double w = fma(L.dt, fma(L.cv, an[c], w0[c]), x[c]);
             num = fma(d, d, num);
             den = fma(w, w, den);
@@ -516,7 +541,7 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
             wn = fma(L.cw, an, w0);
             qn = fma(L.cq, wn, x);
             if (L.with_norm) {
-              const double d = 0.5 * L.dt * (wn - qw[c * WPL]);
+              const double d = 0.5 * L.dt * (wn - qw[c * QWS]);
               const double w = fma(L.dt, fma(L.cv, an, w0), x);
               num = fma(d, d, num);
               den = fma(w, w, den);
@@ -541,7 +566,10 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
 }
 
 // Persistent: CTA b processes tiles b, b + gridDim.x, ... with one continuous TMA plane stream.
-__global__ void __launch_bounds__(NT, 2)
+#ifndef OSAM_MINB
+#define OSAM_MINB 2
+#endif
+__global__ void __launch_bounds__(NT, OSAM_MINB)
     fom_tiled_kernel(const __grid_constant__ FomLaunch L, const __grid_constant__ InteriorStencil S,
                      const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
                      const __grid_constant__ CUtensorMap tmwp) {
@@ -710,7 +738,7 @@ __global__ void pack_kernel(Geom g, const double* __restrict__ src, double* __re
   const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (p >= n) return;
   const long long i = p % g.nn[0], j = (p / g.nn[0]) % g.nn[1], k = p / ((long long)g.nn[0] * g.nn[1]);
-  const long long q = i + g.px * (j + (long long)g.nn[1] * k);
+  const long long q = i + g.px * j + g.plane * k;
   for (int c = 0; c < 3; ++c) dst[c * g.npad + q] = src[c * n + p];
 }
 
@@ -718,7 +746,7 @@ __global__ void unpack_kernel(Geom g, const double* __restrict__ src, double* __
   const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (p >= n) return;
   const long long i = p % g.nn[0], j = (p / g.nn[0]) % g.nn[1], k = p / ((long long)g.nn[0] * g.nn[1]);
-  const long long q = i + g.px * (j + (long long)g.nn[1] * k);
+  const long long q = i + g.px * j + g.plane * k;
   for (int c = 0; c < 3; ++c) dst[c * n + p] = src[c * g.npad + q];
 }
 
@@ -753,8 +781,16 @@ long long tile_count(const Geom& g) {
   return (long long)cdiv(g.nn[0], TX) * cdiv(g.nn[1], TY) * cdiv(g.nn[2], ZC);
 }
 
-// persistent grid: as many CTAs as fit on the device at once (at most one per tile)
+// CTAs of the tiled kernel: one per tile, or (OSAM_PERSISTENT=1) as many as fit on the device at
+// once, each looping over tiles
 int tiled_ctas(const Geom& g) {
+  static const bool persistent = getenv("OSAM_PERSISTENT") && getenv("OSAM_PERSISTENT")[0] == '1';
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fom_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TILED);
+    attr = true;
+  }
+  if (!persistent) return (int)tile_count(g);
   static int resident = 0;
   if (resident == 0) {
     int dev = 0, sms = 0, per_sm = 0;

@@ -374,7 +374,7 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
           else if (d.kind == OSAM_ROM)
             P.out[3 * t + c] = (int)sdof_index[3 * p + c];
           else  // FOM: straight into the checkpoint's q (R30)
-            P.out[3 * t + c] = (int)(c * d.g.npad + idx[0] + (long long)d.g.px * (idx[1] + (long long)d.g.nn[1] * idx[2]));
+            P.out[3 * t + c] = (int)(c * d.g.npad + idx[0] + (long long)d.g.px * idx[1] + d.g.plane * idx[2]);
         }
       }
       pend.push_back(std::move(P));
@@ -429,7 +429,7 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
       } else {
         const long long i0 = node % src.g.nn[0], j0 = (node / src.g.nn[0]) % src.g.nn[1],
                         k0 = node / ((long long)src.g.nn[0] * src.g.nn[1]);
-        idx[q] = (int)(i0 + src.g.px * (j0 + (long long)src.g.nn[1] * k0));
+        idx[q] = (int)(i0 + src.g.px * j0 + src.g.plane * k0);
       }
     }
     TRY(upload(&m.idx, idx, d.stream));
@@ -735,8 +735,18 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
   g.nn[1] = (int)nn1;
   g.nn[2] = (int)nn2;
   g.px = (int)((nn0 + 3) / 4 * 4);
-  g.plane = (long long)g.px * nn1;
-  g.npad = (g.plane * nn2 + 31) / 32 * 32;
+  // layout: component stride npad, z stride plane; OSAM_LAYOUT=soa gives
+  // [c][k][j][i], the default interleaves the components per z-plane: [k][c][j][i]
+  static const bool soa = getenv("OSAM_LAYOUT") && std::string(getenv("OSAM_LAYOUT")) == "soa";
+  if (soa) {
+    g.plane = (long long)g.px * nn1;
+    g.npad = (g.plane * nn2 + 31) / 32 * 32;
+    g.total = 3 * g.npad;
+  } else {
+    g.npad = (long long)g.px * nn1;
+    g.plane = 3 * g.npad;
+    g.total = g.plane * nn2;
+  }
   for (int a = 0; a < 3; ++a) g.h[a] = (d->hi[a] - d->lo[a]) / d->nel[a];
   s.n_nodes = nn0 * nn1 * nn2;
   s.mass_e = d->rho * g.h[0] * g.h[1] * g.h[2] / 8.0;
@@ -797,20 +807,20 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
     if (rc != OSAM_OK) return rc;
     rc = upload(&s.coef, tab, s.stream);
     if (rc != OSAM_OK) return rc;
-    rc = dalloc(&s.scratch_a, (size_t)3 * g.npad);
-    if (rc == OSAM_OK) rc = dalloc(&s.scratch_v, (size_t)3 * g.npad);
+    rc = dalloc(&s.scratch_a, (size_t)g.total);
+    if (rc == OSAM_OK) rc = dalloc(&s.scratch_v, (size_t)g.total);
     if (rc != OSAM_OK) {
       osam_destroy(h.release());
       return rc;
     }
     for (int b = 0; b < 2; ++b)
       for (int q = 0; q < 2; ++q) {
-        rc = dalloc(&s.st[b][q], (size_t)3 * g.npad);
+        rc = dalloc(&s.st[b][q], (size_t)g.total);
         if (rc != OSAM_OK) {
           osam_destroy(h.release());
           return rc;
         }
-        CK(cudaMemsetAsync(s.st[b][q], 0, sizeof(double) * 3 * g.npad, s.stream));
+        CK(cudaMemsetAsync(s.st[b][q], 0, sizeof(double) * g.total, s.stream));
       }
     for (int b = 0; b < 2; ++b) {
       int r = make_field_tmap(g, s.st[b][0], true, &s.tmap[b]);

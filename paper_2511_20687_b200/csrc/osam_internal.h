@@ -17,12 +17,14 @@ namespace osam {
 enum DofCode { DOF_FREE = 0, DOF_DIRICHLET = 1, DOF_SCHWARZ = 2 };
 
 // Structured box geometry in the padded SoA layout used on the device:
-//   field[c * npad + i + px * (j + nn[1] * k)],  px = nn[0] rounded up to a multiple of 4.
+//   field[c * npad + i + px * j + plane * k],  px = nn[0] rounded up to a multiple of 4
+//   (component stride npad, z stride plane; see osam_create_subdomain for the two layouts).
 struct Geom {
   int nn[3];
   int px;
-  long long plane;  // px * nn[1]
-  long long npad;   // component stride (multiple of 32 doubles)
+  long long plane;  // z stride
+  long long npad;   // component stride
+  long long total;  // doubles per field
   double h[3];
 };
 
