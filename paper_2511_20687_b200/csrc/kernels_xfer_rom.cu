@@ -50,22 +50,25 @@ __global__ void transfer_kernel(int n, const int* __restrict__ idx, const double
 
 __global__ void step_begin_kernel(Ctl c, int B) {
   const int b = threadIdx.x;
-  if (b < B) {
-    c.active[b] = 1;
-    c.iters[b] = 0;
+  for (int q = b; q < B; q += blockDim.x) {
+    c.active[q] = 1;
+    c.iters[q] = 0;
   }
   if (b == 0) {
     c.flags[0] = 1;
     c.flags[1] = 0;
+    *c.n_dev = 0;
+    *c.step_dev += 1;
   }
 }
 
-// one block of 256 threads per sample
-__global__ void finalize_kernel(Ctl c, const double2* __restrict__ part, int n_slots, int B, int n, int min_iters,
+// one block of 256 threads per sample; the sweep that just ran is iteration n = *n_dev + 1
+__global__ void finalize_kernel(Ctl c, const double2* __restrict__ part, int n_slots, int B, int min_iters,
                                 double tol_rel, double tol_abs) {
   __shared__ double red[2][8];
   const int b = blockIdx.x;
   const int t = threadIdx.x;
+  const int n = *c.n_dev + 1;
   double num = 0.0, den = 0.0;
   if (n >= min_iters) {
     for (int s = t; s < n_slots; s += blockDim.x) {
@@ -93,7 +96,10 @@ __global__ void finalize_kernel(Ctl c, const double2* __restrict__ part, int n_s
       if (n >= min_iters) {
         c.numden[2 * b] = num;
         c.numden[2 * b + 1] = den;
-        if (!isfinite(num) || !isfinite(den)) c.flags[1] = 1;
+        if (!isfinite(num) || !isfinite(den)) {
+          c.flags[1] = 1;
+          c.sticky[0] = 1;
+        }
         bool conv = (num == 0.0) || (num < tol_rel * tol_rel * den);
         if (tol_abs > 0.0) conv = conv || (num < tol_abs * tol_abs);
         if (conv) c.active[b] = 0;
@@ -102,11 +108,21 @@ __global__ void finalize_kernel(Ctl c, const double2* __restrict__ part, int n_s
   }
 }
 
-// flags[0] = any sample still active (single block, after finalize)
+// after finalize (single thread): n_dev += 1, flags[0] = any sample active, per-step iteration
+// counts, max_iters flag, and (graph mode) the condition of the sweep while-loop
 __global__ void any_active_kernel(Ctl c, int B) {
+  const int n = *c.n_dev + 1;
+  *c.n_dev = n;
   int a = 0;
   for (int b = 0; b < B; ++b) a |= c.active[b];
   c.flags[0] = a;
+  if (c.iters_all) {
+    const long long k = *c.step_dev - 1;
+    for (int b = 0; b < B; ++b) c.iters_all[k * B + b] = c.iters[b];
+  }
+  const bool more = a && n < c.max_iters && !c.flags[1];
+  if (a && n >= c.max_iters) c.sticky[1] = 1;
+  if (c.has_cond) cudaGraphSetConditional(c.cond, more ? 1u : 0u);
 }
 
 // g^[k, b] = sum_q Phi_s[q, k] s[q, b]  (warp per output; fixed lane-strided order + xor tree)
@@ -246,9 +262,9 @@ void launch_transfer(const XferMap& m, const double* src, long long cs, long lon
 
 void launch_step_begin(Ctl c, int B, cudaStream_t s) { step_begin_kernel<<<1, 256, 0, s>>>(c, B); }
 
-void launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int n, int min_iters, double tol_rel,
+void launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int min_iters, double tol_rel,
                      double tol_abs, cudaStream_t s) {
-  finalize_kernel<<<B, 256, 0, s>>>(c, partial, n_slots, B, n, min_iters, tol_rel, tol_abs);
+  finalize_kernel<<<B, 256, 0, s>>>(c, partial, n_slots, B, min_iters, tol_rel, tol_abs);
   debug_check("finalize_kernel", s);
   any_active_kernel<<<1, 1, 0, s>>>(c, B);
   debug_check("any_active_kernel", s);

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <memory>
 #include <string>
 #include <vector>
@@ -175,23 +176,59 @@ void release_binding(Sub& s) {
   s.group.clear();
 }
 
+struct GraphKey {
+  double dt, tol_rel, tol_abs;
+  int max_iters, min_iters;
+  std::vector<int> curs;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(dt, tol_rel, tol_abs, max_iters, min_iters, curs) <
+           std::tie(o.dt, o.tol_rel, o.tol_abs, o.max_iters, o.min_iters, o.curs);
+  }
+};
+
 struct Group {
   std::vector<osam_subdomain*> sds;
   int B = 1;
   int n_slots = 0;
   double2* partial = nullptr;
-  int* ctl_i = nullptr;  // [flags0, flags1, active[B], iters[B]]
+  // device control block: [flags0, flags1, active[B], iters[B], n, step, sticky0, sticky1]
+  int* ctl_i = nullptr;
   double* numden = nullptr;
   int* h_ctl = nullptr;  // pinned copy
+  int* iters_all = nullptr;
+  long long iters_cap = 0;
   std::vector<cudaEvent_t> ev;
+  cudaStream_t cap_main = nullptr;    // private capture streams (the subdomains' stream may be the
+  cudaStream_t cap_stream = nullptr;  // legacy default stream, which cannot be captured)
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  int launches_per_sweep = 0;  // kernels of one sweep (launch accounting in graph mode)
+  int ctl_len() const { return 2 + 2 * B + 4; }
   ~Group() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    if (cap_main) cudaStreamDestroy(cap_main);
     dfree(partial);
     dfree(ctl_i);
     dfree(numden);
+    dfree(iters_all);
     if (h_ctl) cudaFreeHost(h_ctl);
     for (auto e : ev) cudaEventDestroy(e);
   }
-  Ctl ctl() const { return Ctl{ctl_i + 2, ctl_i + 2 + B, numden, ctl_i}; }
+  Ctl ctl(int max_iters) const {
+    Ctl c;
+    c.flags = ctl_i;
+    c.active = ctl_i + 2;
+    c.iters = ctl_i + 2 + B;
+    c.n_dev = ctl_i + 2 + 2 * B;
+    c.step_dev = ctl_i + 3 + 2 * B;
+    c.sticky = ctl_i + 4 + 2 * B;
+    c.numden = numden;
+    c.iters_all = iters_all;
+    c.max_iters = max_iters;
+    c.has_cond = 0;
+    c.cond = 0;
+    return c;
+  }
 };
 std::map<std::vector<osam_subdomain*>, std::unique_ptr<Group>> g_groups;
 
@@ -500,9 +537,10 @@ int get_group(osam_subdomain* const* sds, int n_sd, Group** out) {
     G->n_slots = 0;
     for (auto s : subs) G->n_slots += s->kind == OSAM_FOM ? fom_partial_slots(s->g, s->faces) : rom_partial_slots(s->r);
     TRY(dalloc(&G->partial, (size_t)std::max(1, G->n_slots) * G->B));
-    TRY(dalloc(&G->ctl_i, (size_t)2 + 2 * G->B));
+    TRY(dalloc(&G->ctl_i, (size_t)G->ctl_len()));
+    CK(cudaMemset(G->ctl_i, 0, sizeof(int) * G->ctl_len()));
     TRY(dalloc(&G->numden, (size_t)2 * G->B));
-    CK(cudaMallocHost((void**)&G->h_ctl, sizeof(int) * (2 + 2 * G->B)));
+    CK(cudaMallocHost((void**)&G->h_ctl, sizeof(int) * G->ctl_len()));
     g_groups[key] = std::move(G);
     it = g_groups.find(key);
   }
@@ -553,110 +591,117 @@ int fom_set_step(Sub& d, double dt, int* launches) {
   return OSAM_OK;
 }
 
-// one controller step; returns OSAM_OK / OSAM_WNOTCONVERGED / error; iters (host) [B]
-int controller_step(Group& G, const osam_schwarz_cfg& cfg, int32_t* iters) {
+// One Schwarz sweep of Algorithm 1 over the group, enqueued on `st`: for each
+// subdomain in sweep order, K2 transfers from each source's current field (iterate n; at n = 1 a
+// source later in the sweep supplies its checkpoint, reading R5), then the FOM advance K1 or the
+// ROM advance K4-K6; finally K3 tests eq:conv_criterion and updates the device control
+// block.  `first` selects the n = 1 variant (constant extension, no norm).
+int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool first, cudaStream_t st, int* launches,
+                  int* fom_k) {
   std::vector<Sub*> subs;
   for (auto h : G.sds) subs.push_back(&h->s);
   const int n_sd = (int)subs.size();
-  cudaStream_t st = subs[0]->stream;
   const int B = G.B;
-  const Ctl ctl = G.ctl();
-  int launches = 0;
-  launch_step_begin(ctl, B, st);
-  ++launches;
-  int n = 1;
-  bool done = false, hit_max = false;
+  int slot = 0;
+  for (int i = 0; i < n_sd; ++i) {
+    Sub& d = *subs[i];
+    for (const XferMap& m : d.maps) {
+      const Sub& src = *subs[m.src];
+      const bool newest = (m.src < i) || !first;
+      const double* field;
+      long long cs, bs;
+      if (src.kind == OSAM_FOM) {
+        // a FOM iterate's displacement is its checkpoint q (predictor + current Schwarz values);
+        // iterate 0 (constant extension) is the checkpoint u, kept in st[1-cur][0]
+        field = newest ? src.st[src.cur][0] : src.st[1 - src.cur][0];
+        cs = src.g.npad;
+        bs = 0;
+      } else {
+        field = src.lift[newest ? 1 - src.cur : src.cur];
+        cs = src.n_lift;
+        bs = 3 * src.n_lift;
+      }
+      double* dst;
+      long long dbs;
+      if (d.kind == OSAM_FOM) {
+        dst = d.st[d.cur][0];
+        dbs = 0;
+      } else {
+        dst = d.rst[1 - d.cur][3];
+        dbs = d.n_sdof;
+      }
+      launch_transfer(m, field, cs, bs, dst, dbs, B, B > 1 ? ctl.active : nullptr, st);
+      ++*launches;
+    }
+    const int with_norm = first ? 0 : 1;
+    if (d.kind == OSAM_FOM) {
+      const int c = d.cur;
+      const FomLaunch L = fom_launch(d, d.st[c][0], d.st[c][1], d.st[1 - c][0], d.st[1 - c][1], cfg.dt, cfg.dt,
+                                     0.5 * cfg.dt, cfg.dt, with_norm, G.partial + (size_t)slot * B, nullptr);
+      if (fom_k && g_prof) CK(cudaEventRecord(G.ev[2 * *fom_k], st));
+      launch_fom_advance(L, d.stencil, &d.tmap[c], &d.tmapw[c], &d.tmapw[1 - c], st, launches);
+      if (fom_k && g_prof) CK(cudaEventRecord(G.ev[2 * *fom_k + 1], st));
+      if (fom_k) ++*fom_k;
+      g_k1_bytes += (32.0 + (with_norm ? 8.0 : 0.0)) * 3.0 * (double)d.n_nodes;
+      ++g_k1_launches;
+      slot += fom_partial_slots(d.g, d.faces);
+    } else {
+      const int c = d.cur;
+      RomLaunch L{};
+      L.r = d.r;
+      L.r_b = d.r_b;
+      L.B = d.batch;
+      L.n_sdof = d.n_sdof;
+      L.Phi_s = d.Phi_s;
+      L.Kbar = d.Kbar;
+      L.Bbar = d.Bbar;
+      L.e = d.e;
+      L.uh0 = d.rst[c][0];
+      L.vh0 = d.rst[c][1];
+      L.ah0 = d.rst[c][2];
+      L.uh1 = d.rst[1 - c][0];
+      L.vh1 = d.rst[1 - c][1];
+      L.ah1 = d.rst[1 - c][2];
+      L.s = d.rst[1 - c][3];
+      L.ustar = d.ustar;
+      L.gh = d.gh;
+      L.active = ctl.active;
+      L.dt = cfg.dt;
+      L.with_norm = with_norm;
+      L.partial = G.partial + (size_t)slot * B;
+      launch_rom_advance(L, st, launches);
+      launch_rom_lift(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, d.rst[1 - c][0], d.rst[1 - c][3],
+                      d.n_sdof, d.lift[1 - c], st);
+      *launches += d.n_lift > 0;
+      slot += rom_partial_slots(d.r);
+    }
+  }
+  launch_finalize(ctl, G.partial, G.n_slots, B, cfg.min_iters, cfg.tol_rel, cfg.tol_abs, st);
+  *launches += 2;
+  return OSAM_OK;
+}
+
+// Host-driven controller step (profiling mode, or OSAM_NOGRAPH=1): the host reads the 16-byte
+// convergence flags after every tested sweep.  Returns OSAM_OK / OSAM_WNOTCONVERGED / error.
+int controller_step_host(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t st) {
   int n_fom = 0;
-  for (auto s : subs) n_fom += s->kind == OSAM_FOM;
-  if (g_prof && (int)G.ev.size() < 2 * n_fom) {
+  for (auto h : G.sds) n_fom += h->s.kind == OSAM_FOM;
+  if (g_prof)
     while ((int)G.ev.size() < 2 * n_fom) {
       cudaEvent_t e;
       CK(cudaEventCreate(&e));
       G.ev.push_back(e);
     }
-  }
-  for (n = 1; n <= cfg.max_iters; ++n) {
-    int slot = 0;
+  const Ctl ctl = G.ctl(cfg.max_iters);
+  int launches = 0;
+  launch_step_begin(ctl, G.B, st);
+  ++launches;
+  bool done = false;
+  for (int n = 1; n <= cfg.max_iters; ++n) {
     int fom_k = 0;
-    for (int i = 0; i < n_sd; ++i) {
-      Sub& d = *subs[i];
-      // K2: Schwarz transfer from each source's current field
-      for (const XferMap& m : d.maps) {
-        const Sub& src = *subs[m.src];
-        const bool newest = (m.src < i) || (n > 1);
-        const int sb = newest ? 1 - src.cur : src.cur;
-        const double* field;
-        long long cs, bs;
-        if (src.kind == OSAM_FOM) {
-          // a FOM iterate's displacement is its checkpoint q (predictor + current Schwarz values);
-          // iterate 0 (constant extension) is the checkpoint u, kept in st[1-cur][0]
-          field = newest ? src.st[src.cur][0] : src.st[1 - src.cur][0];
-          cs = src.g.npad;
-          bs = 0;
-        } else {
-          field = src.lift[sb];
-          cs = src.n_lift;
-          bs = 3 * src.n_lift;
-        }
-        double* dst;
-        long long dbs;
-        if (d.kind == OSAM_FOM) {
-          dst = d.st[d.cur][0];
-          dbs = 0;
-        } else {
-          dst = d.rst[1 - d.cur][3];
-          dbs = d.n_sdof;
-        }
-        launch_transfer(m, field, cs, bs, dst, dbs, B, B > 1 ? ctl.active : nullptr, st);
-        ++launches;
-      }
-      const int with_norm = n >= 2 ? 1 : 0;
-      if (d.kind == OSAM_FOM) {
-        const int c = d.cur;
-        const FomLaunch L = fom_launch(d, d.st[c][0], d.st[c][1], d.st[1 - c][0], d.st[1 - c][1], cfg.dt, cfg.dt,
-                                       0.5 * cfg.dt, cfg.dt, with_norm, G.partial + (size_t)slot * B, nullptr);
-        if (g_prof) CK(cudaEventRecord(G.ev[2 * fom_k], st));
-        launch_fom_advance(L, d.stencil, &d.tmap[c], &d.tmapw[c], &d.tmapw[1 - c], st, &launches);
-        if (g_prof) CK(cudaEventRecord(G.ev[2 * fom_k + 1], st));
-        g_k1_bytes += (32.0 + (with_norm ? 8.0 : 0.0)) * 3.0 * (double)d.n_nodes;
-        ++g_k1_launches;
-        ++fom_k;
-        slot += fom_partial_slots(d.g, d.faces);
-      } else {
-        const int c = d.cur;
-        RomLaunch L{};
-        L.r = d.r;
-        L.r_b = d.r_b;
-        L.B = d.batch;
-        L.n_sdof = d.n_sdof;
-        L.Phi_s = d.Phi_s;
-        L.Kbar = d.Kbar;
-        L.Bbar = d.Bbar;
-        L.e = d.e;
-        L.uh0 = d.rst[c][0];
-        L.vh0 = d.rst[c][1];
-        L.ah0 = d.rst[c][2];
-        L.uh1 = d.rst[1 - c][0];
-        L.vh1 = d.rst[1 - c][1];
-        L.ah1 = d.rst[1 - c][2];
-        L.s = d.rst[1 - c][3];
-        L.ustar = d.ustar;
-        L.gh = d.gh;
-        L.active = ctl.active;
-        L.dt = cfg.dt;
-        L.with_norm = with_norm;
-        L.partial = G.partial + (size_t)slot * B;
-        launch_rom_advance(L, st, &launches);
-        launch_rom_lift(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, d.rst[1 - c][0], d.rst[1 - c][3],
-                        d.n_sdof, d.lift[1 - c], st);
-        launches += d.n_lift > 0;
-        slot += rom_partial_slots(d.r);
-      }
-    }
-    launch_finalize(ctl, G.partial, G.n_slots, B, n, cfg.min_iters, cfg.tol_rel, cfg.tol_abs, st);
-    launches += 2;
+    TRY(enqueue_sweep(G, cfg, ctl, n == 1, st, &launches, &fom_k));
     if (n >= cfg.min_iters || g_prof) {
-      CK(cudaMemcpyAsync(G.h_ctl, G.ctl_i, sizeof(int) * (2 + 2 * B), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(G.h_ctl, G.ctl_i, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       if (g_prof) {
         for (int k = 0; k < fom_k; ++k) {
@@ -675,17 +720,89 @@ int controller_step(Group& G, const osam_schwarz_cfg& cfg, int32_t* iters) {
       }
     }
   }
-  if (!done) {
-    hit_max = true;
-    n = cfg.max_iters;
-    CK(cudaMemcpyAsync(G.h_ctl, G.ctl_i, sizeof(int) * (2 + 2 * B), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-  }
   CK(cudaGetLastError());
-  for (int b = 0; b < B; ++b) iters[b] = G.h_ctl[2 + B + b];
-  for (auto s : subs) s->cur = 1 - s->cur;  // commit: working iterate becomes the checkpoint
+  for (auto h : G.sds) h->s.cur = 1 - h->s.cur;  // commit: working iterate becomes the checkpoint
   g_launches += launches;
-  return hit_max ? OSAM_WNOTCONVERGED : OSAM_OK;
+  return done ? OSAM_OK : OSAM_WNOTCONVERGED;
+}
+
+int step_graph_capture(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t st, cudaGraph_t* graph_out,
+                       int* launches_out) {
+  Ctl ctl = G.ctl(cfg.max_iters);
+  int launches = 0;
+  CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  launch_step_begin(ctl, G.B, st);
+  TRY(enqueue_sweep(G, cfg, ctl, true, st, &launches, nullptr));
+  cudaStreamCaptureStatus status;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  cudaGraph_t cap = nullptr;
+  unsigned long long cap_id = 0;
+  CK(cudaStreamGetCaptureInfo(st, &status, &cap_id, &cap, &deps, &ndeps));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, cap, cfg.max_iters >= 2 ? 1u : 0u, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cnode;
+  CK(cudaGraphAddNode(&cnode, cap, deps, ndeps, &cp));
+  CK(cudaStreamUpdateCaptureDependencies(st, &cnode, 1, cudaStreamSetCaptureDependencies));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(G.cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  ctl.has_cond = 1;
+  ctl.cond = h;
+  launches = 0;
+  TRY(enqueue_sweep(G, cfg, ctl, false, G.cap_stream, &launches, nullptr));
+  CK(cudaStreamEndCapture(G.cap_stream, &body));
+  CK(cudaStreamEndCapture(st, graph_out));
+  *launches_out = launches;
+  return OSAM_OK;
+}
+
+// CUDA graph of one controller step: step_begin, sweep 1, then a conditional while node whose
+// body is one sweep n >= 2; K3 (any_active_kernel) sets the loop condition on the device, so a step
+// needs no host round trip.  One graph per (configuration, buffer parity), cached in the group.
+int step_graph_capture(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t st, cudaGraph_t* graph_out,
+                       int* launches_out);
+
+int step_graph(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t, cudaGraphExec_t* out, int* launches_per_sweep) {
+  GraphKey key{cfg.dt, cfg.tol_rel, cfg.tol_abs, cfg.max_iters, cfg.min_iters, {}};
+  for (auto h : G.sds) key.curs.push_back(h->s.cur);
+  auto it = G.graphs.find(key);
+  if (it != G.graphs.end()) {
+    *out = it->second;
+    return OSAM_OK;
+  }
+  if (!G.cap_stream) CK(cudaStreamCreateWithFlags(&G.cap_stream, cudaStreamNonBlocking));
+  if (!G.cap_main) CK(cudaStreamCreateWithFlags(&G.cap_main, cudaStreamNonBlocking));
+  cudaGraph_t graph = nullptr;
+  int launches = 0;
+  const int rc = step_graph_capture(G, cfg, G.cap_main, &graph, &launches);
+  if (rc != OSAM_OK) {  // leave no stream in capture mode
+    cudaGraph_t junk = nullptr;
+    cudaStreamCaptureStatus cs;
+    if (cudaStreamIsCapturing(G.cap_stream, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+      cudaStreamEndCapture(G.cap_stream, &junk);
+      if (junk) cudaGraphDestroy(junk);
+    }
+    junk = nullptr;
+    if (cudaStreamIsCapturing(G.cap_main, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+      cudaStreamEndCapture(G.cap_main, &junk);
+      if (junk) cudaGraphDestroy(junk);
+    }
+    cudaGetLastError();
+    return rc;
+  }
+  cudaGraphExec_t exec = nullptr;
+  CK(cudaGraphInstantiate(&exec, graph, 0));
+  CK(cudaGraphDestroy(graph));
+  G.graphs[key] = exec;
+  G.launches_per_sweep = launches;
+  *out = exec;
+  *launches_per_sweep = launches;
+  return OSAM_OK;
 }
 
 }  // namespace
@@ -928,15 +1045,56 @@ int osam_step(osam_subdomain* const* sds, int32_t n_sd, const osam_schwarz_cfg* 
     g_launches += launches;
   }
   int status = OSAM_OK;
-  std::vector<int32_t> it(B);
-  for (int k = 0; k < n_steps; ++k) {
-    const int rc = controller_step(*G, *cfg, it.data());
-    if (rc < 0) return rc;
-    if (rc == OSAM_WNOTCONVERGED) status = OSAM_WNOTCONVERGED;
-    if (iters_out)
-      for (int b = 0; b < B; ++b) iters_out[(size_t)k * B + b] = it[b];
+  cudaStream_t st = sds[0]->s.stream;
+  if (n_steps > 0) {
+    const long long need = (long long)n_steps * B;
+    if (need > G->iters_cap) {  // graphs hold the buffer pointer: rebuild them after a reallocation
+      for (auto& kv : G->graphs) cudaGraphExecDestroy(kv.second);
+      G->graphs.clear();
+      dfree(G->iters_all);
+      const long long cap = std::max(need, 4096LL * B);
+      TRY(dalloc(&G->iters_all, (size_t)cap));
+      G->iters_cap = cap;
+    }
+    // reset the step counter and the sticky flags of this call
+    CK(cudaMemsetAsync(G->ctl_i + 3 + 2 * B, 0, sizeof(int) * 3, st));
   }
-  CK(cudaStreamSynchronize(sds[0]->s.stream));
+  static const bool nograph = getenv("OSAM_NOGRAPH") && getenv("OSAM_NOGRAPH")[0] == '1';
+  if (g_prof || nograph) {
+    for (int k = 0; k < n_steps; ++k) {
+      const int rc = controller_step_host(*G, *cfg, st);
+      if (rc < 0) return rc;
+      if (rc == OSAM_WNOTCONVERGED) status = OSAM_WNOTCONVERGED;
+    }
+  } else {
+    for (int k = 0; k < n_steps; ++k) {
+      cudaGraphExec_t exec = nullptr;
+      int per_sweep = 0;
+      TRY(step_graph(*G, *cfg, st, &exec, &per_sweep));
+      CK(cudaGraphLaunch(exec, st));
+      for (int i = 0; i < n_sd; ++i) sds[i]->s.cur = 1 - sds[i]->s.cur;  // commit (pointer swap)
+    }
+  }
+  std::vector<int32_t> its;
+  if (n_steps > 0) {
+    its.resize((size_t)n_steps * B);
+    CK(cudaMemcpyAsync(G->h_ctl, G->ctl_i, sizeof(int) * G->ctl_len(), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(its.data(), G->iters_all, sizeof(int32_t) * its.size(), cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  if (n_steps > 0) {
+    if (iters_out) std::memcpy(iters_out, its.data(), sizeof(int32_t) * its.size());
+    if (!(g_prof || nograph)) {  // kernels the graphs ran: step_begin + the sweeps (max over samples)
+      for (int k = 0; k < n_steps; ++k) {
+        int nmax = 0;
+        for (int b = 0; b < B; ++b) nmax = std::max(nmax, its[(size_t)k * B + b]);
+        g_launches += 1 + (long long)nmax * G->launches_per_sweep;
+      }
+    }
+    if (G->h_ctl[4 + 2 * B]) return fail(OSAM_EUNSTABLE, "non-finite Schwarz convergence norm");
+    if (G->h_ctl[5 + 2 * B]) status = OSAM_WNOTCONVERGED;
+  }
   return status;
 }
 

@@ -180,10 +180,18 @@ struct Ctl {
   int* active;       // [B]
   int* iters;        // [B] of the current step
   double* numden;    // [B][2] last check
-  int* flags;        // [0] any active, [1] unstable
+  int* flags;        // [0] any active, [1] unstable (this step)
+  int* n_dev;        // Schwarz iterations done in the current step
+  int* step_dev;     // controller steps started since the last reset
+  int* sticky;       // [0] unstable, [1] hit max_iters (this osam_step call)
+  int* iters_all;    // [steps][B] per-step iteration counts (may be null)
+  int max_iters;
+  int has_cond;      // graph mode: any_active sets the while-loop condition
+  cudaGraphConditionalHandle cond;
 };
 void launch_step_begin(Ctl c, int B, cudaStream_t s);
-void launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int n, int min_iters, double tol_rel,
+// Convergence test of the sweep that just ran (iteration n = *n_dev + 1): K3 + flags/conditional.
+void launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int min_iters, double tol_rel,
                      double tol_abs, cudaStream_t s);
 
 }  // namespace osam
