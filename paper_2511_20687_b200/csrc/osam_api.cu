@@ -172,6 +172,9 @@ void release_binding(Sub& s) {
   dfree(s.sdof_ids);
   dfree(s.Phi_lift);
   dfree(s.lift_code);
+  dfree(s.KB);
+  dfree(s.Z);
+  dfree(s.part);
   s.bound = false;
   s.group.clear();
 }
@@ -348,6 +351,20 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
     }
     TRY(dalloc(&s.ustar, (size_t)s.r * s.batch));
     TRY(dalloc(&s.gh, (size_t)std::max(1, s.r_b) * s.batch));
+    // batched samples: the reduced update is a dense contraction -> FP64 tensor cores (OSAM_ROM_TC=0/1
+    // overrides the default, which is tensor cores iff batch > 1)
+    const char* tc = getenv("OSAM_ROM_TC");
+    s.use_tc = tc ? tc[0] == '1' : s.batch > 1;
+    if (s.use_tc) {
+      const int rz = s.r + s.r_b;
+      std::vector<double> kb((size_t)s.r * rz);
+      for (int j = 0; j < s.r; ++j)
+        for (int q = 0; q < s.r; ++q) kb[(size_t)j * s.r + q] = -s.h_Kbar[(size_t)j * s.r + q];
+      for (int j = 0; j < s.r_b; ++j)
+        for (int q = 0; q < s.r; ++q) kb[(size_t)(s.r + j) * s.r + q] = s.h_Bbar[(size_t)j * s.r + q];
+      TRY(upload(&s.KB, kb, s.stream));
+      TRY(dalloc(&s.Z, (size_t)rz * s.batch));
+    }
   }
   // donor maps: collect, per source, the nodes it must provide (ROM sources: compact lists)
   struct Pending {
@@ -450,6 +467,7 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
     TRY(upload(&s.Phi_lift, phil, s.stream));
     TRY(upload(&s.lift_code, code, s.stream));
     for (int b = 0; b < 2; ++b) TRY(dalloc(&s.lift[b], (size_t)std::max<long long>(nl, 1) * s.batch));
+    if (s.use_tc) TRY(dalloc(&s.part, (size_t)tc_part_size(s.r, s.r_b, s.batch, s.n_sdof, nl)));
   }
   for (auto& P : pend) {
     Sub& d = *subs[P.dst];
@@ -508,9 +526,15 @@ int process_ic(Sub& s, int* launches) {
     L.e = s.e;
     L.s = s.rst[c][3];
     L.gh = s.gh;
-    launch_rom_accel(L, s.rst[c][0], s.rst[c][2], st, launches);
-    launch_rom_lift(s.r, s.batch, 3 * s.n_lift, s.Phi_lift, s.lift_code, s.rst[c][0], s.rst[c][3], s.n_sdof,
-                    s.lift[c], st);
+    if (s.use_tc) {
+      launch_rom_accel_tc(L, s.rst[c][0], s.rst[c][2], s.KB, s.Z, s.part, st, launches);
+      launch_rom_lift_tc(s.r, s.batch, 3 * s.n_lift, s.Phi_lift, s.lift_code, s.rst[c][0], s.rst[c][3], s.n_sdof,
+                         s.lift[c], s.part, st, launches);
+    } else {
+      launch_rom_accel(L, s.rst[c][0], s.rst[c][2], st, launches);
+      launch_rom_lift(s.r, s.batch, 3 * s.n_lift, s.Phi_lift, s.lift_code, s.rst[c][0], s.rst[c][3], s.n_sdof,
+                      s.lift[c], st);
+    }
     *launches += 4;
     CK(cudaStreamSynchronize(st));
   }
@@ -669,10 +693,16 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
       L.dt = cfg.dt;
       L.with_norm = with_norm;
       L.partial = G.partial + (size_t)slot * B;
-      launch_rom_advance(L, st, launches);
-      launch_rom_lift(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, d.rst[1 - c][0], d.rst[1 - c][3],
-                      d.n_sdof, d.lift[1 - c], st);
-      *launches += d.n_lift > 0;
+      if (d.use_tc) {
+        launch_rom_advance_tc(L, d.KB, d.Z, d.part, st, launches);
+        launch_rom_lift_tc(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, d.rst[1 - c][0], d.rst[1 - c][3],
+                           d.n_sdof, d.lift[1 - c], d.part, st, launches);
+      } else {
+        launch_rom_advance(L, st, launches);
+        launch_rom_lift(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, d.rst[1 - c][0], d.rst[1 - c][3],
+                        d.n_sdof, d.lift[1 - c], st);
+        *launches += d.n_lift > 0;
+      }
       slot += rom_partial_slots(d.r);
     }
   }

@@ -110,6 +110,11 @@ struct Sub {
   double* Phi_lift = nullptr;  // [3 n_lift][r] row-major
   int* lift_code = nullptr;    // [3 n_lift]: >= 0 Phi_lift row, -1 Dirichlet, -2-q Schwarz DOF q
   double* lift[2] = {nullptr, nullptr};
+  // batched ROM on the tensor cores (kernels_rom_tc.cu): [-Kbar | Bbar] and scratch
+  bool use_tc = false;
+  double* KB = nullptr;    // r x (r + r_b) column-major
+  double* Z = nullptr;     // (r + r_b) x B
+  double* part = nullptr;  // split-K partial products (tc_part_size doubles)
 
   // pending IC (raw full fields, batch x 3 n)
   bool ic_pending = false;
@@ -171,6 +176,13 @@ void launch_rom_project(long long n_rows, int r, int B, const double* Phi, const
 void launch_gather_dofs(long long n, int B, const int* ids, const double* field, long long field_bstride,
                         long long n_nodes, double* out, cudaStream_t s);
 void launch_rom_accel(const RomLaunch& L, const double* uh, double* ah, cudaStream_t s, int* launches);
+long long tc_part_size(int r, int r_b, int B, long long n_s, long long n_lift3);
+void launch_rom_advance_tc(const RomLaunch& L, const double* KB, double* Z, double* part, cudaStream_t s,
+                           int* launches);
+void launch_rom_accel_tc(const RomLaunch& L, const double* uh, double* ah, const double* KB, double* Z, double* part,
+                         cudaStream_t s, int* launches);
+void launch_rom_lift_tc(int r, int B, long long nl, const double* Phi_lift, const int* code, const double* uh,
+                        const double* sv, long long ns, double* out, double* part, cudaStream_t st, int* launches);
 
 // OSAM_DEBUG_SYNC=1: synchronise after every launch and report the first failing kernel on
 // stderr (development aid only; off by default).

@@ -2,6 +2,7 @@
 # one GPU round: tests, bench, ncu launch list, ncu full capture of the FOM kernels
 set -x
 TAG=${1:-r}
+cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 B="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e"
 nvidia-smi > gpurun_out/smi_$TAG.txt 2>&1

@@ -1,5 +1,6 @@
 #!/bin/bash
 # dram traffic of one K1 tiled launch (Omega1, sweep >= 2) for each variant in var/
+cd "$(dirname "$0")/.."
 for v in var/*.so; do
   n=$(basename $v .so)
   OSAM_LIB=$v timeout 300 python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/vplain_$n.log 2>&1 && \
