@@ -60,7 +60,8 @@ def workload_desc(cfg):
         n = (s["nel"][0] + 1) * (s["nel"][1] + 1) * (s["nel"][2] + 1)
         if s["kind"] == "fom":
             dofs += 3 * n
-        parts.append(f"{s['kind'].upper()} {s['nel'][0]}x{s['nel'][1]}x{s['nel'][2]}")
+        extra = f" r={cfg['rom']['r']}" if s["kind"] == "rom" else ""
+        parts.append(f"{s['kind'].upper()} {s['nel'][0]}x{s['nel'][1]}x{s['nel'][2]}{extra}")
     return " | ".join(parts), dofs
 
 
@@ -80,11 +81,23 @@ def sample_cfg(cfg, lateral=SAMPLE_LATERAL):
     return out
 
 
+def workload_ops(cfg):
+    """Reduced operators of the ROM subdomains: seeded stand-ins of the trained sizes (the offline
+    training runs of c2/c4/c5 are minutes to an hour of CPU work; throughput does not depend on the
+    operator values; parity with trained operators is covered by tests/).  None for FOM-only workloads."""
+    if not any(s["kind"] == "rom" for s in cfg["subdomains"]):
+        return None
+    from paper_2511_20687_b200 import problem
+    return problem.synthetic_rom_ops(cfg)
+
+
 def oracle_rate(cfg, warmup, steps=None, seconds=None):
     """Oracle DOF-updates/s on cfg: `warmup` untimed controller steps then `steps` timed (or
     as many as fit in `seconds`). Returns (rate, steps_timed, wall, threads)."""
     from oracle import schwarz
-    models = schwarz.build_models(cfg)
+    ops = workload_ops(cfg)
+    from paper_2511_20687_b200 import problem
+    models = schwarz.build_models(cfg, rom_ops=ops, e_scale=problem.e_scale(cfg))
     u0s = [I.initial_displacements(cfg, s) for s in cfg["subdomains"]]
     st = [m.init_state(u) for m, u in zip(models, u0s)]
     dofs = sum(3 * m.box.n_nodes for m in models if m.kind == "fom")
@@ -202,7 +215,8 @@ def run_ours(args):
     cfg = I.config(args.workload)
     desc, fom_dofs = workload_desc(cfg)
     stream = torch.cuda.current_stream(dev)
-    subs = problem.build(cfg, stream=stream.cuda_stream)
+    ops = workload_ops(cfg)
+    subs = problem.build(cfg, ops, stream=stream.cuda_stream)
     fields = problem.initial_fields(cfg)
     gpu_fields = [torch.from_numpy(f).to(dev) for f in fields]
     for sub, f in zip(subs, gpu_fields):

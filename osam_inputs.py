@@ -174,3 +174,17 @@ def random_state(n_nodes, seed, scale=1e-3):
     """Seeded random (u, v) fields for unit/parity tests of single operations."""
     rng = np.random.default_rng(seed)
     return scale * rng.standard_normal((n_nodes, 3)), scale * 1e3 * rng.standard_normal((n_nodes, 3))
+
+
+def synthetic_rom_operators(n_free, n_s, r, r_b, dt, seed):
+    """Seeded stand-in reduced operators of the trained sizes (timing of configurations whose offline
+    stage is too large to run per benchmark, e.g. c4's 80^3 ROMs).  Not a trained
+    ROM: Phi, Phi_s have random +-1/sqrt(rows) entries (nearly orthonormal columns), Kbar is diagonal
+    with reduced frequencies below the explicit stability limit of dt, Bbar is small and random."""
+    rng = np.random.default_rng(seed)
+    Phi = np.asfortranarray((rng.integers(0, 2, size=(n_free, r), dtype=np.int8) * 2 - 1) / np.sqrt(n_free))
+    Phi_s = np.asfortranarray((rng.integers(0, 2, size=(n_s, r_b), dtype=np.int8) * 2 - 1) / np.sqrt(n_s))
+    omega = np.linspace(0.05, 0.5, r) / dt
+    Kbar = np.asfortranarray(np.diag(omega ** 2))
+    Bbar = np.asfortranarray(0.1 * rng.standard_normal((r, r_b)) / (dt * dt * np.sqrt(r_b)))
+    return dict(Phi=Phi, Phi_s=Phi_s, Kbar=Kbar, Bbar=Bbar)

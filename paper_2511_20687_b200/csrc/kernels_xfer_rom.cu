@@ -125,19 +125,29 @@ __global__ void any_active_kernel(Ctl c, int B) {
   if (c.has_cond) cudaGraphSetConditional(c.cond, more ? 1u : 0u);
 }
 
-// g^[k, b] = sum_q Phi_s[q, k] s[q, b]  (warp per output; fixed lane-strided order + xor tree)
-__global__ void rom_project_bnd_kernel(int r_b, int B, long long ns, const double* __restrict__ Phi_s,
-                                       const double* __restrict__ s, double* __restrict__ gh) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= r_b * B) return;
-  const int k = w % r_b, b = w / r_b;
+// Fixed-order block sum of one value per thread (blockDim.x = 256).
+__device__ __forceinline__ double block_sum256(double v) {
+  __shared__ double red[8];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < 8; ++w) t += red[w];
+  return t;
+}
+
+// g^[k, b] = sum_q Phi_s[q, k] s[q, b]  (a block per output; thread-strided, fixed order)
+__global__ void __launch_bounds__(256) rom_project_bnd_kernel(int r_b, int B, long long ns,
+                                                              const double* __restrict__ Phi_s,
+                                                              const double* __restrict__ s, double* __restrict__ gh) {
+  const int k = blockIdx.x, b = blockIdx.y;
   const double* col = Phi_s + (long long)k * ns;
   const double* sb = s + (long long)b * ns;
   double acc = 0.0;
-  for (long long q = lane; q < ns; q += 32) acc = fma(col[q], sb[q], acc);
-  acc = warp_sum(acc);
-  if (lane == 0) gh[k + (long long)r_b * b] = acc;
+  for (long long q = threadIdx.x; q < ns; q += 256) acc = fma(col[q], sb[q], acc);
+  acc = block_sum256(acc);
+  if (threadIdx.x == 0) gh[k + (long long)r_b * b] = acc;
 }
 
 __global__ void rom_predict_kernel(int r, int B, const double* __restrict__ uh, const double* __restrict__ vh,
@@ -223,23 +233,21 @@ __global__ void rom_lift_kernel(int r, int B, long long nl, const double* __rest
   if (lane == 0) out[(long long)b * nl + ld] = v;
 }
 
-// out[i, b] = sum_q Phi[q, i] field_b[dof(ids[q])]  (projection onto the POD basis, IC only)
-__global__ void rom_project_kernel(long long nrows, int r, int B, const double* __restrict__ Phi,
-                                   const int* __restrict__ ids, const double* __restrict__ field, long long fbs,
-                                   long long n_nodes, double* __restrict__ out) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= r * B) return;
-  const int i = w % r, b = w / r;
+// out[i, b] = sum_q Phi[q, i] field_b[dof(ids[q])]  (projection onto the POD basis, IC only;
+// a block per output, thread-strided, fixed order)
+__global__ void __launch_bounds__(256) rom_project_kernel(long long nrows, int r, int B, const double* __restrict__ Phi,
+                                                         const int* __restrict__ ids, const double* __restrict__ field,
+                                                         long long fbs, long long n_nodes, double* __restrict__ out) {
+  const int i = blockIdx.x, b = blockIdx.y;
   const double* col = Phi + (long long)i * nrows;
   const double* f = field + (long long)b * fbs;
   double acc = 0.0;
-  for (long long q = lane; q < nrows; q += 32) {
+  for (long long q = threadIdx.x; q < nrows; q += 256) {
     const long long dof = ids[q];
     acc = fma(col[q], f[(dof % 3) * n_nodes + dof / 3], acc);
   }
-  acc = warp_sum(acc);
-  if (lane == 0) out[i + (long long)r * b] = acc;
+  acc = block_sum256(acc);
+  if (threadIdx.x == 0) out[i + (long long)r * b] = acc;
 }
 
 __global__ void gather_dofs_kernel(long long n, int B, const int* __restrict__ ids, const double* __restrict__ field,
@@ -274,7 +282,7 @@ int rom_partial_slots(int r) { return (int)cdiv(r, 256); }
 
 void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches) {
   if (L.r_b > 0)
-    rom_project_bnd_kernel<<<cdiv((long long)L.r_b * L.B * 32, 256), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
+    rom_project_bnd_kernel<<<dim3(L.r_b, L.B), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
                                                                                  L.s, L.gh);
   rom_predict_kernel<<<cdiv((long long)L.r * L.B, 256), 256, 0, s>>>(L.r, L.B, L.uh0, L.vh0, L.ah0, L.dt, L.ustar);
   debug_check("rom_predict_kernel", s);
@@ -288,7 +296,7 @@ void launch_rom_accel(const RomLaunch& L, const double* uh, double* ah, cudaStre
   A.ustar = const_cast<double*>(uh);
   A.ah1 = ah;
   if (L.r_b > 0)
-    rom_project_bnd_kernel<<<cdiv((long long)L.r_b * L.B * 32, 256), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
+    rom_project_bnd_kernel<<<dim3(L.r_b, L.B), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
                                                                                  L.s, L.gh);
   rom_update_kernel<<<dim3(cdiv(L.r, 256), L.B), 256, 0, s>>>(A, 1);
   debug_check("rom_update_kernel", s);
@@ -304,7 +312,7 @@ void launch_rom_lift(int r, int B, long long nl, const double* Phi_lift, const i
 
 void launch_rom_project(long long nrows, int r, int B, const double* Phi, const int* ids, const double* field,
                         long long fbs, long long n_nodes, double* out, cudaStream_t s) {
-  rom_project_kernel<<<cdiv((long long)r * B * 32, 256), 256, 0, s>>>(nrows, r, B, Phi, ids, field, fbs, n_nodes,
+  rom_project_kernel<<<dim3(r, B), 256, 0, s>>>(nrows, r, B, Phi, ids, field, fbs, n_nodes,
                                                                      out);
 }
 

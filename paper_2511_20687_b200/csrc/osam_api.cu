@@ -1007,8 +1007,13 @@ int osam_set_ic(osam_subdomain* h, const double* u0, const double* v0) {
   cudaStream_t st = s.stream;
   const size_t nf = (size_t)s.batch * 3 * s.n_nodes;
   double *du = nullptr, *dv = nullptr;
-  TRY(dalloc(&du, nf));
-  TRY(dalloc(&dv, nf));
+  if (s.kind == OSAM_FOM) {  // stage in the FOM's scratch fields (no allocation per call)
+    du = s.scratch_v;
+    dv = s.scratch_a;
+  } else {
+    TRY(dalloc(&du, nf));
+    TRY(dalloc(&dv, nf));
+  }
   if (is_device_ptr(u0))
     CK(cudaMemcpyAsync(du, u0, nf * sizeof(double), cudaMemcpyDeviceToDevice, st));
   else
@@ -1025,8 +1030,6 @@ int osam_set_ic(osam_subdomain* h, const double* u0, const double* v0) {
     launch_fom_pack(s.g, dv, s.st[c][1], s.n_nodes, st);  // RAW state (u, v) until the first osam_step
     s.w_dt = 0.0;
     CK(cudaStreamSynchronize(st));
-    dfree(du);
-    dfree(dv);
     g_launches += 2;
   } else {
     dfree(s.ic_u);
@@ -1154,13 +1157,11 @@ static int get_field(const osam_subdomain* h, int which, double* out) {
       g_launches += launches;
       field = which == 1 ? s.scratch_v : s.scratch_a;
     }
-    double* tmp = nullptr;
-    TRY(dalloc(&tmp, (size_t)3 * s.n_nodes));
+    double* tmp = which == 2 ? s.scratch_v : s.scratch_a;  // not the source field
     launch_fom_unpack(s.g, field, tmp, s.n_nodes, st);
     ++g_launches;
     const int rc = copy_out(tmp, out, (size_t)3 * s.n_nodes, st);
     CK(cudaStreamSynchronize(st));
-    dfree(tmp);
     return rc;
   }
   if (!s.bound) return fail(OSAM_EINVAL, "ROM state not initialised: call osam_step first");

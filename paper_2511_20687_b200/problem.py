@@ -52,6 +52,54 @@ def set_ics(cfg, subs, device=None, fields=None):
             sub.set_ic(u0)
 
 
+def dof_split(cfg, i):
+    """(n_free, n_s) of subdomain i: the Schwarz faces of a box are the faces strictly inside another
+    box of the workload and laterally covered by it (include/osam.h conventions); Dirichlet components
+    win.  Host-side bookkeeping used to size stand-in ROM operators before the library binds the group."""
+    subs = cfg["subdomains"]
+    a = subs[i]
+    nn = [n + 1 for n in a["nel"]]
+    size = max(a["hi"][d] - a["lo"][d] for d in range(3))
+    tol = 1e-12 * size
+    sw = [False] * 6
+    for f in range(6):
+        ax = f // 2
+        x = a["hi"][ax] if f % 2 else a["lo"][ax]
+        for j, b in enumerate(subs):
+            if j == i:
+                continue
+            inside = b["lo"][ax] + tol < x < b["hi"][ax] - tol
+            lateral = all(b["lo"][d] <= a["lo"][d] + tol and a["hi"][d] <= b["hi"][d] + tol for d in range(3) if d != ax)
+            if inside and lateral:
+                sw[f] = True
+                break
+    idx = np.indices((nn[2], nn[1], nn[0])).reshape(3, -1)[::-1]  # i, j, k per node (node id order)
+    on = [idx[f // 2] == ((nn[f // 2] - 1) if f % 2 else 0) for f in range(6)]
+    swn = np.zeros(idx.shape[1], dtype=bool)
+    for f in range(6):
+        if sw[f]:
+            swn |= on[f]
+    n_free = n_s = 0
+    for c in range(3):
+        dirc = np.zeros(idx.shape[1], dtype=bool)
+        for f in range(6):
+            if (a["dirichlet"][f] >> c) & 1:
+                dirc |= on[f]
+        n_s += int((swn & ~dirc).sum())
+        n_free += int((~swn & ~dirc).sum())
+    return n_free, n_s
+
+
+def synthetic_rom_ops(cfg, r_b=40, seed=7):
+    """Stand-in reduced operators of the trained sizes for every ROM subdomain (osam_inputs)."""
+    ops = {}
+    for i, s in enumerate(cfg["subdomains"]):
+        if s["kind"] == "rom":
+            n_free, n_s = dof_split(cfg, i)
+            ops[i] = osam_inputs.synthetic_rom_operators(n_free, n_s, cfg["rom"]["r"], r_b, cfg["dt"], seed + i)
+    return ops
+
+
 def run(cfg, subs, n_steps=None, max_iters=None):
     return osam_step(subs, cfg["dt"], cfg["tol"], cfg["n_steps"] if n_steps is None else n_steps,
                      max_iters=max_iters or cfg["max_iters"], min_iters=cfg["min_iters"])

@@ -2,8 +2,8 @@
 """Throughput of the latency-bound BASELINE configs (c1, c2, c5) on one GPU, graph mode.
 
 Not the driver's bench line (bench.py times c3); a measurement aid for DESIGN.md / BASELINE.md.
-ROM operators come from the oracle's offline stage (oracle/opinf.py, reading R25), as in the parity
-tests.  Prints one JSON line per config.
+ROM operators are the seeded stand-ins of bench.py (trained operators are used by the parity tests).
+Prints one JSON line per config.
 """
 import json
 import os
@@ -16,14 +16,13 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import osam_inputs as I  # noqa: E402
-from oracle import opinf  # noqa: E402  (offline operators only; the timed path is libosam.so)
 from paper_2511_20687_b200 import osam, problem  # noqa: E402
 
 
 def measure(name, steps, warmup=20):
     cfg = I.config(name)
     t0 = time.time()
-    ops = opinf.train(cfg, I) if "rom" in cfg else None
+    ops = problem.synthetic_rom_ops(cfg) if "rom" in cfg else None
     t_train = time.time() - t0
     stream = torch.cuda.current_stream()
     subs = problem.build(cfg, ops, stream=stream.cuda_stream)
