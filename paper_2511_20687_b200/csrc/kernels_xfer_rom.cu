@@ -157,54 +157,56 @@ __global__ void rom_predict_kernel(int r, int B, const double* __restrict__ uh, 
   us[t] = fma(0.5 * dt * dt, ah[t], fma(dt, vh[t], uh[t]));
 }
 
-// a^'[i,b] = e_b (-sum_j Kbar[i,j] u^*[j,b] + sum_k Bbar[i,k] g^[k,b]); v^', norm partials.
-// grid (ceil(r/256), B); slot = blockIdx.x; partial layout [slot][B].
+// a^'[i,b] = e_b (sum_j KBr[i,j] z[j,b]), z = [u^*; g^], KBr = [-Kbar | Bbar] row-major; v^', norm
+// partials.  A warp per output row (lanes stride the row: coalesced), 8 rows per block; the block's
+// partial (num, den) sums its warps in order: grid (ceil(r/8), B), slot = blockIdx.x, layout [slot][B].
 __global__ void __launch_bounds__(256) rom_update_kernel(const RomLaunch L, int mode) {
   __shared__ double red[2][8];
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = blockIdx.x * 8 + w;
   const int b = blockIdx.y;
-  const int r = L.r;
+  const int r = L.r, rz = L.r + L.r_b;
   const bool on = i < r && (mode == 1 || L.active[b]);
   double num = 0.0, den = 0.0;
   if (on) {
+    const double* row = L.KBr + (long long)i * rz;
     const double* us = L.ustar + (long long)r * b;
     const double* gh = L.gh + (long long)L.r_b * b;
     double acc = 0.0;
-    for (int j = 0; j < r; ++j) acc = fma(L.Kbar[i + (long long)r * j], us[j], acc);
-    double accb = 0.0;
-    for (int k = 0; k < L.r_b; ++k) accb = fma(L.Bbar[i + (long long)r * k], gh[k], accb);
-    const double an = L.e[b] * (accb - acc);
-    const long long id = i + (long long)r * b;
-    if (mode == 1) {  // acceleration only (initial condition)
-      L.ah1[id] = an;
-    } else {
-      const double vn = fma(0.5 * L.dt, L.ah0[id] + an, L.vh0[id]);
-      const double un = us[i];
-      if (L.with_norm) {
-        const double d = (un - L.uh1[id]) + L.dt * (vn - L.vh1[id]);
-        const double w = un + L.dt * vn;
-        num = d * d;
-        den = w * w;
+    for (int j = lane; j < r; j += 32) acc = fma(row[j], us[j], acc);
+    for (int k = lane; k < L.r_b; k += 32) acc = fma(row[r + k], gh[k], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      const double an = L.e[b] * acc;
+      const long long id = i + (long long)r * b;
+      if (mode == 1) {  // acceleration only (initial condition)
+        L.ah1[id] = an;
+      } else {
+        const double vn = fma(0.5 * L.dt, L.ah0[id] + an, L.vh0[id]);
+        const double un = us[i];
+        if (L.with_norm) {
+          const double d = (un - L.uh1[id]) + L.dt * (vn - L.vh1[id]);
+          const double wv = un + L.dt * vn;
+          num = d * d;
+          den = wv * wv;
+        }
+        L.uh1[id] = un;
+        L.vh1[id] = vn;
+        L.ah1[id] = an;
       }
-      L.uh1[id] = un;
-      L.vh1[id] = vn;
-      L.ah1[id] = an;
     }
   }
   if (mode == 1) return;
-  num = warp_sum(num);
-  den = warp_sum(den);
-  const int t = threadIdx.x;
-  if ((t & 31) == 0) {
-    red[0][t >> 5] = num;
-    red[1][t >> 5] = den;
+  if (lane == 0) {
+    red[0][w] = num;
+    red[1][w] = den;
   }
   __syncthreads();
-  if (t == 0) {
+  if (threadIdx.x == 0) {
     double a = 0.0, c = 0.0;
-    for (int w = 0; w < 8; ++w) {
-      a += red[0][w];
-      c += red[1][w];
+    for (int q = 0; q < 8; ++q) {
+      a += red[0][q];
+      c += red[1][q];
     }
     L.partial[(long long)blockIdx.x * L.B + b] = make_double2(a, c);
   }
@@ -278,7 +280,7 @@ void launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int min_
   debug_check("any_active_kernel", s);
 }
 
-int rom_partial_slots(int r) { return (int)cdiv(r, 256); }
+int rom_partial_slots(int r, bool tc) { return (int)(tc ? cdiv(r, 256) : cdiv(r, 8)); }
 
 void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches) {
   if (L.r_b > 0)
@@ -286,7 +288,7 @@ void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches) {
                                                                                  L.s, L.gh);
   rom_predict_kernel<<<cdiv((long long)L.r * L.B, 256), 256, 0, s>>>(L.r, L.B, L.uh0, L.vh0, L.ah0, L.dt, L.ustar);
   debug_check("rom_predict_kernel", s);
-  rom_update_kernel<<<dim3(cdiv(L.r, 256), L.B), 256, 0, s>>>(L, 0);
+  rom_update_kernel<<<dim3(cdiv(L.r, 8), L.B), 256, 0, s>>>(L, 0);
   debug_check("rom_update_kernel", s);
   *launches += (L.r_b > 0) + 2;
 }
@@ -298,7 +300,7 @@ void launch_rom_accel(const RomLaunch& L, const double* uh, double* ah, cudaStre
   if (L.r_b > 0)
     rom_project_bnd_kernel<<<dim3(L.r_b, L.B), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
                                                                                  L.s, L.gh);
-  rom_update_kernel<<<dim3(cdiv(L.r, 256), L.B), 256, 0, s>>>(A, 1);
+  rom_update_kernel<<<dim3(cdiv(L.r, 8), L.B), 256, 0, s>>>(A, 1);
   debug_check("rom_update_kernel", s);
   *launches += (L.r_b > 0) + 1;
 }

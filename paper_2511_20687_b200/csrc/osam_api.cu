@@ -173,6 +173,7 @@ void release_binding(Sub& s) {
   dfree(s.Phi_lift);
   dfree(s.lift_code);
   dfree(s.KB);
+  dfree(s.KBr);
   dfree(s.Z);
   dfree(s.part);
   s.bound = false;
@@ -355,6 +356,15 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
     // overrides the default, which is tensor cores iff batch > 1)
     const char* tc = getenv("OSAM_ROM_TC");
     s.use_tc = tc ? tc[0] == '1' : s.batch > 1;
+    {
+      const int rz = s.r + s.r_b;
+      std::vector<double> kbr((size_t)s.r * rz);
+      for (int q = 0; q < s.r; ++q) {
+        for (int j = 0; j < s.r; ++j) kbr[(size_t)q * rz + j] = -s.h_Kbar[(size_t)j * s.r + q];
+        for (int j = 0; j < s.r_b; ++j) kbr[(size_t)q * rz + s.r + j] = s.h_Bbar[(size_t)j * s.r + q];
+      }
+      TRY(upload(&s.KBr, kbr, s.stream));
+    }
     if (s.use_tc) {
       const int rz = s.r + s.r_b;
       std::vector<double> kb((size_t)s.r * rz);
@@ -523,6 +533,7 @@ int process_ic(Sub& s, int* launches) {
     L.Phi_s = s.Phi_s;
     L.Kbar = s.Kbar;
     L.Bbar = s.Bbar;
+    L.KBr = s.KBr;
     L.e = s.e;
     L.s = s.rst[c][3];
     L.gh = s.gh;
@@ -559,7 +570,7 @@ int get_group(osam_subdomain* const* sds, int n_sd, Group** out) {
     G->B = 1;
     for (auto s : subs) G->B = std::max(G->B, s->batch);
     G->n_slots = 0;
-    for (auto s : subs) G->n_slots += s->kind == OSAM_FOM ? fom_partial_slots(s->g, s->faces) : rom_partial_slots(s->r);
+    for (auto s : subs) G->n_slots += s->kind == OSAM_FOM ? fom_partial_slots(s->g, s->faces) : rom_partial_slots(s->r, s->use_tc);
     TRY(dalloc(&G->partial, (size_t)std::max(1, G->n_slots) * G->B));
     TRY(dalloc(&G->ctl_i, (size_t)G->ctl_len()));
     CK(cudaMemset(G->ctl_i, 0, sizeof(int) * G->ctl_len()));
@@ -679,6 +690,7 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
       L.Phi_s = d.Phi_s;
       L.Kbar = d.Kbar;
       L.Bbar = d.Bbar;
+      L.KBr = d.KBr;
       L.e = d.e;
       L.uh0 = d.rst[c][0];
       L.vh0 = d.rst[c][1];
@@ -703,7 +715,7 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
                         d.n_sdof, d.lift[1 - c], st);
         *launches += d.n_lift > 0;
       }
-      slot += rom_partial_slots(d.r);
+      slot += rom_partial_slots(d.r, d.use_tc);
     }
   }
   launch_finalize(ctl, G.partial, G.n_slots, B, cfg.min_iters, cfg.tol_rel, cfg.tol_abs, st);

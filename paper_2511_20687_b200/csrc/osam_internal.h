@@ -113,6 +113,7 @@ struct Sub {
   // batched ROM on the tensor cores (kernels_rom_tc.cu): [-Kbar | Bbar] and scratch
   bool use_tc = false;
   double* KB = nullptr;    // r x (r + r_b) column-major
+  double* KBr = nullptr;   // the same, row-major (CUDA-core path)
   double* Z = nullptr;     // (r + r_b) x B
   double* part = nullptr;  // split-K partial products (tc_part_size doubles)
 
@@ -158,6 +159,7 @@ struct RomLaunch {
   int r, r_b, B;
   long long n_sdof;
   const double *Phi_s, *Kbar, *Bbar, *e;
+  const double* KBr;  // [-Kbar | Bbar] row-major r x (r + r_b) (CUDA-core path)
   const double *uh0, *vh0, *ah0;  // checkpoint
   double *uh1, *vh1, *ah1;        // working
   const double* s;                // working Schwarz values (n_sdof x B)
@@ -167,7 +169,7 @@ struct RomLaunch {
   int with_norm;
   double2* partial;
 };
-int rom_partial_slots(int r);
+int rom_partial_slots(int r, bool tc);
 void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches);
 void launch_rom_lift(int r, int B, long long n_lift, const double* Phi_lift, const int* code, const double* uh,
                      const double* s, long long n_sdof, double* out, cudaStream_t st);
