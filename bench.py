@@ -71,6 +71,7 @@ def sample_cfg(cfg, lateral=SAMPLE_LATERAL):
     out = dict(cfg)
     subs = []
     ref = cfg["subdomains"][0]
+    lateral = min(lateral, ref["nel"][1], ref["nel"][2])  # a sample never grows the workload
     for s in cfg["subdomains"]:
         ny = max(1, round(lateral * s["nel"][1] / ref["nel"][1]))
         nz = max(1, round(lateral * s["nel"][2] / ref["nel"][2]))
@@ -119,6 +120,16 @@ def oracle_rate(cfg, warmup, steps=None, seconds=None):
     except Exception:
         threads = 1
     return sweeps * dofs / el, n, el, threads
+
+
+def max_over_ranks(x, dist, dev=None):
+    """Max of a per-rank float over all ranks (the timing rule: max over ranks); identity at N=1."""
+    if dist is None:
+        return float(x)
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def measured_peak():
@@ -256,10 +267,7 @@ def run_ours(args):
     osam.set_profiling(False)
     prof = osam.get_profile()
     prof_ms = p0.elapsed_time(p1)
-    if dist is not None:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, dist, dev)
     sweeps = int(iters.max(axis=1).sum())
     value = world * sweeps * fom_dofs / (ms / 1e3)
     steps_per_s = args.steps / (ms / 1e3)
@@ -278,11 +286,7 @@ def run_ours(args):
             n = h.numel() // 2
             sub.get_state(h[:n], h[n:])
         barrier()
-        el = time.perf_counter() - t0
-        if dist is not None:
-            t = torch.tensor([el], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
+        el = max_over_ranks(time.perf_counter() - t0, dist, dev)
         h2d = sum(f.nbytes for f in fields)
         d2h = sum(2 * f.nbytes for f in fields) + 4 * (2 + 2) * int(it2.sum())
         e2e = {"value": world * int(it2.max(axis=1).sum()) * fom_dofs / el, "unit": UNIT,

@@ -185,3 +185,38 @@ def test_invalid_arguments(gpu, c2_ops):
         osam.osam_step(subs, -1.0, 1e-10, 1)
     with pytest.raises(osam.OsamError):
         osam.osam_step(subs, cfg1["dt"], 1e-10, 1, min_iters=1)
+
+
+def test_graph_controller_equals_host_loop_bitwise(gpu):
+    """The CUDA-graph controller (device-side while-loop over sweeps) and the host-driven loop of
+    profiling mode run the same kernels in the same order: bitwise identical states and counts."""
+    from paper_2511_20687_b200 import osam
+    cfg = I.scaled(I.config("c3"), 10.0)
+    out = []
+    for prof in (False, True):
+        osam.set_profiling(prof)
+        try:
+            subs = gpu.build(cfg)
+            gpu.set_ics(cfg, subs, device="cuda:0")
+            _, it = gpu.run(cfg, subs, n_steps=7)
+            out.append((it, [gpu.fom_state(s) for s in subs]))
+        finally:
+            osam.set_profiling(False)
+    assert np.array_equal(out[0][0], out[1][0])
+    for a, b in zip(out[0][1], out[1][1]):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("max_iters", [1, 2])
+def test_max_iters_reached_keeps_last_iterate(gpu, max_iters):
+    """Hitting max_iters returns OSAM_WNOTCONVERGED (1) and keeps the last iterate (reading R9), equal to
+    the oracle run with the same cap."""
+    cfg = dict(I.config("c1"), max_iters=max_iters)
+    subs = gpu.build(cfg)
+    gpu.set_ics(cfg, subs, device="cuda:0")
+    status, iters = gpu.run(cfg, subs, n_steps=5)
+    assert status == 1
+    assert (iters == max_iters).all()
+    models, states, it_ref, _ = oracle_run(cfg, 5)
+    assert np.array_equal(iters, it_ref.reshape(iters.shape))
+    compare(gpu, subs, models, states)
