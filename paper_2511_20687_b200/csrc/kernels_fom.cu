@@ -41,14 +41,17 @@ namespace osam {
 namespace {
 
 constexpr int TX = 32;
-constexpr int TY = 8;
+#ifndef OSAM_TY
+#define OSAM_TY 8
+#endif
+constexpr int TY = OSAM_TY;
 constexpr int NT = TX * TY;
 constexpr int NWARP = NT / 32;
 #ifndef OSAM_EO
 #define OSAM_EO 0
 #endif
 #ifndef OSAM_ZC
-#define OSAM_ZC 8
+#define OSAM_ZC 12
 #endif
 constexpr int ZC = OSAM_ZC;  // target z-planes per block (balanced split)
 constexpr int XF_BLOCK = 128;
@@ -163,7 +166,10 @@ __device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int x, i
 constexpr int PX = TX + 4;
 constexpr int PY = TY + 2;
 constexpr int PLANE = PX * PY;                             // positions per staged plane
-constexpr int NSTAGE = 5;                                  // ring: 3 planes in flight, current, previous
+#ifndef OSAM_NSTAGE
+#define OSAM_NSTAGE 4
+#endif
+constexpr int NSTAGE = OSAM_NSTAGE;  // ring: NSTAGE-2 planes in flight, current, previous
 constexpr int ARR_BYTES = 3 * PLANE * 8;                   // X (x,y,z comps) of one plane, with halo
 constexpr int ARR_STRIDE = (ARR_BYTES + 127) / 128 * 128;  // 128-B aligned TMA destinations
 constexpr int WPL = TX * TY;                               // tile positions of W (no halo)
@@ -637,45 +643,57 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
   block_partial<NT>(num, den, L.partial, blockIdx.x);
 }
 
-// Nodes on an x-face with free DOFs (one per thread): gather X over the 18 neighbours inside
-// the box, class-table stencil.  side_mask bit 0: face x = 0, bit 1: face x = nx.
+// Nodes on an x-face with free DOFs: a group of 4 lanes per node, lane sub = 0, 1, 2 gathers the
+// plane oz = sub - 1 (6 positions: 2 in x, 3 in y; class-table stencil), the partial forces are summed
+// in the order sub = 0, 1, 2 by shuffles and lane sub = 0 finishes the node.  side_mask bit 0: face
+// x = 0, bit 1: face x = nx.
 __global__ void __launch_bounds__(XF_BLOCK) fom_xface_kernel(const FomLaunch L, int slot0, int side_mask) {
   const Geom& g = L.g;
   const long long np = g.npad;
   const long long nf = (long long)g.nn[1] * g.nn[2];
   const int nsides = (side_mask & 1) + ((side_mask >> 1) & 1);
-  const long long t = blockIdx.x * (long long)XF_BLOCK + threadIdx.x;
+  const long long t = (blockIdx.x * (long long)XF_BLOCK + threadIdx.x) >> 2;
+  const int sub = threadIdx.x & 3;
   const int nx = g.nn[0] - 1;
   double num = 0.0, den = 0.0;
-  if (t < nsides * nf) {
-    const int side = (side_mask == 2) ? 1 : (t >= nf ? 1 : 0);
-    const long long r = t - (t >= nf ? nf : 0);
-    const int i = side ? nx : 0;
-    const int j = (int)(r % g.nn[1]);
-    const int k = (int)(r / g.nn[1]);
-    const long long id = gidx(g, i, j, k);
-    const unsigned fm = free_mask(g, L.f, i, j, k);
-    const int cyj = axis_class(j, g.nn[1]), czk = axis_class(k, g.nn[2]);
+  const bool valid = t < nsides * nf;
+  const int side = (side_mask == 2) ? 1 : (t >= nf ? 1 : 0);
+  const long long r = t - (t >= nf ? nf : 0);
+  const int i = side ? nx : 0;
+  const int j = valid ? (int)(r % g.nn[1]) : 0;
+  const int k = valid ? (int)(r / g.nn[1]) : 0;
+  const int cyj = axis_class(j, g.nn[1]), czk = axis_class(k, g.nn[2]);
+  double f[3] = {0.0, 0.0, 0.0};
+  const int oz = sub - 1;
+  if (valid && sub < 3 && k + oz >= 0 && k + oz <= g.nn[2] - 1) {
     const double* coef = L.coef + (size_t)((side ? 2 : 0) + 3 * (cyj + 3 * czk)) * 27 * 9;
     const int oxlo = side ? -1 : 0;
-    const int kl = k > 0 ? -1 : 0, kh = k < g.nn[2] - 1 ? 1 : 0;
-    const int jl = j > 0 ? -1 : 0, jh = j < g.nn[1] - 1 ? 1 : 0;
-    double f[3] = {0.0, 0.0, 0.0};
-    for (int oz = kl; oz <= kh; ++oz) {
-      for (int oy = jl; oy <= jh; ++oy) {
 #pragma unroll
-        for (int dx = 0; dx < 2; ++dx) {
-          const int ox = oxlo + dx;
-          const long long q = gidx(g, i + ox, j + oy, k + oz);
-          const double x[3] = {__ldg(L.x + q), __ldg(L.x + np + q), __ldg(L.x + 2 * np + q)};
-          const double* cb = coef + ((ox + 1) + 3 * ((oy + 1) + 3 * (oz + 1))) * 9;
+    for (int oy = -1; oy <= 1; ++oy) {
+      if (j + oy < 0 || j + oy > g.nn[1] - 1) continue;
 #pragma unroll
-          for (int c = 0; c < 3; ++c)
+      for (int dx = 0; dx < 2; ++dx) {
+        const int ox = oxlo + dx;
+        const long long q = gidx(g, i + ox, j + oy, k + oz);
+        const double x[3] = {__ldg(L.x + q), __ldg(L.x + np + q), __ldg(L.x + 2 * np + q)};
+        const double* cb = coef + ((ox + 1) + 3 * ((oy + 1) + 3 * (oz + 1))) * 9;
 #pragma unroll
-            for (int d = 0; d < 3; ++d) f[c] = fma(__ldg(cb + c * 3 + d), x[d], f[c]);
-        }
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) f[c] = fma(__ldg(cb + c * 3 + d), x[d], f[c]);
       }
     }
+  }
+  // fixed-order sum over the group: ((f_0 + f_1) + f_2)
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double f1 = __shfl_down_sync(0xffffffffu, f[c], 1, 4);
+    const double f2 = __shfl_down_sync(0xffffffffu, f[c], 2, 4);
+    f[c] = (f[c] + f1) + f2;
+  }
+  if (valid && sub == 0) {
+    const long long id = gidx(g, i, j, k);
+    const unsigned fm = free_mask(g, L.f, i, j, k);
     const double inv_m = L.inv_mass[(cyj == 1 ? 2 : 0) + (czk == 1 ? 4 : 0)];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -813,7 +831,7 @@ int xface_sides(const Faces& f) {
 unsigned xface_blocks(const Geom& g, const Faces& f) {
   const int m = xface_sides(f);
   const int ns = (m & 1) + ((m >> 1) & 1);
-  return ns ? cdiv((long long)ns * g.nn[1] * g.nn[2], XF_BLOCK) : 0u;
+  return ns ? cdiv(4LL * ns * g.nn[1] * g.nn[2], XF_BLOCK) : 0u;
 }
 
 }  // namespace

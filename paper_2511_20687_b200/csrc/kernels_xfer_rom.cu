@@ -62,16 +62,18 @@ __global__ void step_begin_kernel(Ctl c, int B) {
   }
 }
 
-// one block of 256 threads per sample; the sweep that just ran is iteration n = *n_dev + 1
-__global__ void finalize_kernel(Ctl c, const double2* __restrict__ part, int n_slots, int B, int min_iters,
-                                double tol_rel, double tol_abs) {
-  __shared__ double red[2][8];
+// one block of FIN_T threads per sample; the sweep that just ran is iteration n = *n_dev + 1
+constexpr int FIN_T = 512;
+__global__ void __launch_bounds__(FIN_T) finalize_kernel(Ctl c, const double2* __restrict__ part, int n_slots, int B,
+                                                         int min_iters, double tol_rel, double tol_abs) {
+  __shared__ double red[2][FIN_T / 32];
   const int b = blockIdx.x;
   const int t = threadIdx.x;
   const int n = *c.n_dev + 1;
   double num = 0.0, den = 0.0;
   if (n >= min_iters) {
-    for (int s = t; s < n_slots; s += blockDim.x) {
+#pragma unroll 4
+    for (int s = t; s < n_slots; s += FIN_T) {
       const double2 v = part[(long long)s * B + b];
       num += v.x;
       den += v.y;
@@ -87,7 +89,7 @@ __global__ void finalize_kernel(Ctl c, const double2* __restrict__ part, int n_s
   if (t == 0) {
     num = 0.0;
     den = 0.0;
-    for (int w = 0; w < 8; ++w) {
+    for (int w = 0; w < FIN_T / 32; ++w) {
       num += red[0][w];
       den += red[1][w];
     }
@@ -274,7 +276,7 @@ void launch_step_begin(Ctl c, int B, cudaStream_t s) { step_begin_kernel<<<1, 25
 
 void launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int min_iters, double tol_rel,
                      double tol_abs, cudaStream_t s) {
-  finalize_kernel<<<B, 256, 0, s>>>(c, partial, n_slots, B, min_iters, tol_rel, tol_abs);
+  finalize_kernel<<<B, FIN_T, 0, s>>>(c, partial, n_slots, B, min_iters, tol_rel, tol_abs);
   debug_check("finalize_kernel", s);
   any_active_kernel<<<1, 1, 0, s>>>(c, B);
   debug_check("any_active_kernel", s);
