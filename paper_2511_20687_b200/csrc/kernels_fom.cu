@@ -174,12 +174,8 @@ constexpr int ARR_BYTES = 3 * PLANE * 8;                   // X (x,y,z comps) of
 constexpr int ARR_STRIDE = (ARR_BYTES + 127) / 128 * 128;  // 128-B aligned TMA destinations
 constexpr int WPL = TX * TY;                               // tile positions of W (no halo)
 constexpr int W_BYTES = 3 * WPL * 8;
-#ifdef OSAM_WP_LDG
-constexpr int STAGE_BYTES = ARR_STRIDE + W_BYTES;  // X, W (W'_prev read from global memory)
-#else
 constexpr int STAGE_BYTES = ARR_STRIDE + 2 * W_BYTES;  // X, W, W'_prev
-#endif
-constexpr int SMEM_TILED = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8;
+constexpr int SMEM_TILED = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8 + 64;  // ring, barriers, producer cursor
 #ifndef OSAM_PF
 #define OSAM_PF 3
 #endif
@@ -376,14 +372,22 @@ __device__ __forceinline__ TileGeo tile_geo(const Geom& g, const TileGrid& G, in
   return o;
 }
 
-// Per-thread constants of the current tile.
+// Per-thread constants of the current tile (kept small: every register counts for occupancy).
 struct Tile {
-  int qo, base, wo;
   int i, j;
-  bool active, xface, writer;
-  int cy, kbeg, kend, nplanes;
-  long long id0;
+  int kbeg, kend, nplanes;
+  unsigned flags;  // bit 0 active, bit 1 x-face lane, bit 2 writer, bits 3-4 cy (class of row j)
+  long long id0;   // node index of (i, j, 0)
+  __device__ __forceinline__ bool active() const { return flags & 1u; }
+  __device__ __forceinline__ bool xface() const { return flags & 2u; }
+  __device__ __forceinline__ bool writer() const { return flags & 4u; }
+  __device__ __forceinline__ int cy() const { return (int)((flags >> 3) & 3u); }
 };
+
+// staged positions of this thread: own node, (-1,-1) neighbour, W tile position
+__device__ __forceinline__ int pos_own() { return ((int)threadIdx.y + 1) * PX + ((int)threadIdx.x + 2); }
+__device__ __forceinline__ int pos_base() { return (int)threadIdx.y * PX + (int)threadIdx.x + 1; }
+__device__ __forceinline__ int pos_w() { return (int)threadIdx.y * TX + (int)threadIdx.x; }
 
 struct Maps {
   const CUtensorMap *x, *w, *wp;
@@ -394,39 +398,24 @@ __device__ __forceinline__ void issue_plane(const FomLaunch& L, const TileGeo& P
                                             unsigned long long* full, const Maps& M) {
   unsigned char* st = ring + (size_t)s * STAGE_BYTES;
   const int m = P.kbeg - 1 + it;
-#ifdef OSAM_WP_LDG
-  mbar_expect_tx(&full[s], ARR_BYTES + W_BYTES);
-#else
   mbar_expect_tx(&full[s], ARR_BYTES + (L.with_norm ? 2 : 1) * W_BYTES);
-#endif
   tma_load_4d(st, M.x, P.x0, P.y0, m, 0, &full[s]);
   tma_load_4d(st + ARR_STRIDE, M.w, P.x0 + 2, P.y0 + 1, m, 0, &full[s]);
-#ifndef OSAM_WP_LDG
   if (L.with_norm) tma_load_4d(st + ARR_STRIDE + W_BYTES, M.wp, P.x0 + 2, P.y0 + 1, m, 0, &full[s]);
-#endif
 }
 
-// Ring bookkeeping over the CTA's whole plane stream (all its tiles, in order).
-struct Ring {
-  int s;         // stage of the current plane
-  int sp;        // stage of the previous plane
-  int sn;        // stage the producer fills next
-  int gi;        // planes consumed so far (all tiles)
-  unsigned fph;  // bit s: parity of the next completion of full[s]
-  unsigned eph;  // bit s: parity of the next completion of empty[s]
-};
-
-// Producer cursor (thread 0 only): the next plane to load, possibly in a later tile of this CTA.
+// Producer cursor (thread 0 only, in shared memory): the next plane to load, possibly in a later
+// tile of this CTA.  Plane p of the CTA's stream lives in stage p % NSTAGE.
 struct Prod {
-  int t;      // tile (>= ntiles: done)
-  int it;     // plane within the tile
-  int issued; // planes issued so far (all tiles)
+  int t;       // tile (>= ntiles: done)
+  int it;      // plane within the tile
+  int issued;  // planes issued so far (all tiles)
   TileGeo P;
 };
 
-__device__ __forceinline__ void prod_issue(const FomLaunch& L, const TileGrid& G, Prod& pr, int s, unsigned char* ring,
+__device__ __forceinline__ void prod_issue(const FomLaunch& L, const TileGrid& G, Prod& pr, unsigned char* ring,
                                            unsigned long long* full, const Maps& M) {
-  issue_plane(L, pr.P, pr.it, s, ring, full, M);
+  issue_plane(L, pr.P, pr.it, pr.issued % NSTAGE, ring, full, M);
   ++pr.issued;
   if (++pr.it == pr.P.nplanes) {
     pr.it = 0;
@@ -435,52 +424,43 @@ __device__ __forceinline__ void prod_issue(const FomLaunch& L, const TileGrid& G
   }
 }
 
-// One staged plane (iteration it of the tile, staged plane m = kbeg - 1 + it).  Accumulator slots
-// rotate by role: A = acc[SA] (node plane m+1), B = acc[SB] (plane m), C = acc[SC] (plane m-1,
-// finished here if it lies in [kbeg, kend], then zeroed to become the next A).  Targets outside the
-// chunk are accumulated too (and never used): that keeps every iteration identical.
+// One staged plane (iteration it of the tile, plane gi of the CTA's stream, staged plane
+// m = kbeg - 1 + it).  Accumulator slots rotate by role: A = acc[SA] (node plane m+1), B = acc[SB]
+// (plane m), C = acc[SC] (plane m-1, finished here if it lies in [kbeg, kend], then zeroed to become
+// the next A).  Targets outside the chunk are accumulated too (and never used): every iteration is
+// identical.
 template <int SA, int SB, int SC>
-__device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStencil& S, const Tile& T, int it,
+__device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStencil& S, const Tile& T, int it, int gi,
                                         double (&acc)[3][3], double& num, double& den, unsigned char* ring,
-                                        unsigned long long* full, unsigned long long* empty, const Maps& M, Ring& R,
-                                        Prod& pr, const TileGrid& G, bool lead) {
+                                        unsigned long long* full, unsigned long long* empty, const Maps& M, Prod* pr,
+                                        const TileGrid& G) {
   const Geom& g = L.g;
   const int nz = g.nn[2] - 1;
   const long long np = g.npad;
   const int m = T.kbeg - 1 + it;
   const int kf = m - 1;
-  const bool fin = T.writer && kf >= T.kbeg && kf <= T.kend;
-#ifdef OSAM_WP_LDG
-  double qwr[3] = {0.0, 0.0, 0.0};  // previous iterate's W' (norm), issued before the waits
-  if (fin && L.with_norm && !T.xface) {
-    const long long idp = T.id0 + (long long)kf * g.plane;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) qwr[c] = L.w_out[c * np + idp];
+  const bool fin = T.writer() && kf >= T.kbeg && kf <= T.kend;
+  // producer: plane gi + NSTAGE - 2 into the stage released by plane gi - 2
+  if (threadIdx.x + threadIdx.y == 0 && pr->t < G.count()) {
+    const int p = pr->issued;
+    if (p >= NSTAGE) mbar_wait(&empty[p % NSTAGE], (unsigned)(((p - NSTAGE) / NSTAGE) & 1));
+    prod_issue(L, G, *pr, ring, full, M);
   }
-#endif
-  // producer: fill the next plane of the stream into the stage released by plane gi - 2
-  if (lead && pr.t < G.count()) {
-    if (R.gi >= 2) {
-      mbar_wait(&empty[R.sn], (R.eph >> R.sn) & 1u);
-      R.eph ^= 1u << R.sn;
-    }
-    prod_issue(L, G, pr, R.sn, ring, full, M);
-  }
-  mbar_wait(&full[R.s], (R.fph >> R.s) & 1u);
-  R.fph ^= 1u << R.s;
-  const double* xs = reinterpret_cast<const double*>(ring + (size_t)R.s * STAGE_BYTES);
-  if (T.active) {
+  const int s = gi % NSTAGE;
+  mbar_wait(&full[s], (unsigned)((gi / NSTAGE) & 1));
+  const double* xs = reinterpret_cast<const double*>(ring + (size_t)s * STAGE_BYTES);
+  if (T.active()) {
     double* A = acc[SA];
     double* B = acc[SB];
     double* C = acc[SC];
 #ifdef OSAM_NOCOMPUTE
     if (false) {
 #else
-    if (T.cy == 1 && m >= 2 && m <= nz - 2) {
-      plane_fast<true, true, true>(A, B, C, xs, T.base, S);
+    if (T.cy() == 1 && m >= 2 && m <= nz - 2) {
+      plane_fast<true, true, true>(A, B, C, xs, pos_base(), S);
     } else {
 #endif
-      const Contrib3 r = plane_slow(xs, T.base, T.cy, axis_class(m + 1, g.nn[2]), axis_class(m, g.nn[2]),
+      const Contrib3 r = plane_slow(xs, pos_base(), T.cy(), axis_class(m + 1, g.nn[2]), axis_class(m, g.nn[2]),
                                     axis_class(kf, g.nn[2]), L.rowc);
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -490,53 +470,41 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
       }
     }
     if (fin) {
-      // own X, W, W'_prev of plane kf, staged in iteration it-1 (released at the end of this one)
-      const unsigned char* sp = ring + (size_t)R.sp * STAGE_BYTES;
-      const double* xo = reinterpret_cast<const double*>(sp) + T.qo;
-      const double* wo = reinterpret_cast<const double*>(sp + ARR_STRIDE) + T.wo;
-#ifdef OSAM_WP_LDG
-      const double* qw = qwr;
-      constexpr int QWS = 1;
-#else
-      const double* qw = reinterpret_cast<const double*>(sp + ARR_STRIDE + W_BYTES) + T.wo;
-      constexpr int QWS = WPL;
-#endif
+      // own X, W, W'_prev of plane kf, staged in the previous iteration (released at the end of this one)
+      const unsigned char* sp = ring + (size_t)((gi + NSTAGE - 1) % NSTAGE) * STAGE_BYTES;
+      const double* xo = reinterpret_cast<const double*>(sp) + pos_own();
+      const double* wo = reinterpret_cast<const double*>(sp + ARR_STRIDE) + pos_w();
+      const double* qw = reinterpret_cast<const double*>(sp + ARR_STRIDE + W_BYTES) + pos_w();
       const long long id = T.id0 + (long long)kf * g.plane;
       const int cz = axis_class(kf, g.nn[2]);
-      if (T.xface) {  // fully constrained x-face node: Q' = X (prescribed), W' = a = 0
+      if (T.xface()) {  // fully constrained x-face node: Q' = X (prescribed), W' = a = 0
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           if (L.q_out) L.q_out[c * np + id] = xo[c * PLANE];
           L.w_out[c * np + id] = 0.0;
           if (L.a_out) L.a_out[c * np + id] = 0.0;
         }
-      } else if (T.cy == 1 && cz == 1 && L.a_out == nullptr && L.q_out != nullptr) {  // interior node
+      } else if (T.cy() == 1 && cz == 1 && L.a_out == nullptr && L.q_out != nullptr) {  // interior node
         const double inv_m = L.inv_mass[7];
         double* qo = L.q_out + id;
         double* wp = L.w_out + id;
-        double an[3], wn[3], x[3], w0[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          x[c] = xo[c * PLANE];
-          w0[c] = wo[c * WPL];
-          an[c] = -C[c] * inv_m;
-          wn[c] = fma(L.cw, an[c], w0[c]);
-          qo[c * np] = fma(L.cq, wn[c], x[c]);
-          wp[c * np] = wn[c];
-        }
-        if (L.with_norm) {
-          const double hdt = 0.5 * L.dt;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const double d = hdt * (wn[c] - qw[c * QWS]);
-            const double w = fma(L.dt, fma(L.cv, an[c], w0[c]), x[c]);
+          const double x = xo[c * PLANE], w0 = wo[c * WPL];
+          const double an = -C[c] * inv_m;
+          const double wn = fma(L.cw, an, w0);
+          qo[c * np] = fma(L.cq, wn, x);
+          wp[c * np] = wn;
+          if (L.with_norm) {
+            const double d = 0.5 * L.dt * (wn - qw[c * WPL]);
+            const double w = fma(L.dt, fma(L.cv, an, w0), x);
             num = fma(d, d, num);
             den = fma(w, w, den);
           }
         }
       } else {
-        const unsigned fm = (T.cy != 1 || cz != 1) ? free_mask(g, L.f, T.i, T.j, kf) : 7u;
-        const double inv_m = L.inv_mass[1 + 2 * (T.cy == 1) + 4 * (cz == 1)];
+        const unsigned fm = (T.cy() != 1 || cz != 1) ? free_mask(g, L.f, T.i, T.j, kf) : 7u;
+        const double inv_m = L.inv_mass[1 + 2 * (T.cy() == 1) + 4 * (cz == 1)];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const double x = xo[c * PLANE];
@@ -547,7 +515,7 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
             wn = fma(L.cw, an, w0);
             qn = fma(L.cq, wn, x);
             if (L.with_norm) {
-              const double d = 0.5 * L.dt * (wn - qw[c * QWS]);
+              const double d = 0.5 * L.dt * (wn - qw[c * WPL]);
               const double w = fma(L.dt, fma(L.cv, an, w0), x);
               num = fma(d, d, num);
               den = fma(w, w, den);
@@ -562,16 +530,11 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
   }
   // this warp is done with the previous plane of the stream (own values above, stencil before)
   __syncwarp();
-  if (R.gi >= 1 && (threadIdx.x & 31) == 0) mbar_arrive(&empty[R.sp]);
+  if (gi >= 1 && (threadIdx.x & 31) == 0) mbar_arrive(&empty[(gi + NSTAGE - 1) % NSTAGE]);
 #pragma unroll
   for (int c = 0; c < 3; ++c) acc[SC][c] = 0.0;
-  ++R.gi;
-  R.sp = R.s;
-  R.s = R.s + 1 == NSTAGE ? 0 : R.s + 1;
-  if (lead) R.sn = R.sn + 1 == NSTAGE ? 0 : R.sn + 1;
 }
 
-// Persistent: CTA b processes tiles b, b + gridDim.x, ... with one continuous TMA plane stream.
 #ifndef OSAM_MINB
 #define OSAM_MINB 2
 #endif
@@ -583,13 +546,12 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
   unsigned char* ring = smem;
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + NSTAGE * STAGE_BYTES);
   unsigned long long* empty = full + NSTAGE;
+  Prod* pr = reinterpret_cast<Prod*>(empty + NSTAGE);
   const Geom& g = L.g;
   const int nx = g.nn[0] - 1, ny = g.nn[1] - 1;
   const Maps M{&tmx, &tmw, &tmwp};
   const TileGrid G = tile_grid(g);
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int t = ty * TX + tx;
-  const bool lead = t == 0;
+  const bool lead = threadIdx.x + threadIdx.y == 0;
 
   if (lead) {
     for (int s = 0; s < NSTAGE; ++s) {
@@ -597,42 +559,42 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
       mbar_init(&empty[s], NWARP);
     }
     mbar_fence_init();
+    pr->t = blockIdx.x;
+    pr->it = 0;
+    pr->issued = 0;
+    if (pr->t < G.count()) {
+      pr->P = tile_geo(g, G, pr->t);
+      for (int p = 0; p < NSTAGE - 2 && pr->t < G.count(); ++p) prod_issue(L, G, *pr, ring, full, M);
+    }
   }
   __syncthreads();
-  Ring R{0, NSTAGE - 1, 0, 0, 0u, 0u};
-  Prod pr{(int)blockIdx.x, 0, 0, TileGeo{}};
-  if (lead) {
-    if (pr.t < G.count()) pr.P = tile_geo(g, G, pr.t);
-    for (int p = 0; p < NSTAGE - 2 && pr.t < G.count(); ++p) prod_issue(L, G, pr, p, ring, full, M);
-    R.sn = pr.issued % NSTAGE;
-  }
 
   double acc[3][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
   double num = 0.0, den = 0.0;
+  int gi = 0;
   for (int tile = blockIdx.x; tile < G.count(); tile += gridDim.x) {
     const TileGeo P = tile_geo(g, G, tile);
     Tile T;
-    T.i = P.x0 + 2 + tx;
-    T.j = P.y0 + 1 + ty;
-    T.active = (T.i <= nx) && (T.j <= ny);
-    T.xface = (T.i == 0) || (T.i == nx);
+    T.i = P.x0 + 2 + (int)threadIdx.x;
+    T.j = P.y0 + 1 + (int)threadIdx.y;
+    const bool active = (T.i <= nx) && (T.j <= ny);
+    const bool xface = (T.i == 0) || (T.i == nx);
     const int xsd = T.i == 0 ? 0 : 1;
-    const bool xf_full = T.xface && (L.f.dir[xsd] == 7 || L.f.sw[xsd]);
-    T.writer = T.active && (!T.xface || xf_full);
-    T.cy = axis_class(T.j, g.nn[1]);  // warp-uniform (a warp is one x-row)
+    const bool writer = active && (!xface || L.f.dir[xsd] == 7 || L.f.sw[xsd]);
+    T.flags = (active ? 1u : 0u) | (xface ? 2u : 0u) | (writer ? 4u : 0u) | ((unsigned)axis_class(T.j, g.nn[1]) << 3);
     T.kbeg = P.kbeg;
     T.kend = P.kend;
     T.nplanes = P.nplanes;
-    T.qo = (ty + 1) * PX + (tx + 2);
-    T.base = ty * PX + tx + 1;
-    T.wo = t;
     T.id0 = T.i + (long long)g.px * T.j;
     for (int it = 0; it < T.nplanes;) {  // unrolled by the period 3 of the slot rotation
-      k1_iter<0, 1, 2>(L, S, T, it, acc, num, den, ring, full, empty, M, R, pr, G, lead);
+      k1_iter<0, 1, 2>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
+      ++gi;
       if (++it >= T.nplanes) break;
-      k1_iter<2, 0, 1>(L, S, T, it, acc, num, den, ring, full, empty, M, R, pr, G, lead);
+      k1_iter<2, 0, 1>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
+      ++gi;
       if (++it >= T.nplanes) break;
-      k1_iter<1, 2, 0>(L, S, T, it, acc, num, den, ring, full, empty, M, R, pr, G, lead);
+      k1_iter<1, 2, 0>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
+      ++gi;
       ++it;
     }
 #pragma unroll
