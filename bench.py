@@ -43,6 +43,7 @@ def parse():
     p.add_argument("--workload", default="c3")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-largest", action="store_true", help="skip the c4 (largest config) K1 roofline entry")
     return p.parse_args()
 
 
@@ -210,6 +211,61 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def k1_profile(cfg, subs, stream, dev, steps):
+    """K1 launch timing: `steps` controller steps in profiling mode (host-driven sweeps, a CUDA event
+    pair around every K1 launch on the subdomains' stream).  Returns (profile dict, elapsed ms)."""
+    import torch
+    from paper_2511_20687_b200 import osam, problem
+    osam.set_profiling(True)
+    osam.reset_profile()
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    problem.run(cfg, subs, n_steps=steps)
+    p1.record(stream)
+    torch.cuda.synchronize(dev)
+    osam.set_profiling(False)
+    return osam.get_profile(), p0.elapsed_time(p1)
+
+
+def roofline_of(prof, prof_ms, peak):
+    k1_ms = prof["k1_ms"] / max(1, prof["k1_launches"])
+    achieved = prof["k1_bytes"] / max(1, prof["k1_launches"]) / (k1_ms / 1e3) / 1e9
+    return {"achieved": achieved, "frac": achieved / peak, "k1_ms_per_launch": k1_ms,
+            "k1_share_of_step": prof["k1_ms"] / prof_ms}
+
+
+def largest_config(dev, stream, steps=30, warmup=3):
+    """North_star's HBM target is stated on the largest config (c4: 256^3 FOM between two r = 200
+    ROMs with stand-in operators): steps/s and the K1 roofline there, measured the same way."""
+    import torch
+    from paper_2511_20687_b200 import problem
+    cfg = I.config("c4")
+    desc, fom_dofs = workload_desc(cfg)
+    subs = problem.build(cfg, workload_ops(cfg), stream=stream.cuda_stream)
+    for sub, f in zip(subs, problem.initial_fields(cfg)):
+        sub.set_ic(torch.from_numpy(f).to(dev))
+    problem.run(cfg, subs, n_steps=warmup)
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    _, iters = problem.run(cfg, subs, n_steps=steps)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    prof, prof_ms = k1_profile(cfg, subs, stream, dev, 10)
+    peak, _ = measured_peak()
+    out = {"workload": f"c4: {desc} ({fom_dofs} FOM DOFs; ROM operators: seeded stand-ins of the trained sizes)",
+           "steps": steps, "schwarz_steps_per_s": 1e3 * steps / ms,
+           "fom_dof_updates_per_s": int(iters.max(axis=1).sum()) * fom_dofs / (ms / 1e3),
+           "schwarz_iters_per_step": float(iters.max(axis=1).mean()),
+           "roofline": dict(bound="hbm", peak=peak, unit="GB/s", **roofline_of(prof, prof_ms, peak))}
+    for sub in subs:
+        sub.close()
+    return out
+
+
 def run_ours(args):
     import torch
     world, rank, local = dist_env()
@@ -253,20 +309,9 @@ def run_ours(args):
     ck = clocks.stop()
     launches = osam.get_profile()["kernel_launches"]
     ms = e0.elapsed_time(e1)
-    # K1 roofline: the same steps again in profiling mode (host-driven sweeps, a CUDA event pair
-    # around every K1 launch on the subdomains' stream)
+    # K1 roofline: the same steps again in profiling mode
     prof_steps = max(3, min(args.steps, 30))
-    osam.set_profiling(True)
-    osam.reset_profile()
-    p0 = torch.cuda.Event(enable_timing=True)
-    p1 = torch.cuda.Event(enable_timing=True)
-    p0.record(stream)
-    problem.run(cfg, subs, n_steps=prof_steps)
-    p1.record(stream)
-    torch.cuda.synchronize(dev)
-    osam.set_profiling(False)
-    prof = osam.get_profile()
-    prof_ms = p0.elapsed_time(p1)
+    prof, prof_ms = k1_profile(cfg, subs, stream, dev, prof_steps)
     ms = max_over_ranks(ms, dist, dev)
     sweeps = int(iters.max(axis=1).sum())
     value = world * sweeps * fom_dofs / (ms / 1e3)
@@ -305,7 +350,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.workload}: {desc} ({fom_dofs} FOM DOFs)",
-                       "l2": "inputs larger than L2 (checkpoint+working state 2 x 3 x 8 B x DOFs = 2.0 GB)",
+                       "l2": "inputs larger than L2 (two state buffers x (q, w) x 8 B x FOM DOFs, > 126 MB)",
                        "parallelism": "replicas" if world > 1 else "1 GPU"},
             "schwarz_steps_per_s": world * steps_per_s,
             "schwarz_iters_per_step": float(iters.max(axis=1).mean()),
@@ -319,6 +364,8 @@ def run_ours(args):
                          "peak_source": peak_src},
             "gpu_launches": int(launches),
             "clocks": ck, "e2e": e2e}
+    if world == 1 and not args.no_largest and args.workload != "c4":
+        line["largest_config"] = largest_config(dev, stream)
     if world == 1 and not args.no_cpu_baseline:
         sample = sample_cfg(cfg)
         sdesc, _ = workload_desc(sample)

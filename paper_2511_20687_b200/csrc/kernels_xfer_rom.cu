@@ -10,6 +10,8 @@
 // K5  u^* = u^ + dt v^ + dt^2/2 a^ ; a^' = e_b(-Kbar u^* + Bbar g^) ; v^' = v^ + dt/2 (a^ + a^')
 //     plus reduced-coordinate norm partials (reading R8)  (P:L617-722 eq:schwarz_opinf_discrete)
 // K6  lift at donor nodes: Phi[donor rows] u^* (free), 0 (Dirichlet), own s (Schwarz)
+#include <algorithm>
+
 #include "osam_internal.h"
 
 namespace osam {
@@ -63,7 +65,7 @@ __global__ void step_begin_kernel(Ctl c, int B) {
 }
 
 // one block of FIN_T threads per sample; the sweep that just ran is iteration n = *n_dev + 1
-constexpr int FIN_T = 512;
+constexpr int FIN_T = 1024;
 __global__ void __launch_bounds__(FIN_T) finalize_kernel(Ctl c, const double2* __restrict__ part, int n_slots, int B,
                                                          int min_iters, double tol_rel, double tol_abs) {
   __shared__ double red[2][FIN_T / 32];
@@ -139,17 +141,21 @@ __device__ __forceinline__ double block_sum256(double v) {
   return t;
 }
 
-// g^[k, b] = sum_q Phi_s[q, k] s[q, b]  (a block per output; thread-strided, fixed order)
+// Partial g^: gpart[z][b][k] = sum over chunk z of the Schwarz DOFs of Phi_s[q, k] s[q, b]
+// (a block per (k, chunk, sample); thread-strided, fixed order).  The consumer sums the chunks in order.
+constexpr int GCHUNK = 2048;
 __global__ void __launch_bounds__(256) rom_project_bnd_kernel(int r_b, int B, long long ns,
                                                               const double* __restrict__ Phi_s,
-                                                              const double* __restrict__ s, double* __restrict__ gh) {
-  const int k = blockIdx.x, b = blockIdx.y;
+                                                              const double* __restrict__ s,
+                                                              double* __restrict__ gpart) {
+  const int k = blockIdx.x, z = blockIdx.y, b = blockIdx.z;
   const double* col = Phi_s + (long long)k * ns;
   const double* sb = s + (long long)b * ns;
+  const long long q0 = (long long)z * GCHUNK, q1 = q0 + GCHUNK < ns ? q0 + GCHUNK : ns;
   double acc = 0.0;
-  for (long long q = threadIdx.x; q < ns; q += 256) acc = fma(col[q], sb[q], acc);
+  for (long long q = q0 + threadIdx.x; q < q1; q += 256) acc = fma(col[q], sb[q], acc);
   acc = block_sum256(acc);
-  if (threadIdx.x == 0) gh[k + (long long)r_b * b] = acc;
+  if (threadIdx.x == 0) gpart[((long long)z * B + b) * r_b + k] = acc;
 }
 
 __global__ void rom_predict_kernel(int r, int B, const double* __restrict__ uh, const double* __restrict__ vh,
@@ -173,10 +179,13 @@ __global__ void __launch_bounds__(256) rom_update_kernel(const RomLaunch L, int 
   if (on) {
     const double* row = L.KBr + (long long)i * rz;
     const double* us = L.ustar + (long long)r * b;
-    const double* gh = L.gh + (long long)L.r_b * b;
     double acc = 0.0;
     for (int j = lane; j < r; j += 32) acc = fma(row[j], us[j], acc);
-    for (int k = lane; k < L.r_b; k += 32) acc = fma(row[r + k], gh[k], acc);
+    for (int k = lane; k < L.r_b; k += 32) {
+      double g = 0.0;  // g^[k, b]: chunk partials in order
+      for (int z = 0; z < L.gchunks; ++z) g += L.gh[((long long)z * L.B + b) * L.r_b + k];
+      acc = fma(row[r + k], g, acc);
+    }
     acc = warp_sum(acc);
     if (lane == 0) {
       const double an = L.e[b] * acc;
@@ -215,6 +224,7 @@ __global__ void __launch_bounds__(256) rom_update_kernel(const RomLaunch L, int 
 }
 
 // out[b][ld] = code>=0 ? sum_j Phi_lift[ld, j] uh[j, b] : (code == -1 ? 0 : s[b][-2-code])
+// (a warp per row; 16-byte loads when r is even)
 __global__ void rom_lift_kernel(int r, int B, long long nl, const double* __restrict__ Phi_lift,
                                 const int* __restrict__ code, const double* __restrict__ uh,
                                 const double* __restrict__ s, long long ns, double* __restrict__ out) {
@@ -229,7 +239,18 @@ __global__ void rom_lift_kernel(int r, int B, long long nl, const double* __rest
     const double* row = Phi_lift + (long long)cd * r;
     const double* u = uh + (long long)r * b;
     double acc = 0.0;
-    for (int j = lane; j < r; j += 32) acc = fma(row[j], u[j], acc);
+    if ((r & 1) == 0) {
+      const double2* row2 = reinterpret_cast<const double2*>(row);
+      const double2* u2 = reinterpret_cast<const double2*>(u);
+#pragma unroll 4
+      for (int j = lane; j < r / 2; j += 32) {
+        const double2 a = row2[j], x = u2[j];
+        acc = fma(a.x, x.x, acc);
+        acc = fma(a.y, x.y, acc);
+      }
+    } else {
+      for (int j = lane; j < r; j += 32) acc = fma(row[j], u[j], acc);
+    }
     v = warp_sum(acc);
   } else if (cd <= -2) {
     v = s[(long long)b * ns + (-2 - cd)];
@@ -282,12 +303,14 @@ void launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int min_
   debug_check("any_active_kernel", s);
 }
 
+int rom_gchunks(long long n_s) { return (int)std::max<long long>(1, cdiv(n_s, GCHUNK)); }
+
 int rom_partial_slots(int r, bool tc) { return (int)(tc ? cdiv(r, 256) : cdiv(r, 8)); }
 
 void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches) {
   if (L.r_b > 0)
-    rom_project_bnd_kernel<<<dim3(L.r_b, L.B), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
-                                                                                 L.s, L.gh);
+    rom_project_bnd_kernel<<<dim3(L.r_b, rom_gchunks(L.n_sdof), L.B), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
+                                                                                   L.s, L.gh);
   rom_predict_kernel<<<cdiv((long long)L.r * L.B, 256), 256, 0, s>>>(L.r, L.B, L.uh0, L.vh0, L.ah0, L.dt, L.ustar);
   debug_check("rom_predict_kernel", s);
   rom_update_kernel<<<dim3(cdiv(L.r, 8), L.B), 256, 0, s>>>(L, 0);
@@ -300,8 +323,8 @@ void launch_rom_accel(const RomLaunch& L, const double* uh, double* ah, cudaStre
   A.ustar = const_cast<double*>(uh);
   A.ah1 = ah;
   if (L.r_b > 0)
-    rom_project_bnd_kernel<<<dim3(L.r_b, L.B), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
-                                                                                 L.s, L.gh);
+    rom_project_bnd_kernel<<<dim3(L.r_b, rom_gchunks(L.n_sdof), L.B), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
+                                                                                   L.s, L.gh);
   rom_update_kernel<<<dim3(cdiv(L.r, 8), L.B), 256, 0, s>>>(A, 1);
   debug_check("rom_update_kernel", s);
   *launches += (L.r_b > 0) + 1;

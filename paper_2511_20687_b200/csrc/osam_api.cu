@@ -351,7 +351,7 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
       TRY(dalloc(&s.rst[b][3], (size_t)std::max<long long>(1, s.n_sdof) * s.batch));
     }
     TRY(dalloc(&s.ustar, (size_t)s.r * s.batch));
-    TRY(dalloc(&s.gh, (size_t)std::max(1, s.r_b) * s.batch));
+    TRY(dalloc(&s.gh, (size_t)std::max(1, s.r_b) * s.batch * rom_gchunks(s.n_sdof)));
     // batched samples: the reduced update is a dense contraction -> FP64 tensor cores (OSAM_ROM_TC=0/1
     // overrides the default, which is tensor cores iff batch > 1)
     const char* tc = getenv("OSAM_ROM_TC");
@@ -537,6 +537,7 @@ int process_ic(Sub& s, int* launches) {
     L.e = s.e;
     L.s = s.rst[c][3];
     L.gh = s.gh;
+    L.gchunks = rom_gchunks(s.n_sdof);
     if (s.use_tc) {
       launch_rom_accel_tc(L, s.rst[c][0], s.rst[c][2], s.KB, s.Z, s.part, st, launches);
       launch_rom_lift_tc(s.r, s.batch, 3 * s.n_lift, s.Phi_lift, s.lift_code, s.rst[c][0], s.rst[c][3], s.n_sdof,
@@ -701,6 +702,7 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
       L.s = d.rst[1 - c][3];
       L.ustar = d.ustar;
       L.gh = d.gh;
+      L.gchunks = rom_gchunks(d.n_sdof);
       L.active = ctl.active;
       L.dt = cfg.dt;
       L.with_norm = with_norm;

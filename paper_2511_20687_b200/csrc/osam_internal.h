@@ -163,13 +163,15 @@ struct RomLaunch {
   const double *uh0, *vh0, *ah0;  // checkpoint
   double *uh1, *vh1, *ah1;        // working
   const double* s;                // working Schwarz values (n_sdof x B)
-  double *ustar, *gh;
+  double *ustar, *gh;  // gh: partial g^ [gchunks][B][r_b] (CUDA-core path)
+  int gchunks;
   const int* active;
   double dt;
   int with_norm;
   double2* partial;
 };
 int rom_partial_slots(int r, bool tc);
+int rom_gchunks(long long n_s);  // chunks of the partial boundary projection (CUDA-core path)
 void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches);
 void launch_rom_lift(int r, int B, long long n_lift, const double* Phi_lift, const int* code, const double* uh,
                      const double* s, long long n_sdof, double* out, cudaStream_t st);

@@ -4,7 +4,7 @@ set -x
 TAG=${1:-r}
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-B="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e"
+B="python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e --no-largest"
 nvidia-smi > gpurun_out/smi_$TAG.txt 2>&1
 timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > gpurun_out/smoke_$TAG.log 2>&1
 timeout 1500 python -m pytest tests -m gpu -q -rA --timeout 900 -x > gpurun_out/pytest_gpu_$TAG.log 2>&1
