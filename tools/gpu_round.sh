@@ -9,6 +9,8 @@ nvidia-smi > gpurun_out/smi_$TAG.txt 2>&1
 timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' > gpurun_out/smoke_$TAG.log 2>&1
 timeout 1500 python -m pytest tests -m gpu -q -rA --timeout 900 -x > gpurun_out/pytest_gpu_$TAG.log 2>&1
 timeout 600 python bench.py > gpurun_out/bench_$TAG.log 2>&1
+# ncu cannot profile kernel nodes of graphs with conditional nodes: host-driven sweeps for ncu
+export OSAM_NOGRAPH=1
 timeout 300 $B > gpurun_out/plain_$TAG.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $B > gpurun_out/ncu1_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:fom_ -s 8 -c 4 -o gpurun_out/prof_$TAG $B > gpurun_out/ncu2_$TAG.log 2>&1
 echo done
