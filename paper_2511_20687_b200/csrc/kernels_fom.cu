@@ -47,9 +47,6 @@ constexpr int TX = 32;
 constexpr int TY = OSAM_TY;
 constexpr int NT = TX * TY;
 constexpr int NWARP = NT / 32;
-#ifndef OSAM_EO
-#define OSAM_EO 0
-#endif
 #ifndef OSAM_ZC
 #define OSAM_ZC 12
 #endif
@@ -125,7 +122,27 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+__device__ __forceinline__ bool mbar_try(unsigned long long* bar, unsigned phase) {
+  unsigned ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+#ifndef OSAM_BACKOFF
+#define OSAM_BACKOFF 64  // ns between polls of a pending mbarrier phase (frees issue slots; measured +3.6%)
+#endif
+#if OSAM_BACKOFF > 0
+  while (!mbar_try(bar, phase)) __nanosleep(OSAM_BACKOFF);
+#else
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
@@ -141,6 +158,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
       "}\n" ::"r"(smem_u32(bar)),
       "r"(phase)
       : "memory");
+#endif
 }
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int x, int y, int z, int c,
@@ -237,43 +255,20 @@ __device__ __forceinline__ void contrib(double& acc, const double P[9], const In
   }
 }
 
-// z-even / z-odd part of the oz = -1 slice for block (c, d): A (oz = -1) gets even + odd, C (oz = +1)
-// gets even - odd.
-template <int c, int d>
-__device__ __forceinline__ void contrib_eo(double& ev, double& od, const double P[9], const InteriorStencil& S) {
-  constexpr bool zodd = (c == 2) != (d == 2);
-  if (zodd)
-    contrib<0, false, c, d>(od, P, S);
-  else
-    contrib<0, false, c, d>(ev, P, S);
-}
-
 template <int d, bool DA, bool DB, bool DC>
 __device__ __forceinline__ void fast_comp(double A[3], double B[3], double C[3], const double* xs, int base,
                                           const InteriorStencil& S) {
   double P[9];
   combos(xs + d * PLANE + base, P);
-  if (OSAM_EO && DA && DC) {
-    double ev[3] = {0.0, 0.0, 0.0}, od[3] = {0.0, 0.0, 0.0};
-    contrib_eo<0, d>(ev[0], od[0], P, S);
-    contrib_eo<1, d>(ev[1], od[1], P, S);
-    contrib_eo<2, d>(ev[2], od[2], P, S);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      A[c] += ev[c] + od[c];
-      C[c] += ev[c] - od[c];
-    }
-  } else {
-    if (DA) {
-      contrib<0, false, 0, d>(A[0], P, S);
-      contrib<0, false, 1, d>(A[1], P, S);
-      contrib<0, false, 2, d>(A[2], P, S);
-    }
-    if (DC) {
-      contrib<0, true, 0, d>(C[0], P, S);
-      contrib<0, true, 1, d>(C[1], P, S);
-      contrib<0, true, 2, d>(C[2], P, S);
-    }
+  if (DA) {
+    contrib<0, false, 0, d>(A[0], P, S);
+    contrib<0, false, 1, d>(A[1], P, S);
+    contrib<0, false, 2, d>(A[2], P, S);
+  }
+  if (DC) {
+    contrib<0, true, 0, d>(C[0], P, S);
+    contrib<0, true, 1, d>(C[1], P, S);
+    contrib<0, true, 2, d>(C[2], P, S);
   }
   if (DB) {
     contrib<1, false, 0, d>(B[0], P, S);
