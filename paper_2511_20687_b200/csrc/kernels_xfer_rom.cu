@@ -258,21 +258,32 @@ __global__ void rom_lift_kernel(int r, int B, long long nl, const double* __rest
   if (lane == 0) out[(long long)b * nl + ld] = v;
 }
 
-// out[i, b] = sum_q Phi[q, i] field_b[dof(ids[q])]  (projection onto the POD basis, IC only;
-// a block per output, thread-strided, fixed order)
+// Projection onto the POD basis (IC only): part[z][b][i] = sum over row chunk z of
+// Phi[q, i] field_b[dof(ids[q])]  (a block per (i, chunk, sample), thread-strided, fixed order), then
+// out[i, b] = sum_z part[z][b][i] in chunk order.
+constexpr int PCHUNK = 65536;
 __global__ void __launch_bounds__(256) rom_project_kernel(long long nrows, int r, int B, const double* __restrict__ Phi,
                                                          const int* __restrict__ ids, const double* __restrict__ field,
-                                                         long long fbs, long long n_nodes, double* __restrict__ out) {
-  const int i = blockIdx.x, b = blockIdx.y;
+                                                         long long fbs, long long n_nodes, double* __restrict__ part) {
+  const int i = blockIdx.x, z = blockIdx.y, b = blockIdx.z;
   const double* col = Phi + (long long)i * nrows;
   const double* f = field + (long long)b * fbs;
+  const long long q0 = (long long)z * PCHUNK, q1 = q0 + PCHUNK < nrows ? q0 + PCHUNK : nrows;
   double acc = 0.0;
-  for (long long q = threadIdx.x; q < nrows; q += 256) {
+  for (long long q = q0 + threadIdx.x; q < q1; q += 256) {
     const long long dof = ids[q];
     acc = fma(col[q], f[(dof % 3) * n_nodes + dof / 3], acc);
   }
   acc = block_sum256(acc);
-  if (threadIdx.x == 0) out[i + (long long)r * b] = acc;
+  if (threadIdx.x == 0) part[((long long)z * B + b) * r + i] = acc;
+}
+
+__global__ void sum_chunks_kernel(int r, int B, int nz, const double* __restrict__ part, double* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= r * B) return;
+  double v = 0.0;
+  for (int z = 0; z < nz; ++z) v += part[(long long)z * r * B + t];
+  out[t] = v;
 }
 
 __global__ void gather_dofs_kernel(long long n, int B, const int* __restrict__ ids, const double* __restrict__ field,
@@ -337,10 +348,16 @@ void launch_rom_lift(int r, int B, long long nl, const double* Phi_lift, const i
   debug_check("rom_lift_kernel", st);
 }
 
-void launch_rom_project(long long nrows, int r, int B, const double* Phi, const int* ids, const double* field,
-                        long long fbs, long long n_nodes, double* out, cudaStream_t s) {
-  rom_project_kernel<<<dim3(r, B), 256, 0, s>>>(nrows, r, B, Phi, ids, field, fbs, n_nodes,
-                                                                     out);
+cudaError_t launch_rom_project(long long nrows, int r, int B, const double* Phi, const int* ids, const double* field,
+                               long long fbs, long long n_nodes, double* out, cudaStream_t s) {
+  const int nz = (int)std::max<long long>(1, cdiv(nrows, PCHUNK));
+  double* part = nullptr;
+  const cudaError_t e = cudaMallocAsync((void**)&part, sizeof(double) * (size_t)nz * r * B, s);
+  if (e != cudaSuccess) return e;
+  rom_project_kernel<<<dim3(r, nz, B), 256, 0, s>>>(nrows, r, B, Phi, ids, field, fbs, n_nodes, part);
+  debug_check("rom_project_kernel", s);
+  sum_chunks_kernel<<<cdiv((long long)r * B, 256), 256, 0, s>>>(r, B, nz, part, out);
+  return cudaFreeAsync(part, s);
 }
 
 void launch_gather_dofs(long long n, int B, const int* ids, const double* field, long long fbs, long long n_nodes,

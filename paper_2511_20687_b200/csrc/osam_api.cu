@@ -522,8 +522,8 @@ int process_ic(Sub& s, int* launches) {
   } else {
     const int c = s.cur;
     const long long fbs = 3 * s.n_nodes;
-    launch_rom_project(s.n_free, s.r, s.batch, s.Phi, s.free_ids, s.ic_u, fbs, s.n_nodes, s.rst[c][0], st);
-    launch_rom_project(s.n_free, s.r, s.batch, s.Phi, s.free_ids, s.ic_v, fbs, s.n_nodes, s.rst[c][1], st);
+    CK(launch_rom_project(s.n_free, s.r, s.batch, s.Phi, s.free_ids, s.ic_u, fbs, s.n_nodes, s.rst[c][0], st));
+    CK(launch_rom_project(s.n_free, s.r, s.batch, s.Phi, s.free_ids, s.ic_v, fbs, s.n_nodes, s.rst[c][1], st));
     launch_gather_dofs(s.n_sdof, s.batch, s.sdof_ids, s.ic_u, fbs, s.n_nodes, s.rst[c][3], st);
     RomLaunch L{};
     L.r = s.r;

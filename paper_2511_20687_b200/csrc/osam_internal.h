@@ -175,7 +175,7 @@ int rom_gchunks(long long n_s);  // chunks of the partial boundary projection (C
 void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches);
 void launch_rom_lift(int r, int B, long long n_lift, const double* Phi_lift, const int* code, const double* uh,
                      const double* s, long long n_sdof, double* out, cudaStream_t st);
-void launch_rom_project(long long n_rows, int r, int B, const double* Phi, const int* ids, const double* field,
+cudaError_t launch_rom_project(long long n_rows, int r, int B, const double* Phi, const int* ids, const double* field,
                         long long field_bstride, long long n_nodes, double* out, cudaStream_t s);
 void launch_gather_dofs(long long n, int B, const int* ids, const double* field, long long field_bstride,
                         long long n_nodes, double* out, cudaStream_t s);
