@@ -170,14 +170,6 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// L2 prefetch of a tensor box (no shared memory, no completion tracking)
-__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* map, int x, int y, int z, int c) {
-  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
-                   reinterpret_cast<unsigned long long>(map)),
-               "r"(x), "r"(y), "r"(z), "r"(c)
-               : "memory");
-}
-
 // Staged x-range [x0, x0 + PX) with x0 = 32 bx - 2: the TMA box must start on a 16-byte
 // boundary in the innermost dimension (an odd fp64 start coordinate raises an illegal
 // instruction on sm_100a), so the left halo is two columns wide (the first is unused).
@@ -194,10 +186,6 @@ constexpr int WPL = TX * TY;                               // tile positions of 
 constexpr int W_BYTES = 3 * WPL * 8;
 constexpr int STAGE_BYTES = ARR_STRIDE + 2 * W_BYTES;  // X, W, W'_prev
 constexpr int SMEM_TILED = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8 + 64;  // ring, barriers, producer cursor
-#ifndef OSAM_PF
-#define OSAM_PF 3
-#endif
-constexpr int PF_AHEAD = OSAM_PF;  // planes beyond the ring that are prefetched into L2
 
 // ---- interior rows: parity-reduced stencil ---------------------------------------------
 // On a uniform box every interior block K_cd(ox, oy, oz) is even or odd in ox and in oy (the 1D

@@ -38,7 +38,6 @@ struct Faces {
 // class = cx + 3 (cy + 3 cz), c_d = 0 low face, 1 interior, 2 high face (per axis);
 // offset = (ox+1) + 3((oy+1) + 3(oz+1)).
 constexpr int NCLASS = 27;
-constexpr int STENCIL_BLOCK = 27 * 9;
 // Interior-class stencil in parity-reduced form: k[slice][c][d] = {K(0,0), K(1,0), K(0,1), K(1,1)}
 // at in-plane offsets (ox, oy), slice = oz + 1 (see kernels_fom.cu "parity-reduced stencil").
 struct InteriorStencil {
