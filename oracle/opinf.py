@@ -7,8 +7,11 @@ are inputs shared by both online paths (the CUDA library reads them through the 
     Euclidean, uncentred; column signs fixed so the largest-|entry| is positive (R17).
   * Energy rule E_r = sum_{i<=r} s_i^2 / sum_i s_i^2 (P:L788-792 eq:pod_energy); the smallest r
     with E_r >= delta_E = 0.999999 (reading R16).
-  * OpInf (P:L263-272 eq:quadratic_opinf, linear form; L609-614 eq:opinf_schwarz_inference):
-        argmin_O || O [U^; G^] - D_t^2(U^) ||_F^2 + lambda ||O||_F^2 ,  O = [-Kbar, Bbar]
+  * OpInf (P:L263-272 eq:quadratic_opinf; L609-614 eq:opinf_schwarz_inference):
+        argmin_O || O [U^; G^; U^*2; U^*3] - D_t^2(U^) ||_F^2 + lambda ||O||_F^2 ,
+        O = [-Kbar, Bbar, -Hbar, -Cbar]   (linear: order 1; QOpInf: order 2; COpInf: order 3)
+    where U^*k is the compressed column-wise Khatri-Rao power (P:L167 footnote; S:L437-445:
+    monomials u_i u_j, i <= j, and u_i u_j u_l, i <= j <= l, in lexicographic order)
     with U^ = Phi^T U, G^ = Phi_dS^T S and D_t^2 the central second difference on interior
     columns (reading R18), one lambda in SI units (R20), solved as augmented least squares.
   * Training recipes per reading R25.
@@ -47,29 +50,81 @@ def second_difference(Ubar, dt):
     return (Ubar[:, 2:] - 2.0 * Ubar[:, 1:-1] + Ubar[:, :-2]) / (dt * dt)
 
 
-def opinf_fit(Ubar, Ghat, dt, lam):
-    """Ridge OpInf for  u^'' + Kbar u^ = Bbar g^  from projected snapshots (columns = time)."""
-    Y = second_difference(Ubar, dt)                      # (r, K-2)
-    D = np.vstack([Ubar[:, 1:-1], Ghat[:, 1:-1]])        # (r + r_b, K-2)
+def khatri_rao_pow(U, k):
+    """Compressed column-wise Kronecker power of U (r x tau): rows u_i u_j (i <= j) for k = 2 and
+    u_i u_j u_l (i <= j <= l) for k = 3, lexicographic; k = 1 returns U."""
+    U = np.atleast_2d(np.asarray(U, dtype=np.float64))
+    r = U.shape[0]
+    if k == 1:
+        return U
+    rows = []
+    if k == 2:
+        for i in range(r):
+            for j in range(i, r):
+                rows.append(U[i] * U[j])
+    elif k == 3:
+        for i in range(r):
+            for j in range(i, r):
+                for l in range(j, r):
+                    rows.append(U[i] * U[j] * U[l])
+    else:
+        raise ValueError("k in {1, 2, 3}")
+    return np.array(rows)
+
+
+def n_poly(r, k):
+    """Length of the compressed k-th power: r (r+1) ... (r+k-1) / k!."""
+    return {1: r, 2: r * (r + 1) // 2, 3: r * (r + 1) * (r + 2) // 6}[k]
+
+
+def opinf_fit_accel(Ubar, Ghat, Ydd, lam, order=1):
+    """Ridge OpInf with given reduced accelerations Ydd (columns = samples):
+    argmin || Ydd + Kbar U + Hbar U*2 + Cbar U*3 - Bbar G ||_F^2 + lam ||[Kbar Hbar Cbar Bbar]||_F^2,
+    solved as augmented least squares.  Returns (Kbar, Bbar, Hbar, Cbar); Hbar/Cbar are None
+    below their order."""
+    blocks = [Ubar, Ghat] + [khatri_rao_pow(Ubar, k) for k in range(2, order + 1)]
+    D = np.vstack(blocks)
     n = D.shape[0]
     A = np.vstack([D.T, np.sqrt(lam) * np.eye(n)])
-    b = np.vstack([Y.T, np.zeros((n, Y.shape[0]))])
+    b = np.vstack([Ydd.T, np.zeros((n, Ydd.shape[0]))])
     Ot, *_ = np.linalg.lstsq(A, b, rcond=None)
-    O = Ot.T                                             # (r, r + r_b)
-    r = Ubar.shape[0]
-    return -O[:, :r], O[:, r:]
+    O = Ot.T                                             # (r, n)
+    r, rb = Ubar.shape[0], Ghat.shape[0]
+    Kbar, Bbar = -O[:, :r], O[:, r:r + rb]
+    Hbar = -O[:, r + rb:r + rb + n_poly(r, 2)] if order >= 2 else None
+    Cbar = -O[:, r + rb + n_poly(r, 2):] if order >= 3 else None
+    return Kbar, Bbar, Hbar, Cbar
 
 
-def build_rom_operators(U, S, dt, r, lam, delta=0.999999, r_b=None):
-    """Phi, Phi_dS, Kbar, Bbar from snapshot matrices U (n_free x K) and S (n_s x K)."""
+def opinf_fit(Ubar, Ghat, dt, lam, order=1):
+    """Ridge OpInf for  u^'' + Kbar u^ (+ Hbar u^*2 + Cbar u^*3) = Bbar g^  from projected snapshots
+    (columns = time), accelerations by central differences on the interior columns (reading R18).
+    order 1 returns (Kbar, Bbar); orders 2, 3 return (Kbar, Bbar, Hbar, Cbar)."""
+    Y = second_difference(Ubar, dt)                      # (r, K-2)
+    out = opinf_fit_accel(Ubar[:, 1:-1], Ghat[:, 1:-1], Y, lam, order)
+    return out[:2] if order == 1 else out
+
+
+def build_rom_operators(U, S, dt, r, lam, delta=0.999999, r_b=None, order=1):
+    """Phi, Phi_dS, Kbar, Bbar (and Hbar, Cbar for order 2, 3) from snapshot matrices U (n_free x K)
+    and S (n_s x K)."""
     Phi, sigma = pod(U, r)
     Phi_s_full, sigma_s = pod(S, min(S.shape))
     if r_b is None:
         r_b = energy_rank(sigma_s, delta)
     Phi_s = Phi_s_full[:, :r_b]
-    Kbar, Bbar = opinf_fit(Phi.T @ U, Phi_s.T @ S, dt, lam)
-    return dict(Phi=Phi, Phi_s=Phi_s, Kbar=Kbar, Bbar=Bbar, sigma=sigma, sigma_s=sigma_s,
-                r=r, r_b=r_b, lam=lam, dt=dt)
+    Kbar, Bbar, Hbar, Cbar = opinf_fit_accel(*_fit_data(Phi.T @ U, Phi_s.T @ S, dt), lam, order)
+    ops = dict(Phi=Phi, Phi_s=Phi_s, Kbar=Kbar, Bbar=Bbar, sigma=sigma, sigma_s=sigma_s,
+               r=r, r_b=r_b, lam=lam, dt=dt, order=order)
+    if order >= 2:
+        ops["Hbar"] = Hbar
+    if order >= 3:
+        ops["Cbar"] = Cbar
+    return ops
+
+
+def _fit_data(Ubar, Ghat, dt):
+    return Ubar[:, 1:-1], Ghat[:, 1:-1], second_difference(Ubar, dt)
 
 
 # ---------------------------------------------------------------------------------------
@@ -111,7 +166,7 @@ def train_single_domain(cfg, inputs):
         sd = np.nonzero(codes == fem.SCHWARZ)[0]
         X = np.stack([u[tnodes].reshape(-1) for u in snaps], axis=1)      # (3 n_rom, K)
         ops[i] = build_rom_operators(X[free], X[sd], cfg["dt"], cfg["rom"]["r"], cfg["rom"]["lam"],
-                                     cfg["rom"]["energy"])
+                                     cfg["rom"]["energy"], order=cfg["rom"].get("order", 1))
     return ops
 
 
@@ -140,7 +195,7 @@ def train_coupled(cfg, inputs):
         m = models[i]
         X = np.stack(snaps[i], axis=1)
         ops[i] = build_rom_operators(X[m.free_dofs], X[m.schwarz_dofs], cfg["dt"], cfg["rom"]["r"],
-                                     cfg["rom"]["lam"], cfg["rom"]["energy"])
+                                     cfg["rom"]["lam"], cfg["rom"]["energy"], order=cfg["rom"].get("order", 1))
     return ops
 
 

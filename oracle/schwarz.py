@@ -25,7 +25,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import fem, transfer
+from . import fem, opinf, transfer
 
 GEOM_TOL = 1e-12
 
@@ -142,6 +142,9 @@ class ROM(_Base):
         self.Phi_s = np.asarray(ops["Phi_s"], dtype=np.float64)   # (n_sdofs, r_b)
         self.Kbar = np.asarray(ops["Kbar"], dtype=np.float64)     # (r, r)
         self.Bbar = np.asarray(ops["Bbar"], dtype=np.float64)     # (r, r_b)
+        # QOpInf / COpInf terms (eq:quadratic_opinf): compressed Khatri-Rao powers
+        self.Hbar = None if ops.get("Hbar") is None else np.asarray(ops["Hbar"], dtype=np.float64)
+        self.Cbar = None if ops.get("Cbar") is None else np.asarray(ops["Cbar"], dtype=np.float64)
         if self.Phi.shape[0] != len(self.free_dofs) or self.Phi_s.shape[0] != len(self.schwarz_dofs):
             raise ValueError("ROM operator shapes do not match the subdomain DOF sets")
         self.e = np.ones(1) if e_scale is None else np.asarray(e_scale, dtype=np.float64)
@@ -152,8 +155,15 @@ class ROM(_Base):
         self.sdof_idx[self.schwarz_dofs] = np.arange(len(self.schwarz_dofs))
 
     def accel(self, uh, s):
+        """a^ = e_b (-Kbar u^ - Hbar u^*2 - Cbar u^*3 + Bbar Phi_dS^T s)  (eq:opinf_model_schwarz P:L550-563;
+        the per-sample modulus scales every stiffness term, reading R22)."""
         gh = s @ self.Phi_s                                          # (B, r_b) = (Phi_s^T s)^T
-        return self.e[:, None] * (-uh @ self.Kbar.T + gh @ self.Bbar.T)
+        f = -uh @ self.Kbar.T + gh @ self.Bbar.T
+        if self.Hbar is not None:
+            f = f - opinf.khatri_rao_pow(uh.T, 2).T @ self.Hbar.T
+        if self.Cbar is not None:
+            f = f - opinf.khatri_rao_pow(uh.T, 3).T @ self.Cbar.T
+        return self.e[:, None] * f
 
     def init_state(self, u0):
         """u^0 = Phi^T u0[free], v^0 = 0, s0 = u0 at the Schwarz DOFs, a^0 = e(-Kbar u^0 + Bbar Phi_s^T s0)

@@ -2,6 +2,8 @@
 import json
 import os
 
+import itertools
+
 import numpy as np
 import pytest
 
@@ -131,3 +133,124 @@ def test_c2_online_matches_independent_prototype(c2_ops):
     assert (iters == 3).all()
     assert np.allclose(got[0], g["after_step_1"], rtol=1e-10)
     assert np.allclose(got[99], g["after_step_100"], rtol=g["rel_tol_100"])
+
+
+# ---- QOpInf / COpInf (P:L263-272 eq:quadratic_opinf; compressed powers P:L167 footnote) -----------------
+
+def test_khatri_rao_hand_expansions():
+    """u = (1, 2) -> (1, 2, 4) for k = 2 (ordering 11, 12, 22) and (1, 2, 4, 8) for k = 3."""
+    u = np.array([[1.0], [2.0]])
+    assert np.array_equal(opinf.khatri_rao_pow(u, 2).ravel(), [1.0, 2.0, 4.0])
+    assert np.array_equal(opinf.khatri_rao_pow(u, 3).ravel(), [1.0, 2.0, 4.0, 8.0])
+    assert opinf.khatri_rao_pow(np.ones((5, 3)), 3).shape == (35, 3) == (opinf.n_poly(5, 3), 3)
+
+
+def test_compressed_power_equals_symmetric_kronecker():
+    """A symmetric operator on the full Kronecker power equals its compressed parameterisation on the
+    compressed power: H (u kron u) = Hc u*2, with Hc[:, ij] = H[:, ij] + H[:, ji] (i < j), H[:, ii]."""
+    rng = np.random.default_rng(4)
+    r = 5
+    u = rng.standard_normal(r)
+    H = rng.standard_normal((3, r * r))
+    Hc = []
+    for i in range(r):
+        for j in range(i, r):
+            Hc.append(H[:, i * r + j] + (H[:, j * r + i] if j != i else 0.0))
+    Hc = np.array(Hc).T
+    assert np.allclose(H @ np.kron(u, u), Hc @ opinf.khatri_rao_pow(u[:, None], 2).ravel(), rtol=1e-13, atol=1e-13)
+    C = rng.standard_normal((3, r ** 3))
+    Cc = np.zeros((3, opinf.n_poly(r, 3)))
+    col = 0
+    for i in range(r):
+        for j in range(i, r):
+            for l in range(j, r):
+                for a, b, c in set(itertools.permutations((i, j, l))):
+                    Cc[:, col] += C[:, a * r * r + b * r + c]
+                col += 1
+    assert np.allclose(C @ np.kron(np.kron(u, u), u), Cc @ opinf.khatri_rao_pow(u[:, None], 3).ravel(),
+                       rtol=1e-12, atol=1e-12)
+
+
+def _poly_system(rng, r=4, rb=2, order=3, scale=0.3):
+    K = rng.standard_normal((r, r))
+    B = rng.standard_normal((r, rb))
+    H = scale * rng.standard_normal((r, opinf.n_poly(r, 2))) if order >= 2 else None
+    C = scale * rng.standard_normal((r, opinf.n_poly(r, 3))) if order >= 3 else None
+    return K, B, H, C
+
+
+def _accel(U, G, K, B, H, C):
+    Y = -K @ U + B @ G
+    if H is not None:
+        Y -= H @ opinf.khatri_rao_pow(U, 2)
+    if C is not None:
+        Y -= C @ opinf.khatri_rao_pow(U, 3)
+    return Y
+
+
+@pytest.mark.parametrize("order", [1, 2, 3])
+def test_opinf_recovers_known_polynomial_operators(order):
+    """data generated exactly by a known reduced polynomial ODE, exact accelerations, lambda = 0,
+    full column rank -> the fit recovers Kbar, Hbar, Cbar, Bbar (P:L278-285 consistency)."""
+    rng = np.random.default_rng(10 + order)
+    K, B, H, C = _poly_system(rng, order=order)
+    U = rng.standard_normal((4, 400))
+    G = rng.standard_normal((2, 400))
+    Kf, Bf, Hf, Cf = opinf.opinf_fit_accel(U, G, _accel(U, G, K, B, H, C), 0.0, order)
+    assert np.abs(Kf - K).max() < 1e-9 and np.abs(Bf - B).max() < 1e-9
+    if order >= 2:
+        assert np.abs(Hf - H).max() < 1e-9
+    if order >= 3:
+        assert np.abs(Cf - C).max() < 1e-9
+
+
+def test_opinf_superset_model_and_ridge_limit():
+    """quadratic data fitted with the cubic model -> Cbar ~ 0; lambda -> infinity -> 0."""
+    rng = np.random.default_rng(21)
+    K, B, H, _ = _poly_system(rng, order=2)
+    U = rng.standard_normal((4, 400))
+    G = rng.standard_normal((2, 400))
+    Y = _accel(U, G, K, B, H, None)
+    Kf, Bf, Hf, Cf = opinf.opinf_fit_accel(U, G, Y, 0.0, 3)
+    assert np.linalg.norm(Cf) < 1e-8 * np.linalg.norm(Kf)
+    Kl, Bl, Hl, Cl = opinf.opinf_fit_accel(U, G, Y, 1e12, 3)
+    assert max(np.abs(x).max() for x in (Kl, Bl, Hl, Cl)) < 1e-6
+
+
+def test_rom_accel_with_polynomial_terms_matches_kronecker_form():
+    """oracle ROM.accel with Hbar, Cbar = e (-Kbar u - H_full (u kron u) - C_full (u kron u kron u) + Bbar g)
+    with the full symmetric tensors rebuilt from the compressed ones (independent evaluation)."""
+    from oracle import schwarz
+    cfg = I.config("c2")
+    boxes = [fem.Box(s["lo"], s["hi"], s["nel"]) for s in cfg["subdomains"]]
+    faces = schwarz.detect_schwarz_faces(boxes)
+    sub = cfg["subdomains"][1]
+    codes = fem.dof_codes(boxes[1], sub["dirichlet"], faces[1].keys()).reshape(-1)
+    nf, ns = int((codes == fem.FREE).sum()), int((codes == fem.SCHWARZ).sum())
+    r, rb = 4, 3
+    rng = np.random.default_rng(5)
+    K, B, H, C = _poly_system(rng, r=r, rb=rb, order=3)
+    ops = dict(Phi=np.linalg.qr(rng.standard_normal((nf, r)))[0], Phi_s=np.linalg.qr(rng.standard_normal((ns, rb)))[0],
+               Kbar=K, Bbar=B, Hbar=H, Cbar=C)
+    m = schwarz.ROM(sub, faces[1], cfg["E"], cfg["nu"], cfg["rho"], cfg["dt"], ops, e_scale=np.array([0.8, 1.1]))
+    uh = rng.standard_normal((2, r))
+    s = rng.standard_normal((2, ns))
+    got = m.accel(uh, s)
+    # full symmetric tensors: Hf[:, i r + j] = Hc[:, (i,j)] / multiplicity
+    idx2 = [(i, j) for i in range(r) for j in range(i, r)]
+    idx3 = [(i, j, l) for i in range(r) for j in range(i, r) for l in range(j, r)]
+    Hf = np.zeros((r, r * r))
+    for q, (i, j) in enumerate(idx2):
+        perms = set(itertools.permutations((i, j)))
+        for a, b in perms:
+            Hf[:, a * r + b] = H[:, q] / len(perms)
+    Cf = np.zeros((r, r ** 3))
+    for q, (i, j, l) in enumerate(idx3):
+        perms = set(itertools.permutations((i, j, l)))
+        for a, b, c in perms:
+            Cf[:, a * r * r + b * r + c] = C[:, q] / len(perms)
+    for bidx, e in enumerate((0.8, 1.1)):
+        u = uh[bidx]
+        g = ops["Phi_s"].T @ s[bidx]
+        ref = e * (-K @ u - Hf @ np.kron(u, u) - Cf @ np.kron(np.kron(u, u), u) + B @ g)
+        assert np.allclose(got[bidx], ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
