@@ -70,7 +70,12 @@ typedef struct {
   const double *Phi_s;    /* n_s x r_b    Schwarz boundary basis Phi_dS (rows = Schwarz DOFs)   */
   const double *Kbar;     /* r x r        inferred linear operator      */
   const double *Bbar;     /* r x r_b      inferred boundary operator  */
-  const double *e_scale;  /* batch factors e_b = E_b/E0 applied to Kbar, Bbar (NULL -> 1)       */
+  const double *e_scale;  /* batch factors e_b = E_b/E0 applied to every reduced operator (NULL -> 1) */
+  /* Polynomial OpInf (QOpInf / COpInf, eq:quadratic_opinf P:L263-272), NULL = absent.  Compressed
+   * Khatri-Rao powers (P:L167 footnote): u^*2 = [u_i u_j, i <= j], u^*3 = [u_i u_j u_l, i <= j <= l],
+   * lexicographic; the reduced model is a^ = e_b (-Kbar u^ - Hbar u^*2 - Cbar u^*3 + Bbar g^).      */
+  const double *Hbar;     /* r x r(r+1)/2        column-major                                         */
+  const double *Cbar;     /* r x r(r+1)(r+2)/6   column-major                                         */
 } osam_subdomain_desc;
 
 typedef struct {

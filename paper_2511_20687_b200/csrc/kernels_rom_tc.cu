@@ -201,8 +201,8 @@ __global__ void tc_lift_reduce_kernel(long long nl, int B, int S, const double* 
 
 // Batched ROM advance (B >= 2) on the tensor cores; scratch Z ((r + r_b) x B) and `part` (split-K
 // partials, tc_part_size doubles).
-long long tc_part_size(int r, int r_b, int B, long long n_s, long long n_lift3) {
-  const long long a = (long long)gemm_splits(r, B, r + r_b) * r * B;
+long long tc_part_size(int r, int r_b, int nf, int B, long long n_s, long long n_lift3) {
+  const long long a = (long long)gemm_splits(r, B, r + r_b + nf) * r * B;
   const long long g = r_b > 0 ? (long long)gemm_splits(r_b, B, (int)n_s) * r_b * B : 0;
   const long long l = n_lift3 > 0 ? (long long)gemm_splits((int)n_lift3, B, r) * n_lift3 * B : 0;
   return std::max(std::max(a, g), std::max<long long>(l, 1));
@@ -210,9 +210,11 @@ long long tc_part_size(int r, int r_b, int B, long long n_s, long long n_lift3) 
 
 void launch_rom_advance_tc(const RomLaunch& L, const double* KB, double* Z, double* part, cudaStream_t s,
                            int* launches) {
-  const int r = L.r, rb = L.r_b, rz = L.r + L.r_b, B = L.B;
+  const int r = L.r, rb = L.r_b, rz = L.r + L.r_b + L.nf, B = L.B;
   tc_predict_kernel<<<cdiv((long long)r * B, 256), 256, 0, s>>>(r, rz, B, L.uh0, L.vh0, L.ah0, L.dt, Z);
   debug_check("tc_predict_kernel", s);
+  launch_rom_features(L.nf, B, L.feat_idx, Z, rz, Z + r + rb, rz, s);  // polynomial OpInf rows of Z
+  *launches += L.nf > 0;
   if (rb > 0) {  // g^ = Phi_dS^T s  -> Z[r:, :]
     const int S = gemm(GemmArgs{rb, B, (int)L.n_sdof, L.Phi_s, L.n_sdof, 1, L.s, 1, L.n_sdof, nullptr, 0}, part, s);
     reduce_splits_kernel<<<cdiv((long long)rb * B, 256), 256, 0, s>>>(rb, B, S, part, Z + r, 1, rz);
@@ -229,11 +231,13 @@ void launch_rom_advance_tc(const RomLaunch& L, const double* KB, double* Z, doub
 // Initial acceleration a^0 = e (-Kbar u^0 + Bbar Phi_dS^T s0) on the same path.
 void launch_rom_accel_tc(const RomLaunch& L, const double* uh, double* ah, const double* KB, double* Z, double* part,
                          cudaStream_t s, int* launches) {
-  const int r = L.r, rb = L.r_b, rz = L.r + L.r_b, B = L.B;
+  const int r = L.r, rb = L.r_b, rz = L.r + L.r_b + L.nf, B = L.B;
   RomLaunch A = L;
   A.ah1 = ah;
   tc_predict_kernel<<<cdiv((long long)r * B, 256), 256, 0, s>>>(r, rz, B, uh, uh, uh, 0.0, Z);  // Z[0:r] = u^0
   debug_check("tc_predict_kernel", s);
+  launch_rom_features(L.nf, B, L.feat_idx, Z, rz, Z + r + rb, rz, s);
+  *launches += L.nf > 0;
   if (rb > 0) {
     const int S = gemm(GemmArgs{rb, B, (int)L.n_sdof, L.Phi_s, L.n_sdof, 1, L.s, 1, L.n_sdof, nullptr, 0}, part, s);
     reduce_splits_kernel<<<cdiv((long long)rb * B, 256), 256, 0, s>>>(rb, B, S, part, Z + r, 1, rz);

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(256) rom_update_kernel(const RomLaunch L, int 
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int i = blockIdx.x * 8 + w;
   const int b = blockIdx.y;
-  const int r = L.r, rz = L.r + L.r_b;
+  const int r = L.r, rz = L.r + L.r_b + L.nf;
   const bool on = i < r && (mode == 1 || L.active[b]);
   double num = 0.0, den = 0.0;
   if (on) {
@@ -186,6 +186,8 @@ __global__ void __launch_bounds__(256) rom_update_kernel(const RomLaunch L, int 
       for (int z = 0; z < L.gchunks; ++z) g += L.gh[((long long)z * L.B + b) * L.r_b + k];
       acc = fma(row[r + k], g, acc);
     }
+    const double* fb = L.F + (long long)L.nf * b;  // polynomial OpInf features
+    for (int q = lane; q < L.nf; q += 32) acc = fma(row[r + L.r_b + q], fb[q], acc);
     acc = warp_sum(acc);
     if (lane == 0) {
       const double an = L.e[b] * acc;
@@ -314,6 +316,25 @@ void launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int min_
   debug_check("any_active_kernel", s);
 }
 
+__global__ void rom_features_kernel(int nf, int B, const int* __restrict__ idx, const double* __restrict__ u,
+                                    long long us, double* __restrict__ F, long long fs) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (q >= nf) return;
+  const double* ub = u + us * b;
+  const int i = idx[3 * q], j = idx[3 * q + 1], l = idx[3 * q + 2];
+  double v = ub[i] * ub[j];
+  if (l >= 0) v *= ub[l];
+  F[q + fs * b] = v;
+}
+
+void launch_rom_features(int nf, int B, const int* idx, const double* u, long long us, double* F, long long fs,
+                         cudaStream_t s) {
+  if (nf == 0) return;
+  rom_features_kernel<<<dim3(cdiv(nf, 256), B), 256, 0, s>>>(nf, B, idx, u, us, F, fs);
+  debug_check("rom_features_kernel", s);
+}
+
 int rom_gchunks(long long n_s) { return (int)std::max<long long>(1, cdiv(n_s, GCHUNK)); }
 
 int rom_partial_slots(int r, bool tc) { return (int)(tc ? cdiv(r, 256) : cdiv(r, 8)); }
@@ -323,6 +344,8 @@ void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches) {
     rom_project_bnd_kernel<<<dim3(L.r_b, rom_gchunks(L.n_sdof), L.B), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
                                                                                    L.s, L.gh);
   rom_predict_kernel<<<cdiv((long long)L.r * L.B, 256), 256, 0, s>>>(L.r, L.B, L.uh0, L.vh0, L.ah0, L.dt, L.ustar);
+  launch_rom_features(L.nf, L.B, L.feat_idx, L.ustar, L.r, L.F, L.nf, s);
+  *launches += L.nf > 0;
   debug_check("rom_predict_kernel", s);
   rom_update_kernel<<<dim3(cdiv(L.r, 8), L.B), 256, 0, s>>>(L, 0);
   debug_check("rom_update_kernel", s);
@@ -333,6 +356,8 @@ void launch_rom_accel(const RomLaunch& L, const double* uh, double* ah, cudaStre
   RomLaunch A = L;
   A.ustar = const_cast<double*>(uh);
   A.ah1 = ah;
+  launch_rom_features(L.nf, L.B, L.feat_idx, uh, L.r, L.F, L.nf, s);
+  *launches += L.nf > 0;
   if (L.r_b > 0)
     rom_project_bnd_kernel<<<dim3(L.r_b, rom_gchunks(L.n_sdof), L.B), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
                                                                                    L.s, L.gh);

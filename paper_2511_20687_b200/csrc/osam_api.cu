@@ -174,6 +174,8 @@ void release_binding(Sub& s) {
   dfree(s.lift_code);
   dfree(s.KB);
   dfree(s.KBr);
+  dfree(s.feat_idx);
+  dfree(s.F);
   dfree(s.Z);
   dfree(s.part);
   s.bound = false;
@@ -356,22 +358,36 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
     // overrides the default, which is tensor cores iff batch > 1)
     const char* tc = getenv("OSAM_ROM_TC");
     s.use_tc = tc ? tc[0] == '1' : s.batch > 1;
-    {
-      const int rz = s.r + s.r_b;
-      std::vector<double> kbr((size_t)s.r * rz);
-      for (int q = 0; q < s.r; ++q) {
-        for (int j = 0; j < s.r; ++j) kbr[(size_t)q * rz + j] = -s.h_Kbar[(size_t)j * s.r + q];
-        for (int j = 0; j < s.r_b; ++j) kbr[(size_t)q * rz + s.r + j] = s.h_Bbar[(size_t)j * s.r + q];
-      }
-      TRY(upload(&s.KBr, kbr, s.stream));
+    // reduced operator [-Kbar | Bbar | -Hbar | -Cbar] acting on z = [u^*; g^; u^*2; u^*3]
+    // (eq:opinf_model_schwarz with the polynomial terms of eq:quadratic_opinf), column-major and
+    // row-major copies, and the monomial index table of the compressed Khatri-Rao powers
+    const int n2 = s.order >= 2 ? s.r * (s.r + 1) / 2 : 0;
+    const int rz = s.r + s.r_b + s.nf;
+    std::vector<double> kb((size_t)s.r * rz);
+    for (int j = 0; j < s.r; ++j)
+      for (int q = 0; q < s.r; ++q) kb[(size_t)j * s.r + q] = -s.h_Kbar[(size_t)j * s.r + q];
+    for (int j = 0; j < s.r_b; ++j)
+      for (int q = 0; q < s.r; ++q) kb[(size_t)(s.r + j) * s.r + q] = s.h_Bbar[(size_t)j * s.r + q];
+    for (int j = 0; j < s.nf; ++j)
+      for (int q = 0; q < s.r; ++q)
+        kb[(size_t)(s.r + s.r_b + j) * s.r + q] =
+            j < n2 ? -s.h_Hbar[(size_t)j * s.r + q] : -s.h_Cbar[(size_t)(j - n2) * s.r + q];
+    std::vector<double> kbr((size_t)s.r * rz);
+    for (int q = 0; q < s.r; ++q)
+      for (int j = 0; j < rz; ++j) kbr[(size_t)q * rz + j] = kb[(size_t)j * s.r + q];
+    TRY(upload(&s.KBr, kbr, s.stream));
+    if (s.nf > 0) {
+      std::vector<int> idx;
+      for (int i = 0; i < s.r; ++i)
+        for (int j = i; j < s.r; ++j) idx.insert(idx.end(), {i, j, -1});
+      if (s.order >= 3)
+        for (int i = 0; i < s.r; ++i)
+          for (int j = i; j < s.r; ++j)
+            for (int l = j; l < s.r; ++l) idx.insert(idx.end(), {i, j, l});
+      TRY(upload(&s.feat_idx, idx, s.stream));
+      TRY(dalloc(&s.F, (size_t)s.nf * s.batch));
     }
     if (s.use_tc) {
-      const int rz = s.r + s.r_b;
-      std::vector<double> kb((size_t)s.r * rz);
-      for (int j = 0; j < s.r; ++j)
-        for (int q = 0; q < s.r; ++q) kb[(size_t)j * s.r + q] = -s.h_Kbar[(size_t)j * s.r + q];
-      for (int j = 0; j < s.r_b; ++j)
-        for (int q = 0; q < s.r; ++q) kb[(size_t)(s.r + j) * s.r + q] = s.h_Bbar[(size_t)j * s.r + q];
       TRY(upload(&s.KB, kb, s.stream));
       TRY(dalloc(&s.Z, (size_t)rz * s.batch));
     }
@@ -477,7 +493,7 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
     TRY(upload(&s.Phi_lift, phil, s.stream));
     TRY(upload(&s.lift_code, code, s.stream));
     for (int b = 0; b < 2; ++b) TRY(dalloc(&s.lift[b], (size_t)std::max<long long>(nl, 1) * s.batch));
-    if (s.use_tc) TRY(dalloc(&s.part, (size_t)tc_part_size(s.r, s.r_b, s.batch, s.n_sdof, nl)));
+    if (s.use_tc) TRY(dalloc(&s.part, (size_t)tc_part_size(s.r, s.r_b, s.nf, s.batch, s.n_sdof, nl)));
   }
   for (auto& P : pend) {
     Sub& d = *subs[P.dst];
@@ -534,6 +550,9 @@ int process_ic(Sub& s, int* launches) {
     L.Kbar = s.Kbar;
     L.Bbar = s.Bbar;
     L.KBr = s.KBr;
+    L.nf = s.nf;
+    L.feat_idx = s.feat_idx;
+    L.F = s.F;
     L.e = s.e;
     L.s = s.rst[c][3];
     L.gh = s.gh;
@@ -692,6 +711,9 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
       L.Kbar = d.Kbar;
       L.Bbar = d.Bbar;
       L.KBr = d.KBr;
+      L.nf = d.nf;
+      L.feat_idx = d.feat_idx;
+      L.F = d.F;
       L.e = d.e;
       L.uh0 = d.rst[c][0];
       L.vh0 = d.rst[c][1];
@@ -1005,6 +1027,12 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
       s.h_Bbar.assign(d->Bbar, d->Bbar + (size_t)d->r * d->r_b);
     }
     s.h_Kbar.assign(d->Kbar, d->Kbar + (size_t)d->r * d->r);
+    if (d->Cbar && !d->Hbar) return fail(OSAM_EINVAL, "Cbar (cubic OpInf) requires Hbar (quadratic term)");
+    s.order = d->Cbar ? 3 : (d->Hbar ? 2 : 1);
+    const long long n2 = (long long)d->r * (d->r + 1) / 2, n3 = (long long)d->r * (d->r + 1) * (d->r + 2) / 6;
+    if (s.order >= 2) s.h_Hbar.assign(d->Hbar, d->Hbar + (size_t)d->r * n2);
+    if (s.order >= 3) s.h_Cbar.assign(d->Cbar, d->Cbar + (size_t)d->r * n3);
+    s.nf = (int)((s.order >= 2 ? n2 : 0) + (s.order >= 3 ? n3 : 0));
     s.h_e.assign((size_t)d->batch, 1.0);
     if (d->e_scale)
       for (int b = 0; b < d->batch; ++b) s.h_e[b] = d->e_scale[b];

@@ -98,6 +98,11 @@ struct Sub {
   // ROM device data
   double *Phi = nullptr, *Phi_s = nullptr, *Kbar = nullptr, *Bbar = nullptr, *e = nullptr;
   std::vector<double> h_Phi, h_Phi_s, h_Kbar, h_Bbar, h_e;  // host copies (create)
+  std::vector<double> h_Hbar, h_Cbar;  // polynomial OpInf terms (empty: absent)
+  int order = 1;                       // 1 linear, 2 QOpInf, 3 COpInf
+  int nf = 0;                          // polynomial features r(r+1)/2 [+ r(r+1)(r+2)/6]
+  int* feat_idx = nullptr;             // device [nf][3] monomial indices (-1: unused third factor)
+  double* F = nullptr;                 // device features [nf][B] (CUDA-core path)
   double* rst[2][4] = {{nullptr}};  // [buf] uh, vh, ah, s   (r x B, r x B, r x B, n_sdof x B)
   double* ustar = nullptr;          // r x B scratch
   double* gh = nullptr;             // r_b x B scratch
@@ -158,7 +163,10 @@ struct RomLaunch {
   int r, r_b, B;
   long long n_sdof;
   const double *Phi_s, *Kbar, *Bbar, *e;
-  const double* KBr;  // [-Kbar | Bbar] row-major r x (r + r_b) (CUDA-core path)
+  const double* KBr;  // [-Kbar | Bbar | -Hbar | -Cbar] row-major r x (r + r_b + nf) (CUDA-core path)
+  int nf;             // polynomial features (0: linear OpInf)
+  const int* feat_idx;
+  double* F;          // features [nf][B] (CUDA-core path)
   const double *uh0, *vh0, *ah0;  // checkpoint
   double *uh1, *vh1, *ah1;        // working
   const double* s;                // working Schwarz values (n_sdof x B)
@@ -179,7 +187,10 @@ cudaError_t launch_rom_project(long long n_rows, int r, int B, const double* Phi
 void launch_gather_dofs(long long n, int B, const int* ids, const double* field, long long field_bstride,
                         long long n_nodes, double* out, cudaStream_t s);
 void launch_rom_accel(const RomLaunch& L, const double* uh, double* ah, cudaStream_t s, int* launches);
-long long tc_part_size(int r, int r_b, int B, long long n_s, long long n_lift3);
+long long tc_part_size(int r, int r_b, int nf, int B, long long n_s, long long n_lift3);
+// F[q, b] = prod of u[idx[q][.], b]  (compressed Khatri-Rao monomials of the reduced state)
+void launch_rom_features(int nf, int B, const int* idx, const double* u, long long ustride, double* F, long long fstride,
+                         cudaStream_t s);
 void launch_rom_advance_tc(const RomLaunch& L, const double* KB, double* Z, double* part, cudaStream_t s,
                            int* launches);
 void launch_rom_accel_tc(const RomLaunch& L, const double* uh, double* ah, const double* KB, double* Z, double* part,

@@ -32,7 +32,8 @@ class osam_subdomain_desc(C.Structure):
                 ("n_free", C.c_int64), ("n_s", C.c_int64),
                 ("Phi", C.POINTER(C.c_double)), ("Phi_s", C.POINTER(C.c_double)),
                 ("Kbar", C.POINTER(C.c_double)), ("Bbar", C.POINTER(C.c_double)),
-                ("e_scale", C.POINTER(C.c_double))]
+                ("e_scale", C.POINTER(C.c_double)),
+                ("Hbar", C.POINTER(C.c_double)), ("Cbar", C.POINTER(C.c_double))]
 
 
 class osam_schwarz_cfg(C.Structure):
@@ -126,6 +127,11 @@ class Subdomain:
             d.n_free, d.n_s = Phi.shape[0], Phi_s.shape[0]
             d.Phi, d.Phi_s, d.Kbar, d.Bbar = _dptr(Phi), _dptr(Phi_s), _dptr(Kbar), _dptr(Bbar)
             self._keep += [Phi, Phi_s, Kbar, Bbar]
+            for name in ("Hbar", "Cbar"):  # polynomial OpInf terms (optional)
+                if rom.get(name) is not None:
+                    M = np.asfortranarray(rom[name], dtype=np.float64)
+                    setattr(d, name, _dptr(M))
+                    self._keep.append(M)
             if e_scale is not None:
                 e = np.ascontiguousarray(e_scale, dtype=np.float64)
                 d.batch = len(e)

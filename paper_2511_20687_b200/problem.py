@@ -26,7 +26,8 @@ def build(cfg, rom_ops=None, stream=None):
         rom = None
         if kind == OSAM_ROM:
             o = rom_ops[i]
-            rom = dict(Phi=o["Phi"], Phi_s=o["Phi_s"], Kbar=o["Kbar"], Bbar=o["Bbar"])
+            rom = dict(Phi=o["Phi"], Phi_s=o["Phi_s"], Kbar=o["Kbar"], Bbar=o["Bbar"], Hbar=o.get("Hbar"),
+                       Cbar=o.get("Cbar"))
         subs.append(Subdomain(kind, s["lo"], s["hi"], s["nel"], cfg["E"], cfg["nu"], cfg["rho"], s["dirichlet"],
                               stream=stream, rom=rom, e_scale=e_scale(cfg) if kind == OSAM_ROM else None))
     return subs

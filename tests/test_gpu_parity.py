@@ -220,3 +220,33 @@ def test_max_iters_reached_keeps_last_iterate(gpu, max_iters):
     models, states, it_ref, _ = oracle_run(cfg, 5)
     assert np.array_equal(iters, it_ref.reshape(iters.shape))
     compare(gpu, subs, models, states)
+
+
+@pytest.mark.parametrize("order", [2, 3])
+def test_c2_polynomial_opinf(gpu, order):
+    """QOpInf / COpInf (eq:quadratic_opinf): c2's FOM-ROM coupling with a quadratic or cubic
+    OpInf ROM trained by the oracle's offline stage (r = 20), 200 steps vs the oracle."""
+    cfg = I.config("c2")
+    cfg["rom"] = dict(cfg["rom"], order=order)
+    ops = opinf.train(cfg, I)
+    assert ("Hbar" in ops[1]) and (("Cbar" in ops[1]) == (order == 3))
+    _, iters, worst = run_both(gpu, cfg, 200, rom_ops=ops, checkpoints=(1,))
+    print(f"c2 order {order} worst rel L2", worst)
+
+
+def test_c5_shaped_batched_cubic_opinf_tensor_cores(gpu):
+    """Batched COpInf on the tensor-core path: c5 geometry and samples (B = 64), r = 10, seeded cubic
+    operators whose polynomial terms are of the order of the linear one, 100 steps vs the oracle."""
+    cfg = I.config("c5")
+    rng = np.random.default_rng(12)
+    ops = {}
+    from paper_2511_20687_b200 import problem
+    for i in (0, 1):
+        n_free, n_s = problem.dof_split(cfg, i)
+        o = I.synthetic_rom_operators(n_free, n_s, 10, 5, cfg["dt"], seed=40 + i)
+        k = np.diag(o["Kbar"]).max()
+        o["Hbar"] = 0.1 * k / 1e-3 * rng.standard_normal((10, opinf.n_poly(10, 2))) / 55
+        o["Cbar"] = 0.1 * k / 1e-6 * rng.standard_normal((10, opinf.n_poly(10, 3))) / 220
+        ops[i] = o
+    _, iters, worst = run_both(gpu, cfg, 100, rom_ops=ops, checkpoints=(1,))
+    print("c5-shaped cubic worst rel L2", worst)
