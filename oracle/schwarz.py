@@ -20,6 +20,17 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
         den = sum_i ||u_i^n + dt v_i^n||^2   over unconstrained DOFs (ROM: reduced coords),
     converged iff num == 0 or num < tol_rel^2 den (or num < tol_abs^2 if tol_abs > 0).
     Per sample when batched; converged samples are frozen; max_iters -> keep last iterate.
+  * Substeps and the temporal interpolant Xi (P:L404-442 eq:schwarz_discrete, L468-490,
+    readings R31-R33): subdomain i takes n_i steps of dt_i = dt / n_i per controller step.
+    Every iterate carries its trace [state at t_{k-1} (checkpoint), state after substep
+    1, ..., n_i]; the Schwarz values of destination substep l (time t_{k-1} + l dt_dst) are
+    Pi applied to the source trace, interpolated linearly in time between the two bracketing
+    source substeps (Xi).  With every n_i = 1 this is exactly the scheme above.
+  * Implicit ROM (reading R32): Newmark beta = 1/4, gamma = 1/2 (average acceleration),
+        u~ = u^ + dt v^ + dt^2 (1/2 - beta) a^ ,
+        (I + beta dt^2 e_b Kbar) a^' = e_b (-Kbar u~ + Bbar g^) ,
+        u^' = u~ + beta dt^2 a^' ,  v^' = v^ + dt ((1 - gamma) a^ + gamma a^')
+    (linear OpInf; polynomial terms with the implicit scheme are not supported).
 """
 from __future__ import annotations
 
@@ -80,11 +91,21 @@ class _Base:
             nodes, w = transfer.projector(models[j].box, X[sel])
             self._proj.append((int(j), sel, nodes, w))
 
-    def gather_s(self, source_states, models):
-        """s at this subdomain's Schwarz DOFs (B, n_sdofs) from the sources' current fields."""
+    def gather_s(self, source_traces, models, l=1):
+        """s at this subdomain's Schwarz DOFs (B, n_sdofs) at its substep l (time t_{k-1} + l dt_i) from
+        each source's trace [checkpoint, substep 1, ..., n_j]: Pi of the two source substeps that
+        bracket the time, combined linearly in time (the temporal interpolant Xi, P:L468-490,
+        reading R31); a source substep at exactly that time is used as is."""
         vals = None
         for j, sel, nodes, w in self._proj:
-            v = transfer.apply(nodes, w, lambda ids: models[j].values_at(source_states[j], ids))
+            tr = source_traces[j]
+            nj = len(tr) - 1
+            lo, rem = divmod(l * nj, self.n_sub)
+            v = transfer.apply(nodes, w, lambda ids: models[j].values_at(tr[lo], ids))
+            if rem:
+                alpha = rem / self.n_sub
+                v1 = transfer.apply(nodes, w, lambda ids: models[j].values_at(tr[lo + 1], ids))
+                v = (1.0 - alpha) * v + alpha * v1
             if vals is None:
                 vals = np.zeros((v.shape[0], len(self.schwarz_nodes), 3))
             vals[:, sel, :] = v
@@ -98,22 +119,25 @@ class FOM(_Base):
     kind = "fom"
     batch = 1
 
-    def __init__(self, sub, schwarz_faces, E, nu, rho, dt):
+    def __init__(self, sub, schwarz_faces, E, nu, rho, dt, n_sub=1):
         super().__init__(sub, schwarz_faces, E, nu, rho)
         self.Ke = fem.hex8_stiffness(self.box.h, E, nu)
         self.m = fem.lumped_mass(self.box, rho)
-        self.dt = dt
+        self.n_sub = int(n_sub)
+        self.dt = dt / self.n_sub          # subdomain step dt_i
 
     def force(self, u):
         return fem.internal_force(self.box, self.Ke, u)
 
-    def init_state(self, u0):
-        """c.1 step 8: Dirichlet DOFs := 0, Schwarz DOFs keep the IC; v0 = 0; a0 = -f(u0)/m (free)."""
+    def init_state(self, u0, v0=None):
+        """c.1 step 8: Dirichlet DOFs := 0, Schwarz DOFs keep the IC; v0 = 0 (or the given v0 on free
+        DOFs, 0 on constrained ones, reading R10); a0 = -f(u0)/m (free)."""
         u0 = np.array(u0[0], dtype=np.float64)
         u0[self.codes == fem.DIRICHLET] = 0.0
         free = self.codes == fem.FREE
         a0 = np.where(free, -self.force(u0) / self.m[:, None], 0.0)
-        return dict(u=u0[None], v=np.zeros_like(u0)[None], a=a0[None])
+        v = np.zeros_like(u0) if v0 is None else np.where(free, np.asarray(v0[0], dtype=np.float64), 0.0)
+        return dict(u=u0[None], v=v[None], a=a0[None])
 
     def advance(self, ckpt, s):
         u, v, a = fem.explicit_newmark_step(ckpt["u"][0], ckpt["v"][0], ckpt["a"][0], s[0], self.codes,
@@ -135,9 +159,13 @@ class ROM(_Base):
 
     kind = "rom"
 
-    def __init__(self, sub, schwarz_faces, E, nu, rho, dt, ops, e_scale=None):
+    def __init__(self, sub, schwarz_faces, E, nu, rho, dt, ops, e_scale=None, n_sub=1, integrator="explicit"):
         super().__init__(sub, schwarz_faces, E, nu, rho)
-        self.dt = dt
+        self.n_sub = int(n_sub)
+        self.dt = dt / self.n_sub          # subdomain step dt_i
+        if integrator not in ("explicit", "implicit"):
+            raise ValueError(integrator)
+        self.beta = 0.25 if integrator == "implicit" else 0.0   # reading R32
         self.Phi = np.asarray(ops["Phi"], dtype=np.float64)       # (n_free, r)
         self.Phi_s = np.asarray(ops["Phi_s"], dtype=np.float64)   # (n_sdofs, r_b)
         self.Kbar = np.asarray(ops["Kbar"], dtype=np.float64)     # (r, r)
@@ -153,6 +181,8 @@ class ROM(_Base):
         self.free_row[self.free_dofs] = np.arange(len(self.free_dofs))
         self.sdof_idx = np.full(3 * self.box.n_nodes, -1, dtype=np.int64)
         self.sdof_idx[self.schwarz_dofs] = np.arange(len(self.schwarz_dofs))
+        if self.beta > 0 and (self.Hbar is not None or self.Cbar is not None):
+            raise ValueError("implicit ROM stepping is implemented for linear OpInf only")
 
     def accel(self, uh, s):
         """a^ = e_b (-Kbar u^ - Hbar u^*2 - Cbar u^*3 + Bbar Phi_dS^T s)  (eq:opinf_model_schwarz P:L550-563;
@@ -165,21 +195,35 @@ class ROM(_Base):
             f = f - opinf.khatri_rao_pow(uh.T, 3).T @ self.Cbar.T
         return self.e[:, None] * f
 
-    def init_state(self, u0):
-        """u^0 = Phi^T u0[free], v^0 = 0, s0 = u0 at the Schwarz DOFs, a^0 = e(-Kbar u^0 + Bbar Phi_s^T s0)
-        (SURVEY c.1 step 10)."""
-        u0 = np.asarray(u0, dtype=np.float64).reshape(u0.shape[0], -1)
-        if u0.shape[0] == 1 and self.batch > 1:
-            u0 = np.repeat(u0, self.batch, axis=0)
+    def init_state(self, u0, v0=None):
+        """u^0 = Phi^T u0[free], v^0 = 0 (or Phi^T v0[free]), s0 = u0 at the Schwarz DOFs,
+        a^0 = e(-Kbar u^0 + Bbar Phi_s^T s0)  (SURVEY c.1 step 10)."""
+        def rows(x):
+            x = np.asarray(x, dtype=np.float64).reshape(x.shape[0], -1)
+            return np.repeat(x, self.batch, axis=0) if x.shape[0] == 1 and self.batch > 1 else x
+        u0 = rows(u0)
         uh = u0[:, self.free_dofs] @ self.Phi
+        vh = np.zeros_like(uh) if v0 is None else rows(v0)[:, self.free_dofs] @ self.Phi
         s0 = u0[:, self.schwarz_dofs]
-        return dict(uh=uh, vh=np.zeros_like(uh), ah=self.accel(uh, s0), s=s0)
+        return dict(uh=uh, vh=vh, ah=self.accel(uh, s0), s=s0)
 
     def advance(self, ckpt, s):
         dt = self.dt
-        uh = ckpt["uh"] + dt * ckpt["vh"] + 0.5 * dt * dt * ckpt["ah"]
-        ah = self.accel(uh, s)
-        vh = ckpt["vh"] + 0.5 * dt * (ckpt["ah"] + ah)
+        if self.beta == 0.0:    # explicit Newmark (beta = 0, gamma = 1/2)
+            uh = ckpt["uh"] + dt * ckpt["vh"] + 0.5 * dt * dt * ckpt["ah"]
+            ah = self.accel(uh, s)
+            vh = ckpt["vh"] + 0.5 * dt * (ckpt["ah"] + ah)
+            return dict(uh=uh, vh=vh, ah=ah, s=np.array(s))
+        # implicit Newmark, average acceleration (reading R32): solve for a^' sample by sample
+        beta, gamma = self.beta, 0.5
+        ut = ckpt["uh"] + dt * ckpt["vh"] + dt * dt * (0.5 - beta) * ckpt["ah"]
+        rhs = self.accel(ut, s)                                      # e_b (-Kbar u~ + Bbar g^)
+        r = self.Kbar.shape[0]
+        ah = np.empty_like(ut)
+        for b in range(ut.shape[0]):
+            ah[b] = np.linalg.solve(np.eye(r) + beta * dt * dt * self.e[b] * self.Kbar, rhs[b])
+        uh = ut + beta * dt * dt * ah
+        vh = ckpt["vh"] + dt * ((1.0 - gamma) * ckpt["ah"] + gamma * ah)
         return dict(uh=uh, vh=vh, ah=ah, s=np.array(s))
 
     def values_at(self, state, nodes):
@@ -223,18 +267,27 @@ def controller_step(models, states, tol_rel, max_iters=50, min_iters=2, tol_abs=
     prev = None
     active = np.ones(B, dtype=bool)
     iters = np.zeros(B, dtype=np.int64)
+    prev_tr = None
     for n in range(1, max_iters + 1):
-        new = []
+        new, new_tr = [], []
         for i, mi in enumerate(models):
-            src_states = [new[j] if j < i else (prev[j] if prev is not None else ckpt[j])
-                          for j in range(len(models))]
-            s = mi.gather_s(src_states, models) if len(mi.schwarz_dofs) else np.zeros((mi.batch, 0))
-            if s.shape[0] != mi.batch:
-                s = s[:1] if mi.batch == 1 else np.repeat(s, mi.batch, axis=0)
-            out = mi.advance(ckpt[i], s)
+            # source traces: iterate n if the source precedes i in the sweep, else iterate n - 1
+            # (iterate 0: the checkpoint held constant over the interval, reading R5)
+            src_tr = [new_tr[j] if j < i else (prev_tr[j] if prev_tr is not None else [ckpt[j]] * (models[j].n_sub + 1))
+                      for j in range(len(models))]
+            out = ckpt[i]
+            tr = [out]
+            for l in range(1, mi.n_sub + 1):
+                s = mi.gather_s(src_tr, models, l) if len(mi.schwarz_dofs) else np.zeros((mi.batch, 0))
+                if s.shape[0] != mi.batch:
+                    s = s[:1] if mi.batch == 1 else np.repeat(s, mi.batch, axis=0)
+                out = mi.advance(out, s)
+                tr.append(out)
             if prev is not None and mi.batch > 1:
-                out = _select(out, prev[i], active)
+                tr = [_select(t, tp, active) for t, tp in zip(tr, prev_tr[i])]
+                out = tr[-1]
             new.append(out)
+            new_tr.append(tr)
         iters[active] = n
         if n >= min_iters:
             num = np.zeros(B)
@@ -249,7 +302,7 @@ def controller_step(models, states, tol_rel, max_iters=50, min_iters=2, tol_abs=
             if trace is not None:
                 trace.append((n, num.copy(), den.copy()))
             active &= ~conv
-        prev = new
+        prev, prev_tr = new, new_tr
         if not active.any():
             break
     return new, iters
@@ -261,18 +314,23 @@ def build_models(cfg, rom_ops=None, e_scale=None):
     faces = detect_schwarz_faces(boxes)
     models = []
     for i, s in enumerate(cfg["subdomains"]):
+        n_sub = s.get("n_sub", 1)
         if s["kind"] == "fom":
-            models.append(FOM(s, faces[i], cfg["E"], cfg["nu"], cfg["rho"], cfg["dt"]))
+            if s.get("integrator", "explicit") != "explicit":
+                raise ValueError("the FOM is explicit (north_star); implicit FOM solves are out of scope")
+            models.append(FOM(s, faces[i], cfg["E"], cfg["nu"], cfg["rho"], cfg["dt"], n_sub))
         else:
-            models.append(ROM(s, faces[i], cfg["E"], cfg["nu"], cfg["rho"], cfg["dt"], rom_ops[i], e_scale))
+            models.append(ROM(s, faces[i], cfg["E"], cfg["nu"], cfg["rho"], cfg["dt"], rom_ops[i], e_scale, n_sub,
+                              s.get("integrator", "explicit")))
     for mdl in models:
         mdl.build_projectors(models)
     return models
 
 
-def run(models, u0s, dt, n_steps, tol_rel, max_iters=50, min_iters=2, tol_abs=0.0, callback=None):
-    """Run n_steps controller steps from the ICs u0s[i] (batch, n_nodes, 3)."""
-    states = [m.init_state(u0) for m, u0 in zip(models, u0s)]
+def run(models, u0s, dt, n_steps, tol_rel, max_iters=50, min_iters=2, tol_abs=0.0, callback=None, v0s=None):
+    """Run n_steps controller steps from the ICs u0s[i] (batch, n_nodes, 3) (and optional v0s[i])."""
+    v0s = [None] * len(models) if v0s is None else v0s
+    states = [m.init_state(u0, v0) for m, u0, v0 in zip(models, u0s, v0s)]
     all_iters = []
     for k in range(n_steps):
         states, it = controller_step(models, states, tol_rel, max_iters, min_iters, tol_abs)

@@ -182,14 +182,14 @@ def test_c4_full_size_one_step_sampled(gpu):
     rom_ref = {}
     for k, mdl in ((0, L), (2, R)):
         st0 = mdl.init_state(u0s[k])
-        s = mdl.gather_s([None, stC, None], models)
+        s = mdl.gather_s([None, [stC, stC], None], models)   # single-substep traces
         rom_ref[k] = mdl.advance(st0, s)
     for k in (0, 2):
         uh, vh, ah = gpu.rom_state(subs[k], accel=True)
         for got, ref in ((uh, rom_ref[k]["uh"]), (vh, rom_ref[k]["vh"]), (ah, rom_ref[k]["ah"])):
             assert np.linalg.norm(got - ref) <= 1e-10 * np.linalg.norm(ref), k
     # FOM: Schwarz values = lifted ROM predictors; slabs checked on every node of their interior planes
-    sC = Cm.gather_s([rom_ref[0], None, rom_ref[2]], models)[0]
+    sC = Cm.gather_s([[rom_ref[0]] * 2, None, [rom_ref[2]] * 2], models)[0]
     ustar_all = u_it.reshape(-1, 3).copy()
     ustar_all.reshape(-1)[Cm.schwarz_dofs] = sC
     u, v, a = gpu.fom_state(subs[1], accel=True)
