@@ -46,6 +46,11 @@ typedef struct osam_subdomain osam_subdomain; /* opaque handle */
 
 enum { OSAM_FOM = 0, OSAM_ROM = 1 };
 
+/* Time integrator of a subdomain (Newmark-beta, gamma = 1/2, eq:schwarz_opinf_discrete
+ * P:L617-722, reading R32): explicit (beta = 0, central difference) or, for a linear OpInf ROM,
+ * implicit average acceleration (beta = 1/4): (I + beta dt_i^2 e_b Kbar) a^' = e_b (-Kbar u~ + Bbar g^). */
+enum { OSAM_EXPLICIT = 0, OSAM_IMPLICIT = 1 };
+
 enum {
   OSAM_OK = 0,
   OSAM_WNOTCONVERGED = 1, /* some controller step hit max_iters; last iterate kept */
@@ -76,10 +81,18 @@ typedef struct {
    * lexicographic; the reduced model is a^ = e_b (-Kbar u^ - Hbar u^*2 - Cbar u^*3 + Bbar g^).      */
   const double *Hbar;     /* r x r(r+1)/2        column-major                                         */
   const double *Cbar;     /* r x r(r+1)(r+2)/6   column-major                                         */
+  /* Time discretisation of this subdomain (footnote: dt_i divides the controller step):
+   * n_substeps steps of dt_i = cfg.dt / n_substeps per controller step (0 or 1: one step).  When the
+   * subdomains of a step differ in n_substeps, Schwarz values at a destination substep come from the
+   * source's iterate trace through the temporal interpolant Xi: linear in time between the
+   * two bracketing source substeps, the interval start being the source's checkpoint (reading R31);
+   * the convergence norm is evaluated at the interval end with dt_i (reading R33).                    */
+  int32_t n_substeps;     /* 0/1 .. 4096                                                              */
+  int32_t integrator;     /* OSAM_EXPLICIT (FOM: required) | OSAM_IMPLICIT (linear ROM only)         */
 } osam_subdomain_desc;
 
 typedef struct {
-  double dt;         /* common time step = controller step (> 0)                                */
+  double dt;         /* controller step (> 0); subdomain i steps with dt / n_substeps_i           */
   double tol_rel;    /* delta_rel of eq:conv_criterion                                          */
   double tol_abs;    /* delta_abs; <= 0 disables the absolute test                              */
   int32_t max_iters; /* Schwarz iteration cap (>= 1)                                             */
@@ -124,7 +137,8 @@ const char* osam_last_error(void);
  * launch (kernel K1) on the subdomain's stream and accumulates their durations; the
  * convergence check then synchronises once per iteration.  osam_get_profile returns the
  * accumulated K1 milliseconds, the number of K1 launches, the algorithmic bytes those
- * launches moved (48 B per FOM DOF per sweep + 16 B per DOF from sweep 2 on),
+ * launches moved (32 B per FOM DOF per launch + 8 B per DOF when the launch tests convergence,
+ * DESIGN.md section 6),
  * and the total number of kernels this library launched since the last reset. */
 void osam_set_profiling(int32_t on);
 void osam_reset_profile(void);

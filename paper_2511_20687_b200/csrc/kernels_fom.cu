@@ -412,7 +412,7 @@ __device__ __forceinline__ void prod_issue(const FomLaunch& L, const TileGrid& G
 // (plane m), C = acc[SC] (plane m-1, finished here if it lies in [kbeg, kend], then zeroed to become
 // the next A).  Targets outside the chunk are accumulated too (and never used): every iteration is
 // identical.
-template <int SA, int SB, int SC>
+template <bool ZN, int SA, int SB, int SC>
 __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStencil& S, const Tile& T, int it, int gi,
                                         double (&acc)[3][3], double& num, double& den, unsigned char* ring,
                                         unsigned long long* full, unsigned long long* empty, const Maps& M, Prod* pr,
@@ -479,11 +479,12 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
           qo[c * np] = fma(L.cq, wn, x);
           wp[c * np] = wn;
           if (L.with_norm) {
-            const double d = 0.5 * L.dt * (wn - qw[c * WPL]);
             const double w = fma(L.dt, fma(L.cv, an, w0), x);
+            const double d = ZN ? w - qw[c * WPL] : 0.5 * L.dt * (wn - qw[c * WPL]);
             num = fma(d, d, num);
             den = fma(w, w, den);
           }
+          if (ZN) L.z_out[c * np + id] = fma(L.dt, fma(L.cv, an, w0), x);
         }
       } else {
         const unsigned fm = (T.cy() != 1 || cz != 1) ? free_mask(g, L.f, T.i, T.j, kf) : 7u;
@@ -498,11 +499,12 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
             wn = fma(L.cw, an, w0);
             qn = fma(L.cq, wn, x);
             if (L.with_norm) {
-              const double d = 0.5 * L.dt * (wn - qw[c * WPL]);
               const double w = fma(L.dt, fma(L.cv, an, w0), x);
+              const double d = ZN ? w - qw[c * WPL] : 0.5 * L.dt * (wn - qw[c * WPL]);
               num = fma(d, d, num);
               den = fma(w, w, den);
             }
+            if (ZN) L.z_out[c * np + id] = fma(L.dt, fma(L.cv, an, w0), x);
           }
           if (L.q_out) L.q_out[c * np + id] = qn;
           L.w_out[c * np + id] = wn;
@@ -521,6 +523,7 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
 #ifndef OSAM_MINB
 #define OSAM_MINB 2
 #endif
+template <bool ZN>
 __global__ void __launch_bounds__(NT, OSAM_MINB)
     fom_tiled_kernel(const __grid_constant__ FomLaunch L, const __grid_constant__ InteriorStencil S,
                      const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
@@ -570,13 +573,13 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
     T.nplanes = P.nplanes;
     T.id0 = T.i + (long long)g.px * T.j;
     for (int it = 0; it < T.nplanes;) {  // unrolled by the period 3 of the slot rotation
-      k1_iter<0, 1, 2>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
+      k1_iter<ZN, 0, 1, 2>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
       ++gi;
       if (++it >= T.nplanes) break;
-      k1_iter<2, 0, 1>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
+      k1_iter<ZN, 2, 0, 1>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
       ++gi;
       if (++it >= T.nplanes) break;
-      k1_iter<1, 2, 0>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
+      k1_iter<ZN, 1, 2, 0>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
       ++gi;
       ++it;
     }
@@ -649,12 +652,13 @@ __global__ void __launch_bounds__(XF_BLOCK) fom_xface_kernel(const FomLaunch L, 
         an = -f[c] * inv_m;
         wn = fma(L.cw, an, w0);
         qn = fma(L.cq, wn, x);
+        const double w = fma(L.dt, fma(L.cv, an, w0), x);
         if (L.with_norm) {
-          const double d = 0.5 * L.dt * (wn - L.w_out[c * np + id]);
-          const double w = fma(L.dt, fma(L.cv, an, w0), x);
+          const double d = L.z_out ? w - L.z_out[c * np + id] : 0.5 * L.dt * (wn - L.w_out[c * np + id]);
           num = fma(d, d, num);
           den = fma(w, w, den);
         }
+        if (L.z_out) L.z_out[c * np + id] = w;
       }
       if (L.q_out) L.q_out[c * np + id] = qn;
       L.w_out[c * np + id] = wn;
@@ -750,7 +754,8 @@ int tiled_ctas(const Geom& g) {
   static const bool persistent = getenv("OSAM_PERSISTENT") && getenv("OSAM_PERSISTENT")[0] == '1';
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(fom_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TILED);
+    cudaFuncSetAttribute(fom_tiled_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TILED);
+    cudaFuncSetAttribute(fom_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TILED);
     attr = true;
   }
   if (!persistent) return (int)tile_count(g);
@@ -759,8 +764,7 @@ int tiled_ctas(const Geom& g) {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(fom_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TILED);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fom_tiled_kernel, NT, SMEM_TILED);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fom_tiled_kernel<false>, NT, SMEM_TILED);
     resident = std::max(1, sms * std::max(1, per_sm));
   }
   return (int)std::min<long long>(resident, tile_count(g));
@@ -786,7 +790,10 @@ int fom_partial_slots(const Geom& g, const Faces& f) { return tiled_ctas(g) + (i
 void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUtensorMap* tmx,
                         const CUtensorMap* tmw, const CUtensorMap* tmwp, cudaStream_t s, int* launches) {
   const int n_int = tiled_ctas(L.g);
-  fom_tiled_kernel<<<n_int, dim3(TX, TY), SMEM_TILED, s>>>(L, st, *tmx, *tmw, *tmwp);
+  if (L.z_out)  // last substep of a multi-substep interval: z = u + dt v out, norm from z - z_prev (R33)
+    fom_tiled_kernel<true><<<n_int, dim3(TX, TY), SMEM_TILED, s>>>(L, st, *tmx, *tmw, *tmwp);
+  else
+    fom_tiled_kernel<false><<<n_int, dim3(TX, TY), SMEM_TILED, s>>>(L, st, *tmx, *tmw, *tmwp);
   debug_check("fom_tiled_kernel", s);
   ++*launches;
   const unsigned xb = xface_blocks(L.g, L.f);

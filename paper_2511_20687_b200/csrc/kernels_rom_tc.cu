@@ -120,17 +120,19 @@ __device__ __forceinline__ double warp_sum(double x) {
   return x;
 }
 
-// Z[0:r, b] = u^* = u^ + dt v^ + dt^2/2 a^   (Z is (r + r_b) x B, column-major)
+// Z[0:r, b] = u~ = u^ + dt v^ + c2 a^   (Z is rz x B, column-major; c2 = dt^2/2 explicit)
 __global__ void tc_predict_kernel(int r, int rz, int B, const double* __restrict__ uh, const double* __restrict__ vh,
-                                  const double* __restrict__ ah, double dt, double* __restrict__ Z) {
+                                  const double* __restrict__ ah, double dt, double c2, double* __restrict__ Z) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= r * B) return;
   const int i = t % r, b = t / r;
-  Z[i + (long long)rz * b] = fma(0.5 * dt * dt, ah[t], fma(dt, vh[t], uh[t]));
+  Z[i + (long long)rz * b] = fma(c2, ah[t], fma(dt, vh[t], uh[t]));
 }
 
 // a^' = e_b * araw, v^' = v^ + dt/2 (a^ + a^'), u^' = u^*, norm partials (active samples only).
-// grid (ceil(r/256), B); partial layout [slot][B] with slot = blockIdx.x.
+// grid (ceil(r/256), B); partial layout [slot][B] with slot = blockIdx.x.  mode 1: a^ only (all
+// samples); mode 2: implicit right-hand side e_b * araw into ah1 (active samples), rom_implicit_kernel
+// finishes.
 __global__ void __launch_bounds__(256) tc_epilogue_kernel(const RomLaunch L, const double* __restrict__ part,
                                                           int S, const double* __restrict__ Z, int rz, int mode) {
   __shared__ double red[2][8];
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(256) tc_epilogue_kernel(const RomLaunch L, con
     double araw = 0.0;
     for (int z = 0; z < S; ++z) araw += part[(size_t)z * r * L.B + id];  // split-K partials, fixed order
     const double an = L.e[b] * araw;
-    if (mode == 1) {
+    if (mode != 0) {
       L.ah1[id] = an;
     } else {
       const double un = Z[i + (long long)rz * b];
@@ -160,7 +162,7 @@ __global__ void __launch_bounds__(256) tc_epilogue_kernel(const RomLaunch L, con
       L.ah1[id] = an;
     }
   }
-  if (mode == 1) return;
+  if (mode != 0) return;
   num = warp_sum(num);
   den = warp_sum(den);
   const int t = threadIdx.x;
@@ -211,7 +213,7 @@ long long tc_part_size(int r, int r_b, int nf, int B, long long n_s, long long n
 void launch_rom_advance_tc(const RomLaunch& L, const double* KB, double* Z, double* part, cudaStream_t s,
                            int* launches) {
   const int r = L.r, rb = L.r_b, rz = L.r + L.r_b + L.nf, B = L.B;
-  tc_predict_kernel<<<cdiv((long long)r * B, 256), 256, 0, s>>>(r, rz, B, L.uh0, L.vh0, L.ah0, L.dt, Z);
+  tc_predict_kernel<<<cdiv((long long)r * B, 256), 256, 0, s>>>(r, rz, B, L.uh0, L.vh0, L.ah0, L.dt, L.c2, Z);
   debug_check("tc_predict_kernel", s);
   launch_rom_features(L.nf, B, L.feat_idx, Z, rz, Z + r + rb, rz, s);  // polynomial OpInf rows of Z
   *launches += L.nf > 0;
@@ -223,9 +225,13 @@ void launch_rom_advance_tc(const RomLaunch& L, const double* KB, double* Z, doub
   }
   // araw = [-Kbar | Bbar] Z, reduced in the epilogue
   const int S = gemm(GemmArgs{r, B, rz, KB, 1, r, Z, 1, rz, nullptr, 0}, part, s);
-  tc_epilogue_kernel<<<dim3(cdiv(r, 256), B), 256, 0, s>>>(L, part, S, Z, rz, 0);
+  tc_epilogue_kernel<<<dim3(cdiv(r, 256), B), 256, 0, s>>>(L, part, S, Z, rz, L.beta > 0.0 ? 2 : 0);
   debug_check("tc_epilogue_kernel", s);
   *launches += 3;
+  if (L.beta > 0.0) {
+    launch_rom_implicit(L, Z, rz, rom_partial_slots(r, true), s);
+    ++*launches;
+  }
 }
 
 // Initial acceleration a^0 = e (-Kbar u^0 + Bbar Phi_dS^T s0) on the same path.
@@ -234,7 +240,7 @@ void launch_rom_accel_tc(const RomLaunch& L, const double* uh, double* ah, const
   const int r = L.r, rb = L.r_b, rz = L.r + L.r_b + L.nf, B = L.B;
   RomLaunch A = L;
   A.ah1 = ah;
-  tc_predict_kernel<<<cdiv((long long)r * B, 256), 256, 0, s>>>(r, rz, B, uh, uh, uh, 0.0, Z);  // Z[0:r] = u^0
+  tc_predict_kernel<<<cdiv((long long)r * B, 256), 256, 0, s>>>(r, rz, B, uh, uh, uh, 0.0, 0.0, Z);  // Z[0:r] = u^0
   debug_check("tc_predict_kernel", s);
   launch_rom_features(L.nf, B, L.feat_idx, Z, rz, Z + r + rb, rz, s);
   *launches += L.nf > 0;

@@ -26,10 +26,11 @@ __device__ __forceinline__ double warp_sum(double x) {
   return x;
 }
 
+// compact = 1: write dst[b][3p + c] (a trace slot) instead of dst[b][out[3p + c]]
 __global__ void transfer_kernel(int n, const int* __restrict__ idx, const double* __restrict__ xi,
                                 const int* __restrict__ out, const double* __restrict__ src, long long cs,
                                 long long bs_src, double* __restrict__ dst, long long bs_dst,
-                                const int* __restrict__ active) {
+                                const int* __restrict__ active, int compact) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
   if (p >= n || (active != nullptr && !active[b])) return;
@@ -46,7 +47,25 @@ __global__ void transfer_kernel(int n, const int* __restrict__ idx, const double
     double acc = 0.0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc = fma(w[q], sb[c * cs + idx[8 * p + q]], acc);
-    dst[b * bs_dst + o] = acc;
+    dst[b * bs_dst + (compact ? 3 * p + c : o)] = acc;
+  }
+}
+
+// Xi (reading R31): s = (1 - alpha) T[lo] + alpha T[lo + 1] from the trace slots of one map
+__global__ void trace_interp_kernel(int n, const int* __restrict__ out, const double* __restrict__ trace,
+                                    long long slot_stride, int lo, double alpha, double* __restrict__ dst,
+                                    long long bs_dst, const int* __restrict__ active) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (p >= n || (active != nullptr && !active[b])) return;
+  const double* T = trace + (long long)b * 3 * n + 3 * p;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const int o = out[3 * p + c];
+    if (o < 0) continue;
+    double v = T[lo * slot_stride + c];
+    if (alpha != 0.0) v = (1.0 - alpha) * v + alpha * T[(lo + 1) * slot_stride + c];
+    dst[b * bs_dst + o] = v;
   }
 }
 
@@ -158,16 +177,19 @@ __global__ void __launch_bounds__(256) rom_project_bnd_kernel(int r_b, int B, lo
   if (threadIdx.x == 0) gpart[((long long)z * B + b) * r_b + k] = acc;
 }
 
+// u~ = u^ + dt v^ + c2 a^  (c2 = dt^2/2 explicit; dt^2 (1/2 - beta) implicit)
 __global__ void rom_predict_kernel(int r, int B, const double* __restrict__ uh, const double* __restrict__ vh,
-                                   const double* __restrict__ ah, double dt, double* __restrict__ us) {
+                                   const double* __restrict__ ah, double dt, double c2, double* __restrict__ us) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= r * B) return;
-  us[t] = fma(0.5 * dt * dt, ah[t], fma(dt, vh[t], uh[t]));
+  us[t] = fma(c2, ah[t], fma(dt, vh[t], uh[t]));
 }
 
 // a^'[i,b] = e_b (sum_j KBr[i,j] z[j,b]), z = [u^*; g^], KBr = [-Kbar | Bbar] row-major; v^', norm
 // partials.  A warp per output row (lanes stride the row: coalesced), 8 rows per block; the block's
 // partial (num, den) sums its warps in order: grid (ceil(r/8), B), slot = blockIdx.x, layout [slot][B].
+// mode 1: acceleration only (initial condition); mode 2 (implicit): the right-hand side
+// e_b (-Kbar u~ + Bbar g^ ...) into ah1, finished by rom_implicit_kernel.
 __global__ void __launch_bounds__(256) rom_update_kernel(const RomLaunch L, int mode) {
   __shared__ double red[2][8];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -192,7 +214,7 @@ __global__ void __launch_bounds__(256) rom_update_kernel(const RomLaunch L, int 
     if (lane == 0) {
       const double an = L.e[b] * acc;
       const long long id = i + (long long)r * b;
-      if (mode == 1) {  // acceleration only (initial condition)
+      if (mode != 0) {  // acceleration only (initial condition) / implicit right-hand side
         L.ah1[id] = an;
       } else {
         const double vn = fma(0.5 * L.dt, L.ah0[id] + an, L.vh0[id]);
@@ -209,7 +231,7 @@ __global__ void __launch_bounds__(256) rom_update_kernel(const RomLaunch L, int 
       }
     }
   }
-  if (mode == 1) return;
+  if (mode != 0) return;
   if (lane == 0) {
     red[0][w] = num;
     red[1][w] = den;
@@ -288,6 +310,89 @@ __global__ void sum_chunks_kernel(int r, int B, int nz, const double* __restrict
   out[t] = v;
 }
 
+// Implicit ROM (reading R32), one block per sample: a^' = Minv_b f (f = ah1 from rom_update mode 2),
+// u^' = u~ + beta dt^2 a^', v^' = v^ + dt ((1 - gamma) a^ + gamma a^'), gamma = 1/2; norm partials in
+// slot 0 of the sample (other slots 0).  ut: u~ with per-sample stride uts.
+__global__ void __launch_bounds__(256) rom_implicit_kernel(const RomLaunch L, const double* __restrict__ ut,
+                                                           long long uts, int n_slots) {
+  extern __shared__ double f[];
+  const int b = blockIdx.x, r = L.r;
+  if (!L.active[b]) return;
+  for (int i = threadIdx.x; i < r; i += 256) f[i] = L.ah1[i + (long long)r * b];
+  __syncthreads();
+  const double* Mb = L.Minv + (long long)b * r * r;
+  const double bdt2 = L.beta * L.dt * L.dt;
+  double num = 0.0, den = 0.0;
+  for (int i = threadIdx.x; i < r; i += 256) {
+    double a = 0.0;
+    for (int j = 0; j < r; ++j) a = fma(Mb[(long long)i * r + j], f[j], a);
+    const long long id = i + (long long)r * b;
+    const double un = fma(bdt2, a, ut[i + uts * b]);
+    const double vn = L.vh0[id] + L.dt * (0.5 * L.ah0[id] + 0.5 * a);
+    if (L.with_norm) {
+      const double d = (un - L.uh1[id]) + L.dt * (vn - L.vh1[id]);
+      const double w = un + L.dt * vn;
+      num = fma(d, d, num);
+      den = fma(w, w, den);
+    }
+    L.uh1[id] = un;
+    L.vh1[id] = vn;
+    L.ah1[id] = a;
+  }
+  const double tn = block_sum256(num);
+  __syncthreads();
+  const double td = block_sum256(den);
+  if (threadIdx.x == 0) {
+    L.partial[b] = make_double2(tn, td);
+    for (int q = 1; q < n_slots; ++q) L.partial[(long long)q * L.B + b] = make_double2(0.0, 0.0);
+  }
+}
+
+// Minv_b = (I + c e_b Kbar)^-1 (Kbar column-major): Gauss-Jordan with partial pivoting on [M | I],
+// one block per sample (setup, once per dt_i).
+__global__ void __launch_bounds__(256) rom_minv_kernel(int r, const double* __restrict__ Kbar,
+                                                       const double* __restrict__ e, double c,
+                                                       double* __restrict__ work, double* __restrict__ Minv) {
+  extern __shared__ double fac[];
+  __shared__ int piv;
+  const int b = blockIdx.x, n2 = 2 * r;
+  double* W = work + (long long)b * r * n2;
+  const double ce = c * e[b];
+  for (long long t = threadIdx.x; t < (long long)r * n2; t += 256) {
+    const int i = (int)(t / n2), j = (int)(t % n2);
+    W[t] = j < r ? (i == j ? 1.0 : 0.0) + ce * Kbar[i + (long long)r * j] : (j - r == i ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    if (threadIdx.x == 0) {
+      int p = k;
+      for (int i = k + 1; i < r; ++i)
+        if (fabs(W[(long long)i * n2 + k]) > fabs(W[(long long)p * n2 + k])) p = i;
+      piv = p;
+    }
+    __syncthreads();
+    if (piv != k)
+      for (int j = threadIdx.x; j < n2; j += 256) {
+        const double t = W[(long long)k * n2 + j];
+        W[(long long)k * n2 + j] = W[(long long)piv * n2 + j];
+        W[(long long)piv * n2 + j] = t;
+      }
+    __syncthreads();
+    const double inv = 1.0 / W[(long long)k * n2 + k];
+    __syncthreads();
+    for (int j = threadIdx.x; j < n2; j += 256) W[(long long)k * n2 + j] *= inv;
+    for (int i = threadIdx.x; i < r; i += 256) fac[i] = W[(long long)i * n2 + k];
+    __syncthreads();
+    for (long long t = threadIdx.x; t < (long long)r * n2; t += 256) {
+      const int i = (int)(t / n2), j = (int)(t % n2);
+      if (i != k) W[t] = fma(-fac[i], W[(long long)k * n2 + j], W[t]);
+    }
+    __syncthreads();
+  }
+  for (long long t = threadIdx.x; t < (long long)r * r; t += 256)
+    Minv[(long long)b * r * r + t] = W[(t / r) * n2 + r + t % r];
+}
+
 __global__ void gather_dofs_kernel(long long n, int B, const int* __restrict__ ids, const double* __restrict__ field,
                                    long long fbs, long long n_nodes, double* __restrict__ out) {
   const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -303,7 +408,36 @@ void launch_transfer(const XferMap& m, const double* src, long long cs, long lon
                      long long bs_dst, int batch, const int* active, cudaStream_t s) {
   if (m.n == 0) return;
   transfer_kernel<<<dim3(cdiv(m.n, 128), batch), 128, 0, s>>>(m.n, m.idx, m.xi, m.out, src, cs, bs_src, dst,
-                                                                bs_dst, active);
+                                                                bs_dst, active, 0);
+  debug_check("transfer_kernel", s);
+}
+
+void launch_transfer_trace(const XferMap& m, const double* src, long long cs, long long bs_src, int slot, int batch,
+                           const int* active, cudaStream_t s) {
+  if (m.n == 0) return;
+  const long long bs = 3LL * m.n;
+  transfer_kernel<<<dim3(cdiv(m.n, 128), batch), 128, 0, s>>>(m.n, m.idx, m.xi, m.out, src, cs, bs_src,
+                                                                m.trace + (long long)slot * batch * bs, bs, active, 1);
+  debug_check("transfer_kernel(trace)", s);
+}
+
+void launch_trace_interp(const XferMap& m, int lo, double alpha, double* dst, long long bs_dst, int batch,
+                         const int* active, cudaStream_t s) {
+  if (m.n == 0) return;
+  trace_interp_kernel<<<dim3(cdiv(m.n, 128), batch), 128, 0, s>>>(m.n, m.out, m.trace, 3LL * m.n * batch, lo, alpha,
+                                                                    dst, bs_dst, active);
+  debug_check("trace_interp_kernel", s);
+}
+
+void launch_rom_minv(int r, int B, const double* Kbar, const double* e, double c, double* work, double* Minv,
+                     cudaStream_t s) {
+  rom_minv_kernel<<<B, 256, sizeof(double) * r, s>>>(r, Kbar, e, c, work, Minv);
+  debug_check("rom_minv_kernel", s);
+}
+
+void launch_rom_implicit(const RomLaunch& L, const double* ut, long long uts, int n_slots, cudaStream_t s) {
+  rom_implicit_kernel<<<L.B, 256, sizeof(double) * L.r, s>>>(L, ut, uts, n_slots);
+  debug_check("rom_implicit_kernel", s);
 }
 
 void launch_step_begin(Ctl c, int B, cudaStream_t s) { step_begin_kernel<<<1, 256, 0, s>>>(c, B); }
@@ -343,13 +477,18 @@ void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches) {
   if (L.r_b > 0)
     rom_project_bnd_kernel<<<dim3(L.r_b, rom_gchunks(L.n_sdof), L.B), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
                                                                                    L.s, L.gh);
-  rom_predict_kernel<<<cdiv((long long)L.r * L.B, 256), 256, 0, s>>>(L.r, L.B, L.uh0, L.vh0, L.ah0, L.dt, L.ustar);
+  rom_predict_kernel<<<cdiv((long long)L.r * L.B, 256), 256, 0, s>>>(L.r, L.B, L.uh0, L.vh0, L.ah0, L.dt, L.c2,
+                                                                     L.ustar);
   launch_rom_features(L.nf, L.B, L.feat_idx, L.ustar, L.r, L.F, L.nf, s);
   *launches += L.nf > 0;
   debug_check("rom_predict_kernel", s);
-  rom_update_kernel<<<dim3(cdiv(L.r, 8), L.B), 256, 0, s>>>(L, 0);
+  rom_update_kernel<<<dim3(cdiv(L.r, 8), L.B), 256, 0, s>>>(L, L.beta > 0.0 ? 2 : 0);
   debug_check("rom_update_kernel", s);
   *launches += (L.r_b > 0) + 2;
+  if (L.beta > 0.0) {
+    launch_rom_implicit(L, L.ustar, L.r, rom_partial_slots(L.r, false), s);
+    ++*launches;
+  }
 }
 
 void launch_rom_accel(const RomLaunch& L, const double* uh, double* ah, cudaStream_t s, int* launches) {

@@ -150,6 +150,7 @@ void release_maps(Sub& s) {
     dfree(m.idx);
     dfree(m.xi);
     dfree(m.out);
+    dfree(m.trace);
   }
   s.maps.clear();
 }
@@ -163,9 +164,15 @@ void release_binding(Sub& s) {
   dfree(s.Bbar);
   dfree(s.e);
   for (int b = 0; b < 2; ++b) {
-    for (int q = 0; q < 4; ++q) dfree(s.rst[b][q]);
+    for (int q = 0; q < 4; ++q) {
+      dfree(s.rst[b][q]);
+      dfree(s.rsub[b][q]);
+    }
     dfree(s.lift[b]);
   }
+  dfree(s.Minv);
+  dfree(s.minv_work);
+  s.minv_dt = 0.0;
   dfree(s.ustar);
   dfree(s.gh);
   dfree(s.free_ids);
@@ -208,6 +215,8 @@ struct Group {
   cudaStream_t cap_stream = nullptr;  // legacy default stream, which cannot be captured)
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int launches_per_sweep = 0;  // kernels of one sweep (launch accounting in graph mode)
+  int launches_begin = 1;      // kernels before sweep 1 (step_begin [+ trace slot 0])
+  bool trace = false;          // some subdomain takes several substeps: transfers through traces + Xi
   int ctl_len() const { return 2 + 2 * B + 4; }
   ~Group() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
@@ -353,6 +362,15 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
       TRY(dalloc(&s.rst[b][3], (size_t)std::max<long long>(1, s.n_sdof) * s.batch));
     }
     TRY(dalloc(&s.ustar, (size_t)s.r * s.batch));
+    if (s.n_sub > 1)
+      for (int b = 0; b < 2; ++b) {
+        for (int q = 0; q < 3; ++q) TRY(dalloc(&s.rsub[b][q], (size_t)s.r * s.batch));
+        TRY(dalloc(&s.rsub[b][3], (size_t)std::max<long long>(1, s.n_sdof) * s.batch));
+      }
+    if (s.beta > 0.0) {
+      TRY(dalloc(&s.Minv, (size_t)s.r * s.r * s.batch));
+      TRY(dalloc(&s.minv_work, (size_t)2 * s.r * s.r * s.batch));
+    }
     TRY(dalloc(&s.gh, (size_t)std::max(1, s.r_b) * s.batch * rom_gchunks(s.n_sdof)));
     // batched samples: the reduced update is a dense contraction -> FP64 tensor cores (OSAM_ROM_TC=0/1
     // overrides the default, which is tensor cores iff batch > 1)
@@ -516,8 +534,20 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
     TRY(upload(&m.idx, idx, d.stream));
     TRY(upload(&m.xi, P.xi, d.stream));
     TRY(upload(&m.out, P.out, d.stream));
+    m.n_src_sub = src.n_sub;
     d.maps.push_back(m);
   }
+  // multi-substep group: a trace of n_src_sub + 1 slots per map (R31)
+  bool trace = false;
+  int Bg = 1;
+  for (int i = 0; i < n; ++i) {
+    trace = trace || subs[i]->n_sub > 1;
+    Bg = std::max(Bg, subs[i]->batch);
+  }
+  if (trace)
+    for (int i = 0; i < n; ++i)
+      for (auto& m : subs[i]->maps)
+        TRY(dalloc(&m.trace, (size_t)(m.n_src_sub + 1) * Bg * 3 * std::max(1, m.n)));
   for (int i = 0; i < n; ++i) subs[i]->bound = true;
   int launches = 0;
   for (int i = 0; i < n; ++i)
@@ -589,6 +619,7 @@ int get_group(osam_subdomain* const* sds, int n_sd, Group** out) {
     G->sds = key;
     G->B = 1;
     for (auto s : subs) G->B = std::max(G->B, s->batch);
+    for (auto s : subs) G->trace = G->trace || s->n_sub > 1;
     G->n_slots = 0;
     for (auto s : subs) G->n_slots += s->kind == OSAM_FOM ? fom_partial_slots(s->g, s->faces) : rom_partial_slots(s->r, s->use_tc);
     TRY(dalloc(&G->partial, (size_t)std::max(1, G->n_slots) * G->B));
@@ -627,23 +658,61 @@ FomLaunch fom_launch(const Sub& d, const double* x, const double* w0, double* q_
 }
 
 // Bring the state to STEP(dt) (R30), with a = -K u / m from one force pass:
-//   RAW (u, v) in st[c]:    w = v + dt/2 a, q = u + dt w  -> st[1-c]; st[c][0] keeps u
-//   STEP(dt0) in st[c]:     u = st[1-c][0] exactly; w <- w + (dt - dt0)/2 a, q = u + dt w in place
+//   RAW (u, v) in st[c]:    w = v + dt/2 a, q = u + dt w  -> st[ux]; st[c][0] keeps u; swap c, ux
+//   STEP(dt0) in st[c]:     u = st[ux][0] exactly; w <- w + (dt - dt0)/2 a, q = u + dt w in place
+// (dt: the subdomain step dt_i)
 int fom_set_step(Sub& d, double dt, int* launches) {
   if (d.w_dt == dt) return OSAM_OK;
-  const int c = d.cur;
+  const int c = d.cur, x = d.ux;
   if (d.w_dt == 0.0) {
-    const FomLaunch L = fom_launch(d, d.st[c][0], d.st[c][1], d.st[1 - c][0], d.st[1 - c][1], 0.5 * dt, dt, 0.0,
+    const FomLaunch L = fom_launch(d, d.st[c][0], d.st[c][1], d.st[x][0], d.st[x][1], 0.5 * dt, dt, 0.0,
                                    dt, 0, d.scratch_partial, nullptr);
-    launch_fom_advance(L, d.stencil, &d.tmap[c], &d.tmapw[c], &d.tmapw[1 - c], d.stream, launches);
-    d.cur = 1 - c;
+    launch_fom_advance(L, d.stencil, &d.tmap[c], &d.tmapw[c], &d.tmapw[x], d.stream, launches);
+    d.cur = x;
+    d.ux = c;
   } else {
-    const FomLaunch L = fom_launch(d, d.st[1 - c][0], d.st[c][1], d.st[c][0], d.st[c][1], 0.5 * (dt - d.w_dt), dt,
+    const FomLaunch L = fom_launch(d, d.st[x][0], d.st[c][1], d.st[c][0], d.st[c][1], 0.5 * (dt - d.w_dt), dt,
                                    0.0, dt, 0, d.scratch_partial, nullptr);
-    launch_fom_advance(L, d.stencil, &d.tmap[1 - c], &d.tmapw[c], &d.tmapw[c], d.stream, launches);
+    launch_fom_advance(L, d.stencil, &d.tmap[x], &d.tmapw[c], &d.tmapw[c], d.stream, launches);
   }
   d.w_dt = dt;
   return OSAM_OK;
+}
+
+// ROM advance description: state `in` -> `out` ({u^, v^, a^, s} buffers), step dt (= dt_i)
+RomLaunch rom_launch(const Sub& d, double* const* in, double* const* out, const int* active, double dt,
+                     int with_norm, double2* partial) {
+  RomLaunch L{};
+  L.r = d.r;
+  L.r_b = d.r_b;
+  L.B = d.batch;
+  L.n_sdof = d.n_sdof;
+  L.Phi_s = d.Phi_s;
+  L.Kbar = d.Kbar;
+  L.Bbar = d.Bbar;
+  L.KBr = d.KBr;
+  L.nf = d.nf;
+  L.feat_idx = d.feat_idx;
+  L.F = d.F;
+  L.e = d.e;
+  L.uh0 = in[0];
+  L.vh0 = in[1];
+  L.ah0 = in[2];
+  L.uh1 = out[0];
+  L.vh1 = out[1];
+  L.ah1 = out[2];
+  L.s = out[3];
+  L.ustar = d.ustar;
+  L.gh = d.gh;
+  L.gchunks = rom_gchunks(d.n_sdof);
+  L.active = active;
+  L.dt = dt;
+  L.c2 = d.beta > 0.0 ? (0.5 - d.beta) * dt * dt : 0.5 * dt * dt;
+  L.beta = d.beta;
+  L.Minv = d.Minv;
+  L.with_norm = with_norm;
+  L.partial = partial;
+  return L;
 }
 
 // One Schwarz sweep of Algorithm 1 over the group, enqueued on `st`: for each
@@ -651,8 +720,12 @@ int fom_set_step(Sub& d, double dt, int* launches) {
 // source later in the sweep supplies its checkpoint, reading R5), then the FOM advance K1 or the
 // ROM advance K4-K6; finally K3 tests eq:conv_criterion and updates the device control
 // block.  `first` selects the n = 1 variant (constant extension, no norm).
+int enqueue_sweep_trace(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool first, cudaStream_t st,
+                        int* launches, int* fom_k);
+
 int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool first, cudaStream_t st, int* launches,
                   int* fom_k) {
+  if (G.trace) return enqueue_sweep_trace(G, cfg, ctl, first, st, launches, fom_k);
   std::vector<Sub*> subs;
   for (auto h : G.sds) subs.push_back(&h->s);
   const int n_sd = (int)subs.size();
@@ -668,7 +741,7 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
       if (src.kind == OSAM_FOM) {
         // a FOM iterate's displacement is its checkpoint q (predictor + current Schwarz values);
         // iterate 0 (constant extension) is the checkpoint u, kept in st[1-cur][0]
-        field = newest ? src.st[src.cur][0] : src.st[1 - src.cur][0];
+        field = newest ? src.st[src.cur][0] : src.st[src.ux][0];
         cs = src.g.npad;
         bs = 0;
       } else {
@@ -690,11 +763,11 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
     }
     const int with_norm = first ? 0 : 1;
     if (d.kind == OSAM_FOM) {
-      const int c = d.cur;
-      const FomLaunch L = fom_launch(d, d.st[c][0], d.st[c][1], d.st[1 - c][0], d.st[1 - c][1], cfg.dt, cfg.dt,
+      const int c = d.cur, x = d.ux;
+      const FomLaunch L = fom_launch(d, d.st[c][0], d.st[c][1], d.st[x][0], d.st[x][1], cfg.dt, cfg.dt,
                                      0.5 * cfg.dt, cfg.dt, with_norm, G.partial + (size_t)slot * B, nullptr);
       if (fom_k && g_prof) CK(cudaEventRecord(G.ev[2 * *fom_k], st));
-      launch_fom_advance(L, d.stencil, &d.tmap[c], &d.tmapw[c], &d.tmapw[1 - c], st, launches);
+      launch_fom_advance(L, d.stencil, &d.tmap[c], &d.tmapw[c], &d.tmapw[x], st, launches);
       if (fom_k && g_prof) CK(cudaEventRecord(G.ev[2 * *fom_k + 1], st));
       if (fom_k) ++*fom_k;
       g_k1_bytes += (32.0 + (with_norm ? 8.0 : 0.0)) * 3.0 * (double)d.n_nodes;
@@ -702,33 +775,8 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
       slot += fom_partial_slots(d.g, d.faces);
     } else {
       const int c = d.cur;
-      RomLaunch L{};
-      L.r = d.r;
-      L.r_b = d.r_b;
-      L.B = d.batch;
-      L.n_sdof = d.n_sdof;
-      L.Phi_s = d.Phi_s;
-      L.Kbar = d.Kbar;
-      L.Bbar = d.Bbar;
-      L.KBr = d.KBr;
-      L.nf = d.nf;
-      L.feat_idx = d.feat_idx;
-      L.F = d.F;
-      L.e = d.e;
-      L.uh0 = d.rst[c][0];
-      L.vh0 = d.rst[c][1];
-      L.ah0 = d.rst[c][2];
-      L.uh1 = d.rst[1 - c][0];
-      L.vh1 = d.rst[1 - c][1];
-      L.ah1 = d.rst[1 - c][2];
-      L.s = d.rst[1 - c][3];
-      L.ustar = d.ustar;
-      L.gh = d.gh;
-      L.gchunks = rom_gchunks(d.n_sdof);
-      L.active = ctl.active;
-      L.dt = cfg.dt;
-      L.with_norm = with_norm;
-      L.partial = G.partial + (size_t)slot * B;
+      const RomLaunch L = rom_launch(d, d.rst[c], d.rst[1 - c], ctl.active, cfg.dt, with_norm,
+                                     G.partial + (size_t)slot * B);
       if (d.use_tc) {
         launch_rom_advance_tc(L, d.KB, d.Z, d.part, st, launches);
         launch_rom_lift_tc(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, d.rst[1 - c][0], d.rst[1 - c][3],
@@ -747,6 +795,146 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
   return OSAM_OK;
 }
 
+// ---- multi-substep controller intervals (R31-R33) -----------------------------
+// A subdomain with n_sub = m takes m steps of dt_i = dt/m per sweep.  FOM buffers: substep l reads
+// X = (l == 0 ? st[cur] : output of substep l-1) and writes st[ux] (l even) / st[fr] (l odd); the
+// last substep also writes z = u + dt_i v (norm, R33) when m > 1.  ROM: rst[cur] -> rsub[0/1] ->
+// ... -> rst[1-cur].  Before substep l the Schwarz values at t + (l+1) dt_i are interpolated from
+// each source's trace (Xi); after it, the subdomain's field at that time is projected into the
+// trace slot l+1 of every map it feeds.
+
+// Source field of a trace transfer: FOM -> the q array holding u (stride npad), ROM -> lift buffer.
+void trace_source(const Sub& src, const double* field_fom, int lift_buf, const double** f, long long* cs,
+                  long long* bs) {
+  if (src.kind == OSAM_FOM) {
+    *f = field_fom;
+    *cs = src.g.npad;
+    *bs = 0;
+  } else {
+    *f = src.lift[lift_buf];
+    *cs = src.n_lift;
+    *bs = 3 * src.n_lift;
+  }
+}
+
+// Slot 0 of every trace: the sources' checkpoints (interval start).
+int enqueue_trace_begin(Group& G, cudaStream_t st, int* launches) {
+  std::vector<Sub*> subs;
+  for (auto h : G.sds) subs.push_back(&h->s);
+  for (auto sp : subs)
+    for (const XferMap& m : sp->maps) {
+      const Sub& src = *subs[m.src];
+      const double* f;
+      long long cs, bs;
+      trace_source(src, src.kind == OSAM_FOM ? src.st[src.ux][0] : nullptr, src.cur, &f, &cs, &bs);
+      launch_transfer_trace(m, f, cs, bs, 0, G.B, nullptr, st);
+      ++*launches;
+    }
+  return OSAM_OK;
+}
+
+int enqueue_sweep_trace(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool first, cudaStream_t st,
+                        int* launches, int* fom_k) {
+  std::vector<Sub*> subs;
+  for (auto h : G.sds) subs.push_back(&h->s);
+  const int n_sd = (int)subs.size();
+  const int B = G.B;
+  const int* act = B > 1 ? ctl.active : nullptr;
+  const int with_norm = first ? 0 : 1;
+  int slot = 0;
+  for (int i = 0; i < n_sd; ++i) {
+    Sub& d = *subs[i];
+    const int m = d.n_sub;
+    const double dti = cfg.dt / m;
+    double2* part = G.partial + (size_t)slot * B;
+    for (int l = 0; l < m; ++l) {
+      const bool last = l == m - 1;
+      const int xb = l == 0 ? d.cur : ((l - 1) % 2 == 0 ? d.ux : d.fr);  // FOM input buffer
+      const int ob = l % 2 == 0 ? d.ux : d.fr;                            // FOM output buffer
+      double* const* rin = l == 0 ? d.rst[d.cur] : d.rsub[(l - 1) % 2];   // ROM states
+      double* const* rout = last ? d.rst[1 - d.cur] : d.rsub[l % 2];
+      // Schwarz values at t + (l+1) dt_i through Xi (R31); at n = 1 later sources give slot 0
+      for (const XferMap& mp : d.maps) {
+        int lo = 0;
+        double alpha = 0.0;
+        if (!(first && mp.src > i)) {
+          const long long num = (long long)(l + 1) * mp.n_src_sub;
+          lo = (int)(num / m);
+          alpha = (double)(num % m) / (double)m;
+        }
+        if (d.kind == OSAM_FOM)
+          launch_trace_interp(mp, lo, alpha, d.st[xb][0], 0, B, act, st);
+        else
+          launch_trace_interp(mp, lo, alpha, rout[3], d.n_sdof, B, act, st);
+        ++*launches;
+      }
+      const double* field_fom = nullptr;
+      if (d.kind == OSAM_FOM) {
+        FomLaunch L = fom_launch(d, d.st[xb][0], d.st[xb][1], d.st[ob][0], d.st[ob][1], dti, dti, 0.5 * dti, dti,
+                                 last ? with_norm : 0, part, nullptr);
+        const bool zn = last && m > 1;
+        if (zn) L.z_out = d.zbuf;
+        if (fom_k && g_prof && last) CK(cudaEventRecord(G.ev[2 * *fom_k], st));
+        launch_fom_advance(L, d.stencil, &d.tmap[xb], &d.tmapw[xb], zn ? &d.tmapz : &d.tmapw[ob], st, launches);
+        if (fom_k && g_prof && last) {
+          CK(cudaEventRecord(G.ev[2 * *fom_k + 1], st));
+          ++*fom_k;
+          g_k1_bytes += (32.0 + (L.with_norm ? 8.0 : 0.0) + (zn ? 8.0 : 0.0)) * 3.0 * (double)d.n_nodes;
+          ++g_k1_launches;
+        }
+        field_fom = d.st[xb][0];  // u at t + (l+1) dt_i: the stencil input with its boundary values
+      } else {
+        const RomLaunch L = rom_launch(d, rin, rout, ctl.active, dti, last ? with_norm : 0, part);
+        if (d.use_tc) {
+          launch_rom_advance_tc(L, d.KB, d.Z, d.part, st, launches);
+          launch_rom_lift_tc(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, rout[0], rout[3], d.n_sdof,
+                             d.lift[1 - d.cur], d.part, st, launches);
+        } else {
+          launch_rom_advance(L, st, launches);
+          launch_rom_lift(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, rout[0], rout[3], d.n_sdof,
+                          d.lift[1 - d.cur], st);
+          *launches += d.n_lift > 0;
+        }
+      }
+      // this subdomain's field at t + (l+1) dt_i into slot l+1 of every map it feeds
+      for (int e = 0; e < n_sd; ++e)
+        for (const XferMap& mp : subs[e]->maps) {
+          if (mp.src != i) continue;
+          const double* f;
+          long long cs, bs;
+          trace_source(d, field_fom, 1 - d.cur, &f, &cs, &bs);
+          launch_transfer_trace(mp, f, cs, bs, l + 1, B, act, st);
+          ++*launches;
+        }
+    }
+    slot += d.kind == OSAM_FOM ? fom_partial_slots(d.g, d.faces) : rom_partial_slots(d.r, d.use_tc);
+  }
+  launch_finalize(ctl, G.partial, G.n_slots, B, cfg.min_iters, cfg.tol_rel, cfg.tol_abs, st);
+  *launches += 2;
+  return OSAM_OK;
+}
+
+// Commit a controller step: the working iterate becomes the checkpoint.  FOM buffer roles after m
+// substeps (R30): m = 1: swap(cur, ux); m odd: (cur, ux, fr) <- (ux, fr, cur); m even: (fr, ux, cur).
+void commit_step(Sub& d) {
+  if (d.kind != OSAM_FOM) {
+    d.cur = 1 - d.cur;
+    return;
+  }
+  const int c = d.cur, x = d.ux, f = d.fr;
+  if (d.n_sub == 1) {
+    d.cur = x;
+    d.ux = c;
+  } else if (d.n_sub % 2 == 1) {
+    d.cur = x;
+    d.ux = f;
+    d.fr = c;
+  } else {
+    d.cur = f;
+    d.fr = c;
+  }
+}
+
 // Host-driven controller step (profiling mode, or OSAM_NOGRAPH=1): the host reads the 16-byte
 // convergence flags after every tested sweep.  Returns OSAM_OK / OSAM_WNOTCONVERGED / error.
 int controller_step_host(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t st) {
@@ -762,6 +950,7 @@ int controller_step_host(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t st)
   int launches = 0;
   launch_step_begin(ctl, G.B, st);
   ++launches;
+  if (G.trace) TRY(enqueue_trace_begin(G, st, &launches));
   bool done = false;
   for (int n = 1; n <= cfg.max_iters; ++n) {
     int fom_k = 0;
@@ -787,7 +976,7 @@ int controller_step_host(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t st)
     }
   }
   CK(cudaGetLastError());
-  for (auto h : G.sds) h->s.cur = 1 - h->s.cur;  // commit: working iterate becomes the checkpoint
+  for (auto h : G.sds) commit_step(h->s);  // commit: working iterate becomes the checkpoint
   g_launches += launches;
   return done ? OSAM_OK : OSAM_WNOTCONVERGED;
 }
@@ -798,6 +987,9 @@ int step_graph_capture(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t st, c
   int launches = 0;
   CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
   launch_step_begin(ctl, G.B, st);
+  int begin = 1;
+  if (G.trace) TRY(enqueue_trace_begin(G, st, &begin));
+  G.launches_begin = begin;
   TRY(enqueue_sweep(G, cfg, ctl, true, st, &launches, nullptr));
   cudaStreamCaptureStatus status;
   const cudaGraphNode_t* deps = nullptr;
@@ -835,7 +1027,10 @@ int step_graph_capture(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t st, c
 
 int step_graph(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t, cudaGraphExec_t* out, int* launches_per_sweep) {
   GraphKey key{cfg.dt, cfg.tol_rel, cfg.tol_abs, cfg.max_iters, cfg.min_iters, {}};
-  for (auto h : G.sds) key.curs.push_back(h->s.cur);
+  for (auto h : G.sds) {
+    key.curs.push_back(h->s.cur);
+    key.curs.push_back(h->s.ux);
+  }
   auto it = G.graphs.find(key);
   if (it != G.graphs.end()) {
     *out = it->second;
@@ -894,6 +1089,13 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
     if (d->dirichlet[f] > 7) return fail(OSAM_EINVAL, "dirichlet[%d] > 7", f);
   const long long nn0 = d->nel[0] + 1LL, nn1 = d->nel[1] + 1LL, nn2 = d->nel[2] + 1LL;
   if (nn0 * nn1 * nn2 > (1LL << 30)) return fail(OSAM_EINVAL, "mesh too large (> 2^30 nodes)");
+  if (d->n_substeps < 0 || d->n_substeps > 4096) return fail(OSAM_EINVAL, "n_substeps must be in 0..4096");
+  if (d->integrator != OSAM_EXPLICIT && d->integrator != OSAM_IMPLICIT)
+    return fail(OSAM_EINVAL, "integrator must be OSAM_EXPLICIT or OSAM_IMPLICIT");
+  if (d->kind == OSAM_FOM && d->integrator != OSAM_EXPLICIT)
+    return fail(OSAM_EINVAL, "the FOM is explicit (implicit FOM solves are out of scope)");
+  if (d->integrator == OSAM_IMPLICIT && (d->Hbar || d->Cbar))
+    return fail(OSAM_EINVAL, "implicit stepping is implemented for linear OpInf ROMs only (no Hbar/Cbar)");
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return fail(OSAM_ECUDA, "cudaGetDevice: %s (no usable GPU)", cudaGetErrorString(e));
@@ -913,6 +1115,8 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
   s.mu = d->E / (2 * (1 + d->nu));
   std::memcpy(s.dirichlet, d->dirichlet, 6);
   s.stream = (cudaStream_t)cuda_stream;
+  s.n_sub = std::max(1, (int)d->n_substeps);
+  s.beta = d->integrator == OSAM_IMPLICIT ? 0.25 : 0.0;
   Geom& g = s.g;
   g.nn[0] = (int)nn0;
   g.nn[1] = (int)nn1;
@@ -996,7 +1200,8 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
       osam_destroy(h.release());
       return rc;
     }
-    for (int b = 0; b < 2; ++b)
+    const int nbuf = s.n_sub > 1 ? 3 : 2;  // substep chains need a third (q, w) buffer and z
+    for (int b = 0; b < nbuf; ++b)
       for (int q = 0; q < 2; ++q) {
         rc = dalloc(&s.st[b][q], (size_t)g.total);
         if (rc != OSAM_OK) {
@@ -1005,9 +1210,18 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
         }
         CK(cudaMemsetAsync(s.st[b][q], 0, sizeof(double) * g.total, s.stream));
       }
-    for (int b = 0; b < 2; ++b) {
+    if (s.n_sub > 1) {
+      rc = dalloc(&s.zbuf, (size_t)g.total);
+      if (rc != OSAM_OK) {
+        osam_destroy(h.release());
+        return rc;
+      }
+      CK(cudaMemsetAsync(s.zbuf, 0, sizeof(double) * g.total, s.stream));
+    }
+    for (int b = 0; b < nbuf; ++b) {
       int r = make_field_tmap(g, s.st[b][0], true, &s.tmap[b]);
       if (r == 0) r = make_field_tmap(g, s.st[b][1], false, &s.tmapw[b]);
+      if (r == 0 && b == 0 && s.zbuf) r = make_field_tmap(g, s.zbuf, false, &s.tmapz);
       if (r != 0) {
         osam_destroy(h.release());
         return fail(OSAM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", r);
@@ -1115,8 +1329,16 @@ int osam_step(osam_subdomain* const* sds, int32_t n_sd, const osam_schwarz_cfg* 
     }
   if (n_steps > 0) {
     int launches = 0;
-    for (int i = 0; i < n_sd; ++i)
-      if (sds[i]->s.kind == OSAM_FOM) TRY(fom_set_step(sds[i]->s, cfg->dt, &launches));
+    for (int i = 0; i < n_sd; ++i) {
+      Sub& d = sds[i]->s;
+      const double dti = cfg->dt / d.n_sub;
+      if (d.kind == OSAM_FOM) TRY(fom_set_step(d, dti, &launches));
+      if (d.kind == OSAM_ROM && d.beta > 0.0 && d.minv_dt != dti) {  // (I + beta dt_i^2 e_b Kbar)^-1
+        launch_rom_minv(d.r, d.batch, d.Kbar, d.e, d.beta * dti * dti, d.minv_work, d.Minv, d.stream);
+        ++launches;
+        d.minv_dt = dti;
+      }
+    }
     g_launches += launches;
   }
   int status = OSAM_OK;
@@ -1147,7 +1369,7 @@ int osam_step(osam_subdomain* const* sds, int32_t n_sd, const osam_schwarz_cfg* 
       int per_sweep = 0;
       TRY(step_graph(*G, *cfg, st, &exec, &per_sweep));
       CK(cudaGraphLaunch(exec, st));
-      for (int i = 0; i < n_sd; ++i) sds[i]->s.cur = 1 - sds[i]->s.cur;  // commit (pointer swap)
+      for (int i = 0; i < n_sd; ++i) commit_step(sds[i]->s);  // commit (buffer roles)
     }
   }
   std::vector<int32_t> its;
@@ -1164,7 +1386,7 @@ int osam_step(osam_subdomain* const* sds, int32_t n_sd, const osam_schwarz_cfg* 
       for (int k = 0; k < n_steps; ++k) {
         int nmax = 0;
         for (int b = 0; b < B; ++b) nmax = std::max(nmax, its[(size_t)k * B + b]);
-        g_launches += 1 + (long long)nmax * G->launches_per_sweep;
+        g_launches += G->launches_begin + (long long)nmax * G->launches_per_sweep;
       }
     }
     if (G->h_ctl[4 + 2 * B]) return fail(OSAM_EUNSTABLE, "non-finite Schwarz convergence norm");
@@ -1186,13 +1408,13 @@ static int get_field(const osam_subdomain* h, int which, double* out) {
   if (s.ic_pending) return fail(OSAM_EINVAL, "initial condition not processed yet: call osam_step first");
   cudaStream_t st = s.stream;
   if (s.kind == OSAM_FOM) {
-    const double* field = s.st[s.w_dt == 0.0 ? s.cur : 1 - s.cur][0];  // u (R30)
+    const double* field = s.st[s.w_dt == 0.0 ? s.cur : s.ux][0];  // u (R30)
     if (which != 0) {
       // a = -K u / m and v = w - w_dt/2 a by one force pass into the spare buffer (the committed
       // state is not modified).
       if (!s.bound) return fail(OSAM_EINVAL, "FOM state not bound: call osam_step first");
       int launches = 0;
-      const int xb = s.w_dt == 0.0 ? s.cur : 1 - s.cur;  // buffer holding u
+      const int xb = s.w_dt == 0.0 ? s.cur : s.ux;  // buffer holding u
       const FomLaunch L = fom_launch(s, s.st[xb][0], s.st[s.cur][1], nullptr, s.scratch_v, -0.5 * s.w_dt, 0.0, 0.0,
                                      0.0, 0, s.scratch_partial, s.scratch_a);
       launch_fom_advance(L, s.stencil, &s.tmap[xb], &s.tmapw[s.cur], &s.tmapw[s.cur], st, &launches);
@@ -1239,8 +1461,9 @@ void osam_destroy(osam_subdomain* h) {
   Sub& s = h->s;
   if (s.stream) cudaStreamSynchronize(s.stream);
   release_binding(s);
-  for (int b = 0; b < 2; ++b)
+  for (int b = 0; b < 3; ++b)
     for (int q = 0; q < 2; ++q) dfree(s.st[b][q]);
+  dfree(s.zbuf);
   dfree(s.scratch_a);
   dfree(s.scratch_v);
   dfree(s.coef);

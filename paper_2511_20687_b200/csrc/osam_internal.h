@@ -53,6 +53,10 @@ struct XferMap {
   double* xi = nullptr;  // [n][3] local coordinates in [0,1]
   int* out = nullptr;    // [n][3] destination index (FOM: c*npad + padded node id in q; ROM: Schwarz DOF
                          // id; -1 skip: Dirichlet component or a node owned by a lower Schwarz face)
+  // multi-substep groups (R31): the source's trace over the controller interval,
+  // [n_src_sub + 1 slots][B][3 n] (slot 0: the interval start), read through the interpolant Xi
+  double* trace = nullptr;
+  int n_src_sub = 1;
 };
 
 struct Sub {
@@ -64,6 +68,8 @@ struct Sub {
   unsigned char dirichlet[6];
   int batch = 1;
   int r = 0, r_b = 0;
+  int n_sub = 1;      // substeps per controller step: dt_i = dt / n_sub
+  double beta = 0.0;  // Newmark beta: 0 explicit, 1/4 implicit average acceleration (ROM only, R32)
   cudaStream_t stream = nullptr;
   Geom g;
   long long n_nodes = 0;
@@ -76,19 +82,23 @@ struct Sub {
   std::vector<int8_t> codes;  // host DOF codes (canonical DOF id 3p + c)
   std::vector<XferMap> maps;  // one per Schwarz face of this (destination) subdomain
 
-  // FOM device state: buffers [2] x {q, w}, each 3 * npad doubles (R30).
+  // FOM device state: buffers [3] x {q, w}, each 3 * npad doubles (R30).
   //   STEP state (w_dt > 0): st[cur] = (q, w) with q = u + w_dt w (boundary values in q) and
-  //   w = v + w_dt/2 a; st[1-cur][0] = u of the checkpoint (exactly).
+  //   w = v + w_dt/2 a; st[ux][0] = u of the checkpoint (exactly).
   //   RAW state (w_dt == 0, after osam_set_ic): st[cur] = (u, v).
-  int cur = 0;
-  double* st[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  //   st[fr]: third buffer of the substep chain (allocated iff n_sub > 1).  Single-substep
+  //   subdomains keep ux = 1 - cur.
+  int cur = 0, ux = 1, fr = 2;
+  double* st[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+  double* zbuf = nullptr;  // n_sub > 1: z = u + dt_i v of the last iterate's last substep (norm, R33)
+  CUtensorMap tmapz;
   double w_dt = 0.0;
   Faces faces;
   double* coef = nullptr;  // device [NCLASS][27][9]
   double* rowc = nullptr;  // device row-form coefficients [cy][cz][slice][c][d][oy][2] (kernels_fom.cu)
   InteriorStencil stencil;
-  CUtensorMap tmap[2];   // TMA descriptors of st[b][0] with the halo box (4D: x, y, z, component)
-  CUtensorMap tmapw[2];  // TMA descriptors of st[b][1] with the tile box
+  CUtensorMap tmap[3];   // TMA descriptors of st[b][0] with the halo box (4D: x, y, z, component)
+  CUtensorMap tmapw[3];  // TMA descriptors of st[b][1] with the tile box
   double mass_e = 0.0;  // rho * V_e / 8
   double inv_mass[8];   // 1 / (mass_e * prod_d (2 if interior on axis d else 1)), index cx + 2 cy + 4 cz
   double* scratch_v = nullptr;         // 3 * npad: v for osam_get_state
@@ -104,6 +114,10 @@ struct Sub {
   int* feat_idx = nullptr;             // device [nf][3] monomial indices (-1: unused third factor)
   double* F = nullptr;                 // device features [nf][B] (CUDA-core path)
   double* rst[2][4] = {{nullptr}};  // [buf] uh, vh, ah, s   (r x B, r x B, r x B, n_sdof x B)
+  double* rsub[2][4] = {{nullptr}};  // n_sub > 1: intermediate substep states (same layout as rst)
+  double* Minv = nullptr;            // implicit: [B][r][r] row-major (I + beta dt_i^2 e_b Kbar)^-1
+  double* minv_work = nullptr;       // implicit: [B][r][2r] Gauss-Jordan scratch
+  double minv_dt = 0.0;              // dt_i Minv was built for
   double* ustar = nullptr;          // r x B scratch
   double* gh = nullptr;             // r_b x B scratch
   int* free_ids = nullptr;          // n_free canonical DOF ids (device)
@@ -135,6 +149,8 @@ struct FomLaunch {
   const double* w0;  // per-node field W
   double* q_out;     // Q' = X + cq W' (may be null: not written)
   double* w_out;     // W' = W + cw a (also read first: previous iterate for the norm)
+  double* z_out;     // optional: z = X + dt (W + cv a) out, and (with_norm) the norm from z - z_prev
+                     // with z_prev staged from the same array (multi-substep intervals, R33)
   double* a_out;     // optional acceleration output (diagnostics), may be null
   double cw, cq;
   double cv;  // v = W + cv a (norm denominator)
@@ -153,6 +169,16 @@ int make_field_tmap(const Geom& g, double* array, bool halo, CUtensorMap* out);
 
 void launch_transfer(const XferMap& m, const double* src, long long src_cstride, long long src_bstride,
                      double* dst, long long dst_bstride, int batch, const int* active, cudaStream_t s);
+// multi-substep groups: Pi of the source field into trace slot `slot` of map m (compact [B][3n]),
+// and the destination's Schwarz values at one of its substeps from the trace through Xi:
+// (1 - alpha) trace[lo] + alpha trace[lo + 1]   (alpha == 0: trace[lo] as is)
+void launch_transfer_trace(const XferMap& m, const double* src, long long src_cstride, long long src_bstride,
+                           int slot, int batch, const int* active, cudaStream_t s);
+void launch_trace_interp(const XferMap& m, int lo, double alpha, double* dst, long long dst_bstride, int batch,
+                         const int* active, cudaStream_t s);
+// implicit ROM: Minv[b] = (I + c e_b Kbar)^-1 by Gauss-Jordan with partial pivoting, one block per sample
+void launch_rom_minv(int r, int B, const double* Kbar, const double* e, double c, double* work, double* Minv,
+                     cudaStream_t s);
 void launch_fom_pack(const Geom& g, const double* src_unpadded, double* dst_padded, long long n_nodes,
                      cudaStream_t s);
 void launch_fom_unpack(const Geom& g, const double* src_padded, double* dst_unpadded, long long n_nodes,
@@ -174,6 +200,9 @@ struct RomLaunch {
   int gchunks;
   const int* active;
   double dt;
+  double c2;           // predictor u~ = u^ + dt v^ + c2 a^: dt^2/2 explicit, dt^2 (1/2 - beta) implicit
+  double beta;         // 0: explicit; > 0: implicit average acceleration through Minv (R32)
+  const double* Minv;  // [B][r][r] row-major
   int with_norm;
   double2* partial;
 };
@@ -187,6 +216,8 @@ cudaError_t launch_rom_project(long long n_rows, int r, int B, const double* Phi
 void launch_gather_dofs(long long n, int B, const int* ids, const double* field, long long field_bstride,
                         long long n_nodes, double* out, cudaStream_t s);
 void launch_rom_accel(const RomLaunch& L, const double* uh, double* ah, cudaStream_t s, int* launches);
+// implicit ROM finish (R32): a^' = Minv f (f in L.ah1), u^', v^', norm partials; u~ at ut (stride uts)
+void launch_rom_implicit(const RomLaunch& L, const double* ut, long long uts, int n_slots, cudaStream_t s);
 long long tc_part_size(int r, int r_b, int nf, int B, long long n_s, long long n_lift3);
 // F[q, b] = prod of u[idx[q][.], b]  (compressed Khatri-Rao monomials of the reduced state)
 void launch_rom_features(int nf, int B, const int* idx, const double* u, long long ustride, double* F, long long fstride,

@@ -16,6 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("OSAM_LIB") or os.path.join(_HERE, "libosam.so")
 
 OSAM_FOM, OSAM_ROM = 0, 1
+OSAM_EXPLICIT, OSAM_IMPLICIT = 0, 1
 OSAM_OK, OSAM_WNOTCONVERGED = 0, 1
 ERRORS = {-1: "OSAM_EINVAL", -2: "OSAM_ENOMEM", -3: "OSAM_ECUDA", -4: "OSAM_EOVERLAP", -5: "OSAM_EUNSTABLE"}
 
@@ -33,7 +34,8 @@ class osam_subdomain_desc(C.Structure):
                 ("Phi", C.POINTER(C.c_double)), ("Phi_s", C.POINTER(C.c_double)),
                 ("Kbar", C.POINTER(C.c_double)), ("Bbar", C.POINTER(C.c_double)),
                 ("e_scale", C.POINTER(C.c_double)),
-                ("Hbar", C.POINTER(C.c_double)), ("Cbar", C.POINTER(C.c_double))]
+                ("Hbar", C.POINTER(C.c_double)), ("Cbar", C.POINTER(C.c_double)),
+                ("n_substeps", C.c_int32), ("integrator", C.c_int32)]
 
 
 class osam_schwarz_cfg(C.Structure):
@@ -108,8 +110,11 @@ def _dptr(a):
 class Subdomain:
     """Owning wrapper of an osam_subdomain handle (osam_create_subdomain / osam_destroy)."""
 
-    def __init__(self, kind, lo, hi, nel, E, nu, rho, dirichlet=(0,) * 6, stream=None, rom=None, e_scale=None):
+    def __init__(self, kind, lo, hi, nel, E, nu, rho, dirichlet=(0,) * 6, stream=None, rom=None, e_scale=None,
+                 n_substeps=1, integrator=OSAM_EXPLICIT):
         d = osam_subdomain_desc()
+        d.n_substeps = int(n_substeps)
+        d.integrator = int(integrator)
         d.kind = kind
         d.lo[:] = [float(x) for x in lo]
         d.hi[:] = [float(x) for x in hi]

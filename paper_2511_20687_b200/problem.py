@@ -10,7 +10,7 @@ import numpy as np
 
 import osam_inputs
 
-from .osam import OSAM_FOM, OSAM_ROM, Subdomain, osam_step
+from .osam import OSAM_EXPLICIT, OSAM_FOM, OSAM_IMPLICIT, OSAM_ROM, Subdomain, osam_step
 
 
 def e_scale(cfg):
@@ -28,8 +28,10 @@ def build(cfg, rom_ops=None, stream=None):
             o = rom_ops[i]
             rom = dict(Phi=o["Phi"], Phi_s=o["Phi_s"], Kbar=o["Kbar"], Bbar=o["Bbar"], Hbar=o.get("Hbar"),
                        Cbar=o.get("Cbar"))
+        integ = OSAM_IMPLICIT if s.get("integrator", "explicit") == "implicit" else OSAM_EXPLICIT
         subs.append(Subdomain(kind, s["lo"], s["hi"], s["nel"], cfg["E"], cfg["nu"], cfg["rho"], s["dirichlet"],
-                              stream=stream, rom=rom, e_scale=e_scale(cfg) if kind == OSAM_ROM else None))
+                              stream=stream, rom=rom, e_scale=e_scale(cfg) if kind == OSAM_ROM else None,
+                              n_substeps=s.get("n_sub", 1), integrator=integ))
     return subs
 
 

@@ -250,3 +250,105 @@ def test_c5_shaped_batched_cubic_opinf_tensor_cores(gpu):
         ops[i] = o
     _, iters, worst = run_both(gpu, cfg, 100, rom_ops=ops, checkpoints=(1,))
     print("c5-shaped cubic worst rel L2", worst)
+
+
+# ---- NEXT-1: multi-substep controller intervals (Xi) and the implicit ROM ------------------------
+
+def _substeps(cfg, n_sub, integrators=None, dt_factor=1.0):
+    import copy
+    c = copy.deepcopy(cfg)
+    for k, s in enumerate(c["subdomains"]):
+        s["n_sub"] = n_sub[k]
+        if integrators:
+            s["integrator"] = integrators[k]
+    c["dt"] = cfg["dt"] * dt_factor
+    return c
+
+
+@pytest.mark.parametrize("n_sub,dt_factor", [((2, 2), 2.0), ((1, 3), 1.5), ((3, 2), 2.0), ((4, 1), 1.0)])
+def test_c1_substeps_xi(gpu, n_sub, dt_factor):
+    """FOM-FOM with n_i substeps per controller step (three-buffer chain, z-form norm, traces + Xi)."""
+    cfg = _substeps(I.config("c1"), n_sub, dt_factor=dt_factor)
+    _, iters, worst = run_both(gpu, cfg, 60, checkpoints=(1, 7))
+    print("c1", n_sub, "worst rel L2", worst, "iters", np.unique(iters))
+
+
+def test_rigid_translation_mixed_substeps_gpu(gpu):
+    """The oracle pin's free-floating bar (uniform translation, v0 through osam_set_ic) on the GPU:
+    parity with the oracle and rigid to rounding."""
+    from paper_2511_20687_b200 import osam
+    subs_cfg = [I._sub("a", "fom", (0, 0, 0), (0.6, 0.1, 0.1), (30, 5, 5)),
+                I._sub("b", "fom", (0.4, 0, 0), (1.0, 0.1, 0.1), (24, 4, 4))]
+    subs_cfg[0]["n_sub"], subs_cfg[1]["n_sub"] = 1, 3
+    cfg = dict(subdomains=subs_cfg, E=I.E0, nu=I.NU, rho=I.RHO, dt=I._dt(subs_cfg), tol=1e-12, max_iters=50,
+               min_iters=2)
+    models = schwarz.build_models(cfg)
+    c = np.array([1e-3, -2e-3, 5e-4])
+    vel = np.array([0.7, -0.3, 1.1])
+    u0s = [np.broadcast_to(c, (1, m.box.n_nodes, 3)).copy() for m in models]
+    v0s = [np.broadcast_to(vel, (1, m.box.n_nodes, 3)).copy() for m in models]
+    states, it_ref = schwarz.run(models, u0s, cfg["dt"], 25, cfg["tol"], 50, 2, v0s=v0s)
+    subs = gpu.build(cfg)
+    for sub, u0, v0 in zip(subs, u0s, v0s):
+        sub.set_ic(gpu.soa(u0), gpu.soa(v0))
+    _, it = gpu.run(cfg, subs, n_steps=25)
+    assert np.array_equal(it.reshape(-1), it_ref.reshape(-1))
+    T = 25 * cfg["dt"]
+    for sub, m, st in zip(subs, models, states):
+        u, v, a = gpu.fom_state(sub, accel=True)
+        assert rel(u, st["u"][0]) <= TOL and rel(v, st["v"][0]) <= TOL
+        # a is rounding noise of K (c + v t) on both sides: bound it by the stiffness scale instead
+        scale = I.E0 / (I.RHO * m.box.h.min() ** 2) * np.abs(u).max()
+        assert np.abs(a).max() <= 1e-12 * scale and np.abs(st["a"]).max() <= 1e-12 * scale
+        free = m.codes == fem.FREE
+        assert np.abs(np.where(free, u - (c + vel * T), 0)).max() <= 1e-12 * np.abs(vel * T).max()
+
+
+@pytest.fixture(scope="module")
+def c2_linear_ops():
+    return opinf.train(I.config("c2"), I)
+
+
+@pytest.mark.parametrize("n_sub,integ,dt_factor", [
+    ((2, 1), ("explicit", "implicit"), 2.0),     # torsion-like pairing: explicit FOM, implicit ROM (P:L1581)
+    ((1, 1), ("explicit", "implicit"), 1.0),
+    ((2, 3), ("explicit", "explicit"), 2.0),
+])
+def test_c2_implicit_rom_and_substeps(gpu, c2_linear_ops, n_sub, integ, dt_factor):
+    cfg = _substeps(I.config("c2"), n_sub, integ, dt_factor)
+    _, iters, worst = run_both(gpu, cfg, 150, rom_ops=c2_linear_ops, checkpoints=(1,))
+    print("c2", n_sub, integ, "worst rel L2", worst, "iters", np.unique(iters))
+
+
+@pytest.mark.parametrize("tc", ["1", "0"])
+def test_c5_shaped_batched_implicit_and_substeps(gpu, monkeypatch, tc):
+    """Batched ROM-ROM (B = 64): implicit ROM (per-sample (I + beta dt^2 e_b Kbar)^-1) coupled to an explicit
+    ROM taking 2 substeps; tensor-core and CUDA-core paths; per-sample freezing with traces."""
+    monkeypatch.setenv("OSAM_ROM_TC", tc)
+    cfg = _substeps(I.config("c5"), (1, 2), ("implicit", "explicit"), 2.0)
+    from paper_2511_20687_b200 import problem
+    ops = {}
+    for i in (0, 1):
+        n_free, n_s = problem.dof_split(cfg, i)
+        ops[i] = I.synthetic_rom_operators(n_free, n_s, 12, 6, I.config("c5")["dt"], seed=60 + i)
+    _, iters, worst = run_both(gpu, cfg, 60, rom_ops=ops, checkpoints=(1,))
+    print("c5-shaped implicit/substeps tc", tc, "worst rel L2", worst, "iters", np.unique(iters))
+
+
+def test_graph_equals_host_controller_with_substeps(gpu):
+    """Graph-mode and host-driven controller steps agree bitwise with traces and substeps."""
+    from paper_2511_20687_b200 import osam
+    cfg = _substeps(I.config("c1"), (3, 2), dt_factor=2.0)
+    out = []
+    for prof in (False, True):
+        osam.set_profiling(prof)
+        try:
+            subs = gpu.build(cfg)
+            gpu.set_ics(cfg, subs)
+            _, it = gpu.run(cfg, subs, n_steps=20)
+            out.append((it, [gpu.fom_state(s) for s in subs]))
+        finally:
+            osam.set_profiling(False)
+    assert np.array_equal(out[0][0], out[1][0])
+    for a, b in zip(out[0][1], out[1][1]):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
