@@ -15,6 +15,11 @@ are inputs shared by both online paths (the CUDA library reads them through the 
     with U^ = Phi^T U, G^ = Phi_dS^T S and D_t^2 the central second difference on interior
     columns (reading R18), one lambda in SI units (R20), solved as augmented least squares.
   * Training recipes per reading R25.
+  * Regularisation selection (grid P:L808; reading R34): for every lambda of the
+    grid 1e-4 * 10^(4 (j-1)/(n-1)), j = 1..n (n = 40), fit the operators, replay the ROM alone
+    with explicit Newmark and the Schwarz boundary data of the training run (g^_k = G^[:, k]),
+    and score ||U^bar - U^hat||_F / ||U^bar||_F in reduced coordinates; lambda* = first argmin
+    (non-finite errors never win).
 """
 from __future__ import annotations
 
@@ -137,9 +142,9 @@ def _online_models_codes(cfg):
     return boxes, faces
 
 
-def train_single_domain(cfg, inputs):
-    """c2: single-domain FOM on the training box, snapshots at steps 0..n-1 restricted to the
-    ROM sub-block (nodes with x >= lo of the ROM box; conformal)."""
+def training_snapshots_single_domain(cfg, inputs):
+    """c2: single-domain FOM on the training box, snapshots at steps 0..n-1 restricted to each ROM
+    sub-block (nodes with x >= lo of the ROM box; conformal).  Returns {i: (X_free, X_schwarz)}."""
     tr = cfg["rom"]["training"]
     dom = tr["domain"]
     train_cfg = dict(cfg, subdomains=[dom])
@@ -151,7 +156,7 @@ def train_single_domain(cfg, inputs):
         state = m.advance(state, np.zeros((1, 0)))
         snaps.append(state["u"][0].copy())
     boxes, faces = _online_models_codes(cfg)
-    ops = {}
+    out = {}
     for i, s in enumerate(cfg["subdomains"]):
         if s["kind"] != "rom":
             continue
@@ -165,9 +170,15 @@ def train_single_domain(cfg, inputs):
         free = np.nonzero(codes == fem.FREE)[0]
         sd = np.nonzero(codes == fem.SCHWARZ)[0]
         X = np.stack([u[tnodes].reshape(-1) for u in snaps], axis=1)      # (3 n_rom, K)
-        ops[i] = build_rom_operators(X[free], X[sd], cfg["dt"], cfg["rom"]["r"], cfg["rom"]["lam"],
-                                     cfg["rom"]["energy"], order=cfg["rom"].get("order", 1))
-    return ops
+        out[i] = (X[free], X[sd])
+    return out
+
+
+def train_single_domain(cfg, inputs):
+    """c2: operators from the single-domain training snapshots."""
+    return {i: build_rom_operators(Xf, Xs, cfg["dt"], cfg["rom"]["r"], cfg["rom"]["lam"], cfg["rom"]["energy"],
+                                   order=cfg["rom"].get("order", 1))
+            for i, (Xf, Xs) in training_snapshots_single_domain(cfg, inputs).items()}
 
 
 def train_coupled(cfg, inputs):
@@ -204,3 +215,73 @@ def train(cfg, inputs):
     if kind == "single_domain":
         return train_single_domain(cfg, inputs)
     return train_coupled(cfg, inputs)
+
+
+# ---------------------------------------------------------------------------------------
+# regularisation selection by subdomain-local replay (reading R34)
+# ---------------------------------------------------------------------------------------
+
+def lambda_grid(n=40):
+    """lambda_j = 1e-4 * 10^(4 (j-1)/(n-1)), j = 1..n  (P:L808)."""
+    return 1e-4 * 10.0 ** (4.0 / (n - 1) * np.arange(n))
+
+
+def replay_accel(O, order, r, r_b, u, g):
+    """a^ = O [u; g; u^*2; u^*3] with O = [-Kbar, Bbar, -Hbar, -Cbar] (r x (r + r_b + nf))."""
+    z = [u, g]
+    if order >= 2:
+        z.append(khatri_rao_pow(u[:, None], 2)[:, 0])
+    if order >= 3:
+        z.append(khatri_rao_pow(u[:, None], 3)[:, 0])
+    return O @ np.concatenate(z)
+
+
+def rom_replay(O, Ubar, Ghat, dt, order=1, vh0=None):
+    """Subdomain-local replay: the OpInf ROM alone, explicit Newmark (c.1 step 10 form),
+    from u^_0 = Ubar[:, 0], v^_0 = vh0 (0: the training runs start at rest), with the Schwarz boundary
+    data of the training run, g^_k = Ghat[:, k].  Returns U^hat (r x K)."""
+    r, K = Ubar.shape
+    r_b = Ghat.shape[0]
+    u = Ubar[:, 0].copy()
+    v = np.zeros(r) if vh0 is None else np.asarray(vh0, dtype=np.float64).copy()
+    a = replay_accel(O, order, r, r_b, u, Ghat[:, 0])
+    out = np.empty((r, K))
+    out[:, 0] = u
+    with np.errstate(all="ignore"):
+        for k in range(1, K):
+            u = u + dt * v + 0.5 * dt * dt * a
+            an = replay_accel(O, order, r, r_b, u, Ghat[:, k])
+            v = v + 0.5 * dt * (a + an)
+            a = an
+            out[:, k] = u
+    return out
+
+
+def trajectory_error(Ubar, Uhat):
+    """||Ubar - Uhat||_F / ||Ubar||_F (reduced coordinates; reading R34)."""
+    with np.errstate(all="ignore"):
+        return float(np.sqrt(np.sum((Ubar - Uhat) ** 2)) / np.sqrt(np.sum(Ubar ** 2)))
+
+
+def operator_matrix(ops, order=1):
+    """O = [-Kbar, Bbar, -Hbar, -Cbar] of a fit."""
+    Kbar, Bbar = ops[0], ops[1]
+    blocks = [-Kbar, Bbar]
+    if order >= 2:
+        blocks.append(-ops[2])
+    if order >= 3:
+        blocks.append(-ops[3])
+    return np.concatenate(blocks, axis=1)
+
+
+def select_lambda(Ubar, Ghat, dt, grid=None, order=1):
+    """lambda* of the grid by subdomain-local replay.  Returns (index, errors (n,), operator matrices)."""
+    grid = lambda_grid() if grid is None else np.asarray(grid)
+    errs, Os = [], []
+    for lam in grid:
+        O = operator_matrix(opinf_fit(Ubar, Ghat, dt, lam, order), order)
+        Os.append(O)
+        errs.append(trajectory_error(Ubar, rom_replay(O, Ubar, Ghat, dt, order)))
+    errs = np.array(errs)
+    score = np.where(np.isfinite(errs), errs, np.inf)
+    return int(np.argmin(score)), errs, Os
