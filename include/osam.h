@@ -132,6 +132,30 @@ void osam_destroy(osam_subdomain* s);
 
 const char* osam_last_error(void);
 
+/* ---- regularisation selection (offline stage, grid P:L808) --------------------
+ * Batched subdomain-local replay: n_models candidate OpInf ROMs of one subdomain (typically one per
+ * lambda of the grid 1e-4 * 10^(4(j-1)/(n-1))), each with its own operator
+ *     O_b = [-Kbar | Bbar | -Hbar | -Cbar]     (r x (r + r_b + nf), column-major, nf as in the descriptor
+ *                                               for order 1 / 2 / 3),
+ * are advanced alone with explicit Newmark over the n_steps of the training run, from u^_0 = Ubar[:, 0]
+ * and v^_0 = vh0 (NULL: 0), with the Schwarz boundary data of the training run g^_k = Ghat[:, k]
+ * (the OpInf part of eq:schwarz_opinf_discrete with the boundary "taken from training data"), and
+ * scored by err_b = ||Ubar - U^hat_b||_F / ||Ubar||_F in reduced coordinates (reading R34).
+ * best = first argmin over the finite errors (-1 if none).  All models run in one launch (one CTA
+ * per model).  Inputs may be host or device pointers; outputs too (traj_out: n_models x n_steps x r,
+ * may be NULL; best_out may be NULL).  Synchronises `cuda_stream` before returning.               */
+typedef struct {
+  int32_t r, r_b, order, n_models, n_steps;
+  double dt;
+  const double *O;     /* n_models blocks of r x (r + r_b + nf), column-major                       */
+  const double *Ubar;  /* r x n_steps   reduced training trajectory (column k = step k)            */
+  const double *Ghat;  /* r_b x n_steps reduced Schwarz data of the training run                   */
+  const double *vh0;   /* r             initial reduced velocity, NULL = 0                          */
+} osam_replay_desc;
+
+int osam_opinf_replay(const osam_replay_desc* d, double* err_out, int32_t* best_out, double* traj_out,
+                      void* cuda_stream);
+
 /* ---- measurement helpers (not part of the method) --------------------------------------
  * When profiling is on, osam_step records a CUDA event pair around every FOM-advance
  * launch (kernel K1) on the subdomain's stream and accumulates their durations; the

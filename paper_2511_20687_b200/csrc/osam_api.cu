@@ -69,6 +69,25 @@ void dfree(T*& p) {
   p = nullptr;
 }
 
+// stream-ordered scratch (per-call buffers of offline routines: no device-wide synchronisation)
+template <class T>
+int dalloc_async(T** p, size_t n, cudaStream_t s) {
+  *p = nullptr;
+  const cudaError_t e = cudaMallocAsync((void**)p, std::max<size_t>(n, 1) * sizeof(T), s);
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    return fail(e == cudaErrorMemoryAllocation ? OSAM_ENOMEM : OSAM_ECUDA, "cudaMallocAsync(%zu bytes): %s",
+                n * sizeof(T), cudaGetErrorString(e));
+  }
+  return OSAM_OK;
+}
+
+template <class T>
+void dfree_async(T*& p, cudaStream_t s) {
+  if (p) cudaFreeAsync(p, s);
+  p = nullptr;
+}
+
 }  // namespace
 
 void debug_check(const char* kernel, cudaStream_t s) {
@@ -1471,6 +1490,100 @@ void osam_destroy(osam_subdomain* h) {
   dfree(s.ic_u);
   dfree(s.ic_v);
   delete h;
+}
+
+int osam_opinf_replay(const osam_replay_desc* d, double* err_out, int32_t* best_out, double* traj_out,
+                      void* cuda_stream) {
+  if (!d || !err_out) return fail(OSAM_EINVAL, "NULL descriptor or err_out");
+  if (d->r < 1 || d->r_b < 0 || d->n_models < 1 || d->n_steps < 1 || d->order < 1 || d->order > 3 || !(d->dt > 0))
+    return fail(OSAM_EINVAL, "replay needs r >= 1, r_b >= 0, n_models >= 1, n_steps >= 1, order 1..3, dt > 0");
+  if (!d->O || !d->Ubar || (d->r_b > 0 && !d->Ghat)) return fail(OSAM_EINVAL, "replay input pointer is NULL");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const long long r = d->r, rb = d->r_b, K = d->n_steps, B = d->n_models;
+  const long long n2 = d->order >= 2 ? r * (r + 1) / 2 : 0, n3 = d->order >= 3 ? r * (r + 1) * (r + 2) / 6 : 0;
+  const long long nf = n2 + n3, rz = r + rb + nf;
+  std::vector<int> idx;
+  for (int i = 0; i < r && d->order >= 2; ++i)
+    for (int j = i; j < r; ++j) idx.insert(idx.end(), {i, j, -1});
+  for (int i = 0; i < r && d->order >= 3; ++i)
+    for (int j = i; j < r; ++j)
+      for (int l = j; l < r; ++l) idx.insert(idx.end(), {i, j, l});
+  // device copies (per call: an offline routine)
+  double *O_cm = nullptr, *O = nullptr, *Ub = nullptr, *Gh = nullptr, *v0 = nullptr, *z = nullptr, *err = nullptr,
+         *traj = nullptr;
+  int *fi = nullptr, *best = nullptr;
+  int rc = OSAM_OK;
+  auto in = [&](double** dst, const double* src, long long n) -> int {
+    TRY(dalloc_async(dst, (size_t)std::max(1LL, n), st));
+    if (n > 0)
+      CK(cudaMemcpyAsync(*dst, src, sizeof(double) * n,
+                         is_device_ptr(src) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    return OSAM_OK;
+  };
+  do {
+    if ((rc = in(&O_cm, d->O, B * r * rz)) != OSAM_OK) break;
+    if ((rc = dalloc_async(&O, (size_t)(B * r * rz), st)) != OSAM_OK) break;
+    if ((rc = in(&Ub, d->Ubar, r * K)) != OSAM_OK) break;
+    if ((rc = in(&Gh, d->Ghat, rb * K)) != OSAM_OK) break;
+    if (d->vh0 && (rc = in(&v0, d->vh0, r)) != OSAM_OK) break;
+    if ((rc = dalloc_async(&z, (size_t)(B * rz), st)) != OSAM_OK) break;
+    if ((rc = dalloc_async(&err, (size_t)B, st)) != OSAM_OK) break;
+    if ((rc = dalloc_async(&best, 1, st)) != OSAM_OK) break;
+    if (traj_out && (rc = dalloc_async(&traj, (size_t)(B * K * r), st)) != OSAM_OK) break;
+    if (!idx.empty()) {
+      if ((rc = dalloc_async(&fi, idx.size(), st)) != OSAM_OK) break;
+      const cudaError_t e = cudaMemcpyAsync(fi, idx.data(), sizeof(int) * idx.size(), cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) {
+        rc = fail(OSAM_ECUDA, "replay: %s", cudaGetErrorString(e));
+        break;
+      }
+    }
+    launch_transpose_ops((int)r, (int)rz, (int)B, O_cm, O, st);
+    ReplayArgs A{};
+    A.r = (int)r;
+    A.r_b = (int)rb;
+    A.nf = (int)nf;
+    A.B = (int)B;
+    A.K = (int)K;
+    A.dt = d->dt;
+    A.O = O;
+    A.feat_idx = fi;
+    A.Ubar = Ub;
+    A.Ghat = Gh;
+    A.vh0 = v0;
+    A.z = z;
+    A.traj = traj;
+    A.err = err;
+    A.best = best;
+    cudaError_t e = launch_replay(A, st);
+    if (e != cudaSuccess) {
+      rc = fail(OSAM_ECUDA, "replay launch: %s", cudaGetErrorString(e));
+      break;
+    }
+    g_launches += 3;
+    if ((rc = copy_out(err, err_out, (size_t)B, st)) != OSAM_OK) break;
+    if (traj_out && (rc = copy_out(traj, traj_out, (size_t)(B * K * r), st)) != OSAM_OK) break;
+    int hb = -1;
+    e = cudaMemcpyAsync(&hb, best, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      rc = fail(OSAM_ECUDA, "replay: %s", cudaGetErrorString(e));
+      break;
+    }
+    if (best_out) *best_out = hb;
+  } while (false);
+  dfree_async(O_cm, st);
+  dfree_async(O, st);
+  dfree_async(Ub, st);
+  dfree_async(Gh, st);
+  dfree_async(v0, st);
+  dfree_async(z, st);
+  dfree_async(err, st);
+  dfree_async(best, st);
+  dfree_async(traj, st);
+  dfree_async(fi, st);
+  cudaStreamSynchronize(st);  // the idx host vector and the caller's outputs must outlive the copies
+  return rc;
 }
 
 void osam_set_profiling(int32_t on) { g_prof = on != 0; }

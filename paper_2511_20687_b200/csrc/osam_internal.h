@@ -229,6 +229,24 @@ void launch_rom_accel_tc(const RomLaunch& L, const double* uh, double* ah, const
 void launch_rom_lift_tc(int r, int B, long long nl, const double* Phi_lift, const int* code, const double* uh,
                         const double* sv, long long ns, double* out, double* part, cudaStream_t st, int* launches);
 
+// Batched subdomain-local OpInf replay (kernels_replay.cu, NEXT-4, reading R34).
+struct ReplayArgs {
+  int r, r_b, nf, B, K;
+  double dt;
+  const double* O;      // [B][r][r + r_b + nf] row-major
+  const int* feat_idx;  // [nf][3]
+  const double* Ubar;   // r x K column-major
+  const double* Ghat;   // r_b x K column-major
+  const double* vh0;    // r or null
+  double* z;            // [B][r + r_b + nf] scratch
+  double* traj;         // [B][K][r] or null
+  double* err;          // [B]
+  int* best;            // [1]
+  int z_in_smem, o_in_smem;  // set by launch_replay
+};
+void launch_transpose_ops(int r, int rz, int B, const double* in_colmajor, double* out_rowmajor, cudaStream_t s);
+cudaError_t launch_replay(ReplayArgs A, cudaStream_t s);
+
 // OSAM_DEBUG_SYNC=1: synchronise after every launch and report the first failing kernel on
 // stderr (development aid only; off by default).
 void debug_check(const char* kernel, cudaStream_t s);

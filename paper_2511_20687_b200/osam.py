@@ -23,7 +23,7 @@ ERRORS = {-1: "OSAM_EINVAL", -2: "OSAM_ENOMEM", -3: "OSAM_ECUDA", -4: "OSAM_EOVE
 # C entry points declared in include/osam.h
 EXPORTS = ("osam_create_subdomain", "osam_set_ic", "osam_step", "osam_get_state", "osam_get_accel",
            "osam_get_sizes", "osam_destroy", "osam_last_error", "osam_set_profiling", "osam_reset_profile",
-           "osam_get_profile")
+           "osam_get_profile", "osam_opinf_replay")
 
 
 class osam_subdomain_desc(C.Structure):
@@ -36,6 +36,12 @@ class osam_subdomain_desc(C.Structure):
                 ("e_scale", C.POINTER(C.c_double)),
                 ("Hbar", C.POINTER(C.c_double)), ("Cbar", C.POINTER(C.c_double)),
                 ("n_substeps", C.c_int32), ("integrator", C.c_int32)]
+
+
+class osam_replay_desc(C.Structure):
+    _fields_ = [("r", C.c_int32), ("r_b", C.c_int32), ("order", C.c_int32), ("n_models", C.c_int32),
+                ("n_steps", C.c_int32), ("dt", C.c_double), ("O", C.c_void_p), ("Ubar", C.c_void_p),
+                ("Ghat", C.c_void_p), ("vh0", C.c_void_p)]
 
 
 class osam_schwarz_cfg(C.Structure):
@@ -77,8 +83,9 @@ def lib():
         L.osam_get_profile.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_int64), C.POINTER(C.c_double),
                                        C.POINTER(C.c_int64)]
         L.osam_get_profile.restype = None
+        L.osam_opinf_replay.argtypes = [C.POINTER(osam_replay_desc), vp, C.POINTER(C.c_int32), vp, vp]
         for name in ("osam_create_subdomain", "osam_set_ic", "osam_step", "osam_get_state", "osam_get_accel",
-                     "osam_get_sizes"):
+                     "osam_get_sizes", "osam_opinf_replay"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -203,3 +210,23 @@ def get_profile():
     ms, n, b, k = C.c_double(), C.c_int64(), C.c_double(), C.c_int64()
     lib().osam_get_profile(C.byref(ms), C.byref(n), C.byref(b), C.byref(k))
     return dict(k1_ms=ms.value, k1_launches=n.value, k1_bytes=b.value, kernel_launches=k.value)
+
+
+def opinf_replay(O, Ubar, Ghat, dt, order=1, vh0=None, trajectories=False, stream=None):
+    """osam_opinf_replay: O (n_models, r, r + r_b + nf) candidate operators [-Kbar|Bbar|-Hbar|-Cbar],
+    Ubar (r, K) and Ghat (r_b, K) training data.  Returns (errors (n_models,), best index[, U^hat
+    (n_models, K, r)])."""
+    O = np.asarray(O, dtype=np.float64)
+    B, r, _ = O.shape
+    Ocm = np.ascontiguousarray(O.transpose(0, 2, 1))               # column-major blocks
+    Ub = np.asfortranarray(Ubar, dtype=np.float64)
+    Gh = np.asfortranarray(Ghat, dtype=np.float64)
+    K = Ub.shape[1]
+    v0 = None if vh0 is None else np.ascontiguousarray(vh0, dtype=np.float64)
+    d = osam_replay_desc(r, Gh.shape[0], int(order), B, K, float(dt), Ocm.ctypes.data, Ub.ctypes.data,
+                         Gh.ctypes.data if Gh.size else None, None if v0 is None else v0.ctypes.data)
+    err = np.empty(B)
+    best = C.c_int32(-2)
+    traj = np.empty((B, K, r)) if trajectories else None
+    _check(lib().osam_opinf_replay(C.byref(d), _ptr(err), C.byref(best), _ptr(traj), C.c_void_p(stream or 0)))
+    return (err, best.value, traj) if trajectories else (err, best.value)
