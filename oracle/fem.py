@@ -9,6 +9,11 @@ definitions read, with no stencil precomputation:
   * force     f = sum_e scatter(K_e u_e)   -- an element loop                  (P:L133-137 eq:matrix_vector_form)
   * mass      row-sum lumping of the consistent mass rho int N_a N_b          (P:L178 footnote, L783)
   * Dirichlet split into free / constrained DOFs
+  * nonlinear materials (readings R35, R36): internal force of the weak form
+        f_a = sum_e sum_q w_q detJ P(F_q) dN_a/dX(q),  F = I + grad u  (same element loop, 2x2x2 Gauss)
+    with P = F S and  Saint Venant-Kirchhoff  S = lambda tr(E) I + 2 mu E, E = 1/2 (F^T F - I)  (A.2)
+                      Neohookean  S = kappa/2 (det C - 1) C^-1 + mu (det C)^(-1/3) (I - tr(C)/3 C^-1),
+                                  C = F^T F, kappa = lambda + 2 mu/3                              (A.3)
   * explicit Newmark beta=0, gamma=1/2 in predictor form (reading R1):
         u* = u + dt v + dt^2/2 a ; a' = -f(u*)/m ; v' = v + dt/2 (a + a')
 
@@ -213,3 +218,64 @@ def explicit_newmark_step(u, v, a, s_values, codes, schwarz_dofs, force, m, dt):
     a_new = np.where(free, -f / m[:, None], 0.0)
     v_new = np.where(free, v + 0.5 * dt * (a + a_new), 0.0)
     return ustar, v_new, a_new
+
+
+# ---------------------------------------------------------------------------------------
+# nonlinear materials (App. A.2/A.3; readings R35, R36)
+# ---------------------------------------------------------------------------------------
+
+def pk1_svk(F, lam, mu):
+    """Saint Venant-Kirchhoff: E = 1/2 (F^T F - I) (reading R35: the printed "1/2 F^T F - I" at P:L1961 is a
+    typo, its own expansion at P:L1975 is 1/2 (F^T F - I)), S = lambda tr(E) I + 2 mu E (eq:svk_S),
+    P = F S (eq:svk_P).  F: (..., 3, 3)."""
+    I = np.eye(3)
+    E = 0.5 * (np.swapaxes(F, -1, -2) @ F - I)
+    trE = np.trace(E, axis1=-2, axis2=-1)
+    S = lam * trE[..., None, None] * I + 2.0 * mu * E
+    return F @ S
+
+
+def pk1_neohookean(F, kappa, mu):
+    """Neohookean (A.3): C = F^T F, S_vol = kappa/2 (det C - 1) C^-1,
+    S_dev = mu (det C)^(-1/3) (I - tr(C)/3 C^-1) (reading R36: S = 2 dA/dC of A_dev = mu/2 ((det C)^(-1/3)
+    tr C - 3), eq:Adev P:L2005; the printed 1/2 in front of C^-1 tr C at P:L2017 is inconsistent with it),
+    P = F S."""
+    I = np.eye(3)
+    C = np.swapaxes(F, -1, -2) @ F
+    detC = np.linalg.det(C)
+    Ci = np.linalg.inv(C)
+    trC = np.trace(C, axis1=-2, axis2=-1)
+    S = (0.5 * kappa * (detC - 1.0))[..., None, None] * Ci \
+        + (mu * detC ** (-1.0 / 3.0))[..., None, None] * (I - (trC / 3.0)[..., None, None] * Ci)
+    return F @ S
+
+
+def material_pk1(material, E, nu):
+    """P(F) for material 'svk' | 'neohookean' with the Lame constants of (E, nu); kappa = lambda + 2 mu/3."""
+    lam, mu = lame(E, nu)
+    if material == "svk":
+        return lambda F: pk1_svk(F, lam, mu)
+    if material == "neohookean":
+        return lambda F: pk1_neohookean(F, lam + 2.0 * mu / 3.0, mu)
+    raise ValueError(material)
+
+
+def internal_force_nonlinear(box: Box, u: np.ndarray, pk1) -> np.ndarray:
+    """f_a = sum_e sum_q w_q detJ P(F_q) dN_a/dX(q), F_q = I + sum_b u_b (x) dN_b/dX(q)  (weak form
+    P:L129-137 with the material's first Piola-Kirchhoff stress; element loop, 2x2x2 Gauss, w = 1)."""
+    ug = box._grid(u)
+    ue = np.stack([ug[box._slice(b)] for b in range(8)], axis=-2).reshape(-1, 8, 3)   # (nel, 8, 3)
+    h = box.h
+    detJ = np.prod(h) / 8.0
+    fe = np.zeros_like(ue)
+    for q in gauss_points():
+        _, dNdxi = shape_functions(q)
+        dNdX = dNdxi / (h[None, :] / 2.0)
+        G = np.einsum("eai,aj->eij", ue, dNdX)        # (grad u)_ij = du_i/dX_j
+        P = pk1(np.eye(3) + G)
+        fe += detJ * np.einsum("eij,aj->eai", P, dNdX)
+    fe = fe.reshape(box.nel[2], box.nel[1], box.nel[0], 8, 3)
+    f = np.zeros_like(ug)
+    for a in range(8):
+        f[box._slice(a)] += fe[..., a, :]
+    return f.reshape(-1, 3)

@@ -119,14 +119,18 @@ class FOM(_Base):
     kind = "fom"
     batch = 1
 
-    def __init__(self, sub, schwarz_faces, E, nu, rho, dt, n_sub=1):
+    def __init__(self, sub, schwarz_faces, E, nu, rho, dt, n_sub=1, material="linear"):
         super().__init__(sub, schwarz_faces, E, nu, rho)
         self.Ke = fem.hex8_stiffness(self.box.h, E, nu)
+        self.material = material
+        self._pk1 = None if material == "linear" else fem.material_pk1(material, E, nu)
         self.m = fem.lumped_mass(self.box, rho)
         self.n_sub = int(n_sub)
         self.dt = dt / self.n_sub          # subdomain step dt_i
 
     def force(self, u):
+        if self._pk1 is not None:    # SVK / Neohookean (NEXT-3)
+            return fem.internal_force_nonlinear(self.box, u, self._pk1)
         return fem.internal_force(self.box, self.Ke, u)
 
     def init_state(self, u0, v0=None):
@@ -318,7 +322,8 @@ def build_models(cfg, rom_ops=None, e_scale=None):
         if s["kind"] == "fom":
             if s.get("integrator", "explicit") != "explicit":
                 raise ValueError("the FOM is explicit (north_star); implicit FOM solves are out of scope")
-            models.append(FOM(s, faces[i], cfg["E"], cfg["nu"], cfg["rho"], cfg["dt"], n_sub))
+            models.append(FOM(s, faces[i], cfg["E"], cfg["nu"], cfg["rho"], cfg["dt"], n_sub,
+                              s.get("material", cfg.get("material", "linear"))))
         else:
             models.append(ROM(s, faces[i], cfg["E"], cfg["nu"], cfg["rho"], cfg["dt"], rom_ops[i], e_scale, n_sub,
                               s.get("integrator", "explicit")))
