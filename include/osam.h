@@ -51,6 +51,12 @@ enum { OSAM_FOM = 0, OSAM_ROM = 1 };
  * implicit average acceleration (beta = 1/4): (I + beta dt_i^2 e_b Kbar) a^' = e_b (-Kbar u~ + Bbar g^). */
 enum { OSAM_EXPLICIT = 0, OSAM_IMPLICIT = 1 };
 
+/* FOM material (App. A; readings R35, R36): linear elasticity (A.1, the merged-stencil kernel K1), or the
+ * nonlinear Saint Venant-Kirchhoff (A.2: P = F S, S = lambda tr(E) I + 2 mu E, E = (F^T F - I)/2) and
+ * Neohookean (A.3: S = kappa/2 (det C - 1) C^-1 + mu (det C)^(-1/3) (I - tr(C)/3 C^-1), kappa = lambda +
+ * 2 mu/3) hex8 forces with 2x2x2 Gauss points (kernel NL1).  lambda, mu from (E, nu).                 */
+enum { OSAM_LINEAR = 0, OSAM_SVK = 1, OSAM_NEOHOOKEAN = 2 };
+
 enum {
   OSAM_OK = 0,
   OSAM_WNOTCONVERGED = 1, /* some controller step hit max_iters; last iterate kept */
@@ -89,6 +95,7 @@ typedef struct {
    * the convergence norm is evaluated at the interval end with dt_i (reading R33).                    */
   int32_t n_substeps;     /* 0/1 .. 4096                                                              */
   int32_t integrator;     /* OSAM_EXPLICIT (FOM: required) | OSAM_IMPLICIT (linear ROM only)         */
+  int32_t material;       /* FOM: OSAM_LINEAR | OSAM_SVK | OSAM_NEOHOOKEAN (ROM: must be OSAM_LINEAR) */
 } osam_subdomain_desc;
 
 typedef struct {

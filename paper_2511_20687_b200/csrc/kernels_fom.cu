@@ -783,12 +783,280 @@ unsigned xface_blocks(const Geom& g, const Faces& f) {
   return ns ? cdiv(4LL * ns * g.nn[1] * g.nn[2], XF_BLOCK) : 0u;
 }
 
+
+// ---- NL1: nonlinear FOM advance (SVK / Neohookean; App. A.2, A.3) ----------
+// The explicit scheme and the (q, w) state of R30 are unchanged; only the internal force is the
+// nonlinear weak form  f_a = sum_e sum_q detJ P(F_q) dN_a/dX(q),  F = I + grad u,  2x2x2 Gauss.
+// A CTA owns a 16 x 14 node tile and a z-chunk of node planes, streams node planes through a 2-plane
+// shared ring (18 x 16 staged nodes: the tile plus a 1-node halo), computes each element layer once
+// per tile -- one thread per element (17 x 15 = 255 elements), 24 nodal force contributions into
+// shared memory -- and finishes a node plane by gathering its 8 element contributions in a fixed
+// order (deterministic; no atomics), then exactly K1's finish (a, w', q', norm partials).  256
+// threads: the element code keeps 36 force accumulators plus a Gauss point's F, P in registers
+// (no spills at <= 255 registers).
+namespace nl {
+constexpr int TXN = 16, TYN = 14, ZCN = 16;
+constexpr int EX = TXN + 1, EY = TYN + 1, NE = EX * EY;
+constexpr int PXN = TXN + 2, PYN = TYN + 2, PLN = PXN * PYN;
+constexpr int NTN = 256;
+constexpr size_t SMEM = sizeof(double) * (2 * 3 * PLN + 2 * 24 * NE);
+}  // namespace nl
+
+template <int MAT>
+__device__ __forceinline__ void pk1(const FomLaunch& L, const double F[3][3], double P[3][3]) {
+  double C[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) C[i][j] = fma(F[0][i], F[0][j], fma(F[1][i], F[1][j], F[2][i] * F[2][j]));
+  double S[3][3];
+  if (MAT == OSAM_SVK) {  // S = lambda tr(E) I + 2 mu E, E = (C - I)/2
+    const double trE = 0.5 * ((C[0][0] - 1.0) + (C[1][1] - 1.0) + (C[2][2] - 1.0));
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) S[i][j] = L.mat_mu * (C[i][j] - (i == j ? 1.0 : 0.0)) + (i == j ? L.mat_lam * trE : 0.0);
+  } else {  // Neohookean: S = kappa/2 (det C - 1) C^-1 + mu (det C)^(-1/3) (I - tr(C)/3 C^-1)
+    const double a00 = C[1][1] * C[2][2] - C[1][2] * C[2][1], a01 = C[0][2] * C[2][1] - C[0][1] * C[2][2],
+                 a02 = C[0][1] * C[1][2] - C[0][2] * C[1][1];
+    const double det = C[0][0] * a00 + C[1][0] * a01 + C[2][0] * a02;
+    const double id = 1.0 / det;
+    double Ci[3][3];
+    Ci[0][0] = a00 * id;
+    Ci[0][1] = a01 * id;
+    Ci[0][2] = a02 * id;
+    Ci[1][0] = (C[1][2] * C[2][0] - C[1][0] * C[2][2]) * id;
+    Ci[1][1] = (C[0][0] * C[2][2] - C[0][2] * C[2][0]) * id;
+    Ci[1][2] = (C[0][2] * C[1][0] - C[0][0] * C[1][2]) * id;
+    Ci[2][0] = (C[1][0] * C[2][1] - C[1][1] * C[2][0]) * id;
+    Ci[2][1] = (C[0][1] * C[2][0] - C[0][0] * C[2][1]) * id;
+    Ci[2][2] = (C[0][0] * C[1][1] - C[0][1] * C[1][0]) * id;
+    const double sv = 0.5 * L.mat_kappa * (det - 1.0);
+    const double sd = L.mat_mu * rcbrt(det);
+    const double t3 = (C[0][0] + C[1][1] + C[2][2]) / 3.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) S[i][j] = sv * Ci[i][j] + sd * ((i == j ? 1.0 : 0.0) - t3 * Ci[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) P[i][j] = fma(F[i][0], S[0][j], fma(F[i][1], S[1][j], F[i][2] * S[2][j]));
+}
+
+// 24 nodal force contributions f[a][c] of one hex8 element (local node a = dx + 2 dy + 4 dz),
+// rectangular, J = diag(h/2).  With N_a = prod_d (1 + s_ad xi_d)/2, dN_a/dX_j = s_aj/h_j prod_{d != j}
+// w(a_d, q_d), w = (1 +- 1/sqrt3)/2 on the same / opposite side, so at Gauss point q
+//     du_i/dX_j = sum_p W_j[p] (u_i(a_j = 1, p) - u_i(a_j = 0, p))    (p: the other two bits of a)
+//     f_a,i     = sum_j s_aj T_j[i][p(a)],   T_j[i][p] = sum_q detJ P_q[i][j] W_j[p](q).
+// The nodal displacements are read from the staged planes (u(a) = ua(a, c)); 36 accumulators T.
+template <int MAT, class UA>
+__device__ __forceinline__ void element_forces(const FomLaunch& L, UA ua, double (&f)[8][3]) {
+  const double r3 = 0.57735026918962576451;  // 1/sqrt(3)
+  const double gpl = 0.5 * (1.0 + r3), gmi = 0.5 * (1.0 - r3);
+  const double ih[3] = {1.0 / L.g.h[0], 1.0 / L.g.h[1], 1.0 / L.g.h[2]};
+  const double detJ = 0.125 * L.g.h[0] * L.g.h[1] * L.g.h[2];
+  double T[3][3][4];
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int p = 0; p < 4; ++p) T[j][i][p] = 0.0;
+#pragma unroll 1
+  for (int q = 0; q < 8; ++q) {
+    double w0[3], w1[3];  // weight of a node with bit 0 / 1 on axis d at this point
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const bool qd = (q >> d) & 1;
+      w0[d] = qd ? gmi : gpl;
+      w1[d] = qd ? gpl : gmi;
+    }
+    double W[3][4];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int o1 = j == 0 ? 1 : 0, o2 = j == 2 ? 1 : 2;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) W[j][p] = ((p & 1) ? w1[o1] : w0[o1]) * ((p & 2) ? w1[o2] : w0[o2]) * ih[j];
+    }
+    double F[3][3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int o1 = j == 0 ? 1 : 0, o2 = j == 2 ? 1 : 2;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        double gsum = 0.0;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const int a0 = ((p & 1) << o1) | (((p >> 1) & 1) << o2);
+          gsum = fma(W[j][p], ua(a0 | (1 << j), i) - ua(a0, i), gsum);
+        }
+        F[i][j] = (i == j ? 1.0 : 0.0) + gsum;
+      }
+    }
+    double P[3][3];
+    pk1<MAT>(L, F, P);
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double pij = P[i][j] * detJ;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) T[j][i][p] = fma(pij, W[j][p], T[j][i][p]);
+      }
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      double v = 0.0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int o1 = j == 0 ? 1 : 0, o2 = j == 2 ? 1 : 2;
+        const int p = ((a >> o1) & 1) | (((a >> o2) & 1) << 1);
+        v = ((a >> j) & 1) ? v + T[j][i][p] : v - T[j][i][p];
+      }
+      f[a][i] = v;
+    }
+}
+
+template <int MAT>
+__global__ void __launch_bounds__(nl::NTN, 1) fom_nl_kernel(const __grid_constant__ FomLaunch L) {
+  using namespace nl;
+  extern __shared__ __align__(16) double nsm[];
+  double* Xs = nsm;               // [2][3][PYN][PXN]
+  double* EF = nsm + 2 * 3 * PLN;  // [2][8][3][NE]
+  const Geom& g = L.g;
+  const long long np = g.npad;
+  const int tid = threadIdx.x, tx = tid % TXN, ty = tid / TXN;
+  const int ntx = (g.nn[0] + TXN - 1) / TXN, nty = (g.nn[1] + TYN - 1) / TYN;
+  const int nzc = (g.nn[2] + ZCN - 1) / ZCN;
+  const int bx = blockIdx.x % ntx, by = (blockIdx.x / ntx) % nty, bz = blockIdx.x / (ntx * nty);
+  const int x0 = bx * TXN, y0 = by * TYN;
+  const int kbeg = (int)((long long)bz * g.nn[2] / nzc), kend = (int)((long long)(bz + 1) * g.nn[2] / nzc) - 1;
+  const int nelx = g.nn[0] - 1, nely = g.nn[1] - 1, nelz = g.nn[2] - 1;
+
+  auto load_plane = [&](int p) {
+    double* dst = Xs + (p & 1) * 3 * PLN;
+    for (int t = tid; t < 3 * PLN; t += NTN) {
+      const int c = t / PLN, rem = t % PLN, yy = rem / PXN, xx = rem % PXN;
+      const int i = x0 - 1 + xx, j = y0 - 1 + yy;
+      double v = 0.0;
+      if (i >= 0 && i < g.nn[0] && j >= 0 && j < g.nn[1] && p >= 0 && p < g.nn[2]) v = __ldg(L.x + c * np + gidx(g, i, j, p));
+      dst[t] = v;
+    }
+  };
+  auto compute_layer = [&](int l) {
+    if (tid >= NE) return;
+    const int lx = tid % EX, ly = tid / EX;
+    const int ex = x0 - 1 + lx, ey = y0 - 1 + ly;
+    double* out = EF + (l & 1) * 24 * NE + tid;
+    if (ex < 0 || ex >= nelx || ey < 0 || ey >= nely || l < 0 || l >= nelz) {
+#pragma unroll
+      for (int q = 0; q < 24; ++q) out[q * NE] = 0.0;
+      return;
+    }
+    const double* p0 = Xs + (l & 1) * 3 * PLN + ly * PXN + lx;
+    const double* p1 = Xs + ((l + 1) & 1) * 3 * PLN + ly * PXN + lx;
+    auto ua = [&](int a, int c) { return ((a >> 2) ? p1 : p0)[c * PLN + ((a >> 1) & 1) * PXN + (a & 1)]; };
+    double f[8][3];
+    element_forces<MAT>(L, ua, f);
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) out[(a * 3 + c) * NE] = f[a][c];
+  };
+
+  double num = 0.0, den = 0.0;
+  load_plane(kbeg - 1);
+  load_plane(kbeg);
+  __syncthreads();
+  compute_layer(kbeg - 1);
+  for (int k = kbeg; k <= kend; ++k) {
+    __syncthreads();
+    load_plane(k + 1);
+    __syncthreads();
+    compute_layer(k);
+    __syncthreads();
+    const int i = x0 + tx, j = y0 + ty;
+    if (ty < TYN && i < g.nn[0] && j < g.nn[1]) {
+      double fsum[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int dz = 0; dz < 2; ++dz)
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy)
+#pragma unroll
+          for (int dx = 0; dx < 2; ++dx) {
+            const int a = (1 - dx) + 2 * (1 - dy) + 4 * (1 - dz);
+            const double* e = EF + ((k - 1 + dz) & 1) * 24 * NE + (tx + dx) + EX * (ty + dy);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) fsum[c] += e[(a * 3 + c) * NE];
+          }
+      const long long id = gidx(g, i, j, k);
+      const unsigned fm = free_mask(g, L.f, i, j, k);
+      const double inv_m = L.inv_mass[(axis_class(i, g.nn[0]) == 1) + 2 * (axis_class(j, g.nn[1]) == 1) +
+                                      4 * (axis_class(k, g.nn[2]) == 1)];
+      const double* xo = Xs + (k & 1) * 3 * PLN + (ty + 1) * PXN + tx + 1;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double x = xo[c * PLN];
+        double an = 0.0, wn = 0.0, qn = x;
+        if ((fm >> c) & 1) {
+          const double w0 = L.w0[c * np + id];
+          an = -fsum[c] * inv_m;
+          wn = fma(L.cw, an, w0);
+          qn = fma(L.cq, wn, x);
+          const double w = fma(L.dt, fma(L.cv, an, w0), x);
+          if (L.with_norm) {
+            const double d = L.z_out ? w - L.z_out[c * np + id] : 0.5 * L.dt * (wn - L.w_out[c * np + id]);
+            num = fma(d, d, num);
+            den = fma(w, w, den);
+          }
+          if (L.z_out) L.z_out[c * np + id] = w;
+        }
+        if (L.q_out) L.q_out[c * np + id] = qn;
+        L.w_out[c * np + id] = wn;
+        if (L.a_out) L.a_out[c * np + id] = an;
+      }
+    }
+  }
+  block_partial<nl::NTN>(num, den, L.partial, blockIdx.x);
+}
+
+int nl_ctas(const Geom& g) {
+  using namespace nl;
+  return ((g.nn[0] + TXN - 1) / TXN) * ((g.nn[1] + TYN - 1) / TYN) * ((g.nn[2] + ZCN - 1) / ZCN);
+}
+
 }  // namespace
 
 int fom_partial_slots(const Geom& g, const Faces& f) { return tiled_ctas(g) + (int)xface_blocks(g, f); }
 
+int fom_nl_partial_slots(const Geom& g) { return nl_ctas(g); }
+
+void launch_fom_advance_nl(const FomLaunch& L, cudaStream_t s, int* launches) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fom_nl_kernel<OSAM_SVK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nl::SMEM);
+    cudaFuncSetAttribute(fom_nl_kernel<OSAM_NEOHOOKEAN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)nl::SMEM);
+    attr = true;
+  }
+  const dim3 block(nl::NTN);
+  if (L.material == OSAM_SVK)
+    fom_nl_kernel<OSAM_SVK><<<nl_ctas(L.g), block, nl::SMEM, s>>>(L);
+  else
+    fom_nl_kernel<OSAM_NEOHOOKEAN><<<nl_ctas(L.g), block, nl::SMEM, s>>>(L);
+  debug_check("fom_nl_kernel", s);
+  ++*launches;
+}
+
 void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUtensorMap* tmx,
                         const CUtensorMap* tmw, const CUtensorMap* tmwp, cudaStream_t s, int* launches) {
+  if (L.material != OSAM_LINEAR) {  // SVK / Neohookean: NL1 (no stencil, no TMA maps)
+    launch_fom_advance_nl(L, s, launches);
+    return;
+  }
   const int n_int = tiled_ctas(L.g);
   if (L.z_out)  // last substep of a multi-substep interval: z = u + dt v out, norm from z - z_prev (R33)
     fom_tiled_kernel<true><<<n_int, dim3(TX, TY), SMEM_TILED, s>>>(L, st, *tmx, *tmw, *tmwp);

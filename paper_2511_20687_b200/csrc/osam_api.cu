@@ -163,6 +163,11 @@ long long face_count(const Geom& g, int f) {
   return (long long)g.nn[o0] * g.nn[o1];
 }
 
+// partial (num, den) slots of one FOM advance launch
+int fom_slots(const Sub& s) {
+  return s.material == OSAM_LINEAR ? fom_partial_slots(s.g, s.faces) : fom_nl_partial_slots(s.g);
+}
+
 // ---- binding ------------------------------------------------------------------------------
 void release_maps(Sub& s) {
   for (auto& m : s.maps) {
@@ -355,7 +360,7 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
         s.faces.dir[f] = s.dirichlet[f];
         s.faces.sw[f] = s.face_src[f] >= 0;
       }
-      TRY(dalloc(&s.scratch_partial, (size_t)fom_partial_slots(s.g, s.faces)));
+      TRY(dalloc(&s.scratch_partial, (size_t)fom_slots(s)));
       continue;
     }
     const long long rows_phi = (long long)(s.h_Phi.size() / std::max(1, s.r));
@@ -640,7 +645,7 @@ int get_group(osam_subdomain* const* sds, int n_sd, Group** out) {
     for (auto s : subs) G->B = std::max(G->B, s->batch);
     for (auto s : subs) G->trace = G->trace || s->n_sub > 1;
     G->n_slots = 0;
-    for (auto s : subs) G->n_slots += s->kind == OSAM_FOM ? fom_partial_slots(s->g, s->faces) : rom_partial_slots(s->r, s->use_tc);
+    for (auto s : subs) G->n_slots += s->kind == OSAM_FOM ? fom_slots(*s) : rom_partial_slots(s->r, s->use_tc);
     TRY(dalloc(&G->partial, (size_t)std::max(1, G->n_slots) * G->B));
     TRY(dalloc(&G->ctl_i, (size_t)G->ctl_len()));
     CK(cudaMemset(G->ctl_i, 0, sizeof(int) * G->ctl_len()));
@@ -673,6 +678,10 @@ FomLaunch fom_launch(const Sub& d, const double* x, const double* w0, double* q_
   L.rowc = d.rowc;
   L.with_norm = with_norm;
   L.partial = partial;
+  L.material = d.material;
+  L.mat_lam = d.lam;
+  L.mat_mu = d.mu;
+  L.mat_kappa = d.lam + 2.0 * d.mu / 3.0;
   return L;
 }
 
@@ -791,7 +800,7 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
       if (fom_k) ++*fom_k;
       g_k1_bytes += (32.0 + (with_norm ? 8.0 : 0.0)) * 3.0 * (double)d.n_nodes;
       ++g_k1_launches;
-      slot += fom_partial_slots(d.g, d.faces);
+      slot += fom_slots(d);
     } else {
       const int c = d.cur;
       const RomLaunch L = rom_launch(d, d.rst[c], d.rst[1 - c], ctl.active, cfg.dt, with_norm,
@@ -926,7 +935,7 @@ int enqueue_sweep_trace(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, b
           ++*launches;
         }
     }
-    slot += d.kind == OSAM_FOM ? fom_partial_slots(d.g, d.faces) : rom_partial_slots(d.r, d.use_tc);
+    slot += d.kind == OSAM_FOM ? fom_slots(d) : rom_partial_slots(d.r, d.use_tc);
   }
   launch_finalize(ctl, G.partial, G.n_slots, B, cfg.min_iters, cfg.tol_rel, cfg.tol_abs, st);
   *launches += 2;
@@ -1113,6 +1122,10 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
     return fail(OSAM_EINVAL, "integrator must be OSAM_EXPLICIT or OSAM_IMPLICIT");
   if (d->kind == OSAM_FOM && d->integrator != OSAM_EXPLICIT)
     return fail(OSAM_EINVAL, "the FOM is explicit (implicit FOM solves are out of scope)");
+  if (d->material != OSAM_LINEAR && d->material != OSAM_SVK && d->material != OSAM_NEOHOOKEAN)
+    return fail(OSAM_EINVAL, "material must be OSAM_LINEAR, OSAM_SVK or OSAM_NEOHOOKEAN");
+  if (d->kind == OSAM_ROM && d->material != OSAM_LINEAR)
+    return fail(OSAM_EINVAL, "a ROM has no material model (its operators are inferred)");
   if (d->integrator == OSAM_IMPLICIT && (d->Hbar || d->Cbar))
     return fail(OSAM_EINVAL, "implicit stepping is implemented for linear OpInf ROMs only (no Hbar/Cbar)");
   int dev = 0;
@@ -1136,6 +1149,7 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
   s.stream = (cudaStream_t)cuda_stream;
   s.n_sub = std::max(1, (int)d->n_substeps);
   s.beta = d->integrator == OSAM_IMPLICIT ? 0.25 : 0.0;
+  s.material = d->material;
   Geom& g = s.g;
   g.nn[0] = (int)nn0;
   g.nn[1] = (int)nn1;

@@ -69,6 +69,7 @@ struct Sub {
   int batch = 1;
   int r = 0, r_b = 0;
   int n_sub = 1;      // substeps per controller step: dt_i = dt / n_sub
+  int material = OSAM_LINEAR;  // FOM material (NL1 for SVK / Neohookean)
   double beta = 0.0;  // Newmark beta: 0 explicit, 1/4 implicit average acceleration (ROM only, R32)
   cudaStream_t stream = nullptr;
   Geom g;
@@ -160,9 +161,12 @@ struct FomLaunch {
   const double* rowc;  // [3][3][3][3][3][3][2] row-form coefficients
   int with_norm;       // 1 from Schwarz iteration 2 on
   double2* partial;    // per-block (num, den)
+  int material;        // OSAM_LINEAR (K1) | OSAM_SVK | OSAM_NEOHOOKEAN (NL1)
+  double mat_lam, mat_mu, mat_kappa;
 };
 // Number of partial slots a K1 launch writes (tiled blocks + x-face blocks).
 int fom_partial_slots(const Geom& g, const Faces& f);
+int fom_nl_partial_slots(const Geom& g);  // NL1 (nonlinear materials): one slot per CTA
 void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUtensorMap* tmx,
                         const CUtensorMap* tmw, const CUtensorMap* tmwp, cudaStream_t s, int* launches);
 int make_field_tmap(const Geom& g, double* array, bool halo, CUtensorMap* out);

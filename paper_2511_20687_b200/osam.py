@@ -17,6 +17,8 @@ LIB_PATH = os.environ.get("OSAM_LIB") or os.path.join(_HERE, "libosam.so")
 
 OSAM_FOM, OSAM_ROM = 0, 1
 OSAM_EXPLICIT, OSAM_IMPLICIT = 0, 1
+OSAM_LINEAR, OSAM_SVK, OSAM_NEOHOOKEAN = 0, 1, 2
+MATERIALS = {"linear": OSAM_LINEAR, "svk": OSAM_SVK, "neohookean": OSAM_NEOHOOKEAN}
 OSAM_OK, OSAM_WNOTCONVERGED = 0, 1
 ERRORS = {-1: "OSAM_EINVAL", -2: "OSAM_ENOMEM", -3: "OSAM_ECUDA", -4: "OSAM_EOVERLAP", -5: "OSAM_EUNSTABLE"}
 
@@ -35,7 +37,7 @@ class osam_subdomain_desc(C.Structure):
                 ("Kbar", C.POINTER(C.c_double)), ("Bbar", C.POINTER(C.c_double)),
                 ("e_scale", C.POINTER(C.c_double)),
                 ("Hbar", C.POINTER(C.c_double)), ("Cbar", C.POINTER(C.c_double)),
-                ("n_substeps", C.c_int32), ("integrator", C.c_int32)]
+                ("n_substeps", C.c_int32), ("integrator", C.c_int32), ("material", C.c_int32)]
 
 
 class osam_replay_desc(C.Structure):
@@ -118,10 +120,11 @@ class Subdomain:
     """Owning wrapper of an osam_subdomain handle (osam_create_subdomain / osam_destroy)."""
 
     def __init__(self, kind, lo, hi, nel, E, nu, rho, dirichlet=(0,) * 6, stream=None, rom=None, e_scale=None,
-                 n_substeps=1, integrator=OSAM_EXPLICIT):
+                 n_substeps=1, integrator=OSAM_EXPLICIT, material=OSAM_LINEAR):
         d = osam_subdomain_desc()
         d.n_substeps = int(n_substeps)
         d.integrator = int(integrator)
+        d.material = int(material)
         d.kind = kind
         d.lo[:] = [float(x) for x in lo]
         d.hi[:] = [float(x) for x in hi]

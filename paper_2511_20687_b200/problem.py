@@ -10,7 +10,7 @@ import numpy as np
 
 import osam_inputs
 
-from .osam import OSAM_EXPLICIT, OSAM_FOM, OSAM_IMPLICIT, OSAM_ROM, Subdomain, osam_step
+from .osam import MATERIALS, OSAM_EXPLICIT, OSAM_FOM, OSAM_IMPLICIT, OSAM_LINEAR, OSAM_ROM, Subdomain, osam_step
 
 
 def e_scale(cfg):
@@ -31,7 +31,9 @@ def build(cfg, rom_ops=None, stream=None):
         integ = OSAM_IMPLICIT if s.get("integrator", "explicit") == "implicit" else OSAM_EXPLICIT
         subs.append(Subdomain(kind, s["lo"], s["hi"], s["nel"], cfg["E"], cfg["nu"], cfg["rho"], s["dirichlet"],
                               stream=stream, rom=rom, e_scale=e_scale(cfg) if kind == OSAM_ROM else None,
-                              n_substeps=s.get("n_sub", 1), integrator=integ))
+                              n_substeps=s.get("n_sub", 1), integrator=integ,
+                              material=MATERIALS[s.get("material", cfg.get("material", "linear"))]
+                              if kind == OSAM_FOM else OSAM_LINEAR))
     return subs
 
 

@@ -352,3 +352,46 @@ def test_graph_equals_host_controller_with_substeps(gpu):
     assert np.array_equal(out[0][0], out[1][0])
     for a, b in zip(out[0][1], out[1][1]):
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+# ---- NEXT-3: nonlinear FOM (Saint Venant-Kirchhoff / Neohookean, kernel NL1) ------------------------
+
+def _nonlinear(cfg, material, amplitude=None):
+    import copy
+    c = copy.deepcopy(cfg)
+    c["material"] = material
+    if amplitude is not None:
+        c["ic"] = dict(c["ic"], A=amplitude)
+    return c
+
+
+@pytest.mark.parametrize("material", ["svk", "neohookean"])
+def test_c1_nonlinear_fom(gpu, material):
+    """c1 geometry at strains ~1e-1 (IC amplitude 2e-2): NL1 against the oracle's element loop."""
+    cfg = _nonlinear(I.config("c1"), material, 2e-2)
+    _, iters, worst = run_both(gpu, cfg, 80, checkpoints=(1, 9))
+    print("c1", material, "worst rel L2", worst, "iters", np.unique(iters))
+
+
+def test_c1_svk_with_substeps(gpu):
+    cfg = _substeps(_nonlinear(I.config("c1"), "svk", 2e-2), (2, 1), dt_factor=2.0)
+    _, iters, worst = run_both(gpu, cfg, 40, checkpoints=(1,))
+    print("c1 svk substeps worst rel L2", worst)
+
+
+@pytest.mark.parametrize("material", ["svk", "neohookean"])
+def test_c3_scaled_nonlinear_multi_tile(gpu, material):
+    """c3 geometry coarsened 5x: several NL1 tiles in x, y and several z-chunks per subdomain, clamped face."""
+    cfg = _nonlinear(I.scaled(I.config("c3"), 5.0), material)
+    _, iters, worst = run_both(gpu, cfg, 4, checkpoints=(1,))
+    print("c3/5", material, "worst rel L2", worst, "iters", np.unique(iters))
+
+
+def test_c2_svk_fom_with_copinf_rom(gpu):
+    """The pairing the paper uses for cubic nonlinearity: SVK FOM coupled to a COpInf ROM trained
+    on SVK single-domain data."""
+    cfg = _nonlinear(I.config("c2"), "svk", 1e-2)
+    cfg["rom"] = dict(cfg["rom"], order=3)
+    ops = opinf.train(cfg, I)
+    _, iters, worst = run_both(gpu, cfg, 100, rom_ops=ops, checkpoints=(1,))
+    print("c2 svk + COpInf worst rel L2", worst, "iters", np.unique(iters))
