@@ -32,6 +32,13 @@ METRIC = "FOM DOF-updates/s"
 UNIT = "DOF-updates/s"
 SAMPLE_LATERAL = 32
 FALLBACK_HBM = 6650.0
+# FP64 CUDA-core peak derived from unit counts and clock: 148 SMs x 64 FP64 FMA/clk
+# x 2 flop x 1.965 GHz (clocks.max.sm, B200_PROFILING.md)
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+# algorithmic FP64 flops of NL1 per element and FOM advance (FMA = 2): 36 edge
+# differences + 8 Gauss points x (gradient 72 + stress (SVK 94 / Neohookean 169) + force accumulation 72)
+# + 72 nodal assembly
+NL1_FLOPS_PER_ELEMENT = {"svk": 36 + 8 * (72 + 94 + 72) + 72, "neohookean": 36 + 8 * (72 + 169 + 72) + 72}
 
 
 def parse():
@@ -44,6 +51,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-largest", action="store_true", help="skip the c4 (largest config) K1 roofline entry")
+    p.add_argument("--material", default="linear", choices=["linear", "svk", "neohookean"],
+                   help="FOM material (NEXT-3): nonlinear materials run kernel NL1 (FP64-ALU roofline)")
     return p.parse_args()
 
 
@@ -280,6 +289,8 @@ def run_ours(args):
     from paper_2511_20687_b200 import osam, problem
 
     cfg = I.config(args.workload)
+    if args.material != "linear":
+        cfg["material"] = args.material
     desc, fom_dofs = workload_desc(cfg)
     stream = torch.cuda.current_stream(dev)
     ops = workload_ops(cfg)
@@ -364,7 +375,21 @@ def run_ours(args):
                          "peak_source": peak_src},
             "gpu_launches": int(launches),
             "clocks": ck, "e2e": e2e}
-    if world == 1 and not args.no_largest and args.workload != "c4":
+    if args.material != "linear":   # NL1 is FP64-ALU bound: roofline in TFLOP/s
+        n_fom = sum(1 for s in cfg["subdomains"] if s["kind"] == "fom")
+        elems = sum(int(np.prod(s["nel"])) for s in cfg["subdomains"] if s["kind"] == "fom")
+        flops = NL1_FLOPS_PER_ELEMENT[args.material] * elems / max(1, n_fom)   # per launch (mean)
+        tf = flops / (k1_ms_per_launch / 1e3) / 1e12
+        line["metric"] = METRIC
+        line["config"]["workload"] += f", material {args.material}"
+        line["roofline"] = {"bound": "alu", "achieved": tf, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                            "frac": tf / FP64_PEAK_TFLOPS, "traffic": None, "kernel": "NL1 fom_nl_kernel",
+                            "flops_model": f"{NL1_FLOPS_PER_ELEMENT[args.material]} FP64 flop per element per "
+                                           "FOM advance (DESIGN.md section 11)",
+                            "hbm_achieved_gbs": achieved, "k1_ms_per_launch": k1_ms_per_launch,
+                            "k1_share_of_step": prof["k1_ms"] / prof_ms,
+                            "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"}
+    if world == 1 and not args.no_largest and args.workload != "c4" and args.material == "linear":
         line["largest_config"] = largest_config(dev, stream)
     if world == 1 and not args.no_cpu_baseline:
         sample = sample_cfg(cfg)

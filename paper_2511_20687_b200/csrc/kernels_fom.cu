@@ -795,27 +795,42 @@ unsigned xface_blocks(const Geom& g, const Faces& f) {
 // threads: the element code keeps 36 force accumulators plus a Gauss point's F, P in registers
 // (no spills at <= 255 registers).
 namespace nl {
-constexpr int TXN = 16, TYN = 14, ZCN = 16;
+constexpr int TXN = 16, TYN = 14, ZCN = 32;
 constexpr int EX = TXN + 1, EY = TYN + 1, NE = EX * EY;
 constexpr int PXN = TXN + 2, PYN = TYN + 2, PLN = PXN * PYN;
 constexpr int NTN = 256;
-constexpr size_t SMEM = sizeof(double) * (2 * 3 * PLN + 2 * 24 * NE);
+constexpr int NN = TXN * TYN;  // nodes finished per plane
+// X ring of 3 planes | element forces of 2 layers | W and W'_prev (or z_prev) of 2 node planes
+constexpr size_t SMEM = sizeof(double) * (3 * 3 * PLN + 2 * 24 * NE + 2 * 2 * 3 * NN);
 }  // namespace nl
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 template <int MAT>
 __device__ __forceinline__ void pk1(const FomLaunch& L, const double F[3][3], double P[3][3]) {
-  double C[3][3];
+  double C[3][3];  // symmetric: 6 products
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
-    for (int j = 0; j < 3; ++j) C[i][j] = fma(F[0][i], F[0][j], fma(F[1][i], F[1][j], F[2][i] * F[2][j]));
+    for (int j = i; j < 3; ++j) {
+      C[i][j] = fma(F[0][i], F[0][j], fma(F[1][i], F[1][j], F[2][i] * F[2][j]));
+      C[j][i] = C[i][j];
+    }
   double S[3][3];
   if (MAT == OSAM_SVK) {  // S = lambda tr(E) I + 2 mu E, E = (C - I)/2
     const double trE = 0.5 * ((C[0][0] - 1.0) + (C[1][1] - 1.0) + (C[2][2] - 1.0));
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
-      for (int j = 0; j < 3; ++j) S[i][j] = L.mat_mu * (C[i][j] - (i == j ? 1.0 : 0.0)) + (i == j ? L.mat_lam * trE : 0.0);
+      for (int j = i; j < 3; ++j) {
+        S[i][j] = i == j ? fma(L.mat_mu, C[i][j] - 1.0, L.mat_lam * trE) : L.mat_mu * C[i][j];
+        S[j][i] = S[i][j];
+      }
   } else {  // Neohookean: S = kappa/2 (det C - 1) C^-1 + mu (det C)^(-1/3) (I - tr(C)/3 C^-1)
     const double a00 = C[1][1] * C[2][2] - C[1][2] * C[2][1], a01 = C[0][2] * C[2][1] - C[0][1] * C[2][2],
                  a02 = C[0][1] * C[1][2] - C[0][2] * C[1][1];
@@ -857,40 +872,52 @@ __device__ __forceinline__ void element_forces(const FomLaunch& L, UA ua, double
   const double gpl = 0.5 * (1.0 + r3), gmi = 0.5 * (1.0 - r3);
   const double ih[3] = {1.0 / L.g.h[0], 1.0 / L.g.h[1], 1.0 / L.g.h[2]};
   const double detJ = 0.125 * L.g.h[0] * L.g.h[1] * L.g.h[2];
-  double T[3][3][4];
+  // the weight of an edge difference is one of gpl^2, gpl gmi, gmi^2 times 1/h_j (gradient) or
+  // detJ/h_j (force accumulation): 9 + 9 constants, selected per (point, pair) without FP64 work
+  double Wg[3][3], Wt[3][3];
 #pragma unroll
-  for (int j = 0; j < 3; ++j)
+  for (int j = 0; j < 3; ++j) {
+    const double base[3] = {gpl * gpl, gpl * gmi, gmi * gmi};
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      Wg[j][m] = base[m] * ih[j];
+      Wt[j][m] = Wg[j][m] * detJ;
+    }
+  }
+  double T[3][3][4], D[3][3][4];  // accumulators; edge differences u_i(a_j = 1, p) - u_i(a_j = 0, p)
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const int o1 = j == 0 ? 1 : 0, o2 = j == 2 ? 1 : 2;
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
-      for (int p = 0; p < 4; ++p) T[j][i][p] = 0.0;
+      for (int p = 0; p < 4; ++p) {
+        const int a0 = ((p & 1) << o1) | (((p >> 1) & 1) << o2);
+        T[j][i][p] = 0.0;
+        D[j][i][p] = ua(a0 | (1 << j), i) - ua(a0, i);
+      }
+  }
 #pragma unroll 1
   for (int q = 0; q < 8; ++q) {
-    double w0[3], w1[3];  // weight of a node with bit 0 / 1 on axis d at this point
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const bool qd = (q >> d) & 1;
-      w0[d] = qd ? gmi : gpl;
-      w1[d] = qd ? gpl : gmi;
-    }
-    double W[3][4];
+    // pair p = (bit o1, bit o2) of the other two axes: the weight is gmi for each bit that differs
+    // from the point's bit on that axis -> index m = number of differing bits
+    int mi[3][4];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
       const int o1 = j == 0 ? 1 : 0, o2 = j == 2 ? 1 : 2;
 #pragma unroll
-      for (int p = 0; p < 4; ++p) W[j][p] = ((p & 1) ? w1[o1] : w0[o1]) * ((p & 2) ? w1[o2] : w0[o2]) * ih[j];
+      for (int p = 0; p < 4; ++p) mi[j][p] = ((p & 1) != ((q >> o1) & 1)) + (((p >> 1) & 1) != ((q >> o2) & 1));
     }
     double F[3][3];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      const int o1 = j == 0 ? 1 : 0, o2 = j == 2 ? 1 : 2;
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
         double gsum = 0.0;
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-          const int a0 = ((p & 1) << o1) | (((p >> 1) & 1) << o2);
-          gsum = fma(W[j][p], ua(a0 | (1 << j), i) - ua(a0, i), gsum);
+          const double wg = mi[j][p] == 0 ? Wg[j][0] : (mi[j][p] == 1 ? Wg[j][1] : Wg[j][2]);
+          gsum = fma(wg, D[j][i][p], gsum);
         }
         F[i][j] = (i == j ? 1.0 : 0.0) + gsum;
       }
@@ -900,10 +927,10 @@ __device__ __forceinline__ void element_forces(const FomLaunch& L, UA ua, double
 #pragma unroll
     for (int j = 0; j < 3; ++j)
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const double pij = P[i][j] * detJ;
+      for (int p = 0; p < 4; ++p) {
+        const double wt = mi[j][p] == 0 ? Wt[j][0] : (mi[j][p] == 1 ? Wt[j][1] : Wt[j][2]);
 #pragma unroll
-        for (int p = 0; p < 4; ++p) T[j][i][p] = fma(pij, W[j][p], T[j][i][p]);
+        for (int i = 0; i < 3; ++i) T[j][i][p] = fma(P[i][j], wt, T[j][i][p]);
       }
   }
 #pragma unroll
@@ -925,8 +952,9 @@ template <int MAT>
 __global__ void __launch_bounds__(nl::NTN, 1) fom_nl_kernel(const __grid_constant__ FomLaunch L) {
   using namespace nl;
   extern __shared__ __align__(16) double nsm[];
-  double* Xs = nsm;               // [2][3][PYN][PXN]
-  double* EF = nsm + 2 * 3 * PLN;  // [2][8][3][NE]
+  double* Xs = nsm;                         // [3][3][PYN][PXN]   node planes, slot p mod 3
+  double* EF = Xs + 3 * 3 * PLN;            // [2][8][3][NE]      element forces, layer mod 2
+  double* Ws = EF + 2 * 24 * NE;            // [2][2][3][NN]      W, W'_prev (or z_prev), plane mod 2
   const Geom& g = L.g;
   const long long np = g.npad;
   const int tid = threadIdx.x, tx = tid % TXN, ty = tid / TXN;
@@ -936,15 +964,31 @@ __global__ void __launch_bounds__(nl::NTN, 1) fom_nl_kernel(const __grid_constan
   const int x0 = bx * TXN, y0 = by * TYN;
   const int kbeg = (int)((long long)bz * g.nn[2] / nzc), kend = (int)((long long)(bz + 1) * g.nn[2] / nzc) - 1;
   const int nelx = g.nn[0] - 1, nely = g.nn[1] - 1, nelz = g.nn[2] - 1;
+  const bool need_prev = L.with_norm != 0;
+  const double* prev = L.z_out ? L.z_out : L.w_out;  // previous iterate for the norm (read before written)
 
-  auto load_plane = [&](int p) {
-    double* dst = Xs + (p & 1) * 3 * PLN;
+  // asynchronous copies (cp.async, zero-filled outside the box): node plane p, and W / previous for
+  // the tile's nodes of plane p
+  auto issue_plane = [&](int p) {
+    double* dst = Xs + ((p + 3) % 3) * 3 * PLN;
     for (int t = tid; t < 3 * PLN; t += NTN) {
       const int c = t / PLN, rem = t % PLN, yy = rem / PXN, xx = rem % PXN;
       const int i = x0 - 1 + xx, j = y0 - 1 + yy;
-      double v = 0.0;
-      if (i >= 0 && i < g.nn[0] && j >= 0 && j < g.nn[1] && p >= 0 && p < g.nn[2]) v = __ldg(L.x + c * np + gidx(g, i, j, p));
-      dst[t] = v;
+      const bool ok = i >= 0 && i < g.nn[0] && j >= 0 && j < g.nn[1] && p >= 0 && p < g.nn[2];
+      cp_async8(dst + t, ok ? L.x + c * np + gidx(g, i, j, p) : L.x, ok);
+    }
+  };
+  auto issue_w = [&](int p) {
+    if (p > kend) return;
+    double* dst = Ws + (p & 1) * 2 * 3 * NN;
+    const int i = x0 + tx, j = y0 + ty;
+    if (ty < TYN && i < g.nn[0] && j < g.nn[1]) {
+      const long long id = gidx(g, i, j, p);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        cp_async8(dst + c * NN + tid, L.w0 + c * np + id, true);
+        if (need_prev) cp_async8(dst + (3 + c) * NN + tid, prev + c * np + id, true);
+      }
     }
   };
   auto compute_layer = [&](int l) {
@@ -957,8 +1001,8 @@ __global__ void __launch_bounds__(nl::NTN, 1) fom_nl_kernel(const __grid_constan
       for (int q = 0; q < 24; ++q) out[q * NE] = 0.0;
       return;
     }
-    const double* p0 = Xs + (l & 1) * 3 * PLN + ly * PXN + lx;
-    const double* p1 = Xs + ((l + 1) & 1) * 3 * PLN + ly * PXN + lx;
+    const double* p0 = Xs + ((l + 3) % 3) * 3 * PLN + ly * PXN + lx;
+    const double* p1 = Xs + ((l + 4) % 3) * 3 * PLN + ly * PXN + lx;
     auto ua = [&](int a, int c) { return ((a >> 2) ? p1 : p0)[c * PLN + ((a >> 1) & 1) * PXN + (a & 1)]; };
     double f[8][3];
     element_forces<MAT>(L, ua, f);
@@ -969,15 +1013,21 @@ __global__ void __launch_bounds__(nl::NTN, 1) fom_nl_kernel(const __grid_constan
   };
 
   double num = 0.0, den = 0.0;
-  load_plane(kbeg - 1);
-  load_plane(kbeg);
+  // prologue: planes kbeg-1, kbeg, kbeg+1 and W of plane kbeg; element layer kbeg-1
+  issue_plane(kbeg - 1);
+  issue_plane(kbeg);
+  issue_plane(kbeg + 1);
+  issue_w(kbeg);
+  cp_async_commit();
+  cp_async_wait_all();
   __syncthreads();
   compute_layer(kbeg - 1);
   for (int k = kbeg; k <= kend; ++k) {
-    __syncthreads();
-    load_plane(k + 1);
-    __syncthreads();
-    compute_layer(k);
+    __syncthreads();  // resident: planes k, k+1 and W(k); free: the slot of plane k-1 and W(k-1)
+    issue_plane(k + 2);
+    issue_w(k + 1);
+    cp_async_commit();
+    compute_layer(k);  // overlaps the copies
     __syncthreads();
     const int i = x0 + tx, j = y0 + ty;
     if (ty < TYN && i < g.nn[0] && j < g.nn[1]) {
@@ -997,19 +1047,21 @@ __global__ void __launch_bounds__(nl::NTN, 1) fom_nl_kernel(const __grid_constan
       const unsigned fm = free_mask(g, L.f, i, j, k);
       const double inv_m = L.inv_mass[(axis_class(i, g.nn[0]) == 1) + 2 * (axis_class(j, g.nn[1]) == 1) +
                                       4 * (axis_class(k, g.nn[2]) == 1)];
-      const double* xo = Xs + (k & 1) * 3 * PLN + (ty + 1) * PXN + tx + 1;
+      const double* xo = Xs + (k % 3) * 3 * PLN + (ty + 1) * PXN + tx + 1;
+      const double* wv = Ws + (k & 1) * 2 * 3 * NN + tid;
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
         const double x = xo[c * PLN];
         double an = 0.0, wn = 0.0, qn = x;
         if ((fm >> c) & 1) {
-          const double w0 = L.w0[c * np + id];
+          const double w0 = wv[c * NN];
           an = -fsum[c] * inv_m;
           wn = fma(L.cw, an, w0);
           qn = fma(L.cq, wn, x);
           const double w = fma(L.dt, fma(L.cv, an, w0), x);
-          if (L.with_norm) {
-            const double d = L.z_out ? w - L.z_out[c * np + id] : 0.5 * L.dt * (wn - L.w_out[c * np + id]);
+          if (need_prev) {
+            const double pv = wv[(3 + c) * NN];
+            const double d = L.z_out ? w - pv : 0.5 * L.dt * (wn - pv);
             num = fma(d, d, num);
             den = fma(w, w, den);
           }
@@ -1020,6 +1072,7 @@ __global__ void __launch_bounds__(nl::NTN, 1) fom_nl_kernel(const __grid_constan
         if (L.a_out) L.a_out[c * np + id] = an;
       }
     }
+    cp_async_wait_all();
   }
   block_partial<nl::NTN>(num, den, L.partial, blockIdx.x);
 }
