@@ -30,7 +30,10 @@ TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
         u~ = u^ + dt v^ + dt^2 (1/2 - beta) a^ ,
         (I + beta dt^2 e_b Kbar) a^' = e_b (-Kbar u~ + Bbar g^) ,
         u^' = u~ + beta dt^2 a^' ,  v^' = v^ + dt ((1 - gamma) a^ + gamma a^')
-    (linear OpInf; polynomial terms with the implicit scheme are not supported).
+    with polynomial terms (QOpInf / COpInf) the implicit step is the root of
+        R(u) = u - u~ - beta dt^2 a(u, s),   a(u, s) = e_b (-Kbar u - Hbar u^*2 - Cbar u^*3 + Bbar g^),
+    solved by Newton from u~ + beta dt^2 a^ with the exact Jacobian I + beta dt^2 e_b (Kbar + Hbar
+    d(u^*2)/du + Cbar d(u^*3)/du) until |du| <= 1e-14 |u| (at most 50 steps); a^' = a(u^', s) (reading R37).
 """
 from __future__ import annotations
 
@@ -185,19 +188,44 @@ class ROM(_Base):
         self.free_row[self.free_dofs] = np.arange(len(self.free_dofs))
         self.sdof_idx = np.full(3 * self.box.n_nodes, -1, dtype=np.int64)
         self.sdof_idx[self.schwarz_dofs] = np.arange(len(self.schwarz_dofs))
-        if self.beta > 0 and (self.Hbar is not None or self.Cbar is not None):
-            raise ValueError("implicit ROM stepping is implemented for linear OpInf only")
 
-    def accel(self, uh, s):
-        """a^ = e_b (-Kbar u^ - Hbar u^*2 - Cbar u^*3 + Bbar Phi_dS^T s)  (eq:opinf_model_schwarz P:L550-563;
-        the per-sample modulus scales every stiffness term, reading R22)."""
-        gh = s @ self.Phi_s                                          # (B, r_b) = (Phi_s^T s)^T
+    def reduced_force(self, uh, s):
+        """-Kbar u^ - Hbar u^*2 - Cbar u^*3 + Bbar Phi_dS^T s, row by row (before the per-sample scale)."""
+        gh = s @ self.Phi_s                                          # (n, r_b) = (Phi_s^T s)^T
         f = -uh @ self.Kbar.T + gh @ self.Bbar.T
         if self.Hbar is not None:
             f = f - opinf.khatri_rao_pow(uh.T, 2).T @ self.Hbar.T
         if self.Cbar is not None:
             f = f - opinf.khatri_rao_pow(uh.T, 3).T @ self.Cbar.T
-        return self.e[:, None] * f
+        return f
+
+    def accel(self, uh, s):
+        """a^ = e_b (-Kbar u^ - Hbar u^*2 - Cbar u^*3 + Bbar Phi_dS^T s)  (eq:opinf_model_schwarz P:L550-563;
+        the per-sample modulus scales every stiffness term, reading R22)."""
+        return self.e[:, None] * self.reduced_force(uh, s)
+
+    def stiffness_jacobian(self, u):
+        """d/du (Kbar u + Hbar u^*2 + Cbar u^*3) for one sample u (r,): derivatives of the compressed
+        monomials u_i u_j (i <= j) and u_i u_j u_l (i <= j <= l), lexicographic (P:L167 footnote)."""
+        r = len(u)
+        J = self.Kbar.copy()
+        if self.Hbar is not None:
+            q = 0
+            for i in range(r):
+                for j in range(i, r):
+                    J[:, i] += self.Hbar[:, q] * u[j]
+                    J[:, j] += self.Hbar[:, q] * u[i]
+                    q += 1
+        if self.Cbar is not None:
+            q = 0
+            for i in range(r):
+                for j in range(i, r):
+                    for l in range(j, r):
+                        J[:, i] += self.Cbar[:, q] * u[j] * u[l]
+                        J[:, j] += self.Cbar[:, q] * u[i] * u[l]
+                        J[:, l] += self.Cbar[:, q] * u[i] * u[j]
+                        q += 1
+        return J
 
     def init_state(self, u0, v0=None):
         """u^0 = Phi^T u0[free], v^0 = 0 (or Phi^T v0[free]), s0 = u0 at the Schwarz DOFs,
@@ -221,12 +249,28 @@ class ROM(_Base):
         # implicit Newmark, average acceleration (reading R32): solve for a^' sample by sample
         beta, gamma = self.beta, 0.5
         ut = ckpt["uh"] + dt * ckpt["vh"] + dt * dt * (0.5 - beta) * ckpt["ah"]
-        rhs = self.accel(ut, s)                                      # e_b (-Kbar u~ + Bbar g^)
         r = self.Kbar.shape[0]
-        ah = np.empty_like(ut)
-        for b in range(ut.shape[0]):
-            ah[b] = np.linalg.solve(np.eye(r) + beta * dt * dt * self.e[b] * self.Kbar, rhs[b])
-        uh = ut + beta * dt * dt * ah
+        if self.Hbar is None and self.Cbar is None:
+            rhs = self.accel(ut, s)                                  # e_b (-Kbar u~ + Bbar g^)
+            ah = np.empty_like(ut)
+            for b in range(ut.shape[0]):
+                ah[b] = np.linalg.solve(np.eye(r) + beta * dt * dt * self.e[b] * self.Kbar, rhs[b])
+            uh = ut + beta * dt * dt * ah
+        else:                                                        # Newton (reading R37)
+            uh = ut + beta * dt * dt * ckpt["ah"]
+            for b in range(ut.shape[0]):
+                u = uh[b].copy()
+                for _ in range(50):
+                    R = u - ut[b] - beta * dt * dt * self.e[b] * self.reduced_force(u[None], s[b:b + 1])[0]
+                    J = np.eye(r) + beta * dt * dt * self.e[b] * self.stiffness_jacobian(u)
+                    du = np.linalg.solve(J, -R)
+                    u = u + du
+                    if np.linalg.norm(du) <= 1e-14 * np.linalg.norm(u):
+                        break
+                else:
+                    raise RuntimeError("implicit ROM step: Newton did not converge in 50 iterations")
+                uh[b] = u
+            ah = self.accel(uh, s)
         vh = ckpt["vh"] + dt * ((1.0 - gamma) * ckpt["ah"] + gamma * ah)
         return dict(uh=uh, vh=vh, ah=ah, s=np.array(s))
 
