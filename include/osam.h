@@ -47,8 +47,11 @@ typedef struct osam_subdomain osam_subdomain; /* opaque handle */
 enum { OSAM_FOM = 0, OSAM_ROM = 1 };
 
 /* Time integrator of a subdomain (Newmark-beta, gamma = 1/2, eq:schwarz_opinf_discrete
- * P:L617-722, reading R32): explicit (beta = 0, central difference) or, for a linear OpInf ROM,
- * implicit average acceleration (beta = 1/4): (I + beta dt_i^2 e_b Kbar) a^' = e_b (-Kbar u~ + Bbar g^). */
+ * P:L617-722, reading R32): explicit (beta = 0, central difference) or, for a ROM, implicit average
+ * acceleration (beta = 1/4): linear OpInf (I + beta dt_i^2 e_b Kbar) a^' = e_b (-Kbar u~ + Bbar g^);
+ * QOpInf / COpInf by Newton per sample with the exact Jacobian (reading R37; OSAM_EUNSTABLE if it does
+ * not converge in 50 steps; OSAM_EINVAL at create if the per-sample system exceeds 200 KB of shared
+ * memory).  The FOM is explicit.                                                                      */
 enum { OSAM_EXPLICIT = 0, OSAM_IMPLICIT = 1 };
 
 /* FOM material (App. A; readings R35, R36): linear elasticity (A.1, the merged-stencil kernel K1), or the
@@ -94,7 +97,7 @@ typedef struct {
    * two bracketing source substeps, the interval start being the source's checkpoint (reading R31);
    * the convergence norm is evaluated at the interval end with dt_i (reading R33).                    */
   int32_t n_substeps;     /* 0/1 .. 4096                                                              */
-  int32_t integrator;     /* OSAM_EXPLICIT (FOM: required) | OSAM_IMPLICIT (linear ROM only)         */
+  int32_t integrator;     /* OSAM_EXPLICIT (FOM: required) | OSAM_IMPLICIT (ROM)                      */
   int32_t material;       /* FOM: OSAM_LINEAR | OSAM_SVK | OSAM_NEOHOOKEAN (ROM: must be OSAM_LINEAR) */
 } osam_subdomain_desc;
 

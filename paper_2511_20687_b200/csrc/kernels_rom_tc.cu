@@ -223,6 +223,11 @@ void launch_rom_advance_tc(const RomLaunch& L, const double* KB, double* Z, doub
     debug_check("reduce_splits_kernel", s);
     *launches += 2;
   }
+  if (L.beta > 0.0 && L.nf > 0) {  // implicit polynomial ROM: Newton per sample on u~ = Z[0:r], g^ = Z[r:]
+    launch_rom_newton(L, Z, rz, Z + r, rz, 0, rom_partial_slots(r, true), s);
+    *launches += 2;
+    return;
+  }
   // araw = [-Kbar | Bbar] Z, reduced in the epilogue
   const int S = gemm(GemmArgs{r, B, rz, KB, 1, r, Z, 1, rz, nullptr, 0}, part, s);
   tc_epilogue_kernel<<<dim3(cdiv(r, 256), B), 256, 0, s>>>(L, part, S, Z, rz, L.beta > 0.0 ? 2 : 0);

@@ -348,6 +348,162 @@ __global__ void __launch_bounds__(256) rom_implicit_kernel(const RomLaunch L, co
   }
 }
 
+// Implicit polynomial ROM (reading R37), one block per active sample: Newton on
+//   R(u) = u - u~ - beta dt^2 a(u),  a(u) = e_b O [u; g^; u^*2; u^*3],  O = [-Kbar | Bbar | -Hbar | -Cbar]
+// from u = u~ + beta dt^2 a^, Jacobian I - beta dt^2 e_b (O_u + O_f dF/du) (each thread builds its own
+// rows), Gauss-Jordan with partial pivoting in shared memory, until |du| <= 1e-14 |u| (<= 50 steps; a
+// non-converged sample writes NaN into its norm partial -> OSAM_EUNSTABLE).  Then a^' = a(u^'),
+// v^' = v^ + dt (a^ + a^')/2 and the norm partials (slot 0 of the sample, other slots 0).
+// g^: gchunks > 0 -> chunk partials gsrc[(z B + b) r_b + j] summed in order (CUDA-core path), else
+// gsrc[j + gstride b] (tensor-core path, Z rows).
+__device__ __forceinline__ double newton_block_sum(double v, double* red) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < 8; ++w) t += red[w];
+  __syncthreads();
+  return t;
+}
+
+__global__ void __launch_bounds__(256) rom_newton_kernel(const RomLaunch L, const double* __restrict__ ut_all,
+                                                         long long uts, const double* __restrict__ gsrc,
+                                                         long long gstride, int gchunks, int n_slots) {
+  extern __shared__ double sm[];
+  __shared__ double red[8];
+  __shared__ int piv;
+  const int b = blockIdx.x, r = L.r, rb = L.r_b, nf = L.nf, rz = r + rb + nf, t = threadIdx.x;
+  if (!L.active[b]) return;
+  double* u = sm;
+  double* ut = u + r;
+  double* g = ut + r;
+  double* feat = g + rb;
+  double* a = feat + nf;
+  double* J = a + r;  // [r][r + 1]
+  const int ld = r + 1;
+  const double eb = L.e[b], c = L.beta * L.dt * L.dt;
+  const long long off = (long long)r * b;
+  for (int i = t; i < r; i += 256) {
+    ut[i] = ut_all[i + uts * b];
+    u[i] = fma(c, L.ah0[off + i], ut[i]);
+  }
+  for (int j = t; j < rb; j += 256) {
+    double v = 0.0;
+    if (gchunks > 0)
+      for (int z = 0; z < gchunks; ++z) v += gsrc[((long long)z * L.B + b) * rb + j];
+    else
+      v = gsrc[j + gstride * b];
+    g[j] = v;
+  }
+  __syncthreads();
+  // a(u) into a[] (features of u first)
+  auto accel = [&]() {
+    for (int q = t; q < nf; q += 256) {
+      const int i = L.feat_idx[3 * q], j = L.feat_idx[3 * q + 1], l = L.feat_idx[3 * q + 2];
+      double v = u[i] * u[j];
+      if (l >= 0) v *= u[l];
+      feat[q] = v;
+    }
+    __syncthreads();
+    const int lane = t & 31, w = t >> 5;
+    for (int k = w; k < r; k += 8) {
+      const double* row = L.KBr + (long long)k * rz;
+      double acc = 0.0;
+      for (int j = lane; j < rz; j += 32) acc = fma(row[j], j < r ? u[j] : (j < r + rb ? g[j - r] : feat[j - r - rb]), acc);
+      acc = warp_sum(acc);
+      if (lane == 0) a[k] = eb * acc;
+    }
+    __syncthreads();
+  };
+  bool converged = false;
+  for (int it = 0; it < 50; ++it) {
+    accel();
+    // Jacobian rows and residual (thread k owns row k)
+    for (int k = t; k < r; k += 256) {
+      const double* row = L.KBr + (long long)k * rz;
+      double* Jk = J + (long long)k * ld;
+      for (int m = 0; m < r; ++m) Jk[m] = row[m];
+      for (int q = 0; q < nf; ++q) {
+        const double o = row[r + rb + q];
+        const int i = L.feat_idx[3 * q], j = L.feat_idx[3 * q + 1], l = L.feat_idx[3 * q + 2];
+        if (l < 0) {
+          Jk[i] = fma(o, u[j], Jk[i]);
+          Jk[j] = fma(o, u[i], Jk[j]);
+        } else {
+          Jk[i] = fma(o, u[j] * u[l], Jk[i]);
+          Jk[j] = fma(o, u[i] * u[l], Jk[j]);
+          Jk[l] = fma(o, u[i] * u[j], Jk[l]);
+        }
+      }
+      for (int m = 0; m < r; ++m) Jk[m] = (m == k ? 1.0 : 0.0) - c * eb * Jk[m];
+      Jk[r] = -(u[k] - ut[k] - c * a[k]);  // -R
+    }
+    __syncthreads();
+    // Gauss-Jordan with partial pivoting on [J | -R]
+    for (int k = 0; k < r; ++k) {
+      if (t == 0) {
+        int p = k;
+        for (int i = k + 1; i < r; ++i)
+          if (fabs(J[(long long)i * ld + k]) > fabs(J[(long long)p * ld + k])) p = i;
+        piv = p;
+      }
+      __syncthreads();
+      if (piv != k)
+        for (int m = t; m < ld; m += 256) {
+          const double tmp = J[(long long)k * ld + m];
+          J[(long long)k * ld + m] = J[(long long)piv * ld + m];
+          J[(long long)piv * ld + m] = tmp;
+        }
+      __syncthreads();
+      const double inv = 1.0 / J[(long long)k * ld + k];
+      __syncthreads();
+      for (int m = t; m < ld; m += 256) J[(long long)k * ld + m] *= inv;
+      __syncthreads();
+      for (long long e = t; e < (long long)r * ld; e += 256) {
+        const int i = (int)(e / ld), m = (int)(e % ld);
+        if (i != k && m != k) J[e] = fma(-J[(long long)i * ld + k], J[(long long)k * ld + m], J[e]);
+      }
+      __syncthreads();
+      for (int i = t; i < r; i += 256)
+        if (i != k) J[(long long)i * ld + k] = 0.0;
+      __syncthreads();
+    }
+    double du2 = 0.0, u2 = 0.0;
+    for (int i = t; i < r; i += 256) {
+      const double du = J[(long long)i * ld + r];
+      u[i] += du;
+      du2 = fma(du, du, du2);
+      u2 = fma(u[i], u[i], u2);
+    }
+    const double sdu = newton_block_sum(du2, red), su = newton_block_sum(u2, red);
+    if (sqrt(sdu) <= 1e-14 * sqrt(su)) {
+      converged = true;
+      break;
+    }
+  }
+  accel();  // a^' = a(u^')
+  double num = 0.0, den = 0.0;
+  for (int i = t; i < r; i += 256) {
+    const long long id = off + i;
+    const double un = u[i], an = a[i];
+    const double vn = L.vh0[id] + L.dt * (0.5 * L.ah0[id] + 0.5 * an);
+    if (L.with_norm) {
+      const double d = (un - L.uh1[id]) + L.dt * (vn - L.vh1[id]);
+      const double w = un + L.dt * vn;
+      num = fma(d, d, num);
+      den = fma(w, w, den);
+    }
+    L.uh1[id] = un;
+    L.vh1[id] = vn;
+    L.ah1[id] = an;
+  }
+  const double tn = newton_block_sum(num, red), td = newton_block_sum(den, red);
+  if (t == 0) {
+    L.partial[b] = make_double2(converged ? tn : nan(""), td);
+    for (int q = 1; q < n_slots; ++q) L.partial[(long long)q * L.B + b] = make_double2(0.0, 0.0);
+  }
+}
+
 // Minv_b = (I + c e_b Kbar)^-1 (Kbar column-major): Gauss-Jordan with partial pivoting on [M | I],
 // one block per sample (setup, once per dt_i).
 __global__ void __launch_bounds__(256) rom_minv_kernel(int r, const double* __restrict__ Kbar,
@@ -435,6 +591,19 @@ void launch_rom_minv(int r, int B, const double* Kbar, const double* e, double c
   debug_check("rom_minv_kernel", s);
 }
 
+size_t rom_newton_smem(int r, int r_b, int nf) {
+  return sizeof(double) * ((size_t)3 * r + r_b + nf + (size_t)r * (r + 1));
+}
+
+void launch_rom_newton(const RomLaunch& L, const double* ut, long long uts, const double* gsrc, long long gstride,
+                       int gchunks, int n_slots, cudaStream_t s) {
+  const size_t smem = rom_newton_smem(L.r, L.r_b, L.nf);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(rom_newton_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  rom_newton_kernel<<<L.B, 256, smem, s>>>(L, ut, uts, gsrc, gstride, gchunks, n_slots);
+  debug_check("rom_newton_kernel", s);
+}
+
 void launch_rom_implicit(const RomLaunch& L, const double* ut, long long uts, int n_slots, cudaStream_t s) {
   rom_implicit_kernel<<<L.B, 256, sizeof(double) * L.r, s>>>(L, ut, uts, n_slots);
   debug_check("rom_implicit_kernel", s);
@@ -482,6 +651,11 @@ void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches) {
   launch_rom_features(L.nf, L.B, L.feat_idx, L.ustar, L.r, L.F, L.nf, s);
   *launches += L.nf > 0;
   debug_check("rom_predict_kernel", s);
+  if (L.beta > 0.0 && L.nf > 0) {  // implicit polynomial ROM: Newton (the features above are unused)
+    launch_rom_newton(L, L.ustar, L.r, L.gh, 0, L.r_b > 0 ? L.gchunks : 0, rom_partial_slots(L.r, false), s);
+    *launches += (L.r_b > 0) + 2;
+    return;
+  }
   rom_update_kernel<<<dim3(cdiv(L.r, 8), L.B), 256, 0, s>>>(L, L.beta > 0.0 ? 2 : 0);
   debug_check("rom_update_kernel", s);
   *launches += (L.r_b > 0) + 2;

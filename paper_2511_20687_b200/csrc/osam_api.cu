@@ -1126,8 +1126,11 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
     return fail(OSAM_EINVAL, "material must be OSAM_LINEAR, OSAM_SVK or OSAM_NEOHOOKEAN");
   if (d->kind == OSAM_ROM && d->material != OSAM_LINEAR)
     return fail(OSAM_EINVAL, "a ROM has no material model (its operators are inferred)");
-  if (d->integrator == OSAM_IMPLICIT && (d->Hbar || d->Cbar))
-    return fail(OSAM_EINVAL, "implicit stepping is implemented for linear OpInf ROMs only (no Hbar/Cbar)");
+  if (d->integrator == OSAM_IMPLICIT && (d->Hbar || d->Cbar)) {  // Newton in shared memory (R37)
+    const long long r = d->r, n2 = r * (r + 1) / 2, n3 = d->Cbar ? r * (r + 1) * (r + 2) / 6 : 0;
+    if (rom_newton_smem(d->r, d->r_b, (int)(n2 + n3)) > 200 * 1024)
+      return fail(OSAM_EINVAL, "implicit polynomial ROM too large for the per-sample Newton solve (r = %d)", d->r);
+  }
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return fail(OSAM_ECUDA, "cudaGetDevice: %s (no usable GPU)", cudaGetErrorString(e));

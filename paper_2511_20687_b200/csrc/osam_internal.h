@@ -220,6 +220,10 @@ cudaError_t launch_rom_project(long long n_rows, int r, int B, const double* Phi
 void launch_gather_dofs(long long n, int B, const int* ids, const double* field, long long field_bstride,
                         long long n_nodes, double* out, cudaStream_t s);
 void launch_rom_accel(const RomLaunch& L, const double* uh, double* ah, cudaStream_t s, int* launches);
+// implicit polynomial ROM (R37): Newton per sample (rom_newton_kernel); shared memory it needs
+size_t rom_newton_smem(int r, int r_b, int nf);
+void launch_rom_newton(const RomLaunch& L, const double* ut, long long uts, const double* gsrc, long long gstride,
+                       int gchunks, int n_slots, cudaStream_t s);
 // implicit ROM finish (R32): a^' = Minv f (f in L.ah1), u^', v^', norm partials; u~ at ut (stride uts)
 void launch_rom_implicit(const RomLaunch& L, const double* ut, long long uts, int n_slots, cudaStream_t s);
 long long tc_part_size(int r, int r_b, int nf, int B, long long n_s, long long n_lift3);

@@ -395,3 +395,33 @@ def test_c2_svk_fom_with_copinf_rom(gpu):
     ops = opinf.train(cfg, I)
     _, iters, worst = run_both(gpu, cfg, 100, rom_ops=ops, checkpoints=(1,))
     print("c2 svk + COpInf worst rel L2", worst, "iters", np.unique(iters))
+
+
+def test_c2_implicit_qopinf_rom_with_explicit_fom_substeps(gpu):
+    """Torsion's pairing: explicit FOM with 2 substeps + implicit QOpInf ROM over controller step 2 dt
+    (Newton per step, reading R37), trained operators."""
+    cfg = I.config("c2")
+    cfg["rom"] = dict(cfg["rom"], order=2)
+    ops = opinf.train(cfg, I)
+    cfg = _substeps(cfg, (2, 1), ("explicit", "implicit"), 2.0)
+    _, iters, worst = run_both(gpu, cfg, 120, rom_ops=ops, checkpoints=(1,))
+    print("c2 implicit QOpInf worst rel L2", worst, "iters", np.unique(iters))
+
+
+@pytest.mark.parametrize("tc", ["1", "0"])
+def test_c5_shaped_batched_implicit_cubic_rom(gpu, monkeypatch, tc):
+    monkeypatch.setenv("OSAM_ROM_TC", tc)
+    cfg = _substeps(I.config("c5"), (1, 2), ("implicit", "explicit"), 2.0)
+    rng = np.random.default_rng(21)
+    from paper_2511_20687_b200 import problem
+    ops = {}
+    for i in (0, 1):
+        n_free, n_s = problem.dof_split(cfg, i)
+        o = I.synthetic_rom_operators(n_free, n_s, 8, 5, I.config("c5")["dt"], seed=70 + i)
+        if i == 0:
+            k = np.abs(o["Kbar"]).max()
+            o["Hbar"] = 0.02 * k / 1e-3 * rng.standard_normal((8, opinf.n_poly(8, 2))) / 36
+            o["Cbar"] = 0.02 * k / 1e-6 * rng.standard_normal((8, opinf.n_poly(8, 3))) / 120
+        ops[i] = o
+    _, iters, worst = run_both(gpu, cfg, 40, rom_ops=ops, checkpoints=(1,))
+    print("c5-shaped implicit cubic tc", tc, "worst rel L2", worst, "iters", np.unique(iters))
