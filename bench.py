@@ -367,7 +367,7 @@ def run_ours(args):
             "schwarz_iters_per_step": float(iters.max(axis=1).mean()),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(), "kernel": "K1 fom_advance",
-                         "bytes_model": "32 B/DOF/sweep (read q, w; write q, w) + 8 B/DOF from sweep 2 (read previous w), two-vector form (SURVEY 8(d), DESIGN.md R30)",
+                         "bytes_model": "32 B/DOF/sweep (read q, w; write q, w) + from sweep 2 8 B per DOF within one node layer of a Schwarz face (read previous w'; elsewhere the norm term is exactly 0, DESIGN.md R38), two-vector form (SURVEY 8(d), DESIGN.md R30)",
                          "k1_ms_per_launch": k1_ms_per_launch,
                          "k1_share_of_step": prof["k1_ms"] / prof_ms,
                          "timing": f"K1 CUDA events over {prof_steps} steps in profiling mode (host-driven "

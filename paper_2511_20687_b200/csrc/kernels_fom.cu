@@ -48,7 +48,7 @@ constexpr int TY = OSAM_TY;
 constexpr int NT = TX * TY;
 constexpr int NWARP = NT / 32;
 #ifndef OSAM_ZC
-#define OSAM_ZC 12
+#define OSAM_ZC 16
 #endif
 constexpr int ZC = OSAM_ZC;  // target z-planes per block (balanced split)
 constexpr int XF_BLOCK = 128;
@@ -333,8 +333,21 @@ struct TileGrid {
   __device__ __forceinline__ int count() const { return tx * ty * tz; }
 };
 
-__device__ __forceinline__ TileGrid tile_grid(const Geom& g) {
-  return TileGrid{(g.nn[0] + TX - 1) / TX, (g.nn[1] + TY - 1) / TY, (g.nn[2] + ZC - 1) / ZC};
+// x-tile columns: when the last node column x = nx sits alone in a tile (nx a multiple of TX) and the
+// x+ face is fully constrained (Dirichlet in every component, or Schwarz), that column only copies
+// its prescribed values (Q' = X, W' = a = 0): it is left out of the tiled grid and handled by
+// xlast_copy_kernel (c4's 257^3 FOM: 8 instead of 9 columns).
+__host__ __device__ __forceinline__ bool xlast_excluded(const Geom& g, const Faces& f) {
+  const int nx = g.nn[0] - 1;
+  return nx > 0 && nx % TX == 0 && (f.dir[1] == 7 || f.sw[1]);
+}
+
+__host__ __device__ __forceinline__ int tile_cols(const Geom& g, const Faces& f) {
+  return xlast_excluded(g, f) ? (g.nn[0] - 1) / TX : (g.nn[0] + TX - 1) / TX;
+}
+
+__device__ __forceinline__ TileGrid tile_grid(const Geom& g, const Faces& f) {
+  return TileGrid{tile_cols(g, f), (g.nn[1] + TY - 1) / TY, (g.nn[2] + ZC - 1) / ZC};
 }
 
 // Geometry of one tile as the producer and the consumers see it.
@@ -359,12 +372,14 @@ __device__ __forceinline__ TileGeo tile_geo(const Geom& g, const TileGrid& G, in
 struct Tile {
   int i, j;
   int kbeg, kend, nplanes;
-  unsigned flags;  // bit 0 active, bit 1 x-face lane, bit 2 writer, bits 3-4 cy (class of row j)
+  unsigned flags;  // bit 0 active, bit 1 x-face lane, bit 2 writer, bits 3-4 cy (class of row j),
+                   // bit 5 the tile reads the previous iterate (norm numerator, see needs_prev)
   long long id0;   // node index of (i, j, 0)
   __device__ __forceinline__ bool active() const { return flags & 1u; }
   __device__ __forceinline__ bool xface() const { return flags & 2u; }
   __device__ __forceinline__ bool writer() const { return flags & 4u; }
   __device__ __forceinline__ int cy() const { return (int)((flags >> 3) & 3u); }
+  __device__ __forceinline__ bool prev() const { return flags & 32u; }
 };
 
 // staged positions of this thread: own node, (-1,-1) neighbour, W tile position
@@ -376,15 +391,35 @@ struct Maps {
   const CUtensorMap *x, *w, *wp;
 };
 
+// Does this tile read the previous iterate (W'_prev, or z_prev) for the convergence numerator?
+// Within a controller step the stencil input u* = X changes between Schwarz iterations only at
+// Schwarz DOFs (the predictor and the Dirichlet values are fixed, R30), so a node farther than one
+// layer from every Schwarz face gets a bitwise identical a' and w' in every iteration and its
+// numerator term is exactly 0: only tiles holding a node within one layer of a Schwarz face need it
+// (R38).  Multi-substep intervals (z-form, z_out set) change u everywhere: always.
+__device__ __forceinline__ bool needs_prev(const FomLaunch& L, const TileGeo& P) {
+  if (!L.with_norm) return false;
+  if (L.z_out) return true;
+  const Geom& g = L.g;
+  const int lo[3] = {P.x0 + 2, P.y0 + 1, P.kbeg};
+  const int hi[3] = {min(P.x0 + 1 + TX, g.nn[0] - 1), min(P.y0 + TY, g.nn[1] - 1), P.kend};
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    const int ax = f >> 1;
+    if (L.f.sw[f] && ((f & 1) ? hi[ax] >= g.nn[ax] - 2 : lo[ax] <= 1)) return true;
+  }
+  return false;
+}
+
 // stage layout: X plane (halo box) | W plane (tile box) | W'_prev plane (tile box)
-__device__ __forceinline__ void issue_plane(const FomLaunch& L, const TileGeo& P, int it, int s, unsigned char* ring,
+__device__ __forceinline__ void issue_plane(const TileGeo& P, bool wp, int it, int s, unsigned char* ring,
                                             unsigned long long* full, const Maps& M) {
   unsigned char* st = ring + (size_t)s * STAGE_BYTES;
   const int m = P.kbeg - 1 + it;
-  mbar_expect_tx(&full[s], ARR_BYTES + (L.with_norm ? 2 : 1) * W_BYTES);
+  mbar_expect_tx(&full[s], ARR_BYTES + (wp ? 2 : 1) * W_BYTES);
   tma_load_4d(st, M.x, P.x0, P.y0, m, 0, &full[s]);
   tma_load_4d(st + ARR_STRIDE, M.w, P.x0 + 2, P.y0 + 1, m, 0, &full[s]);
-  if (L.with_norm) tma_load_4d(st + ARR_STRIDE + W_BYTES, M.wp, P.x0 + 2, P.y0 + 1, m, 0, &full[s]);
+  if (wp) tma_load_4d(st + ARR_STRIDE + W_BYTES, M.wp, P.x0 + 2, P.y0 + 1, m, 0, &full[s]);
 }
 
 // Producer cursor (thread 0 only, in shared memory): the next plane to load, possibly in a later
@@ -393,17 +428,21 @@ struct Prod {
   int t;       // tile (>= ntiles: done)
   int it;      // plane within the tile
   int issued;  // planes issued so far (all tiles)
+  int wp;      // the tile stages the previous iterate (needs_prev)
   TileGeo P;
 };
 
 __device__ __forceinline__ void prod_issue(const FomLaunch& L, const TileGrid& G, Prod& pr, unsigned char* ring,
                                            unsigned long long* full, const Maps& M) {
-  issue_plane(L, pr.P, pr.it, pr.issued % NSTAGE, ring, full, M);
+  issue_plane(pr.P, pr.wp != 0, pr.it, pr.issued % NSTAGE, ring, full, M);
   ++pr.issued;
   if (++pr.it == pr.P.nplanes) {
     pr.it = 0;
     pr.t += gridDim.x;
-    if (pr.t < G.count()) pr.P = tile_geo(L.g, G, pr.t);
+    if (pr.t < G.count()) {
+      pr.P = tile_geo(L.g, G, pr.t);
+      pr.wp = needs_prev(L, pr.P);
+    }
   }
 }
 
@@ -478,9 +517,10 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
           const double wn = fma(L.cw, an, w0);
           qo[c * np] = fma(L.cq, wn, x);
           wp[c * np] = wn;
-          if (L.with_norm) {
+          if (L.with_norm) {  // outside the band q = w' itself: d == 0 exactly (R38)
             const double w = fma(L.dt, fma(L.cv, an, w0), x);
-            const double d = ZN ? w - qw[c * WPL] : 0.5 * L.dt * (wn - qw[c * WPL]);
+            const double q = T.prev() ? qw[c * WPL] : (ZN ? w : wn);
+            const double d = ZN ? w - q : 0.5 * L.dt * (wn - q);
             num = fma(d, d, num);
             den = fma(w, w, den);
           }
@@ -500,7 +540,8 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
             qn = fma(L.cq, wn, x);
             if (L.with_norm) {
               const double w = fma(L.dt, fma(L.cv, an, w0), x);
-              const double d = ZN ? w - qw[c * WPL] : 0.5 * L.dt * (wn - qw[c * WPL]);
+              const double q = T.prev() ? qw[c * WPL] : (ZN ? w : wn);
+              const double d = ZN ? w - q : 0.5 * L.dt * (wn - q);
               num = fma(d, d, num);
               den = fma(w, w, den);
             }
@@ -536,7 +577,7 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
   const Geom& g = L.g;
   const int nx = g.nn[0] - 1, ny = g.nn[1] - 1;
   const Maps M{&tmx, &tmw, &tmwp};
-  const TileGrid G = tile_grid(g);
+  const TileGrid G = tile_grid(g, L.f);
   const bool lead = threadIdx.x + threadIdx.y == 0;
 
   if (lead) {
@@ -550,6 +591,7 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
     pr->issued = 0;
     if (pr->t < G.count()) {
       pr->P = tile_geo(g, G, pr->t);
+      pr->wp = needs_prev(L, pr->P);
       for (int p = 0; p < NSTAGE - 2 && pr->t < G.count(); ++p) prod_issue(L, G, *pr, ring, full, M);
     }
   }
@@ -567,7 +609,8 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
     const bool xface = (T.i == 0) || (T.i == nx);
     const int xsd = T.i == 0 ? 0 : 1;
     const bool writer = active && (!xface || L.f.dir[xsd] == 7 || L.f.sw[xsd]);
-    T.flags = (active ? 1u : 0u) | (xface ? 2u : 0u) | (writer ? 4u : 0u) | ((unsigned)axis_class(T.j, g.nn[1]) << 3);
+    T.flags = (active ? 1u : 0u) | (xface ? 2u : 0u) | (writer ? 4u : 0u) | ((unsigned)axis_class(T.j, g.nn[1]) << 3) |
+              (needs_prev(L, P) ? 32u : 0u);
     T.kbeg = P.kbeg;
     T.kend = P.kend;
     T.nplanes = P.nplanes;
@@ -744,13 +787,28 @@ __global__ void zero_constrained_kernel(Geom g, Faces F, double* u, double* w) {
 
 inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
-long long tile_count(const Geom& g) {
-  return (long long)cdiv(g.nn[0], TX) * cdiv(g.nn[1], TY) * cdiv(g.nn[2], ZC);
+long long tile_count(const Geom& g, const Faces& f) {
+  return (long long)tile_cols(g, f) * cdiv(g.nn[1], TY) * cdiv(g.nn[2], ZC);
+}
+
+// the excluded x+ column (see xlast_excluded): Q' = X, W' = 0, a = 0 on every node of the face
+__global__ void xlast_copy_kernel(const FomLaunch L) {
+  const Geom& g = L.g;
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)g.nn[1] * g.nn[2]) return;
+  const int j = (int)(t % g.nn[1]), k = (int)(t / g.nn[1]);
+  const long long id = gidx(g, g.nn[0] - 1, j, k);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    if (L.q_out) L.q_out[c * g.npad + id] = L.x[c * g.npad + id];
+    L.w_out[c * g.npad + id] = 0.0;
+    if (L.a_out) L.a_out[c * g.npad + id] = 0.0;
+  }
 }
 
 // CTAs of the tiled kernel: one per tile, or (OSAM_PERSISTENT=1) as many as fit on the device at
 // once, each looping over tiles
-int tiled_ctas(const Geom& g) {
+int tiled_ctas(const Geom& g, const Faces& f) {
   static const bool persistent = getenv("OSAM_PERSISTENT") && getenv("OSAM_PERSISTENT")[0] == '1';
   static bool attr = false;
   if (!attr) {
@@ -758,7 +816,7 @@ int tiled_ctas(const Geom& g) {
     cudaFuncSetAttribute(fom_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TILED);
     attr = true;
   }
-  if (!persistent) return (int)tile_count(g);
+  if (!persistent) return (int)tile_count(g, f);
   static int resident = 0;
   if (resident == 0) {
     int dev = 0, sms = 0, per_sm = 0;
@@ -767,7 +825,7 @@ int tiled_ctas(const Geom& g) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fom_tiled_kernel<false>, NT, SMEM_TILED);
     resident = std::max(1, sms * std::max(1, per_sm));
   }
-  return (int)std::min<long long>(resident, tile_count(g));
+  return (int)std::min<long long>(resident, tile_count(g, f));
 }
 
 int xface_sides(const Faces& f) {
@@ -1084,7 +1142,7 @@ int nl_ctas(const Geom& g) {
 
 }  // namespace
 
-int fom_partial_slots(const Geom& g, const Faces& f) { return tiled_ctas(g) + (int)xface_blocks(g, f); }
+int fom_partial_slots(const Geom& g, const Faces& f) { return tiled_ctas(g, f) + (int)xface_blocks(g, f); }
 
 int fom_nl_partial_slots(const Geom& g) { return nl_ctas(g); }
 
@@ -1110,7 +1168,7 @@ void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUt
     launch_fom_advance_nl(L, s, launches);
     return;
   }
-  const int n_int = tiled_ctas(L.g);
+  const int n_int = tiled_ctas(L.g, L.f);
   if (L.z_out)  // last substep of a multi-substep interval: z = u + dt v out, norm from z - z_prev (R33)
     fom_tiled_kernel<true><<<n_int, dim3(TX, TY), SMEM_TILED, s>>>(L, st, *tmx, *tmw, *tmwp);
   else
@@ -1121,6 +1179,11 @@ void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUt
   if (xb > 0) {
     fom_xface_kernel<<<xb, XF_BLOCK, 0, s>>>(L, n_int, xface_sides(L.f));
     debug_check("fom_xface_kernel", s);
+    ++*launches;
+  }
+  if (xlast_excluded(L.g, L.f)) {
+    xlast_copy_kernel<<<cdiv((long long)L.g.nn[1] * L.g.nn[2], 256), 256, 0, s>>>(L);
+    debug_check("xlast_copy_kernel", s);
     ++*launches;
   }
 }

@@ -360,6 +360,10 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
         s.faces.dir[f] = s.dirichlet[f];
         s.faces.sw[f] = s.face_src[f] >= 0;
       }
+      long long inner = 1;  // nodes farther than one layer from every Schwarz face
+      for (int a = 0; a < 3; ++a)
+        inner *= std::max(0, s.g.nn[a] - 2 * (int)s.faces.sw[2 * a] - 2 * (int)s.faces.sw[2 * a + 1]);
+      s.n_band = s.n_nodes - inner;
       TRY(dalloc(&s.scratch_partial, (size_t)fom_slots(s)));
       continue;
     }
@@ -798,7 +802,9 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
       launch_fom_advance(L, d.stencil, &d.tmap[c], &d.tmapw[c], &d.tmapw[x], st, launches);
       if (fom_k && g_prof) CK(cudaEventRecord(G.ev[2 * *fom_k + 1], st));
       if (fom_k) ++*fom_k;
-      g_k1_bytes += (32.0 + (with_norm ? 8.0 : 0.0)) * 3.0 * (double)d.n_nodes;
+      // algorithmic bytes: read q, w and write q', w' (32 B/DOF) + the previous w' of the DOFs within one
+      // layer of a Schwarz face from sweep 2 on (R38)
+      g_k1_bytes += 32.0 * 3.0 * (double)d.n_nodes + (with_norm ? 8.0 * 3.0 * (double)d.n_band : 0.0);
       ++g_k1_launches;
       slot += fom_slots(d);
     } else {

@@ -92,6 +92,8 @@ struct Sub {
   int cur = 0, ux = 1, fr = 2;
   double* st[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
   double* zbuf = nullptr;  // n_sub > 1: z = u + dt_i v of the last iterate's last substep (norm, R33)
+  long long n_band = 0;    // nodes within one layer of a Schwarz face (the only ones whose norm term can
+                           // change between iterations, R38)
   CUtensorMap tmapz;
   double w_dt = 0.0;
   Faces faces;

@@ -425,3 +425,25 @@ def test_c5_shaped_batched_implicit_cubic_rom(gpu, monkeypatch, tc):
         ops[i] = o
     _, iters, worst = run_both(gpu, cfg, 40, rom_ops=ops, checkpoints=(1,))
     print("c5-shaped implicit cubic tc", tc, "worst rel L2", worst, "iters", np.unique(iters))
+
+
+def test_xlast_column_excluded_c1_variant(gpu):
+    """nx a multiple of the 32-node tile and a Schwarz x+ face: the last node column leaves the tiled grid
+    (xlast_copy_kernel writes its prescribed values)."""
+    import copy
+    cfg = copy.deepcopy(I.config("c1"))
+    cfg["subdomains"][0] = dict(cfg["subdomains"][0], nel=(32, 5, 5))
+    cfg["dt"] = I._dt(cfg["subdomains"])
+    _, iters, worst = run_both(gpu, cfg, 60, checkpoints=(1,))
+    print("c1 nx=32 worst rel L2", worst)
+
+
+def test_xlast_column_excluded_c4_topology(gpu):
+    """c4 coarsened 8x: FOM 32^3 elements between two ROMs (stand-in operators), both FOM x-faces Schwarz."""
+    from paper_2511_20687_b200 import problem
+    cfg = I.scaled(I.config("c4"), 8.0)
+    assert cfg["subdomains"][1]["nel"][0] == 32
+    cfg["rom"] = dict(cfg["rom"], r=12)
+    ops = problem.synthetic_rom_ops(cfg, r_b=8)
+    _, iters, worst = run_both(gpu, cfg, 6, rom_ops=ops, checkpoints=(1,))
+    print("c4/8 worst rel L2", worst, "iters", np.unique(iters))
