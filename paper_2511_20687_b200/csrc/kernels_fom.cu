@@ -51,7 +51,7 @@ constexpr int NWARP = NT / 32;
 #define OSAM_ZC 16
 #endif
 constexpr int ZC = OSAM_ZC;  // target z-planes per block (balanced split)
-constexpr int XF_BLOCK = 128;
+constexpr int XF_BLOCK = 256;  // x-face work runs in extra CTAs of the tiled kernel (256 threads)
 
 __device__ __forceinline__ long long gidx(const Geom& g, int i, int j, int k) {
   return i + (long long)g.px * j + g.plane * k;
@@ -333,6 +333,14 @@ struct TileGrid {
   __device__ __forceinline__ int count() const { return tx * ty * tz; }
 };
 
+// x-faces whose nodes have free DOFs (bit 0: x = 0, bit 1: x = nx): their forces come from xface_body
+__host__ __device__ __forceinline__ int xface_sides(const Faces& f) {
+  int m = 0;
+  for (int s = 0; s < 2; ++s)
+    if (!(f.dir[s] == 7 || f.sw[s])) m |= 1 << s;
+  return m;
+}
+
 // x-tile columns: when the last node column x = nx sits alone in a tile (nx a multiple of TX) and the
 // x+ face is fully constrained (Dirichlet in every component, or Schwarz), that column only copies
 // its prescribed values (Q' = X, W' = a = 0): it is left out of the tiled grid and handled by
@@ -438,7 +446,7 @@ __device__ __forceinline__ void prod_issue(const FomLaunch& L, const TileGrid& G
   ++pr.issued;
   if (++pr.it == pr.P.nplanes) {
     pr.it = 0;
-    pr.t += gridDim.x;
+    pr.t += L.n_tile_ctas;
     if (pr.t < G.count()) {
       pr.P = tile_geo(L.g, G, pr.t);
       pr.wp = needs_prev(L, pr.P);
@@ -561,6 +569,8 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
   for (int c = 0; c < 3; ++c) acc[SC][c] = 0.0;
 }
 
+__device__ __noinline__ void xface_body(const FomLaunch& L, int side_mask, int blk, int tid, int slot);
+
 #ifndef OSAM_MINB
 #define OSAM_MINB 2
 #endif
@@ -574,6 +584,10 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + NSTAGE * STAGE_BYTES);
   unsigned long long* empty = full + NSTAGE;
   Prod* pr = reinterpret_cast<Prod*>(empty + NSTAGE);
+  if ((int)blockIdx.x >= L.n_tile_ctas) {  // x-face CTAs (after the tile CTAs)
+    xface_body(L, xface_sides(L.f), blockIdx.x - L.n_tile_ctas, threadIdx.x + TX * threadIdx.y, blockIdx.x);
+    return;
+  }
   const Geom& g = L.g;
   const int nx = g.nn[0] - 1, ny = g.nn[1] - 1;
   const Maps M{&tmx, &tmw, &tmwp};
@@ -600,7 +614,7 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
   double acc[3][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
   double num = 0.0, den = 0.0;
   int gi = 0;
-  for (int tile = blockIdx.x; tile < G.count(); tile += gridDim.x) {
+  for (int tile = blockIdx.x; tile < G.count(); tile += L.n_tile_ctas) {
     const TileGeo P = tile_geo(g, G, tile);
     Tile T;
     T.i = P.x0 + 2 + (int)threadIdx.x;
@@ -638,13 +652,15 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
 // plane oz = sub - 1 (6 positions: 2 in x, 3 in y; class-table stencil), the partial forces are summed
 // in the order sub = 0, 1, 2 by shuffles and lane sub = 0 finishes the node.  side_mask bit 0: face
 // x = 0, bit 1: face x = nx.
-__global__ void __launch_bounds__(XF_BLOCK) fom_xface_kernel(const FomLaunch L, int slot0, int side_mask) {
+// Runs as the extra CTAs of the tiled kernel (blockIdx >= the tile CTAs), so it fills the tiled
+// kernel's last wave instead of costing a launch of its own; blk = x-face block, slot = its partial slot.
+__device__ __noinline__ void xface_body(const FomLaunch& L, int side_mask, int blk, int tid, int slot) {
   const Geom& g = L.g;
   const long long np = g.npad;
   const long long nf = (long long)g.nn[1] * g.nn[2];
   const int nsides = (side_mask & 1) + ((side_mask >> 1) & 1);
-  const long long t = (blockIdx.x * (long long)XF_BLOCK + threadIdx.x) >> 2;
-  const int sub = threadIdx.x & 3;
+  const long long t = (blk * (long long)XF_BLOCK + tid) >> 2;
+  const int sub = tid & 3;
   const int nx = g.nn[0] - 1;
   double num = 0.0, den = 0.0;
   const bool valid = t < nsides * nf;
@@ -708,7 +724,7 @@ __global__ void __launch_bounds__(XF_BLOCK) fom_xface_kernel(const FomLaunch L, 
       if (L.a_out) L.a_out[c * np + id] = an;
     }
   }
-  block_partial<XF_BLOCK>(num, den, L.partial, slot0 + blockIdx.x);
+  block_partial<XF_BLOCK>(num, den, L.partial, slot);
 }
 
 __device__ __forceinline__ void surface_node(const Geom& g, long long t, int* i, int* j, int* k) {
@@ -828,12 +844,7 @@ int tiled_ctas(const Geom& g, const Faces& f) {
   return (int)std::min<long long>(resident, tile_count(g, f));
 }
 
-int xface_sides(const Faces& f) {
-  int m = 0;
-  for (int s = 0; s < 2; ++s)
-    if (!(f.dir[s] == 7 || f.sw[s])) m |= 1 << s;
-  return m;
-}
+
 
 unsigned xface_blocks(const Geom& g, const Faces& f) {
   const int m = xface_sides(f);
@@ -1168,19 +1179,15 @@ void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUt
     launch_fom_advance_nl(L, s, launches);
     return;
   }
-  const int n_int = tiled_ctas(L.g, L.f);
+  FomLaunch Lt = L;
+  Lt.n_tile_ctas = tiled_ctas(L.g, L.f);
+  const int grid = Lt.n_tile_ctas + (int)xface_blocks(L.g, L.f);  // tile CTAs, then x-face CTAs
   if (L.z_out)  // last substep of a multi-substep interval: z = u + dt v out, norm from z - z_prev (R33)
-    fom_tiled_kernel<true><<<n_int, dim3(TX, TY), SMEM_TILED, s>>>(L, st, *tmx, *tmw, *tmwp);
+    fom_tiled_kernel<true><<<grid, dim3(TX, TY), SMEM_TILED, s>>>(Lt, st, *tmx, *tmw, *tmwp);
   else
-    fom_tiled_kernel<false><<<n_int, dim3(TX, TY), SMEM_TILED, s>>>(L, st, *tmx, *tmw, *tmwp);
+    fom_tiled_kernel<false><<<grid, dim3(TX, TY), SMEM_TILED, s>>>(Lt, st, *tmx, *tmw, *tmwp);
   debug_check("fom_tiled_kernel", s);
   ++*launches;
-  const unsigned xb = xface_blocks(L.g, L.f);
-  if (xb > 0) {
-    fom_xface_kernel<<<xb, XF_BLOCK, 0, s>>>(L, n_int, xface_sides(L.f));
-    debug_check("fom_xface_kernel", s);
-    ++*launches;
-  }
   if (xlast_excluded(L.g, L.f)) {
     xlast_copy_kernel<<<cdiv((long long)L.g.nn[1] * L.g.nn[2], 256), 256, 0, s>>>(L);
     debug_check("xlast_copy_kernel", s);

@@ -164,6 +164,7 @@ struct FomLaunch {
   int with_norm;       // 1 from Schwarz iteration 2 on
   double2* partial;    // per-block (num, den)
   int material;        // OSAM_LINEAR (K1) | OSAM_SVK | OSAM_NEOHOOKEAN (NL1)
+  int n_tile_ctas;     // K1: CTAs that own tiles (set by launch_fom_advance; the rest do x-face work)
   double mat_lam, mat_mu, mat_kappa;
 };
 // Number of partial slots a K1 launch writes (tiled blocks + x-face blocks).
