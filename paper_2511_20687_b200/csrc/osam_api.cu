@@ -239,11 +239,19 @@ struct Group {
   cudaStream_t cap_stream = nullptr;  // legacy default stream, which cannot be captured)
   std::map<GraphKey, cudaGraphExec_t> graphs;
   int launches_per_sweep = 0;  // kernels of one sweep (launch accounting in graph mode)
+  // FOM advances off the exchange's critical path (enqueue_sweep): one side stream and a fork / join
+  // event pair per subdomain, in two sets (sweep 1 / the while-loop body: the body is captured while the
+  // step graph's capture is still open, and a stream that joined one capture cannot join another)
+  std::vector<cudaStream_t> side;
+  std::vector<cudaEvent_t> fork_ev, join_ev;
   int launches_begin = 1;      // kernels before sweep 1 (step_begin [+ trace slot 0])
   bool trace = false;          // some subdomain takes several substeps: transfers through traces + Xi
   int ctl_len() const { return 2 + 2 * B + 4; }
   ~Group() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (auto x : side) cudaStreamDestroy(x);
+    for (auto e : fork_ev) cudaEventDestroy(e);
+    for (auto e : join_ev) cudaEventDestroy(e);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (cap_main) cudaStreamDestroy(cap_main);
     dfree(partial);
@@ -755,6 +763,22 @@ RomLaunch rom_launch(const Sub& d, double* const* in, double* const* out, const 
 int enqueue_sweep_trace(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool first, cudaStream_t st,
                         int* launches, int* fom_k);
 
+// side streams / events of the parallel FOM advances (created outside any stream capture)
+int ensure_side(Group& G) {
+  const int n = 2 * (int)G.sds.size();
+  while ((int)G.side.size() < n) {
+    cudaStream_t x;
+    cudaEvent_t a, b;
+    CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    G.side.push_back(x);
+    G.fork_ev.push_back(a);
+    G.join_ev.push_back(b);
+  }
+  return OSAM_OK;
+}
+
 int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool first, cudaStream_t st, int* launches,
                   int* fom_k) {
   if (G.trace) return enqueue_sweep_trace(G, cfg, ctl, first, st, launches, fom_k);
@@ -763,6 +787,15 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
   const int n_sd = (int)subs.size();
   const int B = G.B;
   int slot = 0;
+  // In the explicit scheme a FOM iterate's displacement is its stencil input X (R30), so no transfer
+  // reads a FOM advance's output: each FOM advance forks onto a side stream once its Schwarz values are
+  // in and joins before the convergence test (parallel graph branches; their tails overlap).  Profiling
+  // mode (per-launch K1 events) and OSAM_SERIAL_K1=1 keep them on the main stream.
+  static const bool serial_env = getenv("OSAM_SERIAL_K1") && getenv("OSAM_SERIAL_K1")[0] == '1';
+  const bool par = !g_prof && !serial_env;
+  const int set = first ? 0 : n_sd;
+  if (par && (int)G.side.size() < 2 * n_sd) return fail(OSAM_ECUDA, "internal: side streams not created");
+  std::vector<int> joins;
   for (int i = 0; i < n_sd; ++i) {
     Sub& d = *subs[i];
     for (const XferMap& m : d.maps) {
@@ -798,9 +831,17 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
       const int c = d.cur, x = d.ux;
       const FomLaunch L = fom_launch(d, d.st[c][0], d.st[c][1], d.st[x][0], d.st[x][1], cfg.dt, cfg.dt,
                                      0.5 * cfg.dt, cfg.dt, with_norm, G.partial + (size_t)slot * B, nullptr);
+      cudaStream_t ks = st;
+      if (par) {
+        CK(cudaEventRecord(G.fork_ev[set + i], st));
+        CK(cudaStreamWaitEvent(G.side[set + i], G.fork_ev[set + i], 0));
+        ks = G.side[set + i];
+        joins.push_back(set + i);
+      }
       if (fom_k && g_prof) CK(cudaEventRecord(G.ev[2 * *fom_k], st));
-      launch_fom_advance(L, d.stencil, &d.tmap[c], &d.tmapw[c], &d.tmapw[x], st, launches);
+      launch_fom_advance(L, d.stencil, &d.tmap[c], &d.tmapw[c], &d.tmapw[x], ks, launches);
       if (fom_k && g_prof) CK(cudaEventRecord(G.ev[2 * *fom_k + 1], st));
+      if (par) CK(cudaEventRecord(G.join_ev[set + i], ks));
       if (fom_k) ++*fom_k;
       // algorithmic bytes: read q, w and write q', w' (32 B/DOF) + the previous w' of the DOFs within one
       // layer of a Schwarz face from sweep 2 on (R38)
@@ -824,6 +865,7 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
       slot += rom_partial_slots(d.r, d.use_tc);
     }
   }
+  for (int i : joins) CK(cudaStreamWaitEvent(st, G.join_ev[i], 0));  // every FOM advance before the test
   launch_finalize(ctl, G.partial, G.n_slots, B, cfg.min_iters, cfg.tol_rel, cfg.tol_abs, st);
   *launches += 2;
   return OSAM_OK;
@@ -982,6 +1024,7 @@ int controller_step_host(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t st)
     }
   const Ctl ctl = G.ctl(cfg.max_iters);
   int launches = 0;
+  TRY(ensure_side(G));
   launch_step_begin(ctl, G.B, st);
   ++launches;
   if (G.trace) TRY(enqueue_trace_begin(G, st, &launches));
@@ -1072,6 +1115,7 @@ int step_graph(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t, cudaGraphExe
   }
   if (!G.cap_stream) CK(cudaStreamCreateWithFlags(&G.cap_stream, cudaStreamNonBlocking));
   if (!G.cap_main) CK(cudaStreamCreateWithFlags(&G.cap_main, cudaStreamNonBlocking));
+  TRY(ensure_side(G));
   cudaGraph_t graph = nullptr;
   int launches = 0;
   const int rc = step_graph_capture(G, cfg, G.cap_main, &graph, &launches);
