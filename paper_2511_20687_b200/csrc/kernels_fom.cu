@@ -42,16 +42,16 @@ namespace {
 
 constexpr int TX = 32;
 #ifndef OSAM_TY
-#define OSAM_TY 8
+#define OSAM_TY 4
 #endif
 constexpr int TY = OSAM_TY;
 constexpr int NT = TX * TY;
 constexpr int NWARP = NT / 32;
 #ifndef OSAM_ZC
-#define OSAM_ZC 16
+#define OSAM_ZC 24
 #endif
 constexpr int ZC = OSAM_ZC;  // target z-planes per block (balanced split)
-constexpr int XF_BLOCK = 256;  // x-face work runs in extra CTAs of the tiled kernel (256 threads)
+constexpr int XF_BLOCK = NT;  // x-face work runs in extra CTAs of the tiled kernel (same block)
 
 __device__ __forceinline__ long long gidx(const Geom& g, int i, int j, int k) {
   return i + (long long)g.px * j + g.plane * k;
@@ -572,7 +572,7 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
 __device__ __noinline__ void xface_body(const FomLaunch& L, int side_mask, int blk, int tid, int slot);
 
 #ifndef OSAM_MINB
-#define OSAM_MINB 2
+#define OSAM_MINB 4
 #endif
 template <bool ZN>
 __global__ void __launch_bounds__(NT, OSAM_MINB)
