@@ -1181,6 +1181,15 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
     if (rom_newton_smem(d->r, d->r_b, (int)(n2 + n3)) > 200 * 1024)
       return fail(OSAM_EINVAL, "implicit polynomial ROM too large for the per-sample Newton solve (r = %d)", d->r);
   }
+  if (d->kind == OSAM_ROM) {  // ROM descriptor checks (host-side, before any CUDA call)
+    if (d->r < 1 || d->r_b < 0 || d->batch < 1) return fail(OSAM_EINVAL, "ROM needs r >= 1, r_b >= 0, batch >= 1");
+    if (!d->Phi || !d->Kbar || (d->r_b > 0 && (!d->Phi_s || !d->Bbar)))
+      return fail(OSAM_EINVAL, "ROM operator pointer is NULL");
+    if (d->n_free < d->r || d->n_s < 0) return fail(OSAM_EINVAL, "ROM: n_free < r or n_s < 0");
+    if (d->Cbar && !d->Hbar) return fail(OSAM_EINVAL, "Cbar (cubic OpInf) requires Hbar (quadratic term)");
+  } else if (d->batch > 1) {
+    return fail(OSAM_EINVAL, "a FOM subdomain has batch 1");
+  }
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return fail(OSAM_ECUDA, "cudaGetDevice: %s (no usable GPU)", cudaGetErrorString(e));
@@ -1227,7 +1236,6 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
     s.inv_mass[q] = 1.0 / (s.mass_e * ((q & 1) ? 2.0 : 1.0) * ((q & 2) ? 2.0 : 1.0) * ((q & 4) ? 2.0 : 1.0));
   std::memset(&s.faces, 0, sizeof s.faces);
   if (s.kind == OSAM_FOM) {
-    if (d->batch > 1) return fail(OSAM_EINVAL, "a FOM subdomain has batch 1");
     s.batch = 1;
     std::vector<double> tab;
     stencil_table(g.h, s.lam, s.mu, tab);
@@ -1314,10 +1322,6 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
       }
     }
   } else {
-    if (d->r < 1 || d->r_b < 0 || d->batch < 1) return fail(OSAM_EINVAL, "ROM needs r >= 1, r_b >= 0, batch >= 1");
-    if (!d->Phi || !d->Kbar || (d->r_b > 0 && (!d->Phi_s || !d->Bbar)))
-      return fail(OSAM_EINVAL, "ROM operator pointer is NULL");
-    if (d->n_free < d->r || d->n_s < 0) return fail(OSAM_EINVAL, "ROM: n_free < r or n_s < 0");
     s.r = d->r;
     s.r_b = d->r_b;
     s.batch = d->batch;
@@ -1327,7 +1331,6 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
       s.h_Bbar.assign(d->Bbar, d->Bbar + (size_t)d->r * d->r_b);
     }
     s.h_Kbar.assign(d->Kbar, d->Kbar + (size_t)d->r * d->r);
-    if (d->Cbar && !d->Hbar) return fail(OSAM_EINVAL, "Cbar (cubic OpInf) requires Hbar (quadratic term)");
     s.order = d->Cbar ? 3 : (d->Hbar ? 2 : 1);
     const long long n2 = (long long)d->r * (d->r + 1) / 2, n3 = (long long)d->r * (d->r + 1) * (d->r + 2) / 6;
     if (s.order >= 2) s.h_Hbar.assign(d->Hbar, d->Hbar + (size_t)d->r * n2);

@@ -50,3 +50,45 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".h", ".cpp")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="libosam.so not built")
+@pytest.mark.parametrize("case", ["fom_implicit", "rom_material", "bad_material", "neg_substeps", "bad_integrator",
+                                  "cbar_without_hbar"])
+def test_descriptor_validation_before_any_gpu_work(case):
+    """Invalid descriptors are rejected with OSAM_EINVAL by host-side validation (GPU or not): the FOM is explicit,
+    a ROM has no material model, n_substeps in 0..4096, integrator / material enums, COpInf needs Hbar."""
+    import numpy as np
+    from paper_2511_20687_b200 import osam
+    d = osam.osam_subdomain_desc()
+    d.kind = osam.OSAM_FOM
+    d.lo[:] = [0.0, 0.0, 0.0]
+    d.hi[:] = [1.0, 1.0, 1.0]
+    d.nel[:] = [2, 2, 2]
+    d.E, d.nu, d.rho = 1e9, 0.25, 1000.0
+    d.batch = 1
+    keep = []
+    if case == "fom_implicit":
+        d.integrator = osam.OSAM_IMPLICIT
+    elif case == "rom_material":
+        d.kind = osam.OSAM_ROM
+        d.material = osam.OSAM_SVK
+    elif case == "bad_material":
+        d.material = 7
+    elif case == "neg_substeps":
+        d.n_substeps = -1
+    elif case == "bad_integrator":
+        d.integrator = 5
+    elif case == "cbar_without_hbar":
+        d.kind = osam.OSAM_ROM
+        r = 2
+        mats = [np.asfortranarray(np.eye(r)), np.asfortranarray(np.zeros((r, 4)))]
+        keep += mats
+        d.r, d.r_b, d.n_free, d.n_s = r, 0, r, 0
+        d.Phi = osam._dptr(mats[0])
+        d.Kbar = osam._dptr(mats[0])
+        d.Cbar = osam._dptr(mats[1])
+    h = ctypes.c_void_p()
+    rc = osam.lib().osam_create_subdomain(ctypes.byref(d), None, ctypes.byref(h))
+    assert rc == -1, (case, rc, osam.lib().osam_last_error())
+    assert not h.value
