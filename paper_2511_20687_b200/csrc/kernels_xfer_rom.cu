@@ -26,29 +26,28 @@ __device__ __forceinline__ double warp_sum(double x) {
   return x;
 }
 
-// compact = 1: write dst[b][3p + c] (a trace slot) instead of dst[b][out[3p + c]]
+// compact = 1: write dst[b][3p + c] (a trace slot) instead of dst[b][out[3p + c]].  One thread per
+// (node, component): the gather is memory-latency-bound (a y-z slab of an x-fastest field), so more
+// independent loads in flight matter more than sharing the weights.
 __global__ void transfer_kernel(int n, const int* __restrict__ idx, const double* __restrict__ xi,
                                 const int* __restrict__ out, const double* __restrict__ src, long long cs,
                                 long long bs_src, double* __restrict__ dst, long long bs_dst,
                                 const int* __restrict__ active, int compact) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
-  if (p >= n || (active != nullptr && !active[b])) return;
+  if (t >= 3 * n || (active != nullptr && !active[b])) return;
+  const int p = t / 3, c = t - 3 * p;
+  const int o = out[3 * p + c];
+  if (o < 0) return;
   const double x = xi[3 * p], y = xi[3 * p + 1], z = xi[3 * p + 2];
-  double w[8];
+  const double* sb = src + b * bs_src + c * cs;
+  double acc = 0.0;
 #pragma unroll
-  for (int q = 0; q < 8; ++q)
-    w[q] = ((q & 1) ? x : 1.0 - x) * ((q & 2) ? y : 1.0 - y) * ((q & 4) ? z : 1.0 - z);
-  const double* sb = src + b * bs_src;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const int o = out[3 * p + c];
-    if (o < 0) continue;
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc = fma(w[q], sb[c * cs + idx[8 * p + q]], acc);
-    dst[b * bs_dst + (compact ? 3 * p + c : o)] = acc;
+  for (int q = 0; q < 8; ++q) {
+    const double w = ((q & 1) ? x : 1.0 - x) * ((q & 2) ? y : 1.0 - y) * ((q & 4) ? z : 1.0 - z);
+    acc = fma(w, sb[idx[8 * p + q]], acc);
   }
+  dst[b * bs_dst + (compact ? 3 * p + c : o)] = acc;
 }
 
 // Xi (reading R31): s = (1 - alpha) T[lo] + alpha T[lo + 1] from the trace slots of one map
@@ -563,8 +562,8 @@ __global__ void gather_dofs_kernel(long long n, int B, const int* __restrict__ i
 void launch_transfer(const XferMap& m, const double* src, long long cs, long long bs_src, double* dst,
                      long long bs_dst, int batch, const int* active, cudaStream_t s) {
   if (m.n == 0) return;
-  transfer_kernel<<<dim3(cdiv(m.n, 128), batch), 128, 0, s>>>(m.n, m.idx, m.xi, m.out, src, cs, bs_src, dst,
-                                                                bs_dst, active, 0);
+  transfer_kernel<<<dim3(cdiv(3LL * m.n, 128), batch), 128, 0, s>>>(m.n, m.idx, m.xi, m.out, src, cs, bs_src, dst,
+                                                                      bs_dst, active, 0);
   debug_check("transfer_kernel", s);
 }
 
@@ -572,8 +571,9 @@ void launch_transfer_trace(const XferMap& m, const double* src, long long cs, lo
                            const int* active, cudaStream_t s) {
   if (m.n == 0) return;
   const long long bs = 3LL * m.n;
-  transfer_kernel<<<dim3(cdiv(m.n, 128), batch), 128, 0, s>>>(m.n, m.idx, m.xi, m.out, src, cs, bs_src,
-                                                                m.trace + (long long)slot * batch * bs, bs, active, 1);
+  transfer_kernel<<<dim3(cdiv(3LL * m.n, 128), batch), 128, 0, s>>>(m.n, m.idx, m.xi, m.out, src, cs, bs_src,
+                                                                      m.trace + (long long)slot * batch * bs, bs,
+                                                                      active, 1);
   debug_check("transfer_kernel(trace)", s);
 }
 
