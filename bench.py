@@ -370,6 +370,8 @@ def run_ours(args):
                          "bytes_model": "32 B/DOF/sweep (read q, w; write q, w) + from sweep 2 8 B per DOF within one node layer of a Schwarz face (read previous w'; elsewhere the norm term is exactly 0, DESIGN.md R38), two-vector form (SURVEY 8(d), DESIGN.md R30)",
                          "k1_ms_per_launch": k1_ms_per_launch,
                          "k1_share_of_step": prof["k1_ms"] / prof_ms,
+                         # algorithmic bytes per controller step x steps/s / peak
+                         "step_frac": prof["k1_bytes"] / prof_steps * steps_per_s / 1e9 / peak,
                          "timing": f"K1 CUDA events over {prof_steps} steps in profiling mode (host-driven "
                                    "sweeps) right after the timed region; value is timed with CUDA graphs",
                          "peak_source": peak_src},
