@@ -870,7 +870,7 @@ constexpr int PXN = TXN + 2, PYN = TYN + 2, PLN = PXN * PYN;
 constexpr int NTN = 256;
 constexpr int NN = TXN * TYN;  // nodes finished per plane
 // X ring of 3 planes | element forces of 2 layers | W and W'_prev (or z_prev) of 2 node planes
-constexpr size_t SMEM = sizeof(double) * (3 * 3 * PLN + 2 * 24 * NE + 2 * 2 * 3 * NN);
+constexpr size_t SMEM = sizeof(double) * (3 * 3 * PLN + 2 * 24 * NE + 2 * 2 * 3 * NN + 8 * 2 * 12);
 }  // namespace nl
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
@@ -935,24 +935,25 @@ __device__ __forceinline__ void pk1(const FomLaunch& L, const double F[3][3], do
 //     du_i/dX_j = sum_p W_j[p] (u_i(a_j = 1, p) - u_i(a_j = 0, p))    (p: the other two bits of a)
 //     f_a,i     = sum_j s_aj T_j[i][p(a)],   T_j[i][p] = sum_q detJ P_q[i][j] W_j[p](q).
 // The nodal displacements are read from the staged planes (u(a) = ua(a, c)); 36 accumulators T.
-template <int MAT, class UA>
-__device__ __forceinline__ void element_forces(const FomLaunch& L, UA ua, double (&f)[8][3]) {
+// The weights of point q, axis j, pair p (gradient: w w / h_j; accumulation: w w detJ / h_j) come from a
+// per-CTA shared table wtab[q][0|1][j][p] (element_weights), read as broadcasts.
+__device__ __forceinline__ void element_weights(const FomLaunch& L, double* wtab) {
   const double r3 = 0.57735026918962576451;  // 1/sqrt(3)
   const double gpl = 0.5 * (1.0 + r3), gmi = 0.5 * (1.0 - r3);
-  const double ih[3] = {1.0 / L.g.h[0], 1.0 / L.g.h[1], 1.0 / L.g.h[2]};
   const double detJ = 0.125 * L.g.h[0] * L.g.h[1] * L.g.h[2];
-  // the weight of an edge difference is one of gpl^2, gpl gmi, gmi^2 times 1/h_j (gradient) or
-  // detJ/h_j (force accumulation): 9 + 9 constants, selected per (point, pair) without FP64 work
-  double Wg[3][3], Wt[3][3];
-#pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    const double base[3] = {gpl * gpl, gpl * gmi, gmi * gmi};
-#pragma unroll
-    for (int m = 0; m < 3; ++m) {
-      Wg[j][m] = base[m] * ih[j];
-      Wt[j][m] = Wg[j][m] * detJ;
-    }
+  for (int t = threadIdx.x; t < 8 * 2 * 12; t += blockDim.x) {
+    const int q = t / 24, kind = (t / 12) % 2, j = (t % 12) / 4, p = t % 4;
+    const int o1 = j == 0 ? 1 : 0, o2 = j == 2 ? 1 : 2;
+    const double w1 = ((p & 1) == ((q >> o1) & 1)) ? gpl : gmi;
+    const double w2 = (((p >> 1) & 1) == ((q >> o2) & 1)) ? gpl : gmi;
+    const double wg = w1 * w2 * (1.0 / L.g.h[j]);
+    wtab[t] = kind ? wg * detJ : wg;
   }
+}
+
+template <int MAT, class UA>
+__device__ __forceinline__ void element_forces(const FomLaunch& L, UA ua, const double* __restrict__ wtab,
+                                               double (&f)[8][3]) {
   double T[3][3][4], D[3][3][4];  // accumulators; edge differences u_i(a_j = 1, p) - u_i(a_j = 0, p)
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
@@ -968,15 +969,7 @@ __device__ __forceinline__ void element_forces(const FomLaunch& L, UA ua, double
   }
 #pragma unroll 1
   for (int q = 0; q < 8; ++q) {
-    // pair p = (bit o1, bit o2) of the other two axes: the weight is gmi for each bit that differs
-    // from the point's bit on that axis -> index m = number of differing bits
-    int mi[3][4];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      const int o1 = j == 0 ? 1 : 0, o2 = j == 2 ? 1 : 2;
-#pragma unroll
-      for (int p = 0; p < 4; ++p) mi[j][p] = ((p & 1) != ((q >> o1) & 1)) + (((p >> 1) & 1) != ((q >> o2) & 1));
-    }
+    const double* wg = wtab + q * 24;  // [j][p] gradient weights, then [j][p] accumulation weights
     double F[3][3];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
@@ -985,8 +978,7 @@ __device__ __forceinline__ void element_forces(const FomLaunch& L, UA ua, double
         double gsum = 0.0;
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-          const double wg = mi[j][p] == 0 ? Wg[j][0] : (mi[j][p] == 1 ? Wg[j][1] : Wg[j][2]);
-          gsum = fma(wg, D[j][i][p], gsum);
+          gsum = fma(wg[j * 4 + p], D[j][i][p], gsum);
         }
         F[i][j] = (i == j ? 1.0 : 0.0) + gsum;
       }
@@ -997,7 +989,7 @@ __device__ __forceinline__ void element_forces(const FomLaunch& L, UA ua, double
     for (int j = 0; j < 3; ++j)
 #pragma unroll
       for (int p = 0; p < 4; ++p) {
-        const double wt = mi[j][p] == 0 ? Wt[j][0] : (mi[j][p] == 1 ? Wt[j][1] : Wt[j][2]);
+        const double wt = wg[12 + j * 4 + p];
 #pragma unroll
         for (int i = 0; i < 3; ++i) T[j][i][p] = fma(P[i][j], wt, T[j][i][p]);
       }
@@ -1024,6 +1016,7 @@ __global__ void __launch_bounds__(nl::NTN, 1) fom_nl_kernel(const __grid_constan
   double* Xs = nsm;                         // [3][3][PYN][PXN]   node planes, slot p mod 3
   double* EF = Xs + 3 * 3 * PLN;            // [2][8][3][NE]      element forces, layer mod 2
   double* Ws = EF + 2 * 24 * NE;            // [2][2][3][NN]      W, W'_prev (or z_prev), plane mod 2
+  double* Wq = Ws + 2 * 2 * 3 * NN;         // [8][2][3][4]       Gauss weights (element_weights)
   const Geom& g = L.g;
   const long long np = g.npad;
   const int tid = threadIdx.x, tx = tid % TXN, ty = tid / TXN;
@@ -1074,7 +1067,7 @@ __global__ void __launch_bounds__(nl::NTN, 1) fom_nl_kernel(const __grid_constan
     const double* p1 = Xs + ((l + 4) % 3) * 3 * PLN + ly * PXN + lx;
     auto ua = [&](int a, int c) { return ((a >> 2) ? p1 : p0)[c * PLN + ((a >> 1) & 1) * PXN + (a & 1)]; };
     double f[8][3];
-    element_forces<MAT>(L, ua, f);
+    element_forces<MAT>(L, ua, Wq, f);
 #pragma unroll
     for (int a = 0; a < 8; ++a)
 #pragma unroll
@@ -1082,6 +1075,7 @@ __global__ void __launch_bounds__(nl::NTN, 1) fom_nl_kernel(const __grid_constan
   };
 
   double num = 0.0, den = 0.0;
+  element_weights(L, Wq);  // visible after the prologue's barrier
   // prologue: planes kbeg-1, kbeg, kbeg+1 and W of plane kbeg; element layer kbeg-1
   issue_plane(kbeg - 1);
   issue_plane(kbeg);
