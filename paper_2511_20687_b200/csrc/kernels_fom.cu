@@ -967,7 +967,7 @@ __device__ __forceinline__ void element_forces(const FomLaunch& L, UA ua, const 
         D[j][i][p] = ua(a0 | (1 << j), i) - ua(a0, i);
       }
   }
-#pragma unroll 1
+#pragma unroll 2
   for (int q = 0; q < 8; ++q) {
     const double* wg = wtab + q * 24;  // [j][p] gradient weights, then [j][p] accumulation weights
     double F[3][3];
