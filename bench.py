@@ -112,6 +112,8 @@ def oracle_rate(cfg, warmup, steps=None, seconds=None):
     u0s = [I.initial_displacements(cfg, s) for s in cfg["subdomains"]]
     st = [m.init_state(u) for m, u in zip(models, u0s)]
     dofs = sum(3 * m.box.n_nodes for m in models if m.kind == "fom")
+    if dofs == 0:  # ROM-only (c5): reduced updates, r x batch per ROM and sweep
+        dofs = sum(m.Kbar.shape[0] * m.batch for m in models if m.kind == "rom")
     for _ in range(warmup):
         st, _ = schwarz.controller_step(models, st, cfg["tol"], cfg["max_iters"], cfg["min_iters"])
     t0 = time.perf_counter()
@@ -327,6 +329,11 @@ def run_ours(args):
     sweeps = int(iters.max(axis=1).sum())
     value = world * sweeps * fom_dofs / (ms / 1e3)
     steps_per_s = args.steps / (ms / 1e3)
+    # ROM-only workloads (c5): reduced updates/s = sum over sweeps and ROMs of r * batch
+    rom_units = sum(cfg["rom"]["r"] * cfg.get("batch", 1) for s_ in cfg["subdomains"] if s_["kind"] == "rom")
+    rom_only = fom_dofs == 0
+    if rom_only:
+        value = world * sweeps * rom_units / (ms / 1e3)
 
     # end to end through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -345,7 +352,8 @@ def run_ours(args):
         el = max_over_ranks(time.perf_counter() - t0, dist, dev)
         h2d = sum(f.nbytes for f in fields)
         d2h = sum(2 * f.nbytes for f in fields) + 4 * (2 + 2) * int(it2.sum())
-        e2e = {"value": world * int(it2.max(axis=1).sum()) * fom_dofs / el, "unit": UNIT,
+        e2e = {"value": world * int(it2.max(axis=1).sum()) * (rom_units if rom_only else fom_dofs) / el,
+               "unit": "reduced updates/s" if rom_only else UNIT,
                "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
                "note": "set_ic(pinned host IC) + osam_step(K) + get_state(pinned host u,v) per run; bytes / K"}
 
@@ -356,7 +364,7 @@ def run_ours(args):
     peak, peak_src = measured_peak()
     k1_ms_per_launch = prof["k1_ms"] / max(1, prof["k1_launches"])
     bytes_per_launch = prof["k1_bytes"] / max(1, prof["k1_launches"])
-    achieved = bytes_per_launch / (k1_ms_per_launch / 1e3) / 1e9
+    achieved = bytes_per_launch / (k1_ms_per_launch / 1e3) / 1e9 if k1_ms_per_launch > 0 else 0.0
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -377,6 +385,20 @@ def run_ours(args):
                          "peak_source": peak_src},
             "gpu_launches": int(launches),
             "clocks": ck, "e2e": e2e}
+    if rom_only:  # no FOM: the reduced updates are GEMM-shaped (DMMA when batched) but latency-bound
+        line["metric"], line["unit"] = "reduced updates/s", "reduced updates/s"
+        ops = workload_ops(cfg)
+        flops = 0.0  # per controller step: 2 r (r + r_b) + 2 n_s r_b per sample, ROM and sweep (8(d))
+        for i, s_ in enumerate(cfg["subdomains"]):
+            if s_["kind"] == "rom":
+                r_, rb_ = ops[i]["Kbar"].shape[0], ops[i]["Bbar"].shape[1]
+                flops += (2 * r_ * (r_ + rb_) + 2 * ops[i]["Phi_s"].shape[0] * rb_) * cfg.get("batch", 1)
+        tf = flops * sweeps / args.steps * steps_per_s / 1e12
+        line["roofline"] = {"bound": "tensor", "achieved": tf, "peak": 45.0, "unit": "TFLOP/s", "frac": tf / 45.0,
+                            "traffic": None, "kernel": "ROM update + boundary projection (DMMA GEMMs), step level",
+                            "note": "latency-bound (GEMMs of r = 400 x 64 samples); peak = B200 FP64 tensor "
+                                    "(blackwell_cuda_programming.md); the lift GEMM is not counted",
+                            "peak_source": "guide"}
     if args.material != "linear":   # NL1 is FP64-ALU bound: roofline in TFLOP/s
         n_fom = sum(1 for s in cfg["subdomains"] if s["kind"] == "fom")
         elems = sum(int(np.prod(s["nel"])) for s in cfg["subdomains"] if s["kind"] == "fom")
@@ -397,7 +419,7 @@ def run_ours(args):
         sample = sample_cfg(cfg)
         sdesc, _ = workload_desc(sample)
         rate, n, el, threads = oracle_rate(sample, 1, seconds=10.0)
-        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
+        line["cpu_baseline"] = {"value": rate, "unit": line["unit"], "cores": threads, "kind": "oracle",
                                 "sample": f"{args.workload} with lateral extent cut to {SAMPLE_LATERAL} elements "
                                           f"({sdesc}); {n} controller steps, {el:.1f} s"}
     print(json.dumps(line), flush=True)
