@@ -217,7 +217,12 @@ void launch_rom_advance_tc(const RomLaunch& L, const double* KB, double* Z, doub
   debug_check("tc_predict_kernel", s);
   launch_rom_features(L.nf, B, L.feat_idx, Z, rz, Z + r + rb, rz, s);  // polynomial OpInf rows of Z
   *launches += L.nf > 0;
-  if (rb > 0) {  // g^ = Phi_dS^T s  -> Z[r:, :]
+  if (rb > 0 && L.G) {  // folded exchange: g^ = G u^_src -> Z[r:, :]
+    const int S = gemm(GemmArgs{rb, B, L.Gr, L.G, 1, rb, L.Gu, 1, L.Gr, nullptr, 0}, part, s);
+    reduce_splits_kernel<<<cdiv((long long)rb * B, 256), 256, 0, s>>>(rb, B, S, part, Z + r, 1, rz);
+    debug_check("reduce_splits_kernel", s);
+    *launches += 2;
+  } else if (rb > 0) {  // g^ = Phi_dS^T s  -> Z[r:, :]
     const int S = gemm(GemmArgs{rb, B, (int)L.n_sdof, L.Phi_s, L.n_sdof, 1, L.s, 1, L.n_sdof, nullptr, 0}, part, s);
     reduce_splits_kernel<<<cdiv((long long)rb * B, 256), 256, 0, s>>>(rb, B, S, part, Z + r, 1, rz);
     debug_check("reduce_splits_kernel", s);

@@ -175,8 +175,10 @@ void release_maps(Sub& s) {
     dfree(m.xi);
     dfree(m.out);
     dfree(m.trace);
+    dfree(m.G);
   }
   s.maps.clear();
+  s.fold = false;
 }
 
 void release_binding(Sub& s) {
@@ -545,9 +547,35 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
         }
       }
     TRY(upload(&s.Phi_lift, phil, s.stream));
+    s.h_Phi_lift = phil;
     TRY(upload(&s.lift_code, code, s.stream));
     for (int b = 0; b < 2; ++b) TRY(dalloc(&s.lift[b], (size_t)std::max<long long>(nl, 1) * s.batch));
-    if (s.use_tc) TRY(dalloc(&s.part, (size_t)tc_part_size(s.r, s.r_b, s.nf, s.batch, s.n_sdof, nl)));
+    long long r_max = 0;  // a folded boundary GEMM contracts over the source's r instead of n_s
+    for (int q = 0; q < n; ++q) r_max = std::max<long long>(r_max, subs[q]->r);
+    if (s.use_tc)
+      TRY(dalloc(&s.part, (size_t)tc_part_size(s.r, s.r_b, s.nf, s.batch, std::max(s.n_sdof, r_max), nl)));
+  }
+  // Folding ("algebraic folding is allowed"): in a group of batched tensor-core ROMs where
+  // each ROM has one Schwarz map and no donor corner is a source Schwarz DOF (the lift would carry the
+  // source's own s there), g^_dst = Phi_dS^T Pi (Phi_src[donor rows] u^_src) = G u^_src exactly up to
+  // rounding: one small GEMM per sweep replaces the lift, the transfer and the boundary projection.
+  bool fold = !getenv("OSAM_NO_FOLD") && n >= 2;
+  for (int i = 0; i < n && fold; ++i) {
+    const Sub& s = *subs[i];
+    int maps_i = 0;
+    for (auto& P : pend) maps_i += P.dst == i;
+    fold = s.kind == OSAM_ROM && s.use_tc && s.n_sub == 1 && maps_i == 1 && s.r_b > 0;
+  }
+  for (auto& P : pend) {
+    if (!fold) break;
+    const Sub& src = *subs[P.src];
+    for (size_t t = 0; t < P.out.size() && fold; ++t) {
+      if (P.out[t] < 0) continue;
+      const int c = (int)(t % 3);
+      const long long p = (long long)(t / 3);
+      for (int q = 0; q < 8; ++q)  // a donor corner on a source Schwarz DOF: the lift carries s there
+        if (src.codes[3 * P.corner[8 * p + q] + c] == DOF_SCHWARZ) fold = false;
+    }
   }
   for (auto& P : pend) {
     Sub& d = *subs[P.dst];
@@ -571,6 +599,29 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
     TRY(upload(&m.xi, P.xi, d.stream));
     TRY(upload(&m.out, P.out, d.stream));
     m.n_src_sub = src.n_sub;
+    if (fold) {  // G[k + r_b j] = sum over the map's Schwarz DOFs and corners of Phi_dS[sd, k] w Phi_lift[row, j]
+      const long long nl = src.n_lift;
+      std::vector<double> G((size_t)d.r_b * src.r, 0.0);
+      for (size_t t = 0; t < P.out.size(); ++t) {
+        const int sd = P.out[t];
+        if (sd < 0) continue;
+        const int c = (int)(t % 3);
+        const long long p = (long long)(t / 3);
+        const double x = P.xi[3 * p], y = P.xi[3 * p + 1], z = P.xi[3 * p + 2];
+        for (int q = 0; q < 8; ++q) {
+          const double w = ((q & 1) ? x : 1.0 - x) * ((q & 2) ? y : 1.0 - y) * ((q & 4) ? z : 1.0 - z);
+          const double* prow = src.h_Phi_lift.data() + (size_t)(c * nl + idx[8 * p + q]) * src.r;
+          for (int k = 0; k < d.r_b; ++k) {
+            const double a = d.h_Phi_s[(size_t)sd + (size_t)d.n_sdof * k] * w;
+            if (a == 0.0) continue;
+            double* gk = G.data() + k;
+            for (int j = 0; j < src.r; ++j) gk[(size_t)d.r_b * j] += a * prow[j];
+          }
+        }
+      }
+      TRY(upload(&m.G, G, d.stream));
+      d.fold = true;
+    }
     d.maps.push_back(m);
   }
   // multi-substep group: a trace of n_src_sub + 1 slots per map (R31)
@@ -799,6 +850,7 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
   for (int i = 0; i < n_sd; ++i) {
     Sub& d = *subs[i];
     for (const XferMap& m : d.maps) {
+      if (d.fold) continue;  // folded ROM-ROM exchange: g^ = G u^_src inside the ROM advance
       const Sub& src = *subs[m.src];
       const bool newest = (m.src < i) || !first;
       const double* field;
@@ -850,12 +902,21 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
       slot += fom_slots(d);
     } else {
       const int c = d.cur;
-      const RomLaunch L = rom_launch(d, d.rst[c], d.rst[1 - c], ctl.active, cfg.dt, with_norm,
-                                     G.partial + (size_t)slot * B);
+      RomLaunch L = rom_launch(d, d.rst[c], d.rst[1 - c], ctl.active, cfg.dt, with_norm,
+                               G.partial + (size_t)slot * B);
+      if (d.fold) {  // the source's iterate n if it precedes d, else n - 1 (n = 1: its checkpoint)
+        const XferMap& m = d.maps[0];
+        const Sub& src = *subs[m.src];
+        const bool newest = (m.src < i) || !first;
+        L.G = m.G;
+        L.Gu = src.rst[newest ? 1 - src.cur : src.cur][0];
+        L.Gr = src.r;
+      }
       if (d.use_tc) {
         launch_rom_advance_tc(L, d.KB, d.Z, d.part, st, launches);
-        launch_rom_lift_tc(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, d.rst[1 - c][0], d.rst[1 - c][3],
-                           d.n_sdof, d.lift[1 - c], d.part, st, launches);
+        if (!d.fold)  // in a folded group no map reads a lift
+          launch_rom_lift_tc(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, d.rst[1 - c][0], d.rst[1 - c][3],
+                             d.n_sdof, d.lift[1 - c], d.part, st, launches);
       } else {
         launch_rom_advance(L, st, launches);
         launch_rom_lift(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, d.rst[1 - c][0], d.rst[1 - c][3],

@@ -57,6 +57,10 @@ struct XferMap {
   // [n_src_sub + 1 slots][B][3 n] (slot 0: the interval start), read through the interpolant Xi
   double* trace = nullptr;
   int n_src_sub = 1;
+  // folded ROM-ROM exchange (groups of batched ROMs only, osam_api.cu bind_group): the destination's
+  // reduced boundary input g^ = G u^_src with G = Phi_dS^T Pi Phi_src[donor rows] (r_b x r_src, column-
+  // major), replacing lift, transfer and boundary projection
+  double* G = nullptr;
 };
 
 struct Sub {
@@ -131,6 +135,8 @@ struct Sub {
   double* Phi_lift = nullptr;  // [3 n_lift][r] row-major
   int* lift_code = nullptr;    // [3 n_lift]: >= 0 Phi_lift row, -1 Dirichlet, -2-q Schwarz DOF q
   double* lift[2] = {nullptr, nullptr};
+  std::vector<double> h_Phi_lift;  // host copy of Phi_lift (folding)
+  bool fold = false;               // reduced boundary input from the folded operator of its map
   // batched ROM on the tensor cores (kernels_rom_tc.cu): [-Kbar | Bbar] and scratch
   bool use_tc = false;
   double* KB = nullptr;    // r x (r + r_b) column-major
@@ -210,6 +216,9 @@ struct RomLaunch {
   double c2;           // predictor u~ = u^ + dt v^ + c2 a^: dt^2/2 explicit, dt^2 (1/2 - beta) implicit
   double beta;         // 0: explicit; > 0: implicit average acceleration through Minv (R32)
   const double* Minv;  // [B][r][r] row-major
+  const double* G;     // folded exchange: g^ = G Gu (r_b x Gr), null: g^ = Phi_dS^T s
+  const double* Gu;    // the source's reduced state (Gr x B)
+  int Gr;
   int with_norm;
   double2* partial;
 };
