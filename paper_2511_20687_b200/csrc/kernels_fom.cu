@@ -727,6 +727,84 @@ __device__ __noinline__ void xface_body(const FomLaunch& L, int side_mask, int b
   block_partial<XF_BLOCK>(num, den, L.partial, slot);
 }
 
+// Small subdomains (K1S): the TMA-streamed tiled kernel pays a load round trip per z-plane inside each
+// CTA, which dominates for boxes of a few thousand nodes (c1, c2).  Here every node is one group of 4
+// lanes (lane sub = 0, 1, 2 gathers the plane oz = sub - 1 with the class-table stencil, the partial
+// forces are summed in the order sub = 0, 1, 2), all planes at once; the field is L2-resident.
+constexpr int GB = 256;
+__global__ void __launch_bounds__(GB) fom_gather_kernel(const FomLaunch L) {
+  const Geom& g = L.g;
+  const long long np = g.npad;
+  const long long n = (long long)g.nn[0] * g.nn[1] * g.nn[2];
+  const long long t = (blockIdx.x * (long long)GB + threadIdx.x) >> 2;
+  const int sub = threadIdx.x & 3;
+  const bool valid = t < n;
+  const int i = valid ? (int)(t % g.nn[0]) : 0;
+  const int j = valid ? (int)((t / g.nn[0]) % g.nn[1]) : 0;
+  const int k = valid ? (int)(t / ((long long)g.nn[0] * g.nn[1])) : 0;
+  const int cx = axis_class(i, g.nn[0]), cy = axis_class(j, g.nn[1]), cz = axis_class(k, g.nn[2]);
+  double f[3] = {0.0, 0.0, 0.0};
+  const int oz = sub - 1;
+  if (valid && sub < 3 && k + oz >= 0 && k + oz <= g.nn[2] - 1) {
+    const double* coef = L.coef + (size_t)(cx + 3 * (cy + 3 * cz)) * 27 * 9;
+#pragma unroll
+    for (int oy = -1; oy <= 1; ++oy) {
+      if (j + oy < 0 || j + oy > g.nn[1] - 1) continue;
+#pragma unroll
+      for (int ox = -1; ox <= 1; ++ox) {
+        if (i + ox < 0 || i + ox > g.nn[0] - 1) continue;
+        const long long q = gidx(g, i + ox, j + oy, k + oz);
+        const double x[3] = {__ldg(L.x + q), __ldg(L.x + np + q), __ldg(L.x + 2 * np + q)};
+        const double* cb = coef + ((ox + 1) + 3 * ((oy + 1) + 3 * (oz + 1))) * 9;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int d = 0; d < 3; ++d) f[c] = fma(__ldg(cb + c * 3 + d), x[d], f[c]);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const double f1 = __shfl_down_sync(0xffffffffu, f[c], 1, 4);
+    const double f2 = __shfl_down_sync(0xffffffffu, f[c], 2, 4);
+    f[c] = (f[c] + f1) + f2;
+  }
+  double num = 0.0, den = 0.0;
+  if (valid && sub == 0) {
+    const long long id = gidx(g, i, j, k);
+    const unsigned fm = free_mask(g, L.f, i, j, k);
+    const double inv_m = L.inv_mass[(cx == 1 ? 1 : 0) + (cy == 1 ? 2 : 0) + (cz == 1 ? 4 : 0)];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double x = __ldg(L.x + c * np + id);
+      double an = 0.0, wn = 0.0, qn = x;
+      if ((fm >> c) & 1) {
+        const double w0 = L.w0[c * np + id];
+        an = -f[c] * inv_m;
+        wn = fma(L.cw, an, w0);
+        qn = fma(L.cq, wn, x);
+        const double w = fma(L.dt, fma(L.cv, an, w0), x);
+        if (L.with_norm) {
+          const double d = L.z_out ? w - L.z_out[c * np + id] : 0.5 * L.dt * (wn - L.w_out[c * np + id]);
+          num = fma(d, d, num);
+          den = fma(w, w, den);
+        }
+        if (L.z_out) L.z_out[c * np + id] = w;
+      }
+      if (L.q_out) L.q_out[c * np + id] = qn;
+      L.w_out[c * np + id] = wn;
+      if (L.a_out) L.a_out[c * np + id] = an;
+    }
+  }
+  block_partial<GB>(num, den, L.partial, blockIdx.x);
+}
+
+bool small_fom(const Geom& g) {
+  const char* e = getenv("OSAM_GATHER_MAX");  // read per call (tests switch it)
+  const long long cap = e ? atoll(e) : (1LL << 18);
+  return (long long)g.nn[0] * g.nn[1] * g.nn[2] <= cap;
+}
+
 __device__ __forceinline__ void surface_node(const Geom& g, long long t, int* i, int* j, int* k) {
   const long long n0 = g.nn[0], n1 = g.nn[1], n2 = g.nn[2];
   const long long sz = n0 * n1;
@@ -1147,7 +1225,10 @@ int nl_ctas(const Geom& g) {
 
 }  // namespace
 
-int fom_partial_slots(const Geom& g, const Faces& f) { return tiled_ctas(g, f) + (int)xface_blocks(g, f); }
+int fom_partial_slots(const Geom& g, const Faces& f) {
+  if (small_fom(g)) return (int)cdiv(4LL * g.nn[0] * g.nn[1] * g.nn[2], GB);
+  return tiled_ctas(g, f) + (int)xface_blocks(g, f);
+}
 
 int fom_nl_partial_slots(const Geom& g) { return nl_ctas(g); }
 
@@ -1171,6 +1252,12 @@ void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUt
                         const CUtensorMap* tmw, const CUtensorMap* tmwp, cudaStream_t s, int* launches) {
   if (L.material != OSAM_LINEAR) {  // SVK / Neohookean: NL1 (no stencil, no TMA maps)
     launch_fom_advance_nl(L, s, launches);
+    return;
+  }
+  if (small_fom(L.g)) {  // K1S: one gather pass over every node
+    fom_gather_kernel<<<cdiv(4LL * L.g.nn[0] * L.g.nn[1] * L.g.nn[2], GB), GB, 0, s>>>(L);
+    debug_check("fom_gather_kernel", s);
+    ++*launches;
     return;
   }
   FomLaunch Lt = L;

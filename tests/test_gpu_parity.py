@@ -14,6 +14,13 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-10
 
 
+@pytest.fixture(autouse=True)
+def tiled_k1(monkeypatch):
+    """These cases exercise the TMA-streamed tiled K1 at small sizes: force it (OSAM_GATHER_MAX=0); the
+    small-subdomain gather path (K1S) has its own module, tests/test_gpu_small_path.py."""
+    monkeypatch.setenv("OSAM_GATHER_MAX", "0")
+
+
 @pytest.fixture(scope="module")
 def gpu():
     torch = pytest.importorskip("torch")

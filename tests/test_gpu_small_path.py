@@ -1,0 +1,74 @@
+"""GPU parity of the small-subdomain FOM path K1S (fom_gather_kernel: every node one 4-lane gather of the
+class-table stencil, used below OSAM_GATHER_MAX nodes) against the oracle, on the cases that exercise every
+node class, the controller variants and the exchange paths."""
+import numpy as np
+import pytest
+
+import osam_inputs as I
+from test_gpu_parity import _substeps, run_both  # noqa: F401  (shared GPU-vs-oracle driver)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def gather_path(monkeypatch):
+    monkeypatch.setenv("OSAM_GATHER_MAX", str(1 << 30))
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2511_20687_b200 import osam, problem
+    osam.lib()
+    return problem
+
+
+def test_c1_full_horizon_gather(gpu):
+    cfg = I.config("c1")
+    _, iters, worst = run_both(gpu, cfg, cfg["n_steps"], checkpoints=(1, 50))
+    assert (iters == 3).all()
+
+
+@pytest.mark.parametrize("factor,steps", [(8.0, 15), (5.3, 8)])
+def test_scaled_c3_gather(gpu, factor, steps):
+    cfg = I.scaled(I.config("c3"), factor)
+    run_both(gpu, cfg, steps, checkpoints=(1,))
+
+
+@pytest.mark.parametrize("nel", [(1, 1, 1), (3, 2, 5), (40, 9, 3)])
+def test_single_fom_degenerate_gather(gpu, nel):
+    cfg = I.config("c1")
+    s = dict(cfg["subdomains"][0], nel=nel, dirichlet=(I.CLAMP, 0, 0, 0, 0, I.ROLLER_X))
+    cfg = dict(cfg, subdomains=[s], dt=I._dt([s]))
+    run_both(gpu, cfg, 20, checkpoints=(1,))
+
+
+@pytest.mark.parametrize("n_sub,dt_factor", [((2, 2), 2.0), ((1, 3), 1.5)])
+def test_c1_substeps_gather(gpu, n_sub, dt_factor):
+    run_both(gpu, _substeps(I.config("c1"), n_sub, dt_factor=dt_factor), 40, checkpoints=(1,))
+
+
+def test_graph_equals_host_gather(gpu):
+    from paper_2511_20687_b200 import osam
+    cfg = I.scaled(I.config("c3"), 10.0)
+    out = []
+    for prof in (False, True):
+        osam.set_profiling(prof)
+        try:
+            subs = gpu.build(cfg)
+            gpu.set_ics(cfg, subs, device="cuda:0")
+            _, it = gpu.run(cfg, subs, n_steps=7)
+            out.append((it, [gpu.fom_state(s) for s in subs]))
+        finally:
+            osam.set_profiling(False)
+    assert np.array_equal(out[0][0], out[1][0])
+    for a, b in zip(out[0][1], out[1][1]):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_c2_fom_rom_gather(gpu):
+    from oracle import opinf
+    cfg = I.config("c2")
+    run_both(gpu, cfg, 150, rom_ops=opinf.train(cfg, I), checkpoints=(1,))
