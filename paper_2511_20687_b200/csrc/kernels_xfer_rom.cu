@@ -82,10 +82,30 @@ __global__ void step_begin_kernel(Ctl c, int B) {
   }
 }
 
-// one block of FIN_T threads per sample; the sweep that just ran is iteration n = *n_dev + 1
+// after finalize (single thread): n_dev += 1, flags[0] = any sample active, per-step iteration
+// counts, max_iters flag, and (graph mode) the condition of the sweep while-loop
+__device__ __forceinline__ void any_active_body(const Ctl& c, int B) {
+  const int n = *c.n_dev + 1;
+  *c.n_dev = n;
+  int a = 0;
+  for (int b = 0; b < B; ++b) a |= c.active[b];
+  c.flags[0] = a;
+  if (c.iters_all) {
+    const long long k = *c.step_dev - 1;
+    for (int b = 0; b < B; ++b) c.iters_all[k * B + b] = c.iters[b];
+  }
+  const bool more = a && n < c.max_iters && !c.flags[1];
+  if (a && n >= c.max_iters) c.sticky[1] = 1;
+  if (c.has_cond) cudaGraphSetConditional(c.cond, more ? 1u : 0u);
+}
+
+__global__ void any_active_kernel(Ctl c, int B) { any_active_body(c, B); }
+
+// one block of FIN_T threads per sample; the sweep that just ran is iteration n = *n_dev + 1.  fused
+// (B = 1): thread 0 then runs any_active_body itself (every thread read n_dev before the barrier)
 constexpr int FIN_T = 1024;
 __global__ void __launch_bounds__(FIN_T) finalize_kernel(Ctl c, const double2* __restrict__ part, int n_slots, int B,
-                                                         int min_iters, double tol_rel, double tol_abs) {
+                                                         int min_iters, double tol_rel, double tol_abs, int fused) {
   __shared__ double red[2][FIN_T / 32];
   const int b = blockIdx.x;
   const int t = threadIdx.x;
@@ -127,25 +147,10 @@ __global__ void __launch_bounds__(FIN_T) finalize_kernel(Ctl c, const double2* _
         if (conv) c.active[b] = 0;
       }
     }
+    if (fused) any_active_body(c, B);
   }
 }
 
-// after finalize (single thread): n_dev += 1, flags[0] = any sample active, per-step iteration
-// counts, max_iters flag, and (graph mode) the condition of the sweep while-loop
-__global__ void any_active_kernel(Ctl c, int B) {
-  const int n = *c.n_dev + 1;
-  *c.n_dev = n;
-  int a = 0;
-  for (int b = 0; b < B; ++b) a |= c.active[b];
-  c.flags[0] = a;
-  if (c.iters_all) {
-    const long long k = *c.step_dev - 1;
-    for (int b = 0; b < B; ++b) c.iters_all[k * B + b] = c.iters[b];
-  }
-  const bool more = a && n < c.max_iters && !c.flags[1];
-  if (a && n >= c.max_iters) c.sticky[1] = 1;
-  if (c.has_cond) cudaGraphSetConditional(c.cond, more ? 1u : 0u);
-}
 
 // Fixed-order block sum of one value per thread (blockDim.x = 256).
 __device__ __forceinline__ double block_sum256(double v) {
@@ -611,12 +616,14 @@ void launch_rom_implicit(const RomLaunch& L, const double* ut, long long uts, in
 
 void launch_step_begin(Ctl c, int B, cudaStream_t s) { step_begin_kernel<<<1, 256, 0, s>>>(c, B); }
 
-void launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int min_iters, double tol_rel,
-                     double tol_abs, cudaStream_t s) {
-  finalize_kernel<<<B, FIN_T, 0, s>>>(c, partial, n_slots, B, min_iters, tol_rel, tol_abs);
+int launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int min_iters, double tol_rel,
+                    double tol_abs, cudaStream_t s) {
+  finalize_kernel<<<B, FIN_T, 0, s>>>(c, partial, n_slots, B, min_iters, tol_rel, tol_abs, B == 1 ? 1 : 0);
   debug_check("finalize_kernel", s);
+  if (B == 1) return 1;
   any_active_kernel<<<1, 1, 0, s>>>(c, B);
   debug_check("any_active_kernel", s);
+  return 2;
 }
 
 __global__ void rom_features_kernel(int nf, int B, const int* __restrict__ idx, const double* __restrict__ u,

@@ -927,8 +927,7 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
     }
   }
   for (int i : joins) CK(cudaStreamWaitEvent(st, G.join_ev[i], 0));  // every FOM advance before the test
-  launch_finalize(ctl, G.partial, G.n_slots, B, cfg.min_iters, cfg.tol_rel, cfg.tol_abs, st);
-  *launches += 2;
+  *launches += launch_finalize(ctl, G.partial, G.n_slots, B, cfg.min_iters, cfg.tol_rel, cfg.tol_abs, st);
   return OSAM_OK;
 }
 
@@ -1046,8 +1045,7 @@ int enqueue_sweep_trace(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, b
     }
     slot += d.kind == OSAM_FOM ? fom_slots(d) : rom_partial_slots(d.r, d.use_tc);
   }
-  launch_finalize(ctl, G.partial, G.n_slots, B, cfg.min_iters, cfg.tol_rel, cfg.tol_abs, st);
-  *launches += 2;
+  *launches += launch_finalize(ctl, G.partial, G.n_slots, B, cfg.min_iters, cfg.tol_rel, cfg.tol_abs, st);
   return OSAM_OK;
 }
 

@@ -286,7 +286,8 @@ struct Ctl {
 };
 void launch_step_begin(Ctl c, int B, cudaStream_t s);
 // Convergence test of the sweep that just ran (iteration n = *n_dev + 1): K3 + flags/conditional.
-void launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int min_iters, double tol_rel,
-                     double tol_abs, cudaStream_t s);
+// Returns the number of kernels launched (1 for a single sample: K3 and the flag update fused).
+int launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int min_iters, double tol_rel,
+                    double tol_abs, cudaStream_t s);
 
 }  // namespace osam
