@@ -733,6 +733,7 @@ __device__ __noinline__ void xface_body(const FomLaunch& L, int side_mask, int b
 // forces are summed in the order sub = 0, 1, 2), all planes at once; the field is L2-resident.
 constexpr int GB = 256;
 __global__ void __launch_bounds__(GB) fom_gather_kernel(const FomLaunch L) {
+  pdl_enter();
   const Geom& g = L.g;
   const long long np = g.npad;
   const long long n = (long long)g.nn[0] * g.nn[1] * g.nn[2];
@@ -1255,7 +1256,7 @@ void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUt
     return;
   }
   if (small_fom(L.g)) {  // K1S: one gather pass over every node
-    fom_gather_kernel<<<cdiv(4LL * L.g.nn[0] * L.g.nn[1] * L.g.nn[2], GB), GB, 0, s>>>(L);
+    launch_k(fom_gather_kernel, dim3(cdiv(4LL * L.g.nn[0] * L.g.nn[1] * L.g.nn[2], GB)), dim3(GB), 0, s, L);
     debug_check("fom_gather_kernel", s);
     ++*launches;
     return;

@@ -41,6 +41,7 @@ struct GemmArgs {
 // One block: a 32 x 32 tile of C over the K range [z kc, (z+1) kc): A and B staged once in shared
 // memory, then 2 x 2 m8n8k4 fragments per warp accumulate over k in increasing order.
 __global__ void __launch_bounds__(128) dmma_gemm_kernel(const GemmArgs g) {
+  pdl_enter();
   __shared__ double As[KMAX][TM + 1];  // As[k][m]
   __shared__ double Bs[KMAX][TN + 1];  // Bs[k][n]
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -99,7 +100,8 @@ int gemm(GemmArgs g, double* part, cudaStream_t s) {
   const int S = gemm_splits(g.M, g.N, g.K);
   g.kc = (int)(cdiv(cdiv(g.K, S), 4) * 4);
   g.C = part;
-  dmma_gemm_kernel<<<dim3(cdiv(g.M, TM), cdiv(g.N, TN), cdiv(g.K, g.kc)), 128, 0, s>>>(g);
+  // no programmatic early launch for the GEMM: its many CTAs would sit on SMs the predecessors need
+  dmma_gemm_kernel<<<dim3(dim3(cdiv(g.M, TM), cdiv(g.N, TN), cdiv(g.K, g.kc))), 128, 0, s>>>(g);
   debug_check("dmma_gemm_kernel", s);
   return (int)cdiv(g.K, g.kc);
 }
@@ -107,6 +109,7 @@ int gemm(GemmArgs g, double* part, cudaStream_t s) {
 // C(m, n) = sum_z part[z][m + M n] in split order, into a strided destination
 __global__ void reduce_splits_kernel(int M, int N, int S, const double* __restrict__ part, double* __restrict__ C,
                                      long long scm, long long scn) {
+  pdl_enter();
   const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (q >= (long long)M * N) return;
   double v = 0.0;
@@ -123,6 +126,7 @@ __device__ __forceinline__ double warp_sum(double x) {
 // Z[0:r, b] = u~ = u^ + dt v^ + c2 a^   (Z is rz x B, column-major; c2 = dt^2/2 explicit)
 __global__ void tc_predict_kernel(int r, int rz, int B, const double* __restrict__ uh, const double* __restrict__ vh,
                                   const double* __restrict__ ah, double dt, double c2, double* __restrict__ Z) {
+  pdl_enter();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= r * B) return;
   const int i = t % r, b = t / r;
@@ -135,6 +139,7 @@ __global__ void tc_predict_kernel(int r, int rz, int B, const double* __restrict
 // finishes.
 __global__ void __launch_bounds__(256) tc_epilogue_kernel(const RomLaunch L, const double* __restrict__ part,
                                                           int S, const double* __restrict__ Z, int rz, int mode) {
+  pdl_enter();
   __shared__ double red[2][8];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
@@ -186,6 +191,7 @@ __global__ void __launch_bounds__(256) tc_epilogue_kernel(const RomLaunch L, con
 __global__ void tc_lift_reduce_kernel(long long nl, int B, int S, const double* __restrict__ part,
                                       const int* __restrict__ code, const double* __restrict__ s, long long ns,
                                       double* __restrict__ out) {
+  pdl_enter();
   const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
   if (q >= nl) return;
@@ -213,18 +219,18 @@ long long tc_part_size(int r, int r_b, int nf, int B, long long n_s, long long n
 void launch_rom_advance_tc(const RomLaunch& L, const double* KB, double* Z, double* part, cudaStream_t s,
                            int* launches) {
   const int r = L.r, rb = L.r_b, rz = L.r + L.r_b + L.nf, B = L.B;
-  tc_predict_kernel<<<cdiv((long long)r * B, 256), 256, 0, s>>>(r, rz, B, L.uh0, L.vh0, L.ah0, L.dt, L.c2, Z);
+  launch_k(tc_predict_kernel, dim3(cdiv((long long)r * B, 256)), dim3(256), 0, s, r, rz, B, L.uh0, L.vh0, L.ah0, L.dt, L.c2, Z);
   debug_check("tc_predict_kernel", s);
   launch_rom_features(L.nf, B, L.feat_idx, Z, rz, Z + r + rb, rz, s);  // polynomial OpInf rows of Z
   *launches += L.nf > 0;
   if (rb > 0 && L.G) {  // folded exchange: g^ = G u^_src -> Z[r:, :]
     const int S = gemm(GemmArgs{rb, B, L.Gr, L.G, 1, rb, L.Gu, 1, L.Gr, nullptr, 0}, part, s);
-    reduce_splits_kernel<<<cdiv((long long)rb * B, 256), 256, 0, s>>>(rb, B, S, part, Z + r, 1, rz);
+    launch_k(reduce_splits_kernel, dim3(cdiv((long long)rb * B, 256)), dim3(256), 0, s, rb, B, S, part, Z + r, 1, rz);
     debug_check("reduce_splits_kernel", s);
     *launches += 2;
   } else if (rb > 0) {  // g^ = Phi_dS^T s  -> Z[r:, :]
     const int S = gemm(GemmArgs{rb, B, (int)L.n_sdof, L.Phi_s, L.n_sdof, 1, L.s, 1, L.n_sdof, nullptr, 0}, part, s);
-    reduce_splits_kernel<<<cdiv((long long)rb * B, 256), 256, 0, s>>>(rb, B, S, part, Z + r, 1, rz);
+    launch_k(reduce_splits_kernel, dim3(cdiv((long long)rb * B, 256)), dim3(256), 0, s, rb, B, S, part, Z + r, 1, rz);
     debug_check("reduce_splits_kernel", s);
     *launches += 2;
   }
@@ -235,7 +241,7 @@ void launch_rom_advance_tc(const RomLaunch& L, const double* KB, double* Z, doub
   }
   // araw = [-Kbar | Bbar] Z, reduced in the epilogue
   const int S = gemm(GemmArgs{r, B, rz, KB, 1, r, Z, 1, rz, nullptr, 0}, part, s);
-  tc_epilogue_kernel<<<dim3(cdiv(r, 256), B), 256, 0, s>>>(L, part, S, Z, rz, L.beta > 0.0 ? 2 : 0);
+  launch_k(tc_epilogue_kernel, dim3(dim3(cdiv(r, 256), B)), dim3(256), 0, s, L, part, S, Z, rz, L.beta > 0.0 ? 2 : 0);
   debug_check("tc_epilogue_kernel", s);
   *launches += 3;
   if (L.beta > 0.0) {
@@ -250,18 +256,18 @@ void launch_rom_accel_tc(const RomLaunch& L, const double* uh, double* ah, const
   const int r = L.r, rb = L.r_b, rz = L.r + L.r_b + L.nf, B = L.B;
   RomLaunch A = L;
   A.ah1 = ah;
-  tc_predict_kernel<<<cdiv((long long)r * B, 256), 256, 0, s>>>(r, rz, B, uh, uh, uh, 0.0, 0.0, Z);  // Z[0:r] = u^0
+  launch_k(tc_predict_kernel, dim3(cdiv((long long)r * B, 256)), dim3(256), 0, s, r, rz, B, uh, uh, uh, 0.0, 0.0, Z);  // Z[0:r] = u^0
   debug_check("tc_predict_kernel", s);
   launch_rom_features(L.nf, B, L.feat_idx, Z, rz, Z + r + rb, rz, s);
   *launches += L.nf > 0;
   if (rb > 0) {
     const int S = gemm(GemmArgs{rb, B, (int)L.n_sdof, L.Phi_s, L.n_sdof, 1, L.s, 1, L.n_sdof, nullptr, 0}, part, s);
-    reduce_splits_kernel<<<cdiv((long long)rb * B, 256), 256, 0, s>>>(rb, B, S, part, Z + r, 1, rz);
+    launch_k(reduce_splits_kernel, dim3(cdiv((long long)rb * B, 256)), dim3(256), 0, s, rb, B, S, part, Z + r, 1, rz);
     debug_check("reduce_splits_kernel", s);
     *launches += 2;
   }
   const int S = gemm(GemmArgs{r, B, rz, KB, 1, r, Z, 1, rz, nullptr, 0}, part, s);
-  tc_epilogue_kernel<<<dim3(cdiv(r, 256), B), 256, 0, s>>>(A, part, S, Z, rz, 1);
+  launch_k(tc_epilogue_kernel, dim3(dim3(cdiv(r, 256), B)), dim3(256), 0, s, A, part, S, Z, rz, 1);
   debug_check("tc_epilogue_kernel", s);
   *launches += 3;
 }
@@ -271,7 +277,7 @@ void launch_rom_lift_tc(int r, int B, long long nl, const double* Phi_lift, cons
                         const double* sv, long long ns, double* out, double* part, cudaStream_t st, int* launches) {
   if (nl == 0) return;
   const int S = gemm(GemmArgs{(int)nl, B, r, Phi_lift, r, 1, uh, 1, r, nullptr, 0}, part, st);
-  tc_lift_reduce_kernel<<<dim3(cdiv(nl, 256), B), 256, 0, st>>>(nl, B, S, part, code, sv, ns, out);
+  launch_k(tc_lift_reduce_kernel, dim3(dim3(cdiv(nl, 256), B)), dim3(256), 0, st, nl, B, S, part, code, sv, ns, out);
   debug_check("tc_lift_reduce_kernel", st);
   *launches += 2;
 }

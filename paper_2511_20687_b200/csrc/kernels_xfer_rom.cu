@@ -33,6 +33,7 @@ __global__ void transfer_kernel(int n, const int* __restrict__ idx, const double
                                 const int* __restrict__ out, const double* __restrict__ src, long long cs,
                                 long long bs_src, double* __restrict__ dst, long long bs_dst,
                                 const int* __restrict__ active, int compact) {
+  pdl_enter();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
   if (t >= 3 * n || (active != nullptr && !active[b])) return;
@@ -54,6 +55,7 @@ __global__ void transfer_kernel(int n, const int* __restrict__ idx, const double
 __global__ void trace_interp_kernel(int n, const int* __restrict__ out, const double* __restrict__ trace,
                                     long long slot_stride, int lo, double alpha, double* __restrict__ dst,
                                     long long bs_dst, const int* __restrict__ active) {
+  pdl_enter();
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
   if (p >= n || (active != nullptr && !active[b])) return;
@@ -69,6 +71,7 @@ __global__ void trace_interp_kernel(int n, const int* __restrict__ out, const do
 }
 
 __global__ void step_begin_kernel(Ctl c, int B) {
+  pdl_enter();
   const int b = threadIdx.x;
   for (int q = b; q < B; q += blockDim.x) {
     c.active[q] = 1;
@@ -99,13 +102,17 @@ __device__ __forceinline__ void any_active_body(const Ctl& c, int B) {
   if (c.has_cond) cudaGraphSetConditional(c.cond, more ? 1u : 0u);
 }
 
-__global__ void any_active_kernel(Ctl c, int B) { any_active_body(c, B); }
+__global__ void any_active_kernel(Ctl c, int B) {
+  pdl_enter();
+  any_active_body(c, B);
+}
 
 // one block of FIN_T threads per sample; the sweep that just ran is iteration n = *n_dev + 1.  fused
 // (B = 1): thread 0 then runs any_active_body itself (every thread read n_dev before the barrier)
 constexpr int FIN_T = 1024;
 __global__ void __launch_bounds__(FIN_T) finalize_kernel(Ctl c, const double2* __restrict__ part, int n_slots, int B,
                                                          int min_iters, double tol_rel, double tol_abs, int fused) {
+  pdl_enter();
   __shared__ double red[2][FIN_T / 32];
   const int b = blockIdx.x;
   const int t = threadIdx.x;
@@ -171,6 +178,7 @@ __global__ void __launch_bounds__(256) rom_project_bnd_kernel(int r_b, int B, lo
                                                               const double* __restrict__ Phi_s,
                                                               const double* __restrict__ s,
                                                               double* __restrict__ gpart) {
+  pdl_enter();
   const int k = blockIdx.x, z = blockIdx.y, b = blockIdx.z;
   const double* col = Phi_s + (long long)k * ns;
   const double* sb = s + (long long)b * ns;
@@ -184,6 +192,7 @@ __global__ void __launch_bounds__(256) rom_project_bnd_kernel(int r_b, int B, lo
 // u~ = u^ + dt v^ + c2 a^  (c2 = dt^2/2 explicit; dt^2 (1/2 - beta) implicit)
 __global__ void rom_predict_kernel(int r, int B, const double* __restrict__ uh, const double* __restrict__ vh,
                                    const double* __restrict__ ah, double dt, double c2, double* __restrict__ us) {
+  pdl_enter();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= r * B) return;
   us[t] = fma(c2, ah[t], fma(dt, vh[t], uh[t]));
@@ -195,6 +204,7 @@ __global__ void rom_predict_kernel(int r, int B, const double* __restrict__ uh, 
 // mode 1: acceleration only (initial condition); mode 2 (implicit): the right-hand side
 // e_b (-Kbar u~ + Bbar g^ ...) into ah1, finished by rom_implicit_kernel.
 __global__ void __launch_bounds__(256) rom_update_kernel(const RomLaunch L, int mode) {
+  pdl_enter();
   __shared__ double red[2][8];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int i = blockIdx.x * 8 + w;
@@ -256,6 +266,7 @@ __global__ void __launch_bounds__(256) rom_update_kernel(const RomLaunch L, int 
 __global__ void rom_lift_kernel(int r, int B, long long nl, const double* __restrict__ Phi_lift,
                                 const int* __restrict__ code, const double* __restrict__ uh,
                                 const double* __restrict__ s, long long ns, double* __restrict__ out) {
+  pdl_enter();
   const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= nl * B) return;
@@ -319,6 +330,7 @@ __global__ void sum_chunks_kernel(int r, int B, int nz, const double* __restrict
 // slot 0 of the sample (other slots 0).  ut: u~ with per-sample stride uts.
 __global__ void __launch_bounds__(256) rom_implicit_kernel(const RomLaunch L, const double* __restrict__ ut,
                                                            long long uts, int n_slots) {
+  pdl_enter();
   extern __shared__ double f[];
   const int b = blockIdx.x, r = L.r;
   if (!L.active[b]) return;
@@ -373,6 +385,7 @@ __device__ __forceinline__ double newton_block_sum(double v, double* red) {
 __global__ void __launch_bounds__(256) rom_newton_kernel(const RomLaunch L, const double* __restrict__ ut_all,
                                                          long long uts, const double* __restrict__ gsrc,
                                                          long long gstride, int gchunks, int n_slots) {
+  pdl_enter();
   extern __shared__ double sm[];
   __shared__ double red[8];
   __shared__ int piv;
@@ -567,8 +580,8 @@ __global__ void gather_dofs_kernel(long long n, int B, const int* __restrict__ i
 void launch_transfer(const XferMap& m, const double* src, long long cs, long long bs_src, double* dst,
                      long long bs_dst, int batch, const int* active, cudaStream_t s) {
   if (m.n == 0) return;
-  transfer_kernel<<<dim3(cdiv(3LL * m.n, 128), batch), 128, 0, s>>>(m.n, m.idx, m.xi, m.out, src, cs, bs_src, dst,
-                                                                      bs_dst, active, 0);
+  launch_k(transfer_kernel, dim3(cdiv(3LL * m.n, 128), batch), dim3(128), 0, s, m.n, m.idx, m.xi, m.out, src, cs,
+           bs_src, dst, bs_dst, active, 0);
   debug_check("transfer_kernel", s);
 }
 
@@ -576,7 +589,7 @@ void launch_transfer_trace(const XferMap& m, const double* src, long long cs, lo
                            const int* active, cudaStream_t s) {
   if (m.n == 0) return;
   const long long bs = 3LL * m.n;
-  transfer_kernel<<<dim3(cdiv(3LL * m.n, 128), batch), 128, 0, s>>>(m.n, m.idx, m.xi, m.out, src, cs, bs_src,
+  launch_k(transfer_kernel, dim3(dim3(cdiv(3LL * m.n, 128), batch)), dim3(128), 0, s, m.n, m.idx, m.xi, m.out, src, cs, bs_src,
                                                                       m.trace + (long long)slot * batch * bs, bs,
                                                                       active, 1);
   debug_check("transfer_kernel(trace)", s);
@@ -585,7 +598,7 @@ void launch_transfer_trace(const XferMap& m, const double* src, long long cs, lo
 void launch_trace_interp(const XferMap& m, int lo, double alpha, double* dst, long long bs_dst, int batch,
                          const int* active, cudaStream_t s) {
   if (m.n == 0) return;
-  trace_interp_kernel<<<dim3(cdiv(m.n, 128), batch), 128, 0, s>>>(m.n, m.out, m.trace, 3LL * m.n * batch, lo, alpha,
+  launch_k(trace_interp_kernel, dim3(dim3(cdiv(m.n, 128), batch)), dim3(128), 0, s, m.n, m.out, m.trace, 3LL * m.n * batch, lo, alpha,
                                                                     dst, bs_dst, active);
   debug_check("trace_interp_kernel", s);
 }
@@ -605,29 +618,31 @@ void launch_rom_newton(const RomLaunch& L, const double* ut, long long uts, cons
   const size_t smem = rom_newton_smem(L.r, L.r_b, L.nf);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(rom_newton_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  rom_newton_kernel<<<L.B, 256, smem, s>>>(L, ut, uts, gsrc, gstride, gchunks, n_slots);
+  launch_k(rom_newton_kernel, dim3(L.B), dim3(256), smem, s, L, ut, uts, gsrc, gstride, gchunks, n_slots);
   debug_check("rom_newton_kernel", s);
 }
 
 void launch_rom_implicit(const RomLaunch& L, const double* ut, long long uts, int n_slots, cudaStream_t s) {
-  rom_implicit_kernel<<<L.B, 256, sizeof(double) * L.r, s>>>(L, ut, uts, n_slots);
+  launch_k(rom_implicit_kernel, dim3(L.B), dim3(256), sizeof(double) * L.r, s, L, ut, uts, n_slots);
   debug_check("rom_implicit_kernel", s);
 }
 
-void launch_step_begin(Ctl c, int B, cudaStream_t s) { step_begin_kernel<<<1, 256, 0, s>>>(c, B); }
+void launch_step_begin(Ctl c, int B, cudaStream_t s) { launch_k(step_begin_kernel, dim3(1), dim3(256), 0, s, c, B); }
 
 int launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int min_iters, double tol_rel,
                     double tol_abs, cudaStream_t s) {
-  finalize_kernel<<<B, FIN_T, 0, s>>>(c, partial, n_slots, B, min_iters, tol_rel, tol_abs, B == 1 ? 1 : 0);
+  launch_k(finalize_kernel, dim3(B), dim3(FIN_T), 0, s, c, partial, n_slots, B, min_iters, tol_rel, tol_abs,
+           B == 1 ? 1 : 0);
   debug_check("finalize_kernel", s);
   if (B == 1) return 1;
-  any_active_kernel<<<1, 1, 0, s>>>(c, B);
+  launch_k(any_active_kernel, dim3(1), dim3(1), 0, s, c, B);
   debug_check("any_active_kernel", s);
   return 2;
 }
 
 __global__ void rom_features_kernel(int nf, int B, const int* __restrict__ idx, const double* __restrict__ u,
                                     long long us, double* __restrict__ F, long long fs) {
+  pdl_enter();
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
   if (q >= nf) return;
@@ -641,7 +656,7 @@ __global__ void rom_features_kernel(int nf, int B, const int* __restrict__ idx, 
 void launch_rom_features(int nf, int B, const int* idx, const double* u, long long us, double* F, long long fs,
                          cudaStream_t s) {
   if (nf == 0) return;
-  rom_features_kernel<<<dim3(cdiv(nf, 256), B), 256, 0, s>>>(nf, B, idx, u, us, F, fs);
+  launch_k(rom_features_kernel, dim3(dim3(cdiv(nf, 256), B)), dim3(256), 0, s, nf, B, idx, u, us, F, fs);
   debug_check("rom_features_kernel", s);
 }
 
@@ -651,9 +666,9 @@ int rom_partial_slots(int r, bool tc) { return (int)(tc ? cdiv(r, 256) : cdiv(r,
 
 void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches) {
   if (L.r_b > 0)
-    rom_project_bnd_kernel<<<dim3(L.r_b, rom_gchunks(L.n_sdof), L.B), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
+    launch_k(rom_project_bnd_kernel, dim3(dim3(L.r_b, rom_gchunks(L.n_sdof), L.B)), dim3(256), 0, s, L.r_b, L.B, L.n_sdof, L.Phi_s,
                                                                                    L.s, L.gh);
-  rom_predict_kernel<<<cdiv((long long)L.r * L.B, 256), 256, 0, s>>>(L.r, L.B, L.uh0, L.vh0, L.ah0, L.dt, L.c2,
+  launch_k(rom_predict_kernel, dim3(cdiv((long long)L.r * L.B, 256)), dim3(256), 0, s, L.r, L.B, L.uh0, L.vh0, L.ah0, L.dt, L.c2,
                                                                      L.ustar);
   launch_rom_features(L.nf, L.B, L.feat_idx, L.ustar, L.r, L.F, L.nf, s);
   *launches += L.nf > 0;
@@ -663,7 +678,7 @@ void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches) {
     *launches += (L.r_b > 0) + 2;
     return;
   }
-  rom_update_kernel<<<dim3(cdiv(L.r, 8), L.B), 256, 0, s>>>(L, L.beta > 0.0 ? 2 : 0);
+  launch_k(rom_update_kernel, dim3(dim3(cdiv(L.r, 8), L.B)), dim3(256), 0, s, L, L.beta > 0.0 ? 2 : 0);
   debug_check("rom_update_kernel", s);
   *launches += (L.r_b > 0) + 2;
   if (L.beta > 0.0) {
@@ -679,9 +694,9 @@ void launch_rom_accel(const RomLaunch& L, const double* uh, double* ah, cudaStre
   launch_rom_features(L.nf, L.B, L.feat_idx, uh, L.r, L.F, L.nf, s);
   *launches += L.nf > 0;
   if (L.r_b > 0)
-    rom_project_bnd_kernel<<<dim3(L.r_b, rom_gchunks(L.n_sdof), L.B), 256, 0, s>>>(L.r_b, L.B, L.n_sdof, L.Phi_s,
+    launch_k(rom_project_bnd_kernel, dim3(dim3(L.r_b, rom_gchunks(L.n_sdof), L.B)), dim3(256), 0, s, L.r_b, L.B, L.n_sdof, L.Phi_s,
                                                                                    L.s, L.gh);
-  rom_update_kernel<<<dim3(cdiv(L.r, 8), L.B), 256, 0, s>>>(A, 1);
+  launch_k(rom_update_kernel, dim3(dim3(cdiv(L.r, 8), L.B)), dim3(256), 0, s, A, 1);
   debug_check("rom_update_kernel", s);
   *launches += (L.r_b > 0) + 1;
 }
@@ -689,7 +704,7 @@ void launch_rom_accel(const RomLaunch& L, const double* uh, double* ah, cudaStre
 void launch_rom_lift(int r, int B, long long nl, const double* Phi_lift, const int* code, const double* uh,
                      const double* sv, long long ns, double* out, cudaStream_t st) {
   if (nl == 0) return;
-  rom_lift_kernel<<<cdiv(nl * B * 32, 256), 256, 0, st>>>(r, B, nl, Phi_lift, code, uh, sv, ns, out);
+  launch_k(rom_lift_kernel, dim3(cdiv(nl * B * 32, 256)), dim3(256), 0, st, r, B, nl, Phi_lift, code, uh, sv, ns, out);
   debug_check("rom_lift_kernel", st);
 }
 

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -266,6 +268,36 @@ struct ReplayArgs {
 };
 void launch_transpose_ops(int r, int rz, int B, const double* in_colmajor, double* out_rowmajor, cudaStream_t s);
 cudaError_t launch_replay(ReplayArgs A, cudaStream_t s);
+
+// Programmatic dependent launch (sm_90+): kernels launched with launch_k may be scheduled while their
+// stream predecessor finishes; each such kernel calls pdl_enter() first (lets its own dependents launch,
+// then waits for its predecessor's completion and memory), so the semantics are those of plain stream
+// order and only the launch latency overlaps.  OSAM_PDL=0 disables the attribute.
+inline bool pdl_enabled() {
+  static const bool on = !(getenv("OSAM_PDL") && getenv("OSAM_PDL")[0] == '0');
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+#endif
 
 // OSAM_DEBUG_SYNC=1: synchronise after every launch and report the first failing kernel on
 // stderr (development aid only; off by default).
