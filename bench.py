@@ -246,7 +246,7 @@ def roofline_of(prof, prof_ms, peak):
             "k1_share_of_step": prof["k1_ms"] / prof_ms}
 
 
-def largest_config(dev, stream, steps=30, warmup=3):
+def largest_config(dev, stream, steps=60, warmup=5):
     """North_star's HBM target is stated on the largest config (c4: 256^3 FOM between two r = 200
     ROMs with stand-in operators): steps/s and the K1 roofline there, measured the same way."""
     import torch
