@@ -232,6 +232,7 @@ struct Group {
   double2* partial = nullptr;
   // device control block: [flags0, flags1, active[B], iters[B], n, step, sticky0, sticky1]
   int* ctl_i = nullptr;
+  int* go = nullptr;  // persistent small-group controller: continue flag
   double* numden = nullptr;
   int* h_ctl = nullptr;  // pinned copy
   int* iters_all = nullptr;
@@ -258,6 +259,7 @@ struct Group {
     if (cap_main) cudaStreamDestroy(cap_main);
     dfree(partial);
     dfree(ctl_i);
+    dfree(go);
     dfree(numden);
     dfree(iters_all);
     if (h_ctl) cudaFreeHost(h_ctl);
@@ -599,6 +601,10 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
     TRY(upload(&m.xi, P.xi, d.stream));
     TRY(upload(&m.out, P.out, d.stream));
     m.n_src_sub = src.n_sub;
+    for (size_t t = 0; t < P.out.size() && !m.reads_src_schwarz; ++t)
+      if (P.out[t] >= 0)
+        for (int q = 0; q < 8; ++q)
+          if (src.codes[3 * P.corner[8 * (t / 3) + q] + (int)(t % 3)] == DOF_SCHWARZ) m.reads_src_schwarz = true;
     if (fold) {  // G[k + r_b j] = sum over the map's Schwarz DOFs and corners of Phi_dS[sd, k] w Phi_lift[row, j]
       const long long nl = src.n_lift;
       std::vector<double> G((size_t)d.r_b * src.r, 0.0);
@@ -1505,7 +1511,50 @@ int osam_step(osam_subdomain* const* sds, int32_t n_sd, const osam_schwarz_cfg* 
     CK(cudaMemsetAsync(G->ctl_i + 3 + 2 * B, 0, sizeof(int) * 3, st));
   }
   static const bool nograph = getenv("OSAM_NOGRAPH") && getenv("OSAM_NOGRAPH")[0] == '1';
-  if (g_prof || nograph) {
+  // small all-FOM groups: one cooperative persistent launch for every step of this call
+  bool persist = n_steps > 0 && !g_prof && !nograph && B == 1 && n_sd <= SMALL_MAX_SD && !G->trace &&
+                 !(getenv("OSAM_SMALL_PERSIST") && getenv("OSAM_SMALL_PERSIST")[0] == '0');
+  for (int i = 0; i < n_sd && persist; ++i) {
+    const Sub& d = sds[i]->s;
+    persist = d.kind == OSAM_FOM && d.material == OSAM_LINEAR && d.n_sub == 1 && fom_small(d.g) &&
+              d.maps.size() <= 6 && d.ux == 1 - d.cur;
+  }
+  if (persist) {
+    SmallArgs A{};
+    A.n_sd = n_sd;
+    int slot = 0;
+    for (int i = 0; i < n_sd; ++i) {
+      Sub& d = sds[i]->s;
+      SmallSub& ss = A.s[i];
+      ss.L = fom_launch(d, nullptr, nullptr, nullptr, nullptr, cfg->dt, cfg->dt, 0.5 * cfg->dt, cfg->dt, 0, nullptr,
+                        nullptr);
+      for (int b = 0; b < 2; ++b)
+        for (int q = 0; q < 2; ++q) ss.st[b][q] = d.st[b][q];
+      ss.cur0 = d.cur;
+      ss.slot0 = slot;
+      ss.nvb = fom_slots(d);
+      slot += ss.nvb;
+      ss.n_maps = (int)d.maps.size();
+      for (int k = 0; k < ss.n_maps; ++k) {
+        const XferMap& m = d.maps[k];
+        ss.maps[k] = SmallMap{m.n, m.src, m.idx, m.out, m.xi};
+      }
+    }
+    A.n_steps = n_steps;
+    A.tol_rel = cfg->tol_rel;
+    A.tol_abs = cfg->tol_abs;
+    A.min_iters = cfg->min_iters;
+    A.max_iters = cfg->max_iters;
+    A.n_slots = G->n_slots;
+    A.partial = G->partial;
+    A.ctl = G->ctl(cfg->max_iters);
+    if (!G->go) TRY(dalloc(&G->go, 1));
+    A.go = G->go;
+    CK(launch_small_persistent(A, st));
+    ++g_launches;
+    if (n_steps & 1)
+      for (int i = 0; i < n_sd; ++i) commit_step(sds[i]->s);  // the roles alternate every step
+  } else if (g_prof || nograph) {
     for (int k = 0; k < n_steps; ++k) {
       const int rc = controller_step_host(*G, *cfg, st);
       if (rc < 0) return rc;
@@ -1530,7 +1579,7 @@ int osam_step(osam_subdomain* const* sds, int32_t n_sd, const osam_schwarz_cfg* 
   CK(cudaGetLastError());
   if (n_steps > 0) {
     if (iters_out) std::memcpy(iters_out, its.data(), sizeof(int32_t) * its.size());
-    if (!(g_prof || nograph)) {  // kernels the graphs ran: step_begin + the sweeps (max over samples)
+    if (!(g_prof || nograph) && !persist) {  // kernels the graphs ran: step_begin + the sweeps (max over samples)
       for (int k = 0; k < n_steps; ++k) {
         int nmax = 0;
         for (int b = 0; b < B; ++b) nmax = std::max(nmax, its[(size_t)k * B + b]);

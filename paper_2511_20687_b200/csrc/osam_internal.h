@@ -63,6 +63,7 @@ struct XferMap {
   // reduced boundary input g^ = G u^_src with G = Phi_dS^T Pi Phi_src[donor rows] (r_b x r_src, column-
   // major), replacing lift, transfer and boundary projection
   double* G = nullptr;
+  bool reads_src_schwarz = false;  // some donor corner is a Schwarz DOF of the source (its s enters)
 };
 
 struct Sub {
@@ -269,6 +270,7 @@ struct ReplayArgs {
 void launch_transpose_ops(int r, int rz, int B, const double* in_colmajor, double* out_rowmajor, cudaStream_t s);
 cudaError_t launch_replay(ReplayArgs A, cudaStream_t s);
 
+
 // Programmatic dependent launch (sm_90+): kernels launched with launch_k may be scheduled while their
 // stream predecessor finishes; each such kernel calls pdl_enter() first (lets its own dependents launch,
 // then waits for its predecessor's completion and memory), so the semantics are those of plain stream
@@ -317,6 +319,40 @@ struct Ctl {
   cudaGraphConditionalHandle cond;
 };
 void launch_step_begin(Ctl c, int B, cudaStream_t s);
+
+// Persistent controller for small all-FOM groups (kernels_fom.cu small_persistent_kernel): one cooperative
+// launch runs every controller step of an osam_step call -- the transfers in sweep order, the K1S node blocks
+// of every subdomain, K3 and the controller flags, separated by grid-wide barriers -- with the buffer roles
+// alternating by step parity on the device.
+struct SmallMap {
+  int n, src;
+  const int *idx, *out;
+  const double* xi;
+};
+struct SmallSub {
+  FomLaunch L;           // template: geometry, faces, stencil table, masses, coefficients
+  double* st[2][2];      // the two (q, w) buffers
+  int slot0, nvb;        // first partial slot, K1S node blocks
+  int cur0;              // checkpoint buffer index at the first step
+  int n_maps;
+  SmallMap maps[6];
+};
+constexpr int SMALL_MAX_SD = 4;
+struct SmallArgs {
+  int n_sd;
+  SmallSub s[SMALL_MAX_SD];
+  int n_steps;
+  double tol_rel, tol_abs;
+  int min_iters, max_iters;
+  int n_slots;
+  double2* partial;
+  Ctl ctl;
+  int* go;             // device int: the sweep loop continues (written by K3, read after the barrier)
+};
+cudaError_t launch_small_persistent(const SmallArgs& A, cudaStream_t s);
+int small_persistent_grid();  // CTAs that can be co-resident (cooperative launch bound)
+bool fom_small(const Geom& g);  // the K1S (gather) path applies (OSAM_GATHER_MAX)
+
 // Convergence test of the sweep that just ran (iteration n = *n_dev + 1): K3 + flags/conditional.
 // Returns the number of kernels launched (1 for a single sample: K3 and the flag update fused).
 int launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int min_iters, double tol_rel,

@@ -1,4 +1,4 @@
-"""GPU parity of the small-subdomain FOM path K1S (fom_gather_kernel: every node one 4-lane gather of the
+"""GPU parity of the small-subdomain FOM path K1S and of the persistent controller for small all-FOM groups (fom_gather_kernel: every node one 4-lane gather of the
 class-table stencil, used below OSAM_GATHER_MAX nodes) against the oracle, on the cases that exercise every
 node class, the controller variants and the exchange paths."""
 import numpy as np
@@ -10,9 +10,12 @@ from test_gpu_parity import _substeps, run_both  # noqa: F401  (shared GPU-vs-or
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True)
-def gather_path(monkeypatch):
+@pytest.fixture(autouse=True, params=["persistent", "graph"])
+def gather_path(monkeypatch, request):
+    """K1S everywhere; small all-FOM groups run either the cooperative persistent controller (default) or the
+    per-step CUDA graph (OSAM_SMALL_PERSIST=0)."""
     monkeypatch.setenv("OSAM_GATHER_MAX", str(1 << 30))
+    monkeypatch.setenv("OSAM_SMALL_PERSIST", "1" if request.param == "persistent" else "0")
 
 
 @pytest.fixture(scope="module")
