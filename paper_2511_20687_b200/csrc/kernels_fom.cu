@@ -446,6 +446,10 @@ struct Prod {
 
 __device__ __forceinline__ void prod_issue(const FomLaunch& L, const TileGrid& G, Prod& pr, unsigned char* ring,
                                            unsigned long long* full, const Maps& M) {
+#ifdef OSAM_NOLOAD  // probe: only the first ring fill is loaded; later planes reuse stale (finite) data
+  if (pr.issued >= NSTAGE) mbar_arrive(&full[pr.issued % NSTAGE]);
+  else
+#endif
   issue_plane(pr.P, pr.wp != 0, pr.it, pr.issued % NSTAGE, ring, full, M);
   ++pr.issued;
   if (++pr.it == pr.P.nplanes) {
