@@ -1020,17 +1020,30 @@ long long tile_count(const Geom& g, const Faces& f) {
 }
 
 // the excluded x+ column (see xlast_excluded): Q' = X, W' = 0, a = 0 on every node of the face
-__global__ void xlast_copy_kernel(const FomLaunch L) {
+// The excluded last x column: Q' = X (prescribed), W' = a = 0.  XL_PER nodes per thread with every
+// load issued first (each node is its own cache line, so the kernel is latency-bound).
+constexpr int XL_PER = 8;
+__global__ void __launch_bounds__(128) xlast_copy_kernel(const FomLaunch L) {
   const Geom& g = L.g;
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (t >= (long long)g.nn[1] * g.nn[2]) return;
-  const int j = (int)(t % g.nn[1]), k = (int)(t / g.nn[1]);
-  const long long id = gidx(g, g.nn[0] - 1, j, k);
+  const long long n = (long long)g.nn[1] * g.nn[2], np = g.npad;
+  long long ids[XL_PER];
+  double v[XL_PER][3];
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    if (L.q_out) L.q_out[c * g.npad + id] = L.x[c * g.npad + id];
-    L.w_out[c * g.npad + id] = 0.0;
-    if (L.a_out) L.a_out[c * g.npad + id] = 0.0;
+  for (int q = 0; q < XL_PER; ++q) {
+    const long long t = ((long long)blockIdx.x * XL_PER + q) * 128 + threadIdx.x;
+    ids[q] = t < n ? gidx(g, g.nn[0] - 1, (int)(t % g.nn[1]), (int)(t / g.nn[1])) : -1;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) v[q][c] = (ids[q] >= 0 && L.q_out) ? L.x[c * np + ids[q]] : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < XL_PER; ++q) {
+    if (ids[q] < 0) continue;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      if (L.q_out) L.q_out[c * np + ids[q]] = v[q][c];
+      L.w_out[c * np + ids[q]] = 0.0;
+      if (L.a_out) L.a_out[c * np + ids[q]] = 0.0;
+    }
   }
 }
 
@@ -1404,8 +1417,16 @@ void launch_fom_advance_nl(const FomLaunch& L, cudaStream_t s, int* launches) {
   ++*launches;
 }
 
+void launch_fom_xlast(const FomLaunch& L, cudaStream_t s, int* launches) {
+  if (L.material != OSAM_LINEAR || small_fom(L.g) || !xlast_excluded(L.g, L.f)) return;
+  xlast_copy_kernel<<<cdiv((long long)L.g.nn[1] * L.g.nn[2], 128 * XL_PER), 128, 0, s>>>(L);
+  debug_check("xlast_copy_kernel", s);
+  ++*launches;
+}
+
 void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUtensorMap* tmx,
-                        const CUtensorMap* tmw, const CUtensorMap* tmwp, cudaStream_t s, int* launches) {
+                        const CUtensorMap* tmw, const CUtensorMap* tmwp, cudaStream_t s, int* launches,
+                        bool with_xlast) {
   if (L.material != OSAM_LINEAR) {  // SVK / Neohookean: NL1 (no stencil, no TMA maps)
     launch_fom_advance_nl(L, s, launches);
     return;
@@ -1425,11 +1446,7 @@ void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUt
     fom_tiled_kernel<false><<<grid, dim3(TX, TY), SMEM_TILED, s>>>(Lt, st, *tmx, *tmw, *tmwp);
   debug_check("fom_tiled_kernel", s);
   ++*launches;
-  if (xlast_excluded(L.g, L.f)) {
-    xlast_copy_kernel<<<cdiv((long long)L.g.nn[1] * L.g.nn[2], 256), 256, 0, s>>>(L);
-    debug_check("xlast_copy_kernel", s);
-    ++*launches;
-  }
+  if (with_xlast) launch_fom_xlast(L, s, launches);
 }
 
 // 4D (x, y, z, component) descriptor of a padded SoA field; halo = true: the X box (tile plus a

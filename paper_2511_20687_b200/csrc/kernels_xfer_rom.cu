@@ -203,6 +203,7 @@ __global__ void rom_predict_kernel(int r, int B, const double* __restrict__ uh, 
 // partial (num, den) sums its warps in order: grid (ceil(r/8), B), slot = blockIdx.x, layout [slot][B].
 // mode 1: acceleration only (initial condition); mode 2 (implicit): the right-hand side
 // e_b (-Kbar u~ + Bbar g^ ...) into ah1, finished by rom_implicit_kernel.
+constexpr int UPD_GS_MAX = 1024;  // r_b staged in shared memory up to this (else per row, same order)
 __global__ void __launch_bounds__(256) rom_update_kernel(const RomLaunch L, int mode) {
   pdl_enter();
   __shared__ double red[2][8];
@@ -211,15 +212,30 @@ __global__ void __launch_bounds__(256) rom_update_kernel(const RomLaunch L, int 
   const int b = blockIdx.y;
   const int r = L.r, rz = L.r + L.r_b + L.nf;
   const bool on = i < r && (mode == 1 || L.active[b]);
+  // g^[., b] = chunk partials summed in order, once per block (every row of the block reads it)
+  __shared__ double gs[UPD_GS_MAX];
+  const bool gsm = L.r_b <= UPD_GS_MAX;
+  if (gsm) {
+    for (int k = threadIdx.x; k < L.r_b; k += 256) {
+      double g = 0.0;
+      for (int z = 0; z < L.gchunks; ++z) g += L.gh[((long long)z * L.B + b) * L.r_b + k];
+      gs[k] = g;
+    }
+    __syncthreads();
+  }
   double num = 0.0, den = 0.0;
   if (on) {
     const double* row = L.KBr + (long long)i * rz;
     const double* us = L.ustar + (long long)r * b;
     double acc = 0.0;
+#pragma unroll 4
     for (int j = lane; j < r; j += 32) acc = fma(row[j], us[j], acc);
     for (int k = lane; k < L.r_b; k += 32) {
       double g = 0.0;  // g^[k, b]: chunk partials in order
-      for (int z = 0; z < L.gchunks; ++z) g += L.gh[((long long)z * L.B + b) * L.r_b + k];
+      if (gsm)
+        g = gs[k];
+      else
+        for (int z = 0; z < L.gchunks; ++z) g += L.gh[((long long)z * L.B + b) * L.r_b + k];
       acc = fma(row[r + k], g, acc);
     }
     const double* fb = L.F + (long long)L.nf * b;  // polynomial OpInf features
@@ -262,39 +278,61 @@ __global__ void __launch_bounds__(256) rom_update_kernel(const RomLaunch L, int 
 }
 
 // out[b][ld] = code>=0 ? sum_j Phi_lift[ld, j] uh[j, b] : (code == -1 ? 0 : s[b][-2-code])
-// (a warp per row; 16-byte loads when r is even)
+// A warp per LIFT_ROWS consecutive rows (their loads interleaved: more bytes in flight per warp, the
+// read of Phi_lift is the HBM-relevant ROM traffic of c4), 16-byte loads when r is even; each row is
+// summed per lane over j and then by the butterfly, as with one row per warp.
+constexpr int LIFT_ROWS = 4;
 __global__ void rom_lift_kernel(int r, int B, long long nl, const double* __restrict__ Phi_lift,
                                 const int* __restrict__ code, const double* __restrict__ uh,
                                 const double* __restrict__ s, long long ns, double* __restrict__ out) {
   pdl_enter();
   const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (w >= nl * B) return;
-  const long long ld = w % nl;
-  const int b = (int)(w / nl);
-  const int cd = code[ld];
-  double v = 0.0;
-  if (cd >= 0) {
-    const double* row = Phi_lift + (long long)cd * r;
-    const double* u = uh + (long long)r * b;
-    double acc = 0.0;
-    if ((r & 1) == 0) {
-      const double2* row2 = reinterpret_cast<const double2*>(row);
-      const double2* u2 = reinterpret_cast<const double2*>(u);
-#pragma unroll 4
-      for (int j = lane; j < r / 2; j += 32) {
-        const double2 a = row2[j], x = u2[j];
-        acc = fma(a.x, x.x, acc);
-        acc = fma(a.y, x.y, acc);
-      }
-    } else {
-      for (int j = lane; j < r; j += 32) acc = fma(row[j], u[j], acc);
-    }
-    v = warp_sum(acc);
-  } else if (cd <= -2) {
-    v = s[(long long)b * ns + (-2 - cd)];
+  const long long nw = (nl + LIFT_ROWS - 1) / LIFT_ROWS;  // warps per sample
+  if (w >= nw * B) return;
+  const int b = (int)(w / nw);
+  const long long ld0 = (w % nw) * LIFT_ROWS;
+  int cd[LIFT_ROWS];
+  const double* row[LIFT_ROWS];
+  double acc[LIFT_ROWS];
+#pragma unroll
+  for (int q = 0; q < LIFT_ROWS; ++q) {
+    cd[q] = ld0 + q < nl ? code[ld0 + q] : -1;
+    row[q] = Phi_lift + (long long)(cd[q] >= 0 ? cd[q] : 0) * r;
+    acc[q] = 0.0;
   }
-  if (lane == 0) out[(long long)b * nl + ld] = v;
+  const double* u = uh + (long long)r * b;
+  if ((r & 1) == 0) {
+    const double2* u2 = reinterpret_cast<const double2*>(u);
+#pragma unroll 2
+    for (int j = lane; j < r / 2; j += 32) {
+      const double2 x = u2[j];
+#pragma unroll
+      for (int q = 0; q < LIFT_ROWS; ++q)
+        if (cd[q] >= 0) {
+          const double2 a = reinterpret_cast<const double2*>(row[q])[j];
+          acc[q] = fma(a.x, x.x, acc[q]);
+          acc[q] = fma(a.y, x.y, acc[q]);
+        }
+    }
+  } else {
+    for (int j = lane; j < r; j += 32) {
+      const double x = u[j];
+#pragma unroll
+      for (int q = 0; q < LIFT_ROWS; ++q)
+        if (cd[q] >= 0) acc[q] = fma(row[q][j], x, acc[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < LIFT_ROWS; ++q) {
+    if (ld0 + q >= nl) break;
+    double v = 0.0;
+    if (cd[q] >= 0)
+      v = warp_sum(acc[q]);
+    else if (cd[q] <= -2)
+      v = s[(long long)b * ns + (-2 - cd[q])];
+    if (lane == 0) out[(long long)b * nl + ld0 + q] = v;
+  }
 }
 
 // Projection onto the POD basis (IC only): part[z][b][i] = sum over row chunk z of
@@ -704,7 +742,8 @@ void launch_rom_accel(const RomLaunch& L, const double* uh, double* ah, cudaStre
 void launch_rom_lift(int r, int B, long long nl, const double* Phi_lift, const int* code, const double* uh,
                      const double* sv, long long ns, double* out, cudaStream_t st) {
   if (nl == 0) return;
-  launch_k(rom_lift_kernel, dim3(cdiv(nl * B * 32, 256)), dim3(256), 0, st, r, B, nl, Phi_lift, code, uh, sv, ns, out);
+  launch_k(rom_lift_kernel, dim3(cdiv(cdiv(nl, LIFT_ROWS) * B * 32, 256)), dim3(256), 0, st, r, B, nl, Phi_lift, code, uh,
+           sv, ns, out);
   debug_check("rom_lift_kernel", st);
 }
 

@@ -897,9 +897,12 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
         joins.push_back(set + i);
       }
       if (fom_k && g_prof) CK(cudaEventRecord(G.ev[2 * *fom_k], st));
-      launch_fom_advance(L, d.stencil, &d.tmap[c], &d.tmapw[c], &d.tmapw[x], ks, launches);
+      launch_fom_advance(L, d.stencil, &d.tmap[c], &d.tmapw[c], &d.tmapw[x], ks, launches, !par);
       if (fom_k && g_prof) CK(cudaEventRecord(G.ev[2 * *fom_k + 1], st));
-      if (par) CK(cudaEventRecord(G.join_ev[set + i], ks));
+      if (par) {
+        CK(cudaEventRecord(G.join_ev[set + i], ks));
+        launch_fom_xlast(L, st, launches);  // concurrently with the tiled kernel on the side stream
+      }
       if (fom_k) ++*fom_k;
       // algorithmic bytes: read q, w and write q', w' (32 B/DOF) + the previous w' of the DOFs within one
       // layer of a Schwarz face from sweep 2 on (R38)

@@ -179,8 +179,12 @@ struct FomLaunch {
 // Number of partial slots a K1 launch writes (tiled blocks + x-face blocks).
 int fom_partial_slots(const Geom& g, const Faces& f);
 int fom_nl_partial_slots(const Geom& g);  // NL1 (nonlinear materials): one slot per CTA
+// with_xlast = false: the caller launches the excluded last x column (launch_fom_xlast) itself, e.g. on
+// another stream concurrently with the tiled kernel (it reads only X and writes only that column).
 void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUtensorMap* tmx,
-                        const CUtensorMap* tmw, const CUtensorMap* tmwp, cudaStream_t s, int* launches);
+                        const CUtensorMap* tmw, const CUtensorMap* tmwp, cudaStream_t s, int* launches,
+                        bool with_xlast = true);
+void launch_fom_xlast(const FomLaunch& L, cudaStream_t s, int* launches);
 int make_field_tmap(const Geom& g, double* array, bool halo, CUtensorMap* out);
 
 void launch_transfer(const XferMap& m, const double* src, long long src_cstride, long long src_bstride,

@@ -436,7 +436,7 @@ def test_c5_shaped_batched_implicit_cubic_rom(gpu, monkeypatch, tc):
 
 def test_xlast_column_excluded_c1_variant(gpu):
     """nx a multiple of the 32-node tile and a Schwarz x+ face: the last node column leaves the tiled grid
-    (xlast_copy_kernel writes its prescribed values)."""
+    (the xlast CTAs of the tiled launch write its prescribed values)."""
     import copy
     cfg = copy.deepcopy(I.config("c1"))
     cfg["subdomains"][0] = dict(cfg["subdomains"][0], nel=(32, 5, 5))
