@@ -229,6 +229,24 @@ def test_max_iters_reached_keeps_last_iterate(gpu, max_iters):
     compare(gpu, subs, models, states)
 
 
+@pytest.mark.parametrize("prof", [False, True])
+def test_unstable_returns_eunstable(gpu, prof):
+    """Tiled K1, graph controller and host-driven loop: dt 40x the stability limit overflows the state and
+    osam_step returns OSAM_EUNSTABLE (include/osam.h: non-finite convergence norm)."""
+    from paper_2511_20687_b200 import osam
+    cfg = I.scaled(I.config("c3"), 10.0)
+    cfg = dict(cfg, dt=40.0 * cfg["dt"])
+    osam.set_profiling(prof)
+    try:
+        subs = gpu.build(cfg)
+        gpu.set_ics(cfg, subs, device="cuda:0")
+        with pytest.raises(osam.OsamError) as e:
+            gpu.run(cfg, subs, n_steps=200)
+        assert e.value.code == -5
+    finally:
+        osam.set_profiling(False)
+
+
 @pytest.mark.parametrize("order", [2, 3])
 def test_c2_polynomial_opinf(gpu, order):
     """QOpInf / COpInf (eq:quadratic_opinf): c2's FOM-ROM coupling with a quadratic or cubic

@@ -75,3 +75,32 @@ def test_c2_fom_rom_gather(gpu):
     from oracle import opinf
     cfg = I.config("c2")
     run_both(gpu, cfg, 150, rom_ops=opinf.train(cfg, I), checkpoints=(1,))
+
+
+@pytest.mark.parametrize("max_iters", [1, 2])
+def test_max_iters_gather(gpu, max_iters):
+    """The cap on the small path (both controllers): OSAM_WNOTCONVERGED, the last iterate kept (R9), equal
+    to the oracle run with the same cap, over an odd number of steps (the persistent kernel's role swap)."""
+    from test_gpu_parity import compare, oracle_run
+    cfg = dict(I.config("c1"), max_iters=max_iters)
+    subs = gpu.build(cfg)
+    gpu.set_ics(cfg, subs, device="cuda:0")
+    status, iters = gpu.run(cfg, subs, n_steps=5)
+    assert status == 1
+    assert (iters == max_iters).all()
+    models, states, it_ref, _ = oracle_run(cfg, 5)
+    assert np.array_equal(iters, it_ref.reshape(iters.shape))
+    compare(gpu, subs, models, states)
+
+
+def test_unstable_gather(gpu):
+    """dt 40x the explicit stability limit: the state overflows within ~100 steps and osam_step returns
+    OSAM_EUNSTABLE (non-finite convergence norm) on both controllers."""
+    from paper_2511_20687_b200 import osam
+    cfg = I.config("c1")
+    cfg = dict(cfg, dt=40.0 * cfg["dt"])
+    subs = gpu.build(cfg)
+    gpu.set_ics(cfg, subs, device="cuda:0")
+    with pytest.raises(osam.OsamError) as e:
+        gpu.run(cfg, subs, n_steps=200)
+    assert e.value.code == -5
