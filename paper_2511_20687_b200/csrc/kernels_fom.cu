@@ -582,6 +582,12 @@ __device__ __noinline__ void xface_body(const FomLaunch& L, int side_mask, int b
 #ifndef OSAM_MINB
 #define OSAM_MINB 4
 #endif
+#ifndef OSAM_K1_ROT
+// 0 (default): one copy of k1_iter per plane, the accumulator roles moved through the slots (9 moves per
+// plane); 1: k1_iter unrolled by the period 3 of the roles (no moves).  The single copy keeps the loop in
+// the instruction cache: c3 845 -> 891 steps/s (K1 0.203 -> 0.193 ms), 80 KB -> 54 KB of SASS, no spills.
+#define OSAM_K1_ROT 0
+#endif
 template <bool ZN>
 __global__ void __launch_bounds__(NT, OSAM_MINB)
     fom_tiled_kernel(const __grid_constant__ FomLaunch L, const __grid_constant__ InteriorStencil S,
@@ -637,6 +643,7 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
     T.kend = P.kend;
     T.nplanes = P.nplanes;
     T.id0 = T.i + (long long)g.px * T.j;
+#if OSAM_K1_ROT
     for (int it = 0; it < T.nplanes;) {  // unrolled by the period 3 of the slot rotation
       k1_iter<ZN, 0, 1, 2>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
       ++gi;
@@ -648,6 +655,19 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
       ++gi;
       ++it;
     }
+#else
+    // one copy of the iteration; the roles move through the slots (C, zeroed by k1_iter, becomes A)
+#pragma unroll 1
+    for (int it = 0; it < T.nplanes; ++it, ++gi) {
+      k1_iter<ZN, 0, 1, 2>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        acc[2][c] = acc[1][c];
+        acc[1][c] = acc[0][c];
+        acc[0][c] = 0.0;
+      }
+    }
+#endif
 #pragma unroll
     for (int q = 0; q < 3; ++q)
 #pragma unroll
