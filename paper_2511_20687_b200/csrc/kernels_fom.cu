@@ -191,6 +191,11 @@ constexpr int W_BYTES = 3 * WPL * 8;
 constexpr int STAGE_BYTES = ARR_STRIDE + 2 * W_BYTES;  // X, W, W'_prev
 constexpr int SMEM_TILED = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8 + 64;  // ring, barriers, producer cursor
 
+#ifndef OSAM_NL_UNROLL
+#define OSAM_NL_UNROLL 2
+#endif
+constexpr int NL_UNROLL = OSAM_NL_UNROLL;  // NL1: unroll of the Gauss-point loop
+
 // ---- interior rows: parity-reduced stencil ---------------------------------------------
 // On a uniform box every interior block K_cd(ox, oy, oz) is even or odd in ox and in oy (the 1D
 // factors M, S are symmetric, G, Gt antisymmetric): diagonal blocks even-even, xy/yx odd-odd,
@@ -1212,7 +1217,7 @@ __device__ __forceinline__ void element_forces(const FomLaunch& L, UA ua, const 
         D[j][i][p] = ua(a0 | (1 << j), i) - ua(a0, i);
       }
   }
-#pragma unroll 2
+#pragma unroll NL_UNROLL
   for (int q = 0; q < 8; ++q) {
     const double* wg = wtab + q * 24;  // [j][p] gradient weights, then [j][p] accumulation weights
     double F[3][3];

@@ -12,5 +12,5 @@ timeout 600 python bench.py > gpurun_out/bench_$TAG.log 2>&1
 # ncu cannot profile kernel nodes of graphs with conditional nodes: host-driven sweeps for ncu
 export OSAM_NOGRAPH=1
 timeout 300 $B > gpurun_out/plain_$TAG.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv $B > gpurun_out/ncu1_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fom_ -s 8 -c 4 -o gpurun_out/prof_$TAG $B > gpurun_out/ncu2_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fom_tiled -s 6 -c 6 -o gpurun_out/prof_$TAG $B > gpurun_out/ncu2_$TAG.log 2>&1
 echo done
