@@ -25,10 +25,12 @@
 //     wait for data, the producer waits for the slowest warp to release a stage).  Each thread
 //     forms, per staged plane and component, the 9 parity combinations of its 3x3 in-plane
 //     neighbourhood and applies them to the forces of node planes m+1, m, m-1 held in registers
-//     (2.5D streaming; accumulator roles rotate with period 3, unrolled).  A warp is one x-row, so
-//     the (y, z) boundary class is warp-uniform: interior rows use the parity-reduced interior
-//     stencil, face rows their class table (out of line).  Lanes on an x-face write it only when
-//     the face is fully constrained (no force needed).
+//     (2.5D streaming; the accumulator roles move through three register slots once per plane).
+//     Two tile shapes are compiled from k1_tiled.cuh and picked per subdomain by k1_shape: 32 x 4 (a
+//     warp is one x-row, so the (y, z) boundary class is warp-uniform) and 16 x 8 (a warp is two
+//     16-node rows; for boxes whose x extent leaves most of a 32-wide column idle).  Interior rows use
+//     the parity-reduced interior stencil, face rows their class table (out of line).  Lanes on an
+//     x-face write it only when the face is fully constrained (no force needed).
 //   * the x-face kernel covers x-faces with free DOFs (a node per thread, class table).
 // No atomics; every sum has a fixed order, so results are bitwise repeatable.
 #include <algorithm>
@@ -44,18 +46,6 @@ namespace osam {
 
 namespace {
 
-constexpr int TX = 32;
-#ifndef OSAM_TY
-#define OSAM_TY 4
-#endif
-constexpr int TY = OSAM_TY;
-constexpr int NT = TX * TY;
-constexpr int NWARP = NT / 32;
-#ifndef OSAM_ZC
-#define OSAM_ZC 24
-#endif
-constexpr int ZC = OSAM_ZC;  // target z-planes per block (balanced split)
-constexpr int XF_BLOCK = NT;  // x-face work runs in extra CTAs of the tiled kernel (same block)
 
 __device__ __forceinline__ long long gidx(const Geom& g, int i, int j, int k) {
   return i + (long long)g.px * j + g.plane * k;
@@ -174,591 +164,51 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// Staged x-range [x0, x0 + PX) with x0 = 32 bx - 2: the TMA box must start on a 16-byte
-// boundary in the innermost dimension (an odd fp64 start coordinate raises an illegal
-// instruction on sm_100a), so the left halo is two columns wide (the first is unused).
-constexpr int PX = TX + 4;
-constexpr int PY = TY + 2;
-constexpr int PLANE = PX * PY;                             // positions per staged plane
-#ifndef OSAM_NSTAGE
-#define OSAM_NSTAGE 4
+
+inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+// ---- K1 tiled kernel, one instance per tile shape (k1_tiled.cuh) --------------------------------
+// k1a: 32 x OSAM_TY (default 4) -- a warp is one x-row; k1b: 16 x 8 -- a warp is two 16-node rows, for
+// boxes whose x extent leaves most of a 32-wide tile column idle (c3: 142 / 111 nodes).  k1_shape picks
+// per subdomain from the lane occupancy of the two tilings.
+#ifndef OSAM_TY
+#define OSAM_TY 4
 #endif
-constexpr int NSTAGE = OSAM_NSTAGE;  // ring: NSTAGE-2 planes in flight, current, previous
-constexpr int ARR_BYTES = 3 * PLANE * 8;                   // X (x,y,z comps) of one plane, with halo
-constexpr int ARR_STRIDE = (ARR_BYTES + 127) / 128 * 128;  // 128-B aligned TMA destinations
-constexpr int WPL = TX * TY;                               // tile positions of W (no halo)
-constexpr int W_BYTES = 3 * WPL * 8;
-constexpr int STAGE_BYTES = ARR_STRIDE + 2 * W_BYTES;  // X, W, W'_prev
-constexpr int SMEM_TILED = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8 + 64;  // ring, barriers, producer cursor
+namespace k1a {
+#define K1_TX 32
+#define K1_TY OSAM_TY
+#include "k1_tiled.cuh"
+#undef K1_TX
+#undef K1_TY
+}  // namespace k1a
+namespace k1b {
+#define K1_TX 16
+#define K1_TY 8
+#include "k1_tiled.cuh"
+#undef K1_TX
+#undef K1_TY
+}  // namespace k1b
+
+// Tile shape of a subdomain's K1 (0: k1a, 1: k1b): the fraction of lanes that own a node, over x (the
+// tile columns, the excluded last column not counted) and y; k1b only when it is clearly better (it
+// pays ~1% in the two-row warps).  OSAM_K1_SHAPE=0/1 forces one (read per call: tests switch it).
+int k1_shape(const Geom& g, const Faces& f) {
+  const char* e = getenv("OSAM_K1_SHAPE");
+  if (e && (e[0] == '0' || e[0] == '1')) return e[0] - '0';
+  auto occ = [&](int tx, int ty, int cols, bool xl) {
+    const double nx = (double)(xl ? g.nn[0] - 1 : g.nn[0]);
+    return nx / ((double)cols * tx) * (double)g.nn[1] / ((double)((g.nn[1] + ty - 1) / ty) * ty);
+  };
+  const double a = occ(k1a::TX, k1a::TY, k1a::tile_cols(g, f), k1a::xlast_excluded(g, f));
+  const double b = occ(k1b::TX, k1b::TY, k1b::tile_cols(g, f), k1b::xlast_excluded(g, f));
+  return b > 1.03 * a ? 1 : 0;
+}
 
 #ifndef OSAM_NL_UNROLL
 #define OSAM_NL_UNROLL 2
 #endif
 constexpr int NL_UNROLL = OSAM_NL_UNROLL;  // NL1: unroll of the Gauss-point loop
 
-// ---- interior rows: parity-reduced stencil ---------------------------------------------
-// On a uniform box every interior block K_cd(ox, oy, oz) is even or odd in ox and in oy (the 1D
-// factors M, S are symmetric, G, Gt antisymmetric): diagonal blocks even-even, xy/yx odd-odd,
-// xz/zx odd-even, yz/zy even-odd (verified entry by entry on the host at create).  So the 3x3
-// in-plane sum collapses onto 9 symmetric combinations P[xk][yk] of each component (xk, yk in
-// {C: centre, E: pair sum, O: pair difference}), formed once per staged plane and applied to
-// the three target planes with 14 (oz = 0) or 22 (oz = +-1) coefficients; the oz = +1 slice reuses
-// the oz = -1 coefficients with the sign of the z-parity (odd for the xz, zx, yz, zy blocks).
-enum { PC = 0, PE = 1, PO = 2 };
-
-// the 9 combinations of one component around the thread's node (a = staged (-1,-1) neighbour)
-__device__ __forceinline__ void combos(const double* a, double P[9]) {
-  double cr[3], er[3], orr[3];
-#pragma unroll
-  for (int oy = 0; oy < 3; ++oy) {
-    const double l = a[oy * PX], c = a[oy * PX + 1], r = a[oy * PX + 2];
-    cr[oy] = c;
-    er[oy] = l + r;
-    orr[oy] = r - l;
-  }
-  P[PC * 3 + PC] = cr[1];
-  P[PC * 3 + PE] = cr[0] + cr[2];
-  P[PC * 3 + PO] = cr[2] - cr[0];
-  P[PE * 3 + PC] = er[1];
-  P[PE * 3 + PE] = er[0] + er[2];
-  P[PE * 3 + PO] = er[2] - er[0];
-  P[PO * 3 + PC] = orr[1];
-  P[PO * 3 + PE] = orr[0] + orr[2];
-  P[PO * 3 + PO] = orr[2] - orr[0];
-}
-
-// acc += sum_{ox,oy} K_cd(ox, oy, slice) w_d(ox, oy) for one block (c, d); ZNEG: use the oz = -1
-// slice with the sign of the z-parity (the oz = +1 slice)
-template <int SL, bool ZNEG, int c, int d>
-__device__ __forceinline__ void contrib(double& acc, const double P[9], const InteriorStencil& S) {
-  const double* k = S.k[SL][c][d];  // K00, K10, K01, K11
-  constexpr bool zodd = (c == 2) != (d == 2);
-  constexpr double sg = (ZNEG && zodd) ? -1.0 : 1.0;
-  if (c == d) {
-    acc = fma(sg * k[0], P[PC * 3 + PC], acc);
-    acc = fma(sg * k[1], P[PE * 3 + PC], acc);
-    acc = fma(sg * k[2], P[PC * 3 + PE], acc);
-    acc = fma(sg * k[3], P[PE * 3 + PE], acc);
-  } else if (c != 2 && d != 2) {  // xy, yx: odd-odd
-    acc = fma(sg * k[3], P[PO * 3 + PO], acc);
-  } else if (SL != 1) {
-    if (c == 0 || d == 0) {  // xz, zx: odd in x, even in y
-      acc = fma(sg * k[1], P[PO * 3 + PC], acc);
-      acc = fma(sg * k[3], P[PO * 3 + PE], acc);
-    } else {  // yz, zy: even in x, odd in y
-      acc = fma(sg * k[2], P[PC * 3 + PO], acc);
-      acc = fma(sg * k[3], P[PE * 3 + PO], acc);
-    }
-  }
-}
-
-template <int d, bool DA, bool DB, bool DC>
-__device__ __forceinline__ void fast_comp(double A[3], double B[3], double C[3], const double* xs, int base,
-                                          const InteriorStencil& S) {
-  double P[9];
-  combos(xs + d * PLANE + base, P);
-  if (DA) {
-    contrib<0, false, 0, d>(A[0], P, S);
-    contrib<0, false, 1, d>(A[1], P, S);
-    contrib<0, false, 2, d>(A[2], P, S);
-  }
-  if (DC) {
-    contrib<0, true, 0, d>(C[0], P, S);
-    contrib<0, true, 1, d>(C[1], P, S);
-    contrib<0, true, 2, d>(C[2], P, S);
-  }
-  if (DB) {
-    contrib<1, false, 0, d>(B[0], P, S);
-    contrib<1, false, 1, d>(B[1], P, S);
-    contrib<1, false, 2, d>(B[2], P, S);
-  }
-}
-
-// interior rows: the staged plane's contributions to the targets
-// (A: node plane m+1 sees plane m at oz = -1; B: plane m, oz = 0; C: plane m-1, oz = +1)
-template <bool DA, bool DB, bool DC>
-__device__ __forceinline__ void plane_fast(double A[3], double B[3], double C[3], const double* xs, int base,
-                                           const InteriorStencil& S) {
-  fast_comp<0, DA, DB, DC>(A, B, C, xs, base, S);
-  fast_comp<1, DA, DB, DC>(A, B, C, xs, base, S);
-  fast_comp<2, DA, DB, DC>(A, B, C, xs, base, S);
-}
-
-// Face rows / face planes (rare): "row form" of the stencil, valid for every (y, z) class because
-// the x-parity of each block holds for all lanes of the tiled kernel (x-face lanes never use the
-// force): sum_ox K(ox, oy) w(ox, oy) = K(0, oy) c_row + K(1, oy) e_row (x-even blocks) or
-// K(1, oy) o_row (x-odd blocks).  rowc holds {K(0, oy), K(1, oy)} per (cy, cz, slice, c, d, oy),
-// built and checked on the host; out of line to keep the hot loop small.
-struct Contrib3 {
-  double v[9];
-};
-
-__device__ __noinline__ Contrib3 plane_slow(const double* xs, int base, int cy, int czA, int czB, int czC,
-                                             const double* __restrict__ rowc) {
-  const double* kt[3] = {rowc + ((cy * 3 + czA) * 3 + 0) * 54, rowc + ((cy * 3 + czB) * 3 + 1) * 54,
-                         rowc + ((cy * 3 + czC) * 3 + 2) * 54};
-  double acc[3][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const double* a = xs + d * PLANE + base;
-    double cr[3], er[3], orr[3];
-#pragma unroll
-    for (int oy = 0; oy < 3; ++oy) {
-      const double l = a[oy * PX], c = a[oy * PX + 1], r = a[oy * PX + 2];
-      cr[oy] = c;
-      er[oy] = l + r;
-      orr[oy] = r - l;
-    }
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const bool even = (c == 0) == (d == 0);
-#pragma unroll
-        for (int oy = 0; oy < 3; ++oy) {
-          const double* k = kt[t] + ((c * 3 + d) * 3 + oy) * 2;
-          if (even) {
-            acc[t][c] = fma(__ldg(k), cr[oy], acc[t][c]);
-            acc[t][c] = fma(__ldg(k + 1), er[oy], acc[t][c]);
-          } else {
-            acc[t][c] = fma(__ldg(k + 1), orr[oy], acc[t][c]);
-          }
-        }
-      }
-    }
-  }
-  Contrib3 r;
-#pragma unroll
-  for (int t = 0; t < 3; ++t)
-#pragma unroll
-    for (int c = 0; c < 3; ++c) r.v[3 * t + c] = acc[t][c];
-  return r;
-}
-
-// Tiles of the persistent tiled kernel: TX x TY nodes in (x, y), a balanced chunk of ~ZC node
-// planes in z; tile t -> (bx, by, bz) with bx fastest.
-struct TileGrid {
-  int tx, ty, tz;
-  __device__ __forceinline__ int count() const { return tx * ty * tz; }
-};
-
-// x-faces whose nodes have free DOFs (bit 0: x = 0, bit 1: x = nx): their forces come from xface_body
-__host__ __device__ __forceinline__ int xface_sides(const Faces& f) {
-  int m = 0;
-  for (int s = 0; s < 2; ++s)
-    if (!(f.dir[s] == 7 || f.sw[s])) m |= 1 << s;
-  return m;
-}
-
-// x-tile columns: when the last node column x = nx sits alone in a tile (nx a multiple of TX) and the
-// x+ face is fully constrained (Dirichlet in every component, or Schwarz), that column only copies
-// its prescribed values (Q' = X, W' = a = 0): it is left out of the tiled grid and handled by
-// xlast_copy_kernel (c4's 257^3 FOM: 8 instead of 9 columns).
-__host__ __device__ __forceinline__ bool xlast_excluded(const Geom& g, const Faces& f) {
-  const int nx = g.nn[0] - 1;
-  return nx > 0 && nx % TX == 0 && (f.dir[1] == 7 || f.sw[1]);
-}
-
-__host__ __device__ __forceinline__ int tile_cols(const Geom& g, const Faces& f) {
-  return xlast_excluded(g, f) ? (g.nn[0] - 1) / TX : (g.nn[0] + TX - 1) / TX;
-}
-
-__device__ __forceinline__ TileGrid tile_grid(const Geom& g, const Faces& f) {
-  return TileGrid{tile_cols(g, f), (g.nn[1] + TY - 1) / TY, (g.nn[2] + ZC - 1) / ZC};
-}
-
-// Geometry of one tile as the producer and the consumers see it.
-struct TileGeo {
-  int x0, y0;        // node coordinates of staged position (0, 0)
-  int kbeg, kend;    // node planes finished by this tile
-  int nplanes;       // staged planes kbeg-1 .. kend+1
-};
-
-__device__ __forceinline__ TileGeo tile_geo(const Geom& g, const TileGrid& G, int t) {
-  const int bx = t % G.tx, by = (t / G.tx) % G.ty, bz = t / (G.tx * G.ty);
-  TileGeo o;
-  o.x0 = bx * TX - 2;
-  o.y0 = by * TY - 1;
-  o.kbeg = (int)((long long)bz * g.nn[2] / G.tz);
-  o.kend = (int)((long long)(bz + 1) * g.nn[2] / G.tz) - 1;
-  o.nplanes = o.kend - o.kbeg + 3;
-  return o;
-}
-
-// Per-thread constants of the current tile (kept small: every register counts for occupancy).
-struct Tile {
-  int i, j;
-  int kbeg, kend, nplanes;
-  unsigned flags;  // bit 0 active, bit 1 x-face lane, bit 2 writer, bits 3-4 cy (class of row j),
-                   // bit 5 the tile reads the previous iterate (norm numerator, see needs_prev)
-  long long id0;   // node index of (i, j, 0)
-  __device__ __forceinline__ bool active() const { return flags & 1u; }
-  __device__ __forceinline__ bool xface() const { return flags & 2u; }
-  __device__ __forceinline__ bool writer() const { return flags & 4u; }
-  __device__ __forceinline__ int cy() const { return (int)((flags >> 3) & 3u); }
-  __device__ __forceinline__ bool prev() const { return flags & 32u; }
-};
-
-// staged positions of this thread: own node, (-1,-1) neighbour, W tile position
-__device__ __forceinline__ int pos_own() { return ((int)threadIdx.y + 1) * PX + ((int)threadIdx.x + 2); }
-__device__ __forceinline__ int pos_base() { return (int)threadIdx.y * PX + (int)threadIdx.x + 1; }
-__device__ __forceinline__ int pos_w() { return (int)threadIdx.y * TX + (int)threadIdx.x; }
-
-struct Maps {
-  const CUtensorMap *x, *w, *wp;
-};
-
-// Does this tile read the previous iterate (W'_prev, or z_prev) for the convergence numerator?
-// Within a controller step the stencil input u* = X changes between Schwarz iterations only at
-// Schwarz DOFs (the predictor and the Dirichlet values are fixed, R30), so a node farther than one
-// layer from every Schwarz face gets a bitwise identical a' and w' in every iteration and its
-// numerator term is exactly 0: only tiles holding a node within one layer of a Schwarz face need it
-// (R38).  Multi-substep intervals (z-form, z_out set) change u everywhere: always.
-__device__ __forceinline__ bool needs_prev(const FomLaunch& L, const TileGeo& P) {
-  if (!L.with_norm) return false;
-  if (L.z_out) return true;
-  const Geom& g = L.g;
-  const int lo[3] = {P.x0 + 2, P.y0 + 1, P.kbeg};
-  const int hi[3] = {min(P.x0 + 1 + TX, g.nn[0] - 1), min(P.y0 + TY, g.nn[1] - 1), P.kend};
-#pragma unroll
-  for (int f = 0; f < 6; ++f) {
-    const int ax = f >> 1;
-    if (L.f.sw[f] && ((f & 1) ? hi[ax] >= g.nn[ax] - 2 : lo[ax] <= 1)) return true;
-  }
-  return false;
-}
-
-// stage layout: X plane (halo box) | W plane (tile box) | W'_prev plane (tile box)
-__device__ __forceinline__ void issue_plane(const TileGeo& P, bool wp, int it, int s, unsigned char* ring,
-                                            unsigned long long* full, const Maps& M) {
-  unsigned char* st = ring + (size_t)s * STAGE_BYTES;
-  const int m = P.kbeg - 1 + it;
-  mbar_expect_tx(&full[s], ARR_BYTES + (wp ? 2 : 1) * W_BYTES);
-  tma_load_4d(st, M.x, P.x0, P.y0, m, 0, &full[s]);
-  tma_load_4d(st + ARR_STRIDE, M.w, P.x0 + 2, P.y0 + 1, m, 0, &full[s]);
-  if (wp) tma_load_4d(st + ARR_STRIDE + W_BYTES, M.wp, P.x0 + 2, P.y0 + 1, m, 0, &full[s]);
-}
-
-// Producer cursor (thread 0 only, in shared memory): the next plane to load, possibly in a later
-// tile of this CTA.  Plane p of the CTA's stream lives in stage p % NSTAGE.
-struct Prod {
-  int t;       // tile (>= ntiles: done)
-  int it;      // plane within the tile
-  int issued;  // planes issued so far (all tiles)
-  int wp;      // the tile stages the previous iterate (needs_prev)
-  TileGeo P;
-};
-
-__device__ __forceinline__ void prod_issue(const FomLaunch& L, const TileGrid& G, Prod& pr, unsigned char* ring,
-                                           unsigned long long* full, const Maps& M) {
-#ifdef OSAM_NOLOAD  // probe: only the first ring fill is loaded; later planes reuse stale (finite) data
-  if (pr.issued >= NSTAGE) mbar_arrive(&full[pr.issued % NSTAGE]);
-  else
-#endif
-  issue_plane(pr.P, pr.wp != 0, pr.it, pr.issued % NSTAGE, ring, full, M);
-  ++pr.issued;
-  if (++pr.it == pr.P.nplanes) {
-    pr.it = 0;
-    pr.t += L.n_tile_ctas;
-    if (pr.t < G.count()) {
-      pr.P = tile_geo(L.g, G, pr.t);
-      pr.wp = needs_prev(L, pr.P);
-    }
-  }
-}
-
-// One staged plane (iteration it of the tile, plane gi of the CTA's stream, staged plane
-// m = kbeg - 1 + it).  Accumulator slots rotate by role: A = acc[SA] (node plane m+1), B = acc[SB]
-// (plane m), C = acc[SC] (plane m-1, finished here if it lies in [kbeg, kend], then zeroed to become
-// the next A).  Targets outside the chunk are accumulated too (and never used): every iteration is
-// identical.
-template <bool ZN, int SA, int SB, int SC>
-__device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStencil& S, const Tile& T, int it, int gi,
-                                        double (&acc)[3][3], double& num, double& den, unsigned char* ring,
-                                        unsigned long long* full, unsigned long long* empty, const Maps& M, Prod* pr,
-                                        const TileGrid& G) {
-  const Geom& g = L.g;
-  const int nz = g.nn[2] - 1;
-  const long long np = g.npad;
-  const int m = T.kbeg - 1 + it;
-  const int kf = m - 1;
-  const bool fin = T.writer() && kf >= T.kbeg && kf <= T.kend;
-  // producer: plane gi + NSTAGE - 2 into the stage released by plane gi - 2
-  if (threadIdx.x + threadIdx.y == 0 && pr->t < G.count()) {
-    const int p = pr->issued;
-    if (p >= NSTAGE) mbar_wait(&empty[p % NSTAGE], (unsigned)(((p - NSTAGE) / NSTAGE) & 1));
-    prod_issue(L, G, *pr, ring, full, M);
-  }
-  const int s = gi % NSTAGE;
-  mbar_wait(&full[s], (unsigned)((gi / NSTAGE) & 1));
-  const double* xs = reinterpret_cast<const double*>(ring + (size_t)s * STAGE_BYTES);
-  if (T.active()) {
-    double* A = acc[SA];
-    double* B = acc[SB];
-    double* C = acc[SC];
-#ifdef OSAM_NOCOMPUTE
-    if (false) {
-#else
-    if (T.cy() == 1 && m >= 2 && m <= nz - 2) {
-      plane_fast<true, true, true>(A, B, C, xs, pos_base(), S);
-    } else {
-#endif
-      const Contrib3 r = plane_slow(xs, pos_base(), T.cy(), axis_class(m + 1, g.nn[2]), axis_class(m, g.nn[2]),
-                                    axis_class(kf, g.nn[2]), L.rowc);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        A[c] += r.v[c];
-        B[c] += r.v[3 + c];
-        C[c] += r.v[6 + c];
-      }
-    }
-    if (fin) {
-      // own X, W, W'_prev of plane kf, staged in the previous iteration (released at the end of this one)
-      const unsigned char* sp = ring + (size_t)((gi + NSTAGE - 1) % NSTAGE) * STAGE_BYTES;
-      const double* xo = reinterpret_cast<const double*>(sp) + pos_own();
-      const double* wo = reinterpret_cast<const double*>(sp + ARR_STRIDE) + pos_w();
-      const double* qw = reinterpret_cast<const double*>(sp + ARR_STRIDE + W_BYTES) + pos_w();
-      const long long id = T.id0 + (long long)kf * g.plane;
-      const int cz = axis_class(kf, g.nn[2]);
-      if (T.xface()) {  // fully constrained x-face node: Q' = X (prescribed), W' = a = 0
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          if (L.q_out) L.q_out[c * np + id] = xo[c * PLANE];
-          L.w_out[c * np + id] = 0.0;
-          if (L.a_out) L.a_out[c * np + id] = 0.0;
-        }
-      } else if (T.cy() == 1 && cz == 1 && L.a_out == nullptr && L.q_out != nullptr) {  // interior node
-        const double inv_m = L.inv_mass[7];
-        double* qo = L.q_out + id;
-        double* wp = L.w_out + id;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double x = xo[c * PLANE], w0 = wo[c * WPL];
-          const double an = -C[c] * inv_m;
-          const double wn = fma(L.cw, an, w0);
-          qo[c * np] = fma(L.cq, wn, x);
-          wp[c * np] = wn;
-          if (L.with_norm) {  // outside the band q = w' itself: d == 0 exactly (R38)
-            const double w = fma(L.dt, fma(L.cv, an, w0), x);
-            const double q = T.prev() ? qw[c * WPL] : (ZN ? w : wn);
-            const double d = ZN ? w - q : 0.5 * L.dt * (wn - q);
-            num = fma(d, d, num);
-            den = fma(w, w, den);
-          }
-          if (ZN) L.z_out[c * np + id] = fma(L.dt, fma(L.cv, an, w0), x);
-        }
-      } else {
-        const unsigned fm = (T.cy() != 1 || cz != 1) ? free_mask(g, L.f, T.i, T.j, kf) : 7u;
-        const double inv_m = L.inv_mass[1 + 2 * (T.cy() == 1) + 4 * (cz == 1)];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double x = xo[c * PLANE];
-          double an = 0.0, wn = 0.0, qn = x;
-          if ((fm >> c) & 1) {
-            const double w0 = wo[c * WPL];
-            an = -C[c] * inv_m;
-            wn = fma(L.cw, an, w0);
-            qn = fma(L.cq, wn, x);
-            if (L.with_norm) {
-              const double w = fma(L.dt, fma(L.cv, an, w0), x);
-              const double q = T.prev() ? qw[c * WPL] : (ZN ? w : wn);
-              const double d = ZN ? w - q : 0.5 * L.dt * (wn - q);
-              num = fma(d, d, num);
-              den = fma(w, w, den);
-            }
-            if (ZN) L.z_out[c * np + id] = fma(L.dt, fma(L.cv, an, w0), x);
-          }
-          if (L.q_out) L.q_out[c * np + id] = qn;
-          L.w_out[c * np + id] = wn;
-          if (L.a_out) L.a_out[c * np + id] = an;
-        }
-      }
-    }
-  }
-  // this warp is done with the previous plane of the stream (own values above, stencil before)
-  __syncwarp();
-  if (gi >= 1 && (threadIdx.x & 31) == 0) mbar_arrive(&empty[(gi + NSTAGE - 1) % NSTAGE]);
-#pragma unroll
-  for (int c = 0; c < 3; ++c) acc[SC][c] = 0.0;
-}
-
-__device__ __noinline__ void xface_body(const FomLaunch& L, int side_mask, int blk, int tid, int slot);
-
-#ifndef OSAM_MINB
-#define OSAM_MINB 4
-#endif
-#ifndef OSAM_K1_ROT
-// 0 (default): one copy of k1_iter per plane, the accumulator roles moved through the slots (9 moves per
-// plane); 1: k1_iter unrolled by the period 3 of the roles (no moves).  The single copy keeps the loop in
-// the instruction cache: c3 845 -> 891 steps/s (K1 0.203 -> 0.193 ms), 80 KB -> 54 KB of SASS, no spills.
-#define OSAM_K1_ROT 0
-#endif
-template <bool ZN>
-__global__ void __launch_bounds__(NT, OSAM_MINB)
-    fom_tiled_kernel(const __grid_constant__ FomLaunch L, const __grid_constant__ InteriorStencil S,
-                     const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
-                     const __grid_constant__ CUtensorMap tmwp) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char* ring = smem;
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + NSTAGE * STAGE_BYTES);
-  unsigned long long* empty = full + NSTAGE;
-  Prod* pr = reinterpret_cast<Prod*>(empty + NSTAGE);
-  if ((int)blockIdx.x >= L.n_tile_ctas) {  // x-face CTAs (after the tile CTAs)
-    xface_body(L, xface_sides(L.f), blockIdx.x - L.n_tile_ctas, threadIdx.x + TX * threadIdx.y, blockIdx.x);
-    return;
-  }
-  const Geom& g = L.g;
-  const int nx = g.nn[0] - 1, ny = g.nn[1] - 1;
-  const Maps M{&tmx, &tmw, &tmwp};
-  const TileGrid G = tile_grid(g, L.f);
-  const bool lead = threadIdx.x + threadIdx.y == 0;
-
-  if (lead) {
-    for (int s = 0; s < NSTAGE; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NWARP);
-    }
-    mbar_fence_init();
-    pr->t = blockIdx.x;
-    pr->it = 0;
-    pr->issued = 0;
-    if (pr->t < G.count()) {
-      pr->P = tile_geo(g, G, pr->t);
-      pr->wp = needs_prev(L, pr->P);
-      for (int p = 0; p < NSTAGE - 2 && pr->t < G.count(); ++p) prod_issue(L, G, *pr, ring, full, M);
-    }
-  }
-  __syncthreads();
-
-  double acc[3][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
-  double num = 0.0, den = 0.0;
-  int gi = 0;
-  for (int tile = blockIdx.x; tile < G.count(); tile += L.n_tile_ctas) {
-    const TileGeo P = tile_geo(g, G, tile);
-    Tile T;
-    T.i = P.x0 + 2 + (int)threadIdx.x;
-    T.j = P.y0 + 1 + (int)threadIdx.y;
-    const bool active = (T.i <= nx) && (T.j <= ny);
-    const bool xface = (T.i == 0) || (T.i == nx);
-    const int xsd = T.i == 0 ? 0 : 1;
-    const bool writer = active && (!xface || L.f.dir[xsd] == 7 || L.f.sw[xsd]);
-    T.flags = (active ? 1u : 0u) | (xface ? 2u : 0u) | (writer ? 4u : 0u) | ((unsigned)axis_class(T.j, g.nn[1]) << 3) |
-              (needs_prev(L, P) ? 32u : 0u);
-    T.kbeg = P.kbeg;
-    T.kend = P.kend;
-    T.nplanes = P.nplanes;
-    T.id0 = T.i + (long long)g.px * T.j;
-#if OSAM_K1_ROT
-    for (int it = 0; it < T.nplanes;) {  // unrolled by the period 3 of the slot rotation
-      k1_iter<ZN, 0, 1, 2>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
-      ++gi;
-      if (++it >= T.nplanes) break;
-      k1_iter<ZN, 2, 0, 1>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
-      ++gi;
-      if (++it >= T.nplanes) break;
-      k1_iter<ZN, 1, 2, 0>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
-      ++gi;
-      ++it;
-    }
-#else
-    // one copy of the iteration; the roles move through the slots (C, zeroed by k1_iter, becomes A)
-#pragma unroll 1
-    for (int it = 0; it < T.nplanes; ++it, ++gi) {
-      k1_iter<ZN, 0, 1, 2>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        acc[2][c] = acc[1][c];
-        acc[1][c] = acc[0][c];
-        acc[0][c] = 0.0;
-      }
-    }
-#endif
-#pragma unroll
-    for (int q = 0; q < 3; ++q)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) acc[q][c] = 0.0;
-  }
-  block_partial<NT>(num, den, L.partial, blockIdx.x);
-}
-
-// Nodes on an x-face with free DOFs: a group of 4 lanes per node, lane sub = 0, 1, 2 gathers the
-// plane oz = sub - 1 (6 positions: 2 in x, 3 in y; class-table stencil), the partial forces are summed
-// in the order sub = 0, 1, 2 by shuffles and lane sub = 0 finishes the node.  side_mask bit 0: face
-// x = 0, bit 1: face x = nx.
-// Runs as the extra CTAs of the tiled kernel (blockIdx >= the tile CTAs), so it fills the tiled
-// kernel's last wave instead of costing a launch of its own; blk = x-face block, slot = its partial slot.
-__device__ __noinline__ void xface_body(const FomLaunch& L, int side_mask, int blk, int tid, int slot) {
-  const Geom& g = L.g;
-  const long long np = g.npad;
-  const long long nf = (long long)g.nn[1] * g.nn[2];
-  const int nsides = (side_mask & 1) + ((side_mask >> 1) & 1);
-  const long long t = (blk * (long long)XF_BLOCK + tid) >> 2;
-  const int sub = tid & 3;
-  const int nx = g.nn[0] - 1;
-  double num = 0.0, den = 0.0;
-  const bool valid = t < nsides * nf;
-  const int side = (side_mask == 2) ? 1 : (t >= nf ? 1 : 0);
-  const long long r = t - (t >= nf ? nf : 0);
-  const int i = side ? nx : 0;
-  const int j = valid ? (int)(r % g.nn[1]) : 0;
-  const int k = valid ? (int)(r / g.nn[1]) : 0;
-  const int cyj = axis_class(j, g.nn[1]), czk = axis_class(k, g.nn[2]);
-  double f[3] = {0.0, 0.0, 0.0};
-  const int oz = sub - 1;
-  if (valid && sub < 3 && k + oz >= 0 && k + oz <= g.nn[2] - 1) {
-    const double* coef = L.coef + (size_t)((side ? 2 : 0) + 3 * (cyj + 3 * czk)) * 27 * 9;
-    const int oxlo = side ? -1 : 0;
-#pragma unroll
-    for (int oy = -1; oy <= 1; ++oy) {
-      if (j + oy < 0 || j + oy > g.nn[1] - 1) continue;
-#pragma unroll
-      for (int dx = 0; dx < 2; ++dx) {
-        const int ox = oxlo + dx;
-        const long long q = gidx(g, i + ox, j + oy, k + oz);
-        const double x[3] = {__ldg(L.x + q), __ldg(L.x + np + q), __ldg(L.x + 2 * np + q)};
-        const double* cb = coef + ((ox + 1) + 3 * ((oy + 1) + 3 * (oz + 1))) * 9;
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-          for (int d = 0; d < 3; ++d) f[c] = fma(__ldg(cb + c * 3 + d), x[d], f[c]);
-      }
-    }
-  }
-  // fixed-order sum over the group: ((f_0 + f_1) + f_2)
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const double f1 = __shfl_down_sync(0xffffffffu, f[c], 1, 4);
-    const double f2 = __shfl_down_sync(0xffffffffu, f[c], 2, 4);
-    f[c] = (f[c] + f1) + f2;
-  }
-  if (valid && sub == 0) {
-    const long long id = gidx(g, i, j, k);
-    const unsigned fm = free_mask(g, L.f, i, j, k);
-    const double inv_m = L.inv_mass[(cyj == 1 ? 2 : 0) + (czk == 1 ? 4 : 0)];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const double x = __ldg(L.x + c * np + id);
-      double an = 0.0, wn = 0.0, qn = x;
-      if ((fm >> c) & 1) {
-        const double w0 = L.w0[c * np + id];
-        an = -f[c] * inv_m;
-        wn = fma(L.cw, an, w0);
-        qn = fma(L.cq, wn, x);
-        const double w = fma(L.dt, fma(L.cv, an, w0), x);
-        if (L.with_norm) {
-          const double d = L.z_out ? w - L.z_out[c * np + id] : 0.5 * L.dt * (wn - L.w_out[c * np + id]);
-          num = fma(d, d, num);
-          den = fma(w, w, den);
-        }
-        if (L.z_out) L.z_out[c * np + id] = w;
-      }
-      if (L.q_out) L.q_out[c * np + id] = qn;
-      L.w_out[c * np + id] = wn;
-      if (L.a_out) L.a_out[c * np + id] = an;
-    }
-  }
-  block_partial<XF_BLOCK>(num, den, L.partial, slot);
-}
 
 // Small subdomains (K1S): the TMA-streamed tiled kernel pays a load round trip per z-plane inside each
 // CTA, which dominates for boxes of a few thousand nodes (c1, c2).  Here every node is one group of 4
@@ -1038,11 +488,7 @@ __global__ void zero_constrained_kernel(Geom g, Faces F, double* u, double* w) {
   }
 }
 
-inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
-long long tile_count(const Geom& g, const Faces& f) {
-  return (long long)tile_cols(g, f) * cdiv(g.nn[1], TY) * cdiv(g.nn[2], ZC);
-}
 
 // the excluded x+ column (see xlast_excluded): Q' = X, W' = 0, a = 0 on every node of the face
 // The excluded last x column: Q' = X (prescribed), W' = a = 0.  XL_PER nodes per thread with every
@@ -1072,35 +518,9 @@ __global__ void __launch_bounds__(128) xlast_copy_kernel(const FomLaunch L) {
   }
 }
 
-// CTAs of the tiled kernel: one per tile, or (OSAM_PERSISTENT=1) as many as fit on the device at
-// once, each looping over tiles
-int tiled_ctas(const Geom& g, const Faces& f) {
-  static const bool persistent = getenv("OSAM_PERSISTENT") && getenv("OSAM_PERSISTENT")[0] == '1';
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fom_tiled_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TILED);
-    cudaFuncSetAttribute(fom_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TILED);
-    attr = true;
-  }
-  if (!persistent) return (int)tile_count(g, f);
-  static int resident = 0;
-  if (resident == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fom_tiled_kernel<false>, NT, SMEM_TILED);
-    resident = std::max(1, sms * std::max(1, per_sm));
-  }
-  return (int)std::min<long long>(resident, tile_count(g, f));
-}
 
 
 
-unsigned xface_blocks(const Geom& g, const Faces& f) {
-  const int m = xface_sides(f);
-  const int ns = (m & 1) + ((m >> 1) & 1);
-  return ns ? cdiv(4LL * ns * g.nn[1] * g.nn[2], XF_BLOCK) : 0u;
-}
 
 
 // ---- NL1: nonlinear FOM advance (SVK / Neohookean; App. A.2, A.3) ----------
@@ -1399,7 +819,7 @@ int nl_ctas(const Geom& g) {
 
 int fom_partial_slots(const Geom& g, const Faces& f) {
   if (small_fom(g)) return (int)cdiv(4LL * g.nn[0] * g.nn[1] * g.nn[2], GB);
-  return tiled_ctas(g, f) + (int)xface_blocks(g, f);
+  return k1_shape(g, f) ? k1b::partial_slots(g, f) : k1a::partial_slots(g, f);
 }
 
 int fom_nl_partial_slots(const Geom& g) { return nl_ctas(g); }
@@ -1443,7 +863,8 @@ void launch_fom_advance_nl(const FomLaunch& L, cudaStream_t s, int* launches) {
 }
 
 void launch_fom_xlast(const FomLaunch& L, cudaStream_t s, int* launches) {
-  if (L.material != OSAM_LINEAR || small_fom(L.g) || !xlast_excluded(L.g, L.f)) return;
+  if (L.material != OSAM_LINEAR || small_fom(L.g)) return;
+  if (!(k1_shape(L.g, L.f) ? k1b::xlast_excluded(L.g, L.f) : k1a::xlast_excluded(L.g, L.f))) return;
   xlast_copy_kernel<<<cdiv((long long)L.g.nn[1] * L.g.nn[2], 128 * XL_PER), 128, 0, s>>>(L);
   debug_check("xlast_copy_kernel", s);
   ++*launches;
@@ -1462,37 +883,16 @@ void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUt
     ++*launches;
     return;
   }
-  FomLaunch Lt = L;
-  Lt.n_tile_ctas = tiled_ctas(L.g, L.f);
-  const int grid = Lt.n_tile_ctas + (int)xface_blocks(L.g, L.f);  // tile CTAs, then x-face CTAs
-  if (L.z_out)  // last substep of a multi-substep interval: z = u + dt v out, norm from z - z_prev (R33)
-    fom_tiled_kernel<true><<<grid, dim3(TX, TY), SMEM_TILED, s>>>(Lt, st, *tmx, *tmw, *tmwp);
+  if (k1_shape(L.g, L.f))
+    k1b::launch_tiled(L, st, tmx, tmw, tmwp, s);
   else
-    fom_tiled_kernel<false><<<grid, dim3(TX, TY), SMEM_TILED, s>>>(Lt, st, *tmx, *tmw, *tmwp);
-  debug_check("fom_tiled_kernel", s);
+    k1a::launch_tiled(L, st, tmx, tmw, tmwp, s);
   ++*launches;
   if (with_xlast) launch_fom_xlast(L, s, launches);
 }
 
-// 4D (x, y, z, component) descriptor of a padded SoA field; halo = true: the X box (tile plus a
-// 2/1-node halo in x/y), false: the W box (tile only).
-int make_field_tmap(const Geom& g, double* array, bool halo, CUtensorMap* out) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
-    cudaDriverEntryPointQueryResult q;
-    void* fn = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
-      return -1;
-    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-  }
-  const cuuint64_t dims[4] = {(cuuint64_t)g.px, (cuuint64_t)g.nn[1], (cuuint64_t)g.nn[2], 3};
-  const cuuint64_t strides[3] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.plane * 8, (cuuint64_t)g.npad * 8};
-  const cuuint32_t box[4] = {halo ? (cuuint32_t)PX : (cuuint32_t)TX, halo ? (cuuint32_t)PY : (cuuint32_t)TY, 1, 3};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, array, dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? 0 : (int)r;
+int make_field_tmap(const Geom& g, const Faces& f, double* array, bool halo, CUtensorMap* out) {
+  return k1_shape(g, f) ? k1b::make_tmap(g, array, halo, out) : k1a::make_tmap(g, array, halo, out);
 }
 
 void launch_fom_pack(const Geom& g, const double* src, double* dst, long long n, cudaStream_t s) {

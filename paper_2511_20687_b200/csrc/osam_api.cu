@@ -356,6 +356,19 @@ int upload(T** d, const std::vector<T>& h, cudaStream_t st) {
 
 int process_ic(Sub& s, int* launches);
 
+// TMA descriptors of a FOM's state buffers.  Their boxes follow the K1 tile shape, which depends on the
+// faces (kernels_fom.cu k1_shape): encoded at create and again at bind, once the Schwarz faces are known.
+int encode_tmaps(Sub& s) {
+  const int nbuf = s.n_sub > 1 ? 3 : 2;
+  for (int b = 0; b < nbuf; ++b) {
+    int r = make_field_tmap(s.g, s.faces, s.st[b][0], true, &s.tmap[b]);
+    if (r == 0) r = make_field_tmap(s.g, s.faces, s.st[b][1], false, &s.tmapw[b]);
+    if (r == 0 && b == 0 && s.zbuf) r = make_field_tmap(s.g, s.faces, s.zbuf, false, &s.tmapz);
+    if (r != 0) return r;
+  }
+  return 0;
+}
+
 int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>& handles) {
   const int n = (int)subs.size();
   for (int i = 0; i < n; ++i) {
@@ -377,6 +390,7 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
         inner *= std::max(0, s.g.nn[a] - 2 * (int)s.faces.sw[2 * a] - 2 * (int)s.faces.sw[2 * a + 1]);
       s.n_band = s.n_nodes - inner;
       TRY(dalloc(&s.scratch_partial, (size_t)fom_slots(s)));
+      if (const int r = encode_tmaps(s)) return fail(OSAM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", r);
       continue;
     }
     const long long rows_phi = (long long)(s.h_Phi.size() / std::max(1, s.r));
@@ -1380,14 +1394,10 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
       }
       CK(cudaMemsetAsync(s.zbuf, 0, sizeof(double) * g.total, s.stream));
     }
-    for (int b = 0; b < nbuf; ++b) {
-      int r = make_field_tmap(g, s.st[b][0], true, &s.tmap[b]);
-      if (r == 0) r = make_field_tmap(g, s.st[b][1], false, &s.tmapw[b]);
-      if (r == 0 && b == 0 && s.zbuf) r = make_field_tmap(g, s.zbuf, false, &s.tmapz);
-      if (r != 0) {
-        osam_destroy(h.release());
-        return fail(OSAM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", r);
-      }
+    const int r = encode_tmaps(s);
+    if (r != 0) {
+      osam_destroy(h.release());
+      return fail(OSAM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", r);
     }
   } else {
     s.r = d->r;

@@ -185,7 +185,8 @@ void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUt
                         const CUtensorMap* tmw, const CUtensorMap* tmwp, cudaStream_t s, int* launches,
                         bool with_xlast = true);
 void launch_fom_xlast(const FomLaunch& L, cudaStream_t s, int* launches);
-int make_field_tmap(const Geom& g, double* array, bool halo, CUtensorMap* out);
+// TMA descriptor of a padded SoA field for the K1 tile shape of (g, f) (halo: the X box, else the W box)
+int make_field_tmap(const Geom& g, const Faces& f, double* array, bool halo, CUtensorMap* out);
 
 void launch_transfer(const XferMap& m, const double* src, long long src_cstride, long long src_bstride,
                      double* dst, long long dst_bstride, int batch, const int* active, cudaStream_t s);
