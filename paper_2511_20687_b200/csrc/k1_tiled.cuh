@@ -7,10 +7,7 @@ constexpr int TX = K1_TX;  // tile width in x (a multiple of 16: even TMA start 
 constexpr int TY = K1_TY;
 constexpr int NT = TX * TY;
 constexpr int NWARP = NT / 32;
-#ifndef OSAM_ZC
-#define OSAM_ZC 24
-#endif
-constexpr int ZC = OSAM_ZC;  // target z-planes per block (balanced split)
+constexpr int ZC = K1_ZC;  // target z-planes per block (balanced split)
 constexpr int XF_BLOCK = NT;  // x-face work runs in extra CTAs of the tiled kernel (same block)
 
 // Staged x-range [x0, x0 + PX) with x0 = 32 bx - 2: the TMA box must start on a 16-byte

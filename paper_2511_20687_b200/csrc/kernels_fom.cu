@@ -174,19 +174,29 @@ inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) /
 #ifndef OSAM_TY
 #define OSAM_TY 4
 #endif
+#ifndef OSAM_ZC
+#define OSAM_ZC 24  // target z-planes per CTA, 32 x TY tiles
+#endif
+#ifndef OSAM_ZC_B
+#define OSAM_ZC_B 24  // the same, 16 x 8 tiles
+#endif
 namespace k1a {
 #define K1_TX 32
 #define K1_TY OSAM_TY
+#define K1_ZC OSAM_ZC
 #include "k1_tiled.cuh"
 #undef K1_TX
 #undef K1_TY
+#undef K1_ZC
 }  // namespace k1a
 namespace k1b {
 #define K1_TX 16
 #define K1_TY 8
+#define K1_ZC OSAM_ZC_B
 #include "k1_tiled.cuh"
 #undef K1_TX
 #undef K1_TY
+#undef K1_ZC
 }  // namespace k1b
 
 // Tile shape of a subdomain's K1 (0: k1a, 1: k1b): the fraction of lanes that own a node, over x (the
