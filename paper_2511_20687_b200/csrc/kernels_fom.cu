@@ -18,8 +18,9 @@
 // because u* depends on the checkpoint only (eq:conv_criterion P:L443-467).  Other coefficient
 // choices convert the state (initial condition: X = u0, W = v0, cw = dt/2; a new dt; v for output).
 //
-// Two kernels make one K1:
-//   * the tiled kernel covers every node.  A block owns a TX x TY tile in (x, y) and a balanced
+// One launch of the tiled kernel makes a K1 (kernels of their own: K1S, the gather path for small
+// boxes; NL1 for the nonlinear materials; the excluded last x column's copy):
+//   * its tile CTAs cover every node.  A block owns a TX x TY tile in (x, y) and a balanced
 //     chunk of node planes in z.  One thread streams X planes (tile + halo) with 4D TMA loads into
 //     a 4-deep ring guarded by full/empty mbarriers (no block-wide barrier in the loop: warps only
 //     wait for data, the producer waits for the slowest warp to release a stage).  Each thread
@@ -31,7 +32,8 @@
 //     16-node rows; for boxes whose x extent leaves most of a 32-wide column idle).  Interior rows use
 //     the parity-reduced interior stencil, face rows their class table (out of line).  Lanes on an
 //     x-face write it only when the face is fully constrained (no force needed).
-//   * the x-face kernel covers x-faces with free DOFs (a node per thread, class table).
+//   * its extra CTAs (after the tile CTAs) gather the x-faces with free DOFs: 4 lanes per node, one
+//     per z-offset, class table, fixed-order shuffle sum (xface_body).
 // No atomics; every sum has a fixed order, so results are bitwise repeatable.
 #include <algorithm>
 #include <cstdlib>
