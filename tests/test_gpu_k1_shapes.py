@@ -17,3 +17,24 @@ pytestmark = pytest.mark.gpu
 def k1_shape(monkeypatch, request):
     monkeypatch.setenv("OSAM_GATHER_MAX", "0")          # the tiled K1 at every size
     monkeypatch.setenv("OSAM_K1_SHAPE", "0" if request.param == "k1a" else "1")
+
+
+@pytest.mark.timeout(300, method="thread")
+@pytest.mark.parametrize("created,stepped", [("1", "0"), ("0", "1")])
+def test_tmaps_follow_the_shape_at_bind(gpu, monkeypatch, created, stepped):
+    """The TMA boxes follow the tile shape, which is fixed only at bind (it depends on the Schwarz faces):
+    subdomains created (and given their IC) under one shape and stepped under the other still match the
+    oracle, because bind encodes the descriptors again.  Without that re-encoding the kernel waits for TMA
+    bytes that never arrive (checked once with such a build: it hangs), hence the timeout."""
+    from test_gpu_parity import compare, oracle_run
+    import osam_inputs as I
+    cfg = I.scaled(I.config("c3"), 8.0)
+    monkeypatch.setenv("OSAM_K1_SHAPE", created)
+    subs = gpu.build(cfg)
+    gpu.set_ics(cfg, subs, device="cuda:0")
+    monkeypatch.setenv("OSAM_K1_SHAPE", stepped)
+    n = 6
+    _, iters = gpu.run(cfg, subs, n_steps=n)
+    models, states, it_ref, _ = oracle_run(cfg, n, e=gpu.e_scale(cfg))
+    assert (iters.reshape(-1) == it_ref.reshape(-1)).all()
+    compare(gpu, subs, models, states)
