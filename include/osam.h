@@ -99,6 +99,15 @@ typedef struct {
   int32_t n_substeps;     /* 0/1 .. 4096                                                              */
   int32_t integrator;     /* OSAM_EXPLICIT (FOM: required) | OSAM_IMPLICIT (ROM)                      */
   int32_t material;       /* FOM: OSAM_LINEAR | OSAM_SVK | OSAM_NEOHOOKEAN (ROM: must be OSAM_LINEAR) */
+  /* ROM only, optional: Phi given on a subset of its rows.  The online loop reads Phi only where the
+   * Schwarz transfer lifts the ROM's field to a neighbour's Schwarz nodes ("Phi restricted to the relevant
+   * boundary DoFs") and, in osam_set_ic, to restrict a full field.  phi_rows (host, copied at
+   * create): n_phi_rows strictly ascending free-row indices in [0, n_free); Phi is then n_phi_rows x r
+   * column-major (its row q = free row phi_rows[q]).  NULL: Phi has all n_free rows.  The first osam_step
+   * returns OSAM_EINVAL if the transfer needs a row that is not given; osam_set_ic returns OSAM_EINVAL
+   * (use osam_set_ic_reduced).                                                                         */
+  const int64_t *phi_rows;
+  int64_t n_phi_rows;
 } osam_subdomain_desc;
 
 typedef struct {
@@ -109,9 +118,12 @@ typedef struct {
   int32_t min_iters; /* first iteration at which convergence is tested (2)                      */
 } osam_schwarz_cfg;
 
-/* Create a subdomain on `cuda_stream` (a cudaStream_t; NULL = legacy default stream).
- * Validates the descriptor, uploads ROM operators, allocates the double-buffered state.
- * Returns OSAM_OK and *out, or a negative code (then *out = NULL). */
+/* Create a subdomain on `cuda_stream` (a cudaStream_t; NULL = legacy default stream): one subdomain
+ * Omega_i of the coupled problem with its mesh, material and Dirichlet boundary (the inputs
+ * of Algorithm 1); a FOM (hex8 linear/SVK/Neohookean FE, App. A) or an OpInf
+ * ROM with its operators (eq:opinf_model_schwarz P:L550-583).  Validates the descriptor (every check
+ * before the first CUDA call), copies the host arrays, allocates the double-buffered state.
+ * Returns OSAM_OK and *out, or a negative code (then *out = NULL and nothing is leaked). */
 int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_subdomain** out);
 
 /* Initial condition from full-mesh physical fields (batch x 3n doubles each; v0 may be NULL = 0).
@@ -120,6 +132,14 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
  *      a^0 = e_b (-Kbar u^0 + Bbar Phi_dS^T s0)  (SURVEY c.1 step 10). */
 int osam_set_ic(osam_subdomain* s, const double* u0, const double* v0);
 
+/* Reduced initial condition of a ROM (the restriction step of SURVEY c.1 step 10 / S:L558-565 done by the
+ * caller, e.g. when Phi is given on a row subset): u^0 = uh0, v^0 = vh0 (NULL = 0), both r x batch
+ * (uh0[b*r + i]); s0 = the Schwarz-DOF values of the initial field (n_s x batch, s0[b*n_s + q], Schwarz
+ * DOFs in ascending DOF id; NULL only if the ROM has no Schwarz DOF); a^0 = e_b(-Kbar u^0 + Bbar
+ * Phi_dS^T s0) is computed at the first osam_step.  Host or device pointers, read only during the call.
+ * OSAM_EINVAL for a FOM. */
+int osam_set_ic_reduced(osam_subdomain* s, const double* uh0, const double* vh0, const double* s0);
+
 /* Advance `n_steps` controller steps of Algorithm 1 over the subdomains `sds` (sweep order =
  * array order).  Schwarz maps are built on the first call (n_steps = 0 only builds them).
  * iters_out (host, may be NULL): n_steps x max(batch) Schwarz iteration counts, step-major.
@@ -127,8 +147,10 @@ int osam_set_ic(osam_subdomain* s, const double* u0, const double* v0);
 int osam_step(osam_subdomain* const* sds, int32_t n_sd, const osam_schwarz_cfg* cfg, int32_t n_steps,
               int32_t* iters_out);
 
-/* Current converged state.  FOM: u (all DOFs) and v as physical fields, 3n doubles each.
- * ROM: u^ and v^ as r x batch column-major (u_out[b*r + i]).  Either pointer may be NULL. */
+/* Current converged state phi_i(t_k) of the subdomain (the output of Algorithm 1).
+ * FOM: u (all DOFs) and v as physical fields, 3n doubles each (constrained v = 0, reading R10).
+ * ROM: u^ and v^ as r x batch column-major (u_out[b*r + i]).  Either pointer may be NULL.  Host or
+ * device pointers; synchronises the stream.  OSAM_EINVAL before the first osam_step. */
 int osam_get_state(const osam_subdomain* s, double* u_out, double* v_out);
 
 /* Diagnostic: acceleration (FOM: 3n physical field; ROM: a^, r x batch). */
@@ -138,6 +160,8 @@ int osam_get_accel(const osam_subdomain* s, double* a_out);
 int osam_get_sizes(const osam_subdomain* s, int64_t* n_nodes, int64_t* n_free, int64_t* n_schwarz,
                    int32_t* batch);
 
+/* Release a subdomain and every device buffer the library allocated for it (the end of the online stage,
+ * Algorithm 2); waits for its stream.  Step groups that contain it are forgotten.  NULL: no-op. */
 void osam_destroy(osam_subdomain* s);
 
 const char* osam_last_error(void);
@@ -175,6 +199,16 @@ int osam_opinf_replay(const osam_replay_desc* d, double* err_out, int32_t* best_
  * DESIGN.md section 6),
  * and the total number of kernels this library launched since the last reset. */
 void osam_set_profiling(int32_t on);
+
+/* Convergence trace (diagnostics of eq:conv_criterion): with max_n > 0, every later osam_step
+ * records, for each controller step k, each tested Schwarz iteration n <= max_n and each sample b, the
+ * (num, den) pair K3 compared (num = sum_i ||du_i + dt dv_i||^2, den = sum_i ||u_i + dt v_i||^2 over
+ * unconstrained DOFs, ROM terms in reduced coordinates); untested entries are NaN.  0 disables.
+ * osam_get_conv_trace copies the trace of the last osam_step call on the list `sds` (same order) into out
+ * ([n_steps][max_n][batch][2] doubles, host or device; may be NULL to query the sizes). */
+void osam_set_conv_trace(int32_t max_n);
+int osam_get_conv_trace(osam_subdomain* const* sds, int32_t n_sd, double* out, int32_t* n_steps, int32_t* max_n,
+                        int32_t* batch);
 void osam_reset_profile(void);
 void osam_get_profile(double* k1_ms, int64_t* k1_launches, double* k1_bytes, int64_t* kernel_launches);
 

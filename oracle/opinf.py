@@ -190,9 +190,11 @@ def train_coupled(cfg, inputs):
     u0s = [inputs.initial_displacement(train_cfg, s)[None] for s in tr["subdomains"]]
     snaps = [[] for _ in models]
 
-    def record(states):
-        for i, st in enumerate(states):
-            snaps[i].append(st["u"][0].reshape(-1).copy())
+    rom_ids = [i for i, s in enumerate(cfg["subdomains"]) if s["kind"] == "rom"]
+
+    def record(states):   # only the subdomains that become ROMs online (storage; c4: 1.6M DOFs x 501 each)
+        for i in rom_ids:
+            snaps[i].append(states[i]["u"][0].reshape(-1).copy())
 
     states = [m.init_state(u0) for m, u0 in zip(models, u0s)]
     record(states)
@@ -205,6 +207,7 @@ def train_coupled(cfg, inputs):
             continue
         m = models[i]
         X = np.stack(snaps[i], axis=1)
+        snaps[i] = None
         ops[i] = build_rom_operators(X[m.free_dofs], X[m.schwarz_dofs], cfg["dt"], cfg["rom"]["r"],
                                      cfg["rom"]["lam"], cfg["rom"]["energy"], order=cfg["rom"].get("order", 1))
     return ops

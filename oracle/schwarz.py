@@ -39,7 +39,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import fem, opinf, transfer
+from . import cfem, fem, opinf, transfer
 
 GEOM_TOL = 1e-12
 
@@ -131,9 +131,15 @@ class FOM(_Base):
         self.n_sub = int(n_sub)
         self.dt = dt / self.n_sub          # subdomain step dt_i
 
+    # boxes of at least this many elements use the C element loop (oracle/cfem.c, the same definition,
+    # pinned by the same tests); smaller ones the NumPy loop
+    C_FORCE_MIN_ELEMS = 100_000
+
     def force(self, u):
         if self._pk1 is not None:    # SVK / Neohookean (NEXT-3)
             return fem.internal_force_nonlinear(self.box, u, self._pk1)
+        if self.box.n_elems >= self.C_FORCE_MIN_ELEMS:
+            return cfem.internal_force_c(self.box, self.Ke, u)
         return fem.internal_force(self.box, self.Ke, u)
 
     def init_state(self, u0, v0=None):

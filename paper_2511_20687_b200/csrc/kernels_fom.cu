@@ -203,8 +203,10 @@ namespace k1b {
 
 // Tile shape of a subdomain's K1 (0: k1a, 1: k1b): the fraction of lanes that own a node, over x (the
 // tile columns, the excluded last column not counted) and y; k1b only when it is clearly better (it
-// pays ~1% in the two-row warps).  OSAM_K1_SHAPE=0/1 forces one (read per call: tests switch it).
-int k1_shape(const Geom& g, const Faces& f) {
+// pays ~1% in the two-row warps).  OSAM_K1_SHAPE=0/1 forces one.  Chosen once per subdomain by
+// choose_fom_path (at create and at bind, with the TMA descriptors) and read from Faces::shape by every
+// launch, so the shape, the descriptors and the partial-slot counts always agree.
+static int k1_shape_choice(const Geom& g, const Faces& f) {
   const char* e = getenv("OSAM_K1_SHAPE");
   if (e && (e[0] == '0' || e[0] == '1')) return e[0] - '0';
   auto occ = [&](int tx, int ty, int cols, bool xl) {
@@ -215,6 +217,7 @@ int k1_shape(const Geom& g, const Faces& f) {
   const double b = occ(k1b::TX, k1b::TY, k1b::tile_cols(g, f), k1b::xlast_excluded(g, f));
   return b > 1.03 * a ? 1 : 0;
 }
+int k1_shape(const Geom&, const Faces& f) { return f.shape; }
 
 #ifndef OSAM_NL_UNROLL
 #define OSAM_NL_UNROLL 2
@@ -396,6 +399,11 @@ __global__ void __launch_bounds__(GB) small_persistent_kernel(const __grid_const
             if (n >= A.min_iters) {
               C.numden[0] = num;
               C.numden[1] = den;
+              if (C.trace && n <= C.trace_T) {  // convergence trace (osam_set_conv_trace), B = 1
+                double* tr = C.trace + 2 * ((long long)(*C.step_dev - 1) * C.trace_T + (n - 1));
+                tr[0] = num;
+                tr[1] = den;
+              }
               if (!isfinite(num) || !isfinite(den)) {
                 C.flags[1] = 1;
                 C.sticky[0] = 1;
@@ -420,10 +428,13 @@ __global__ void __launch_bounds__(GB) small_persistent_kernel(const __grid_const
   }
 }
 
-bool small_fom(const Geom& g) {
-  const char* e = getenv("OSAM_GATHER_MAX");  // read per call (tests switch it)
+bool small_fom(const Geom& g) { return g.small != 0; }
+
+void choose_fom_path_impl(Geom& g, Faces& f) {
+  const char* e = getenv("OSAM_GATHER_MAX");
   const long long cap = e ? atoll(e) : (1LL << 18);
-  return (long long)g.nn[0] * g.nn[1] * g.nn[2] <= cap;
+  g.small = (long long)g.nn[0] * g.nn[1] * g.nn[2] <= cap ? 1 : 0;
+  f.shape = (unsigned char)k1_shape_choice(g, f);
 }
 
 __device__ __forceinline__ void surface_node(const Geom& g, long long t, int* i, int* j, int* k) {
@@ -837,6 +848,7 @@ int fom_partial_slots(const Geom& g, const Faces& f) {
 int fom_nl_partial_slots(const Geom& g) { return nl_ctas(g); }
 
 bool fom_small(const Geom& g) { return small_fom(g); }
+void choose_fom_path(Geom& g, Faces& f) { choose_fom_path_impl(g, f); }
 
 int small_persistent_grid() {
   static int g = 0;

@@ -145,6 +145,11 @@ __global__ void __launch_bounds__(FIN_T) finalize_kernel(Ctl c, const double2* _
       if (n >= min_iters) {
         c.numden[2 * b] = num;
         c.numden[2 * b + 1] = den;
+        if (c.trace && n <= c.trace_T) {  // convergence trace (osam_set_conv_trace)
+          double* tr = c.trace + 2 * (((long long)(*c.step_dev - 1) * c.trace_T + (n - 1)) * B + b);
+          tr[0] = num;
+          tr[1] = den;
+        }
         if (!isfinite(num) || !isfinite(den)) {
           c.flags[1] = 1;
           c.sticky[0] = 1;

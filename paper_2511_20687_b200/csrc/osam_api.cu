@@ -105,6 +105,7 @@ double g_k1_ms = 0.0;
 long long g_k1_launches = 0;
 double g_k1_bytes = 0.0;
 long long g_launches = 0;
+int g_trace_T = 0;  // osam_set_conv_trace: record (num, den) of tested iterations n <= g_trace_T
 
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes a;
@@ -237,6 +238,9 @@ struct Group {
   int* h_ctl = nullptr;  // pinned copy
   int* iters_all = nullptr;
   long long iters_cap = 0;
+  double* ctrace = nullptr;  // [steps][trace_T][B][2] convergence trace of the last osam_step call
+  long long trace_cap = 0;
+  int trace_T = 0, trace_steps = 0;
   std::vector<cudaEvent_t> ev;
   cudaStream_t cap_main = nullptr;    // private capture streams (the subdomains' stream may be the
   cudaStream_t cap_stream = nullptr;  // legacy default stream, which cannot be captured)
@@ -262,6 +266,7 @@ struct Group {
     dfree(go);
     dfree(numden);
     dfree(iters_all);
+    dfree(ctrace);
     if (h_ctl) cudaFreeHost(h_ctl);
     for (auto e : ev) cudaEventDestroy(e);
   }
@@ -275,6 +280,8 @@ struct Group {
     c.sticky = ctl_i + 4 + 2 * B;
     c.numden = numden;
     c.iters_all = iters_all;
+    c.trace = ctrace;
+    c.trace_T = trace_T;
     c.max_iters = max_iters;
     c.has_cond = 0;
     c.cond = 0;
@@ -359,6 +366,7 @@ int process_ic(Sub& s, int* launches);
 // TMA descriptors of a FOM's state buffers.  Their boxes follow the K1 tile shape, which depends on the
 // faces (kernels_fom.cu k1_shape): encoded at create and again at bind, once the Schwarz faces are known.
 int encode_tmaps(Sub& s) {
+  choose_fom_path(s.g, s.faces);  // K1S vs tiled, tile shape: fixed with the descriptors
   const int nbuf = s.n_sub > 1 ? 3 : 2;
   for (int b = 0; b < nbuf; ++b) {
     int r = make_field_tmap(s.g, s.faces, s.st[b][0], true, &s.tmap[b]);
@@ -393,8 +401,12 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
       if (const int r = encode_tmaps(s)) return fail(OSAM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", r);
       continue;
     }
-    const long long rows_phi = (long long)(s.h_Phi.size() / std::max(1, s.r));
+    const bool subset = !s.h_phi_rows.empty();
+    const long long rows_phi = subset ? s.desc_n_free : (long long)(s.h_Phi.size() / std::max(1, s.r));
     const long long rows_phis = s.r_b > 0 ? (long long)(s.h_Phi_s.size() / s.r_b) : s.n_sdof;
+    if (subset && s.h_phi_rows.back() >= s.n_free)
+      return fail(OSAM_EINVAL, "ROM subdomain %d: phi_rows entry %lld >= n_free = %lld", i, s.h_phi_rows.back(),
+                  s.n_free);
     if (rows_phi != s.n_free || rows_phis != s.n_sdof)
       return fail(OSAM_EINVAL, "ROM subdomain %d: Phi has %lld rows, Phi_s %lld, but the geometric split gives "
                   "n_free=%lld, n_s=%lld", i, rows_phi, rows_phis, s.n_free, s.n_sdof);
@@ -404,7 +416,7 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
       if (s.codes[q] == DOF_FREE) fid.push_back((int)q);
       if (s.codes[q] == DOF_SCHWARZ) sid.push_back((int)q);
     }
-    TRY(upload(&s.Phi, s.h_Phi, s.stream));
+    if (!subset) TRY(upload(&s.Phi, s.h_Phi, s.stream));  // full Phi: the IC restriction u^0 = Phi^T u0
     TRY(upload(&s.Phi_s, s.h_Phi_s, s.stream));
     TRY(upload(&s.Kbar, s.h_Kbar, s.stream));
     TRY(upload(&s.Bbar, s.h_Bbar, s.stream));
@@ -557,7 +569,16 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
         const long long dof = 3 * nodes[qi] + c;
         if (s.codes[dof] == DOF_FREE) {
           code[ld] = (int)ld;
-          for (int k = 0; k < s.r; ++k) phil[ld * s.r + k] = s.h_Phi[free_row[dof] + (size_t)s.n_free * k];
+          long long row = free_row[dof], ld_phi = s.n_free;  // row of h_Phi and its leading dimension
+          if (!s.h_phi_rows.empty()) {  // Phi given on a subset of rows: the lift needs this one
+            auto it = std::lower_bound(s.h_phi_rows.begin(), s.h_phi_rows.end(), row);
+            if (it == s.h_phi_rows.end() || *it != row)
+              return fail(OSAM_EINVAL, "ROM subdomain %d: the Schwarz transfer reads free row %lld of Phi, which is "
+                          "not among phi_rows", j, row);
+            row = (long long)(it - s.h_phi_rows.begin());
+            ld_phi = (long long)s.h_phi_rows.size();
+          }
+          for (int k = 0; k < s.r; ++k) phil[ld * s.r + k] = s.h_Phi[row + (size_t)ld_phi * k];
         } else if (s.codes[dof] == DOF_SCHWARZ) {
           code[ld] = -2 - (int)sidx[dof];
         }
@@ -674,10 +695,20 @@ int process_ic(Sub& s, int* launches) {
     CK(cudaStreamSynchronize(st));
   } else {
     const int c = s.cur;
-    const long long fbs = 3 * s.n_nodes;
-    CK(launch_rom_project(s.n_free, s.r, s.batch, s.Phi, s.free_ids, s.ic_u, fbs, s.n_nodes, s.rst[c][0], st));
-    CK(launch_rom_project(s.n_free, s.r, s.batch, s.Phi, s.free_ids, s.ic_v, fbs, s.n_nodes, s.rst[c][1], st));
-    launch_gather_dofs(s.n_sdof, s.batch, s.sdof_ids, s.ic_u, fbs, s.n_nodes, s.rst[c][3], st);
+    if (s.ic_reduced) {  // osam_set_ic_reduced: u^0, v^0 (r x B) and s0 (n_s x B) as given
+      if (s.ic_s == nullptr && s.n_sdof > 0)
+        return fail(OSAM_EINVAL, "reduced IC: s0 missing although the subdomain has %lld Schwarz DOFs", s.n_sdof);
+      CK(cudaMemcpyAsync(s.rst[c][0], s.ic_u, sizeof(double) * s.r * s.batch, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(s.rst[c][1], s.ic_v, sizeof(double) * s.r * s.batch, cudaMemcpyDeviceToDevice, st));
+      if (s.n_sdof > 0)
+        CK(cudaMemcpyAsync(s.rst[c][3], s.ic_s, sizeof(double) * s.n_sdof * s.batch, cudaMemcpyDeviceToDevice, st));
+    } else {
+      if (!s.Phi) return fail(OSAM_EINVAL, "ROM with a row subset of Phi: use osam_set_ic_reduced");
+      const long long fbs = 3 * s.n_nodes;
+      CK(launch_rom_project(s.n_free, s.r, s.batch, s.Phi, s.free_ids, s.ic_u, fbs, s.n_nodes, s.rst[c][0], st));
+      CK(launch_rom_project(s.n_free, s.r, s.batch, s.Phi, s.free_ids, s.ic_v, fbs, s.n_nodes, s.rst[c][1], st));
+      launch_gather_dofs(s.n_sdof, s.batch, s.sdof_ids, s.ic_u, fbs, s.n_nodes, s.rst[c][3], st);
+    }
     RomLaunch L{};
     L.r = s.r;
     L.r_b = s.r_b;
@@ -709,7 +740,9 @@ int process_ic(Sub& s, int* launches) {
   CK(cudaGetLastError());
   dfree(s.ic_u);
   dfree(s.ic_v);
+  dfree(s.ic_s);
   s.ic_pending = false;
+  s.ic_reduced = false;
   return OSAM_OK;
 }
 
@@ -1226,6 +1259,7 @@ int step_graph(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t, cudaGraphExe
   return OSAM_OK;
 }
 
+int create_body(Sub& s, const osam_subdomain_desc* d, void* cuda_stream);
 }  // namespace
 }  // namespace osam
 
@@ -1272,12 +1306,36 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
   } else if (d->batch > 1) {
     return fail(OSAM_EINVAL, "a FOM subdomain has batch 1");
   }
+  if (d->kind == OSAM_ROM && d->phi_rows) {  // Phi given on a subset of its rows (ascending free-row ids)
+    if (d->n_phi_rows < d->r) return fail(OSAM_EINVAL, "ROM: n_phi_rows < r");
+    for (int64_t q = 0; q < d->n_phi_rows; ++q)
+      if (d->phi_rows[q] < 0 || d->phi_rows[q] >= d->n_free || (q > 0 && d->phi_rows[q] <= d->phi_rows[q - 1]))
+        return fail(OSAM_EINVAL, "ROM: phi_rows must be strictly ascending in [0, n_free)");
+  }
+  {  // device offsets (transfer maps, TMA coordinates) are int32: 3 * padded nodes < 2^31
+    const long long px = (nn0 + 3) / 4 * 4;
+    if (3 * px * nn1 * nn2 >= (1LL << 31)) return fail(OSAM_EINVAL, "mesh too large (3 x padded nodes >= 2^31)");
+  }
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return fail(OSAM_ECUDA, "cudaGetDevice: %s (no usable GPU)", cudaGetErrorString(e));
 
   auto h = std::make_unique<osam_subdomain>();
-  Sub& s = h->s;
+  const int rc = create_body(h->s, d, cuda_stream);
+  if (rc != OSAM_OK) {  // frees whatever create_body allocated (no leak on any error path)
+    osam_destroy(h.release());
+    return rc;
+  }
+  *out = h.release();
+  return OSAM_OK;
+}
+
+}  // extern "C"
+
+namespace osam {
+namespace {
+int create_body(Sub& s, const osam_subdomain_desc* d, void* cuda_stream) {
+  const long long nn0 = d->nel[0] + 1LL, nn1 = d->nel[1] + 1LL, nn2 = d->nel[2] + 1LL;
   s.kind = d->kind;
   for (int a = 0; a < 3; ++a) {
     s.lo[a] = d->lo[a];
@@ -1299,18 +1357,11 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
   g.nn[1] = (int)nn1;
   g.nn[2] = (int)nn2;
   g.px = (int)((nn0 + 3) / 4 * 4);
-  // layout: component stride npad, z stride plane; OSAM_LAYOUT=soa gives
-  // [c][k][j][i], the default interleaves the components per z-plane: [k][c][j][i]
-  static const bool soa = getenv("OSAM_LAYOUT") && std::string(getenv("OSAM_LAYOUT")) == "soa";
-  if (soa) {
-    g.plane = (long long)g.px * nn1;
-    g.npad = (g.plane * nn2 + 31) / 32 * 32;
-    g.total = 3 * g.npad;
-  } else {
-    g.npad = (long long)g.px * nn1;
-    g.plane = 3 * g.npad;
-    g.total = g.plane * nn2;
-  }
+  // layout: the components interleaved per z-plane, [k][c][j][i]: component
+  // stride npad (one component plane), z stride plane = 3 npad
+  g.npad = (long long)g.px * nn1;
+  g.plane = 3 * g.npad;
+  g.total = g.plane * nn2;
   for (int a = 0; a < 3; ++a) g.h[a] = (d->hi[a] - d->lo[a]) / d->nel[a];
   s.n_nodes = nn0 * nn1 * nn2;
   s.mass_e = d->rho * g.h[0] * g.h[1] * g.h[2] / 8.0;
@@ -1366,44 +1417,33 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
                 rowc[2 * at + 1] = K(1);
               }
         }
-    int rc = upload(&s.rowc, rowc, s.stream);
-    if (rc != OSAM_OK) return rc;
-    rc = upload(&s.coef, tab, s.stream);
-    if (rc != OSAM_OK) return rc;
-    rc = dalloc(&s.scratch_a, (size_t)g.total);
-    if (rc == OSAM_OK) rc = dalloc(&s.scratch_v, (size_t)g.total);
-    if (rc != OSAM_OK) {
-      osam_destroy(h.release());
-      return rc;
-    }
+    TRY(upload(&s.rowc, rowc, s.stream));
+    TRY(upload(&s.coef, tab, s.stream));
+    TRY(dalloc(&s.scratch_a, (size_t)g.total));
+    TRY(dalloc(&s.scratch_v, (size_t)g.total));
     const int nbuf = s.n_sub > 1 ? 3 : 2;  // substep chains need a third (q, w) buffer and z
     for (int b = 0; b < nbuf; ++b)
       for (int q = 0; q < 2; ++q) {
-        rc = dalloc(&s.st[b][q], (size_t)g.total);
-        if (rc != OSAM_OK) {
-          osam_destroy(h.release());
-          return rc;
-        }
+        TRY(dalloc(&s.st[b][q], (size_t)g.total));
         CK(cudaMemsetAsync(s.st[b][q], 0, sizeof(double) * g.total, s.stream));
       }
     if (s.n_sub > 1) {
-      rc = dalloc(&s.zbuf, (size_t)g.total);
-      if (rc != OSAM_OK) {
-        osam_destroy(h.release());
-        return rc;
-      }
+      TRY(dalloc(&s.zbuf, (size_t)g.total));
       CK(cudaMemsetAsync(s.zbuf, 0, sizeof(double) * g.total, s.stream));
     }
     const int r = encode_tmaps(s);
-    if (r != 0) {
-      osam_destroy(h.release());
-      return fail(OSAM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", r);
-    }
+    if (r != 0) return fail(OSAM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", r);
   } else {
     s.r = d->r;
     s.r_b = d->r_b;
     s.batch = d->batch;
-    s.h_Phi.assign(d->Phi, d->Phi + (size_t)d->n_free * d->r);
+    s.desc_n_free = d->n_free;
+    if (d->phi_rows) {
+      s.h_phi_rows.assign(d->phi_rows, d->phi_rows + d->n_phi_rows);
+      s.h_Phi.assign(d->Phi, d->Phi + (size_t)d->n_phi_rows * d->r);
+    } else {
+      s.h_Phi.assign(d->Phi, d->Phi + (size_t)d->n_free * d->r);
+    }
     if (d->r_b > 0) {
       s.h_Phi_s.assign(d->Phi_s, d->Phi_s + (size_t)d->n_s * d->r_b);
       s.h_Bbar.assign(d->Bbar, d->Bbar + (size_t)d->r * d->r_b);
@@ -1420,13 +1460,18 @@ int osam_create_subdomain(const osam_subdomain_desc* d, void* cuda_stream, osam_
     if (d->r_b == 0) s.h_Phi_s.clear();
   }
   CK(cudaStreamSynchronize(s.stream));
-  *out = h.release();
   return OSAM_OK;
 }
+}  // namespace
+}  // namespace osam
+
+extern "C" {
 
 int osam_set_ic(osam_subdomain* h, const double* u0, const double* v0) {
   if (!h || !u0) return fail(OSAM_EINVAL, "NULL handle or u0");
   Sub& s = h->s;
+  if (s.kind == OSAM_ROM && !s.h_phi_rows.empty())
+    return fail(OSAM_EINVAL, "ROM with a row subset of Phi cannot restrict a full field: use osam_set_ic_reduced");
   cudaStream_t st = s.stream;
   const size_t nf = (size_t)s.batch * 3 * s.n_nodes;
   double *du = nullptr, *dv = nullptr;
@@ -1435,31 +1480,93 @@ int osam_set_ic(osam_subdomain* h, const double* u0, const double* v0) {
     dv = s.scratch_a;
   } else {
     TRY(dalloc(&du, nf));
-    TRY(dalloc(&dv, nf));
+    const int rc = dalloc(&dv, nf);
+    if (rc != OSAM_OK) {
+      dfree(du);
+      return rc;
+    }
   }
-  if (is_device_ptr(u0))
-    CK(cudaMemcpyAsync(du, u0, nf * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  else
-    CK(cudaMemcpyAsync(du, u0, nf * sizeof(double), cudaMemcpyHostToDevice, st));
-  if (v0 == nullptr)
-    CK(cudaMemsetAsync(dv, 0, nf * sizeof(double), st));
-  else if (is_device_ptr(v0))
-    CK(cudaMemcpyAsync(dv, v0, nf * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  else
-    CK(cudaMemcpyAsync(dv, v0, nf * sizeof(double), cudaMemcpyHostToDevice, st));
-  if (s.kind == OSAM_FOM) {
+  // copy the caller's fields, then synchronise: the caller's buffers are read only during this call
+  cudaError_t e = cudaMemcpyAsync(du, u0, nf * sizeof(double),
+                                  is_device_ptr(u0) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = v0 == nullptr ? cudaMemsetAsync(dv, 0, nf * sizeof(double), st)
+                      : cudaMemcpyAsync(dv, v0, nf * sizeof(double),
+                                        is_device_ptr(v0) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && s.kind == OSAM_FOM) {
     const int c = s.cur;
     launch_fom_pack(s.g, du, s.st[c][0], s.n_nodes, st);
     launch_fom_pack(s.g, dv, s.st[c][1], s.n_nodes, st);  // RAW state (u, v) until the first osam_step
-    s.w_dt = 0.0;
-    CK(cudaStreamSynchronize(st));
     g_launches += 2;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    if (s.kind == OSAM_ROM) {
+      dfree(du);
+      dfree(dv);
+    }
+    return fail(OSAM_ECUDA, "osam_set_ic copies: %s", cudaGetErrorString(e));
+  }
+  if (s.kind == OSAM_FOM) {
+    s.w_dt = 0.0;
   } else {
     dfree(s.ic_u);
     dfree(s.ic_v);
+    dfree(s.ic_s);
     s.ic_u = du;
     s.ic_v = dv;
+    s.ic_reduced = false;
   }
+  s.ic_pending = true;
+  if (s.bound) {
+    int launches = 0;
+    TRY(process_ic(s, &launches));
+    g_launches += launches;
+  }
+  return OSAM_OK;
+}
+
+int osam_set_ic_reduced(osam_subdomain* h, const double* uh0, const double* vh0, const double* s0) {
+  if (!h || !uh0) return fail(OSAM_EINVAL, "NULL handle or uh0");
+  Sub& s = h->s;
+  if (s.kind != OSAM_ROM) return fail(OSAM_EINVAL, "osam_set_ic_reduced applies to a ROM subdomain");
+  cudaStream_t st = s.stream;
+  const size_t nr = (size_t)s.r * s.batch;
+  // the Schwarz DOF count is known only after binding, or from the descriptor's n_s
+  const long long ns = s.bound ? s.n_sdof : (s.r_b > 0 ? (long long)(s.h_Phi_s.size() / s.r_b) : -1);
+  if (s0 && ns < 0) return fail(OSAM_EINVAL, "s0 given but the Schwarz DOF count is unknown (r_b = 0): bind first");
+  double *du = nullptr, *dv = nullptr, *ds = nullptr;
+  int rc = dalloc(&du, nr);
+  if (rc == OSAM_OK) rc = dalloc(&dv, nr);
+  if (rc == OSAM_OK && s0 && ns > 0) rc = dalloc(&ds, (size_t)ns * s.batch);
+  cudaError_t e = cudaSuccess;
+  if (rc == OSAM_OK) {
+    e = cudaMemcpyAsync(du, uh0, nr * sizeof(double),
+                        is_device_ptr(uh0) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+      e = vh0 == nullptr ? cudaMemsetAsync(dv, 0, nr * sizeof(double), st)
+                         : cudaMemcpyAsync(dv, vh0, nr * sizeof(double),
+                                           is_device_ptr(vh0) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && ds)
+      e = cudaMemcpyAsync(ds, s0, sizeof(double) * ns * s.batch,
+                          is_device_ptr(s0) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(OSAM_ECUDA, "osam_set_ic_reduced copies: %s", cudaGetErrorString(e));
+  }
+  if (rc != OSAM_OK) {
+    dfree(du);
+    dfree(dv);
+    dfree(ds);
+    return rc;
+  }
+  dfree(s.ic_u);
+  dfree(s.ic_v);
+  dfree(s.ic_s);
+  s.ic_u = du;
+  s.ic_v = dv;
+  s.ic_s = ds;
+  s.ic_reduced = true;
   s.ic_pending = true;
   if (s.bound) {
     int launches = 0;
@@ -1520,6 +1627,21 @@ int osam_step(osam_subdomain* const* sds, int32_t n_sd, const osam_schwarz_cfg* 
       TRY(dalloc(&G->iters_all, (size_t)cap));
       G->iters_cap = cap;
     }
+    // convergence trace (osam_set_conv_trace): graphs hold the buffer pointer, rebuild them on a change
+    const long long tneed = g_trace_T > 0 ? (long long)n_steps * g_trace_T * B * 2 : 0;
+    if (tneed > G->trace_cap || g_trace_T != G->trace_T) {
+      for (auto& kv : G->graphs) cudaGraphExecDestroy(kv.second);
+      G->graphs.clear();
+      dfree(G->ctrace);
+      G->trace_cap = 0;
+      G->trace_T = g_trace_T;
+      if (tneed > 0) {
+        TRY(dalloc(&G->ctrace, (size_t)tneed));
+        G->trace_cap = tneed;
+      }
+    }
+    if (G->ctrace) CK(cudaMemsetAsync(G->ctrace, 0xff, sizeof(double) * G->trace_cap, st));  // NaN: not tested
+    G->trace_steps = G->ctrace ? n_steps : 0;
     // reset the step counter and the sticky flags of this call
     CK(cudaMemsetAsync(G->ctl_i + 3 + 2 * B, 0, sizeof(int) * 3, st));
   }
@@ -1680,6 +1802,7 @@ void osam_destroy(osam_subdomain* h) {
   dfree(s.rowc);
   dfree(s.ic_u);
   dfree(s.ic_v);
+  dfree(s.ic_s);
   delete h;
 }
 
@@ -1778,6 +1901,25 @@ int osam_opinf_replay(const osam_replay_desc* d, double* err_out, int32_t* best_
 }
 
 void osam_set_profiling(int32_t on) { g_prof = on != 0; }
+
+void osam_set_conv_trace(int32_t max_n) { g_trace_T = max_n > 0 ? max_n : 0; }
+
+int osam_get_conv_trace(osam_subdomain* const* sds, int32_t n_sd, double* out, int32_t* n_steps, int32_t* max_n,
+                        int32_t* batch) {
+  if (!sds || n_sd < 1) return fail(OSAM_EINVAL, "bad osam_get_conv_trace arguments");
+  auto it = g_groups.find(std::vector<osam_subdomain*>(sds, sds + n_sd));
+  if (it == g_groups.end()) return fail(OSAM_EINVAL, "no osam_step call on this subdomain list");
+  const Group& G = *it->second;
+  if (n_steps) *n_steps = G.trace_steps;
+  if (max_n) *max_n = G.trace_T;
+  if (batch) *batch = G.B;
+  if (out && G.ctrace && G.trace_steps > 0) {
+    cudaStream_t st = sds[0]->s.stream;
+    TRY(copy_out(G.ctrace, out, (size_t)G.trace_steps * G.trace_T * G.B * 2, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return OSAM_OK;
+}
 
 void osam_reset_profile(void) {
   g_k1_ms = 0.0;

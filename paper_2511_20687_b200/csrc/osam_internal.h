@@ -28,12 +28,14 @@ struct Geom {
   long long npad;   // component stride
   long long total;  // doubles per field
   double h[3];
+  int small;        // the K1S gather path applies (OSAM_GATHER_MAX, decided at create and at bind)
 };
 
 // Per-subdomain boundary description passed to kernels by value.
 struct Faces {
   unsigned char dir[6];  // Dirichlet component bitmask per face
   unsigned char sw[6];   // 1 if the face is a Schwarz face
+  unsigned char shape;   // K1 tile shape 0: 32x4, 1: 16x8 (kernels_fom.cu k1_shape; decided at create and bind)
 };
 
 // 27 boundary classes x 27 neighbour offsets x 3x3 blocks of the merged hex8 stencil.
@@ -147,10 +149,17 @@ struct Sub {
   double* Z = nullptr;     // (r + r_b) x B
   double* part = nullptr;  // split-K partial products (tc_part_size doubles)
 
-  // pending IC (raw full fields, batch x 3 n)
+  // Phi given on a subset of its rows (osam.h phi_rows): the free-row index of each row of h_Phi,
+  // ascending; empty = all n_free rows.  desc_n_free = the descriptor's n_free.
+  std::vector<long long> h_phi_rows;
+  long long desc_n_free = 0;
+
+  // pending IC (raw full fields, batch x 3 n; or reduced: u^0, v^0 (r x B), s0 (n_s x B))
   bool ic_pending = false;
+  bool ic_reduced = false;
   double* ic_u = nullptr;
   double* ic_v = nullptr;
+  double* ic_s = nullptr;
 };
 
 // ---- kernel launchers (defined in the .cu files) ---------------------------------------
@@ -319,6 +328,8 @@ struct Ctl {
   int* step_dev;     // controller steps started since the last reset
   int* sticky;       // [0] unstable, [1] hit max_iters (this osam_step call)
   int* iters_all;    // [steps][B] per-step iteration counts (may be null)
+  double* trace;     // [steps][trace_T][B][2] (num, den) of every tested iteration n <= trace_T (may be null)
+  int trace_T;
   int max_iters;
   int has_cond;      // graph mode: any_active sets the while-loop condition
   cudaGraphConditionalHandle cond;
@@ -356,7 +367,10 @@ struct SmallArgs {
 };
 cudaError_t launch_small_persistent(const SmallArgs& A, cudaStream_t s);
 int small_persistent_grid();  // CTAs that can be co-resident (cooperative launch bound)
-bool fom_small(const Geom& g);  // the K1S (gather) path applies (OSAM_GATHER_MAX)
+bool fom_small(const Geom& g);  // the K1S (gather) path applies (g.small)
+// Decide the FOM kernel path of a subdomain once (OSAM_GATHER_MAX -> g.small, OSAM_K1_SHAPE or the lane
+// occupancy -> f.shape); called at create and at bind, before the TMA descriptors are encoded.
+void choose_fom_path(Geom& g, Faces& f);
 
 // Convergence test of the sweep that just ran (iteration n = *n_dev + 1): K3 + flags/conditional.
 // Returns the number of kernels launched (1 for a single sample: K3 and the flag update fused).

@@ -25,7 +25,8 @@ ERRORS = {-1: "OSAM_EINVAL", -2: "OSAM_ENOMEM", -3: "OSAM_ECUDA", -4: "OSAM_EOVE
 # C entry points declared in include/osam.h
 EXPORTS = ("osam_create_subdomain", "osam_set_ic", "osam_step", "osam_get_state", "osam_get_accel",
            "osam_get_sizes", "osam_destroy", "osam_last_error", "osam_set_profiling", "osam_reset_profile",
-           "osam_get_profile", "osam_opinf_replay")
+           "osam_get_profile", "osam_opinf_replay", "osam_set_ic_reduced", "osam_set_conv_trace",
+           "osam_get_conv_trace")
 
 
 class osam_subdomain_desc(C.Structure):
@@ -37,7 +38,8 @@ class osam_subdomain_desc(C.Structure):
                 ("Kbar", C.POINTER(C.c_double)), ("Bbar", C.POINTER(C.c_double)),
                 ("e_scale", C.POINTER(C.c_double)),
                 ("Hbar", C.POINTER(C.c_double)), ("Cbar", C.POINTER(C.c_double)),
-                ("n_substeps", C.c_int32), ("integrator", C.c_int32), ("material", C.c_int32)]
+                ("n_substeps", C.c_int32), ("integrator", C.c_int32), ("material", C.c_int32),
+                ("phi_rows", C.POINTER(C.c_int64)), ("n_phi_rows", C.c_int64)]
 
 
 class osam_replay_desc(C.Structure):
@@ -86,8 +88,13 @@ def lib():
                                        C.POINTER(C.c_int64)]
         L.osam_get_profile.restype = None
         L.osam_opinf_replay.argtypes = [C.POINTER(osam_replay_desc), vp, C.POINTER(C.c_int32), vp, vp]
+        L.osam_set_ic_reduced.argtypes = [vp, vp, vp, vp]
+        L.osam_set_conv_trace.argtypes = [C.c_int32]
+        L.osam_set_conv_trace.restype = None
+        i32p = C.POINTER(C.c_int32)
+        L.osam_get_conv_trace.argtypes = [C.POINTER(vp), C.c_int32, vp, i32p, i32p, i32p]
         for name in ("osam_create_subdomain", "osam_set_ic", "osam_step", "osam_get_state", "osam_get_accel",
-                     "osam_get_sizes", "osam_opinf_replay"):
+                     "osam_get_sizes", "osam_opinf_replay", "osam_set_ic_reduced", "osam_get_conv_trace"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -99,17 +106,25 @@ def _check(rc):
     return rc
 
 
-def _ptr(x):
-    """Device pointer of a torch CUDA tensor, host pointer of a C-contiguous float64 ndarray."""
+def _ptr(x, numel=None):
+    """Device pointer of a contiguous float64 torch tensor, host pointer of a C-contiguous float64 ndarray;
+    `numel` (if given) is the element count the library will read or write there."""
     if x is None:
         return None
     if hasattr(x, "data_ptr"):
-        if not x.is_contiguous():
-            raise ValueError("tensor must be contiguous")
-        return C.c_void_p(x.data_ptr())
-    if not (isinstance(x, np.ndarray) and x.dtype == np.float64 and x.flags.c_contiguous):
+        import torch
+        if x.dtype != torch.float64 or not x.is_contiguous():
+            raise ValueError("expected a contiguous float64 tensor")
+        n = x.numel()
+        p = x.data_ptr()
+    elif isinstance(x, np.ndarray) and x.dtype == np.float64 and x.flags.c_contiguous:
+        n = x.size
+        p = x.ctypes.data
+    else:
         raise ValueError("expected a contiguous float64 ndarray or torch tensor")
-    return C.c_void_p(x.ctypes.data)
+    if numel is not None and n != numel:
+        raise ValueError(f"buffer holds {n} doubles, the call needs {numel}")
+    return C.c_void_p(p)
 
 
 def _dptr(a):
@@ -140,6 +155,14 @@ class Subdomain:
             Bbar = np.asfortranarray(rom["Bbar"], dtype=np.float64)
             d.r, d.r_b = Phi.shape[1], Phi_s.shape[1]
             d.n_free, d.n_s = Phi.shape[0], Phi_s.shape[0]
+            if rom.get("phi_rows") is not None:   # Phi on a subset of its rows (include/osam.h)
+                rows = np.ascontiguousarray(rom["phi_rows"], dtype=np.int64)
+                if len(rows) != Phi.shape[0]:
+                    raise ValueError("phi_rows must list one free row per row of Phi")
+                d.phi_rows = rows.ctypes.data_as(C.POINTER(C.c_int64))
+                d.n_phi_rows = len(rows)
+                d.n_free = int(rom["n_free"])
+                self._keep.append(rows)
             d.Phi, d.Phi_s, d.Kbar, d.Bbar = _dptr(Phi), _dptr(Phi_s), _dptr(Kbar), _dptr(Bbar)
             self._keep += [Phi, Phi_s, Kbar, Bbar]
             for name in ("Hbar", "Cbar"):  # polynomial OpInf terms (optional)
@@ -153,6 +176,7 @@ class Subdomain:
                 d.e_scale = _dptr(e)
                 self._keep.append(e)
             self.r = d.r
+            self.n_s = d.n_s
         self.kind = kind
         self.batch = d.batch
         self.nn = tuple(int(n) + 1 for n in nel)
@@ -162,14 +186,29 @@ class Subdomain:
         self.handle = h
         self._keep = []  # the library copied the host arrays
 
+    def _field_size(self):
+        """doubles of a state field: batch x 3n (FOM / full ROM field) or r x batch (ROM state)."""
+        return 3 * self.n_nodes * self.batch
+
     def set_ic(self, u0, v0=None):
-        _check(lib().osam_set_ic(self.handle, _ptr(u0), _ptr(v0)))
+        n = self._field_size()
+        _check(lib().osam_set_ic(self.handle, _ptr(u0, n), _ptr(v0, n)))
+
+    def set_ic_reduced(self, uh0, vh0=None, s0=None):
+        """ROM: u^0, v^0 (batch, r) and s0 (batch, n_s) given directly (osam_set_ic_reduced)."""
+        n = self.r * self.batch
+        _check(lib().osam_set_ic_reduced(self.handle, _ptr(uh0, n), _ptr(vh0, n),
+                                         _ptr(s0, None if s0 is None else self.n_s * self.batch)))
+
+    def _state_size(self):
+        return 3 * self.n_nodes if self.kind == OSAM_FOM else self.r * self.batch
 
     def get_state(self, u_out=None, v_out=None):
-        _check(lib().osam_get_state(self.handle, _ptr(u_out), _ptr(v_out)))
+        n = self._state_size()
+        _check(lib().osam_get_state(self.handle, _ptr(u_out, n), _ptr(v_out, n)))
 
     def get_accel(self, a_out):
-        _check(lib().osam_get_accel(self.handle, _ptr(a_out)))
+        _check(lib().osam_get_accel(self.handle, _ptr(a_out, self._state_size())))
 
     def sizes(self):
         n, f, s = C.c_int64(), C.c_int64(), C.c_int64()
@@ -196,9 +235,29 @@ def osam_step(subdomains, dt, tol_rel, n_steps, max_iters=50, min_iters=2, tol_a
     B = max(s.batch for s in subdomains)
     if iters_out is None:
         iters_out = np.zeros((max(n_steps, 1), B), dtype=np.int32)
+    elif not (isinstance(iters_out, np.ndarray) and iters_out.dtype == np.int32 and iters_out.flags.c_contiguous
+              and iters_out.size >= n_steps * B):
+        raise ValueError("iters_out must be a contiguous int32 array of at least n_steps x batch entries")
     ip = iters_out.ctypes.data_as(C.POINTER(C.c_int32)) if n_steps > 0 else None
     rc = _check(lib().osam_step(arr, len(subdomains), C.byref(cfg), int(n_steps), ip))
     return rc, iters_out[:n_steps]
+
+
+def set_conv_trace(max_n):
+    """Record (num, den) of every tested Schwarz iteration n <= max_n in later osam_step calls (0: off)."""
+    lib().osam_set_conv_trace(int(max_n))
+
+
+def get_conv_trace(subdomains):
+    """Convergence trace of the last osam_step on this list: (n_steps, max_n, batch, 2) float64, NaN = not
+    tested."""
+    arr = (C.c_void_p * len(subdomains))(*[s.handle for s in subdomains])
+    ns, T, B = C.c_int32(), C.c_int32(), C.c_int32()
+    _check(lib().osam_get_conv_trace(arr, len(subdomains), None, C.byref(ns), C.byref(T), C.byref(B)))
+    out = np.empty((ns.value, T.value, B.value, 2))
+    if out.size:
+        _check(lib().osam_get_conv_trace(arr, len(subdomains), _ptr(out), None, None, None))
+    return out
 
 
 def set_profiling(on):
