@@ -27,7 +27,7 @@ def build(cfg, rom_ops=None, stream=None):
         if kind == OSAM_ROM:
             o = rom_ops[i]
             rom = dict(Phi=o["Phi"], Phi_s=o["Phi_s"], Kbar=o["Kbar"], Bbar=o["Bbar"], Hbar=o.get("Hbar"),
-                       Cbar=o.get("Cbar"))
+                       Cbar=o.get("Cbar"), phi_rows=o.get("phi_rows"), n_free=o.get("n_free"))
         integ = OSAM_IMPLICIT if s.get("integrator", "explicit") == "implicit" else OSAM_EXPLICIT
         subs.append(Subdomain(kind, s["lo"], s["hi"], s["nel"], cfg["E"], cfg["nu"], cfg["rho"], s["dirichlet"],
                               stream=stream, rom=rom, e_scale=e_scale(cfg) if kind == OSAM_ROM else None,
