@@ -102,9 +102,29 @@ def workload_ops(cfg):
     return problem.synthetic_rom_ops(cfg)
 
 
-def oracle_rate(cfg, warmup, steps=None, seconds=None):
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def oracle_rate(cfg, warmup, steps=None, seconds=None, threads=None):
     """Oracle DOF-updates/s on cfg: `warmup` untimed controller steps then `steps` timed (or
-    as many as fit in `seconds`). Returns (rate, steps_timed, wall, threads)."""
+    as many as fit in `seconds`), with `threads` threads in the C element loop and the BLAS pool (None:
+    all host cores).  Returns (rate, steps_timed, wall, threads used)."""
+    from threadpoolctl import threadpool_limits
+    from oracle import cfem
+    n_thr = cfem.set_threads(threads or 0)
+    with threadpool_limits(limits=n_thr):
+        return _oracle_rate(cfg, warmup, steps, seconds) + (n_thr,)
+
+
+def _oracle_rate(cfg, warmup, steps=None, seconds=None):
     from oracle import schwarz
     ops = workload_ops(cfg)
     from paper_2511_20687_b200 import problem
@@ -126,12 +146,7 @@ def oracle_rate(cfg, warmup, steps=None, seconds=None):
         el = time.perf_counter() - t0
         if (steps is not None and n >= steps) or (seconds is not None and el >= seconds and n >= 3):
             break
-    try:
-        from threadpoolctl import threadpool_info
-        threads = max([d.get("num_threads", 1) for d in threadpool_info()] + [1])
-    except Exception:
-        threads = 1
-    return sweeps * dofs / el, n, el, threads
+    return sweeps * dofs / el, n, el
 
 
 def max_over_ranks(x, dist, dev=None):
@@ -215,7 +230,7 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / n, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.workload}: {desc}", "sample": sdesc, "parallelism": "rank 0 only"},
-            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "oracle", "cpu": cpu_model(),
                              "sample": f"{args.workload} with lateral extent cut to {SAMPLE_LATERAL} elements: {sdesc}; "
                                        f"{n} controller steps after {args.warmup} warm-up"},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -246,18 +261,36 @@ def roofline_of(prof, prof_ms, peak):
             "k1_share_of_step": prof["k1_ms"] / prof_ms}
 
 
+def c4_trained_ops():
+    """c4's oracle-trained ROMs (tools/gen_c4_rom.py: Phi on the rows the transfer reads, reduced IC), or None."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    try:
+        import gen_c4_rom
+        return gen_c4_rom.load_online_ops()
+    except Exception:
+        return None
+
+
 def largest_config(dev, stream, steps=60, warmup=5):
-    """North_star's HBM target is stated on the largest config (c4: 256^3 FOM between two r = 200
-    ROMs with stand-in operators): steps/s and the K1 roofline there, measured the same way."""
+    """North_star's HBM target is stated on the largest config (c4: 256^3 FOM between two r = 200 ROMs):
+    steps/s and the K1 roofline there, measured the same way as the headline (in-schedule K1 timeline).  The
+    ROMs are the oracle-trained ones when cache/c4_rom_ops.npz exists, else seeded stand-ins of their sizes."""
     import torch
-    from paper_2511_20687_b200 import problem
+    from paper_2511_20687_b200 import osam, problem
     cfg = I.config("c4")
     desc, fom_dofs = workload_desc(cfg)
-    subs = problem.build(cfg, workload_ops(cfg), stream=stream.cuda_stream)
-    for sub, f in zip(subs, problem.initial_fields(cfg)):
-        sub.set_ic(torch.from_numpy(f).to(dev))
+    trained = c4_trained_ops()
+    ops = trained if trained is not None else workload_ops(cfg)
+    subs = problem.build(cfg, {i: dict(o) for i, o in ops.items()}, stream=stream.cuda_stream)
+    fields = problem.initial_fields(cfg)
+    for i, (sub, f) in enumerate(zip(subs, fields)):
+        if trained is not None and cfg["subdomains"][i]["kind"] == "rom":
+            sub.set_ic_reduced(np.ascontiguousarray(ops[i]["uh0"]), None, np.ascontiguousarray(ops[i]["s0"]))
+        else:
+            sub.set_ic(torch.from_numpy(f).to(dev))
     problem.run(cfg, subs, n_steps=warmup)
     torch.cuda.synchronize(dev)
+    osam.k1_timeline(subs, reset=True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -265,13 +298,23 @@ def largest_config(dev, stream, steps=60, warmup=5):
     e1.record(stream)
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1)
+    tl = osam.k1_timeline(subs, reset=True)
     prof, prof_ms = k1_profile(cfg, subs, stream, dev, 10)
     peak, _ = measured_peak()
-    out = {"workload": f"c4: {desc} ({fom_dofs} FOM DOFs; ROM operators: seeded stand-ins of the trained sizes)",
-           "steps": steps, "schwarz_steps_per_s": 1e3 * steps / ms,
+    achieved = tl["bytes"] / (tl["union_ms"] / 1e3) / 1e9 if tl["union_ms"] > 0 else 0.0
+    rs = roofline_of(prof, prof_ms, peak)
+    out = {"workload": f"c4: {desc} ({fom_dofs} FOM DOFs; ROM operators: "
+                       + ("oracle-trained (tools/gen_c4_rom.py)" if trained is not None else
+                          "seeded stand-ins of the trained sizes (cache/c4_rom_ops.npz absent)") + ")",
+           "steps": steps, "ms_per_step": ms / steps, "schwarz_steps_per_s": 1e3 * steps / ms,
            "fom_dof_updates_per_s": int(iters.max(axis=1).sum()) * fom_dofs / (ms / 1e3),
            "schwarz_iters_per_step": float(iters.max(axis=1).mean()),
-           "roofline": dict(bound="hbm", peak=peak, unit="GB/s", **roofline_of(prof, prof_ms, peak))}
+           "roofline": {"bound": "hbm", "peak": peak, "unit": "GB/s", "achieved": achieved, "frac": achieved / peak,
+                        "k1_busy_ms_per_step": tl["union_ms"] / steps, "k1_share_of_step": tl["union_ms"] / ms,
+                        "k1_ms_per_launch": tl["sum_ms"] / max(1, tl["launches"]),
+                        "serial_profile": {"achieved": rs["achieved"], "frac": rs["frac"],
+                                           "k1_ms_per_launch": rs["k1_ms_per_launch"],
+                                           "k1_share_of_step": rs["k1_share_of_step"]}}}
     for sub in subs:
         sub.close()
     return out
@@ -311,6 +354,7 @@ def run_ours(args):
 
     clocks = Clocks(local)
     osam.reset_profile()
+    osam.k1_timeline(subs, reset=True)
     barrier()
     clocks.start()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -322,7 +366,10 @@ def run_ours(args):
     ck = clocks.stop()
     launches = osam.get_profile()["kernel_launches"]
     ms = e0.elapsed_time(e1)
-    # K1 roofline: the same steps again in profiling mode
+    # K1 roofline in the timed schedule itself: first-CTA-start / last-CTA-end stamps of every K1 launch,
+    # folded per sweep on the device (osam_get_k1_timeline)
+    tl = osam.k1_timeline(subs, reset=True)
+    # serialised per-launch K1 times (comparable with the ncu launch list): the same steps in profiling mode
     prof_steps = max(3, min(args.steps, 30))
     prof, prof_ms = k1_profile(cfg, subs, stream, dev, prof_steps)
     ms = max_over_ranks(ms, dist, dev)
@@ -364,7 +411,8 @@ def run_ours(args):
     peak, peak_src = measured_peak()
     k1_ms_per_launch = prof["k1_ms"] / max(1, prof["k1_launches"])
     bytes_per_launch = prof["k1_bytes"] / max(1, prof["k1_launches"])
-    achieved = bytes_per_launch / (k1_ms_per_launch / 1e3) / 1e9 if k1_ms_per_launch > 0 else 0.0
+    achieved_serial = bytes_per_launch / (k1_ms_per_launch / 1e3) / 1e9 if k1_ms_per_launch > 0 else 0.0
+    achieved = tl["bytes"] / (tl["union_ms"] / 1e3) / 1e9 if tl["union_ms"] > 0 else 0.0
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -376,12 +424,22 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(), "kernel": "K1 fom_advance",
                          "bytes_model": "32 B/DOF/sweep (read q, w; write q, w) + from sweep 2 8 B per DOF within one node layer of a Schwarz face (read previous w'; elsewhere the norm term is exactly 0, DESIGN.md R38), two-vector form (SURVEY 8(d), DESIGN.md R30)",
-                         "k1_ms_per_launch": k1_ms_per_launch,
-                         "k1_share_of_step": prof["k1_ms"] / prof_ms,
+                         "k1_bytes_per_step": tl["bytes"] / args.steps,
+                         "k1_busy_ms_per_step": tl["union_ms"] / args.steps,
+                         "k1_ms_per_launch": tl["sum_ms"] / max(1, tl["launches"]),
+                         "k1_launches_per_step": tl["launches"] / args.steps,
+                         "k1_share_of_step": tl["union_ms"] / ms,
                          # algorithmic bytes per controller step x steps/s / peak
-                         "step_frac": prof["k1_bytes"] / prof_steps * steps_per_s / 1e9 / peak,
-                         "timing": f"K1 CUDA events over {prof_steps} steps in profiling mode (host-driven "
-                                   "sweeps) right after the timed region; value is timed with CUDA graphs",
+                         "step_frac": tl["bytes"] / args.steps * steps_per_s / 1e9 / peak,
+                         "timing": "in the timed region itself: every K1 launch stamps its first CTA start and last "
+                                   "CTA end (%globaltimer); K3 folds them per sweep into the time some K1 runs (the "
+                                   "union of the concurrent subdomains' launches); achieved = K1 algorithmic bytes / "
+                                   "that time, so k1_share_of_step <= 1",
+                         "serial_profile": {"k1_ms_per_launch": k1_ms_per_launch, "achieved": achieved_serial,
+                                            "frac": achieved_serial / peak, "k1_share_of_step": prof["k1_ms"] / prof_ms,
+                                            "timing": f"CUDA events around each K1 over {prof_steps} steps in "
+                                                      "profiling mode (host-driven sweeps, K1s serialised on one "
+                                                      "stream), as the ncu launch list sees them"},
                          "peak_source": peak_src},
             "gpu_launches": int(launches),
             "clocks": ck, "e2e": e2e}
@@ -410,7 +468,7 @@ def run_ours(args):
                             "frac": tf / FP64_PEAK_TFLOPS, "traffic": None, "kernel": "NL1 fom_nl_kernel",
                             "flops_model": f"{NL1_FLOPS_PER_ELEMENT[args.material]} FP64 flop per element per "
                                            "FOM advance (DESIGN.md section 11)",
-                            "hbm_achieved_gbs": achieved, "k1_ms_per_launch": k1_ms_per_launch,
+                            "hbm_achieved_gbs": achieved_serial, "k1_ms_per_launch": k1_ms_per_launch,
                             "k1_share_of_step": prof["k1_ms"] / prof_ms,
                             "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"}
     if world == 1 and not args.no_largest and args.workload != "c4" and args.material == "linear":
@@ -419,9 +477,14 @@ def run_ours(args):
         sample = sample_cfg(cfg)
         sdesc, _ = workload_desc(sample)
         rate, n, el, threads = oracle_rate(sample, 1, seconds=10.0)
+        rate1, n1, el1, _ = oracle_rate(sample, 1, seconds=8.0, threads=1)
         line["cpu_baseline"] = {"value": rate, "unit": line["unit"], "cores": threads, "kind": "oracle",
+                                "cpu": cpu_model(), "host_cores": os.cpu_count(),
+                                "one_thread": {"value": rate1, "steps": n1, "seconds": round(el1, 1)},
                                 "sample": f"{args.workload} with lateral extent cut to {SAMPLE_LATERAL} elements "
-                                          f"({sdesc}); {n} controller steps, {el:.1f} s"}
+                                          f"({sdesc}); {n} controller steps, {el:.1f} s; threads = the C element "
+                                          "loop's OpenMP threads and the BLAS pool (the rest of the NumPy loop is "
+                                          "single-threaded)"}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

@@ -207,6 +207,15 @@ void osam_set_profiling(int32_t on);
  * osam_get_conv_trace copies the trace of the last osam_step call on the list `sds` (same order) into out
  * ([n_steps][max_n][batch][2] doubles, host or device; may be NULL to query the sizes). */
 void osam_set_conv_trace(int32_t max_n);
+
+/* In-schedule timeline of the FOM advance K1 (measurement, not part of the method): every tiled K1 launch of
+ * a sweep records its first CTA start and last CTA end (%globaltimer) and K3 folds them per sweep, in the
+ * timed schedule itself (CUDA graph, concurrent branches).  out[6] (host) for the group `sds`, accumulated
+ * since its first osam_step or the last reset: [0] ms during which some K1 ran (the union of the sweep's K1
+ * intervals), [1] ms summed over K1 launches, [2] K1 launches, [3] sweeps, [4] sweeps with the convergence
+ * test (n >= 2), [5] algorithmic bytes of those launches (32 B per DOF per sweep + 8 B per DOF within one
+ * layer of a Schwarz face per tested sweep).  reset != 0 zeroes the accumulators. */
+int osam_get_k1_timeline(osam_subdomain* const* sds, int32_t n_sd, int32_t reset, double* out);
 int osam_get_conv_trace(osam_subdomain* const* sds, int32_t n_sd, double* out, int32_t* n_steps, int32_t* max_n,
                         int32_t* batch);
 void osam_reset_profile(void);

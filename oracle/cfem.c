@@ -16,8 +16,13 @@
  * element contributions in colour order whatever the thread count -> deterministic.
  * Node id p = i + (nx+1)(j + (ny+1)k); arrays node-major (n_nodes, 3).
  */
+#include <omp.h>
 #include <stdint.h>
 #include <string.h>
+
+/* thread count of the element loop (timing of the oracle baseline at 1 thread and at all cores) */
+void oracle_set_threads(int32_t n) { omp_set_num_threads(n > 0 ? n : omp_get_num_procs()); }
+int32_t oracle_get_threads(void) { return omp_get_max_threads(); }
 
 static const int LOC[8][3] = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0},
                               {0, 0, 1}, {1, 0, 1}, {1, 1, 1}, {0, 1, 1}};

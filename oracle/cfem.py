@@ -20,8 +20,14 @@ SRC_PATH = os.path.join(_HERE, "cfem.c")
 _lib = None
 
 
-def build(cc: str = "gcc") -> str:
-    subprocess.run([cc, "-O2", "-fopenmp", "-fPIC", "-shared", "-o", LIB_PATH, SRC_PATH], check=True)
+def build(cc: str = "gcc", force: bool = False) -> str:
+    """Compile cfem.c unless the library is newer than the source; the new file replaces the old one by rename,
+    so a process that has the old library mapped keeps running."""
+    if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= os.path.getmtime(SRC_PATH):
+        return LIB_PATH
+    tmp = f"{LIB_PATH}.{os.getpid()}.tmp"
+    subprocess.run([cc, "-O2", "-fopenmp", "-fPIC", "-shared", "-o", tmp, SRC_PATH], check=True)
+    os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
 
@@ -37,8 +43,18 @@ def _load():
         lib = ctypes.CDLL(LIB_PATH)
         lib.oracle_internal_force.argtypes = [ctypes.c_int32] * 3 + [ctypes.c_void_p] * 3
         lib.oracle_internal_force.restype = None
+        lib.oracle_set_threads.argtypes = [ctypes.c_int32]
+        lib.oracle_set_threads.restype = None
+        lib.oracle_get_threads.restype = ctypes.c_int32
         _lib = lib
     return _lib
+
+
+def set_threads(n: int) -> int:
+    """Threads of the C element loop (n <= 0: all processors); returns the count now in effect."""
+    lib = _load()
+    lib.oracle_set_threads(int(n))
+    return int(lib.oracle_get_threads())
 
 
 def internal_force_c(box, Ke: np.ndarray, u: np.ndarray) -> np.ndarray:

@@ -434,8 +434,10 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + NSTAGE * STAGE_BYTES);
   unsigned long long* empty = full + NSTAGE;
   Prod* pr = reinterpret_cast<Prod*>(empty + NSTAGE);
+  if (L.stamp && threadIdx.x + threadIdx.y == 0) atomicMin(L.stamp, global_ns());  // in-schedule timeline
   if ((int)blockIdx.x >= L.n_tile_ctas) {  // x-face CTAs (after the tile CTAs)
     xface_body(L, xface_sides(L.f), blockIdx.x - L.n_tile_ctas, threadIdx.x + TX * threadIdx.y, blockIdx.x);
+    if (L.stamp && threadIdx.x + threadIdx.y == 0) atomicMax(L.stamp + 1, global_ns());
     return;
   }
   const Geom& g = L.g;
@@ -510,6 +512,7 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
       for (int c = 0; c < 3; ++c) acc[q][c] = 0.0;
   }
   block_partial<NT>(num, den, L.partial, blockIdx.x);
+  if (L.stamp && threadIdx.x + threadIdx.y == 0) atomicMax(L.stamp + 1, global_ns());
 }
 
 // Nodes on an x-face with free DOFs: a group of 4 lanes per node, lane sub = 0, 1, 2 gathers the

@@ -78,6 +78,12 @@ __device__ __forceinline__ double warp_sum(double x) {
   return x;
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Fixed-order block reduction of (num, den) -> partial[slot].
 template <int N>
 __device__ __forceinline__ void block_partial(double num, double den, double2* partial, int slot) {

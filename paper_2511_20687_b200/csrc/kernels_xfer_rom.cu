@@ -90,6 +90,41 @@ __global__ void step_begin_kernel(Ctl c, int B) {
 __device__ __forceinline__ void any_active_body(const Ctl& c, int B) {
   const int n = *c.n_dev + 1;
   *c.n_dev = n;
+  if (c.stamps) {  // K1 timeline of this sweep (every K1 of the sweep joined before K3)
+    unsigned long long s[8], e[8];
+    int m = 0;
+    for (int i = 0; i < c.n_stamp && m < 8; ++i) {
+      const unsigned long long a = c.stamps[2 * i], b = c.stamps[2 * i + 1];
+      c.stamps[2 * i] = ~0ULL;
+      c.stamps[2 * i + 1] = 0ULL;
+      if (a == ~0ULL || b < a) continue;  // no K1 of subdomain i in this sweep
+      int q = m++;
+      for (; q > 0 && s[q - 1] > a; --q) {  // insertion sort by start
+        s[q] = s[q - 1];
+        e[q] = e[q - 1];
+      }
+      s[q] = a;
+      e[q] = b;
+    }
+    double uni = 0.0, sum = 0.0;
+    unsigned long long lo = 0, hi = 0;
+    for (int q = 0; q < m; ++q) {
+      sum += (double)(e[q] - s[q]);
+      if (q == 0 || s[q] > hi) {
+        if (q > 0) uni += (double)(hi - lo);
+        lo = s[q];
+        hi = e[q];
+      } else if (e[q] > hi) {
+        hi = e[q];
+      }
+    }
+    if (m > 0) uni += (double)(hi - lo);
+    c.busy[0] += uni;
+    c.busy[1] += sum;
+    c.busy[2] += m;
+    c.busy[3] += 1.0;
+    c.busy[4] += n >= 2 ? 1.0 : 0.0;
+  }
   int a = 0;
   for (int b = 0; b < B; ++b) a |= c.active[b];
   c.flags[0] = a;

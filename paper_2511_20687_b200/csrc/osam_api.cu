@@ -238,6 +238,8 @@ struct Group {
   int* h_ctl = nullptr;  // pinned copy
   int* iters_all = nullptr;
   long long iters_cap = 0;
+  unsigned long long* stamps = nullptr;  // K1 timeline stamps [n_sd][2] (Ctl::stamps)
+  double* busy = nullptr;                // [5] K1 timeline accumulators (Ctl::busy)
   double* ctrace = nullptr;  // [steps][trace_T][B][2] convergence trace of the last osam_step call
   long long trace_cap = 0;
   int trace_T = 0, trace_steps = 0;
@@ -267,6 +269,8 @@ struct Group {
     dfree(numden);
     dfree(iters_all);
     dfree(ctrace);
+    dfree(stamps);
+    dfree(busy);
     if (h_ctl) cudaFreeHost(h_ctl);
     for (auto e : ev) cudaEventDestroy(e);
   }
@@ -282,6 +286,9 @@ struct Group {
     c.iters_all = iters_all;
     c.trace = ctrace;
     c.trace_T = trace_T;
+    c.stamps = stamps;
+    c.n_stamp = (int)sds.size();
+    c.busy = busy;
     c.max_iters = max_iters;
     c.has_cond = 0;
     c.cond = 0;
@@ -767,6 +774,17 @@ int get_group(osam_subdomain* const* sds, int n_sd, Group** out) {
     CK(cudaMemset(G->ctl_i, 0, sizeof(int) * G->ctl_len()));
     TRY(dalloc(&G->numden, (size_t)2 * G->B));
     CK(cudaMallocHost((void**)&G->h_ctl, sizeof(int) * G->ctl_len()));
+    {  // K1 timeline: stamps (start = ~0, end = 0) and zeroed accumulators
+      std::vector<unsigned long long> st0(2 * G->sds.size());
+      for (size_t q = 0; q < G->sds.size(); ++q) {
+        st0[2 * q] = ~0ULL;
+        st0[2 * q + 1] = 0ULL;
+      }
+      TRY(dalloc(&G->stamps, st0.size()));
+      CK(cudaMemcpy(G->stamps, st0.data(), sizeof(unsigned long long) * st0.size(), cudaMemcpyHostToDevice));
+      TRY(dalloc(&G->busy, 5));
+      CK(cudaMemset(G->busy, 0, sizeof(double) * 5));
+    }
     g_groups[key] = std::move(G);
     it = g_groups.find(key);
   }
@@ -934,8 +952,9 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
     const int with_norm = first ? 0 : 1;
     if (d.kind == OSAM_FOM) {
       const int c = d.cur, x = d.ux;
-      const FomLaunch L = fom_launch(d, d.st[c][0], d.st[c][1], d.st[x][0], d.st[x][1], cfg.dt, cfg.dt,
-                                     0.5 * cfg.dt, cfg.dt, with_norm, G.partial + (size_t)slot * B, nullptr);
+      FomLaunch L = fom_launch(d, d.st[c][0], d.st[c][1], d.st[x][0], d.st[x][1], cfg.dt, cfg.dt,
+                               0.5 * cfg.dt, cfg.dt, with_norm, G.partial + (size_t)slot * B, nullptr);
+      L.stamp = G.stamps + 2 * i;  // in-schedule K1 timeline (tiled K1; folded by K3)
       cudaStream_t ks = st;
       if (par) {
         CK(cudaEventRecord(G.fork_ev[set + i], st));
@@ -1903,6 +1922,35 @@ int osam_opinf_replay(const osam_replay_desc* d, double* err_out, int32_t* best_
 void osam_set_profiling(int32_t on) { g_prof = on != 0; }
 
 void osam_set_conv_trace(int32_t max_n) { g_trace_T = max_n > 0 ? max_n : 0; }
+
+int osam_get_k1_timeline(osam_subdomain* const* sds, int32_t n_sd, int32_t reset, double* out) {
+  if (!sds || n_sd < 1 || !out) return fail(OSAM_EINVAL, "bad osam_get_k1_timeline arguments");
+  auto it = g_groups.find(std::vector<osam_subdomain*>(sds, sds + n_sd));
+  if (it == g_groups.end()) return fail(OSAM_EINVAL, "no osam_step call on this subdomain list");
+  const Group& G = *it->second;
+  cudaStream_t st = sds[0]->s.stream;
+  double b[5];
+  CK(cudaMemcpyAsync(b, G.busy, sizeof b, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  double base = 0.0, band = 0.0;  // algorithmic bytes per sweep (R38) of the timed K1s
+  for (auto h : G.sds) {
+    const Sub& d = h->s;
+    if (d.kind != OSAM_FOM || d.material != OSAM_LINEAR || d.n_sub != 1 || fom_small(d.g)) continue;
+    base += 32.0 * 3.0 * (double)d.n_nodes;
+    band += 8.0 * 3.0 * (double)d.n_band;
+  }
+  out[0] = b[0] * 1e-6;
+  out[1] = b[1] * 1e-6;
+  out[2] = b[2];
+  out[3] = b[3];
+  out[4] = b[4];
+  out[5] = b[3] * base + b[4] * band;
+  if (reset) {
+    CK(cudaMemsetAsync(G.busy, 0, sizeof(double) * 5, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return OSAM_OK;
+}
 
 int osam_get_conv_trace(osam_subdomain* const* sds, int32_t n_sd, double* out, int32_t* n_steps, int32_t* max_n,
                         int32_t* batch) {

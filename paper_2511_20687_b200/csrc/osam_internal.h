@@ -183,6 +183,8 @@ struct FomLaunch {
   double2* partial;    // per-block (num, den)
   int material;        // OSAM_LINEAR (K1) | OSAM_SVK | OSAM_NEOHOOKEAN (NL1)
   int n_tile_ctas;     // K1: CTAs that own tiles (set by launch_fom_advance; the rest do x-face work)
+  unsigned long long* stamp;  // K1 in-schedule timeline (may be null): [0] earliest CTA start, [1] latest
+                              // CTA end, %globaltimer ns (atomicMin / atomicMax); folded by K3, see Ctl
   double mat_lam, mat_mu, mat_kappa;
 };
 // Number of partial slots a K1 launch writes (tiled blocks + x-face blocks).
@@ -330,6 +332,12 @@ struct Ctl {
   int* iters_all;    // [steps][B] per-step iteration counts (may be null)
   double* trace;     // [steps][trace_T][B][2] (num, den) of every tested iteration n <= trace_T (may be null)
   int trace_T;
+  // K1 timeline (may be null): stamps[2 i], [2 i + 1] = first start / last end of subdomain i's K1 in the
+  // sweep that just ran; K3 adds, per sweep, busy[0] += the union of those intervals (ns), busy[1] += their
+  // sum, busy[2] += launches, busy[3] += sweeps, busy[4] += sweeps n >= 2, and resets the stamps
+  unsigned long long* stamps;
+  int n_stamp;
+  double* busy;
   int max_iters;
   int has_cond;      // graph mode: any_active sets the while-loop condition
   cudaGraphConditionalHandle cond;

@@ -26,7 +26,7 @@ ERRORS = {-1: "OSAM_EINVAL", -2: "OSAM_ENOMEM", -3: "OSAM_ECUDA", -4: "OSAM_EOVE
 EXPORTS = ("osam_create_subdomain", "osam_set_ic", "osam_step", "osam_get_state", "osam_get_accel",
            "osam_get_sizes", "osam_destroy", "osam_last_error", "osam_set_profiling", "osam_reset_profile",
            "osam_get_profile", "osam_opinf_replay", "osam_set_ic_reduced", "osam_set_conv_trace",
-           "osam_get_conv_trace")
+           "osam_get_conv_trace", "osam_get_k1_timeline")
 
 
 class osam_subdomain_desc(C.Structure):
@@ -93,8 +93,10 @@ def lib():
         L.osam_set_conv_trace.restype = None
         i32p = C.POINTER(C.c_int32)
         L.osam_get_conv_trace.argtypes = [C.POINTER(vp), C.c_int32, vp, i32p, i32p, i32p]
+        L.osam_get_k1_timeline.argtypes = [C.POINTER(vp), C.c_int32, C.c_int32, C.POINTER(C.c_double)]
         for name in ("osam_create_subdomain", "osam_set_ic", "osam_step", "osam_get_state", "osam_get_accel",
-                     "osam_get_sizes", "osam_opinf_replay", "osam_set_ic_reduced", "osam_get_conv_trace"):
+                     "osam_get_sizes", "osam_opinf_replay", "osam_set_ic_reduced", "osam_get_conv_trace",
+                     "osam_get_k1_timeline"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -258,6 +260,15 @@ def get_conv_trace(subdomains):
     if out.size:
         _check(lib().osam_get_conv_trace(arr, len(subdomains), _ptr(out), None, None, None))
     return out
+
+
+def k1_timeline(subdomains, reset=False):
+    """In-schedule K1 timeline of the group (osam_get_k1_timeline): dict(union_ms, sum_ms, launches, sweeps,
+    tested_sweeps, bytes)."""
+    arr = (C.c_void_p * len(subdomains))(*[s.handle for s in subdomains])
+    out = (C.c_double * 6)()
+    _check(lib().osam_get_k1_timeline(arr, len(subdomains), 1 if reset else 0, out))
+    return dict(zip(("union_ms", "sum_ms", "launches", "sweeps", "tested_sweeps", "bytes"), list(out)))
 
 
 def set_profiling(on):

@@ -22,6 +22,7 @@ import argparse
 import hashlib
 import json
 import os
+import pickle
 import platform
 import subprocess
 import sys
@@ -76,6 +77,7 @@ def main():
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--record", type=str, default=None, help="comma-separated steps with node samples")
     ap.add_argument("--out", type=str, default=None)
+    ap.add_argument("--resume", action="store_true", help="continue from var/<out>_ckpt.pkl")
     args = ap.parse_args()
     cfg = I.config(args.config)
     n_steps = args.steps or cfg["n_steps"]
@@ -96,8 +98,18 @@ def main():
     trace_n, trace_num, trace_den, trace_step = [], [], [], []
     norms = {i: [] for i in range(len(models))}
     vals = {i: [] for i in samples}
-    t0 = time.time()
-    for k in range(1, n_steps + 1):
+    ckpt_path = os.path.join(ROOT, "var", f"{args.out or args.config + '_long'}_ckpt.pkl")
+    k0 = 1
+    el0 = 0.0
+    if args.resume and os.path.exists(ckpt_path):     # oracle state and records of an interrupted run
+        with open(ckpt_path, "rb") as fh:
+            ck = pickle.load(fh)
+        states, iters[:len(ck["iters"])] = ck["states"], ck["iters"]
+        trace_n, trace_num, trace_den, trace_step = ck["trace_n"], ck["trace_num"], ck["trace_den"], ck["trace_step"]
+        norms, vals, k0, el0 = ck["norms"], ck["vals"], ck["k"] + 1, ck["elapsed"]
+        print(f"resumed after step {ck['k']}", flush=True)
+    t0 = time.time() - el0
+    for k in range(k0, n_steps + 1):
         tr = []
         states, it = schwarz.controller_step(models, states, cfg["tol"], cfg["max_iters"], cfg["min_iters"],
                                              trace=tr)
@@ -123,6 +135,13 @@ def main():
         if k in record or k == n_steps:
             _write(args, cfg, n_steps, k, record, iters, trace_step, trace_n, trace_num, trace_den, norms,
                    samples, vals, el)
+        if k % 25 == 0 and k < n_steps:
+            os.makedirs(os.path.dirname(ckpt_path), exist_ok=True)
+            with open(ckpt_path + ".tmp", "wb") as fh:
+                pickle.dump(dict(k=k, states=states, iters=iters[:k].copy(), trace_n=trace_n, trace_num=trace_num,
+                                 trace_den=trace_den, trace_step=trace_step, norms=norms, vals=vals, elapsed=el),
+                            fh, protocol=5)
+            os.replace(ckpt_path + ".tmp", ckpt_path)
 
 
 def _write(args, cfg, n_steps, k_done, record, iters, trace_step, trace_n, trace_num, trace_den, norms, samples,

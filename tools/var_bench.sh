@@ -1,8 +1,8 @@
 #!/bin/bash
-# time variant builds var/*.so with bench.py (no ncu) under the env settings in VARENV
+# time variant builds ab/*.so with bench.py (no ncu) under the env settings in VARENV
 VARENV=${VARENV:-"X=0"}
 cd "$(dirname "$0")/.."
-for v in var/*.so; do
+for v in ab/*.so; do
   for e in $VARENV; do
     echo "== $v $e"; env $e OSAM_LIB=$v timeout 300 python bench.py --steps 30 --warmup 3 --no-cpu-baseline --no-e2e --no-largest 2>&1 | tail -1
   done
