@@ -367,8 +367,14 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
           const double x = xo[c * PLANE], w0 = wo[c * WPL];
           const double an = -C[c] * inv_m;
           const double wn = fma(L.cw, an, w0);
-          qo[c * np] = fma(L.cq, wn, x);
-          wp[c * np] = wn;
+#ifdef OSAM_NOSTORE  // probe: the arithmetic stays, the global stores go (results wrong by design)
+          if (wn == 1.2345e300) {
+#else
+          {
+#endif
+            qo[c * np] = fma(L.cq, wn, x);
+            wp[c * np] = wn;
+          }
           if (L.with_norm) {  // outside the band q = w' itself: d == 0 exactly (R38)
             const double w = fma(L.dt, fma(L.cv, an, w0), x);
             const double q = T.prev() ? qw[c * WPL] : (ZN ? w : wn);
