@@ -103,3 +103,83 @@ def test_reference_arm_under_torchrun_rank0_prints_once():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+# ---- multi-GPU sample sharding of c5 (paper_2511_20687_b200/shard.py) -------------------
+
+def test_sample_slice_partitions_the_batch():
+    from paper_2511_20687_b200 import shard
+    for B in (1, 5, 63, 64):
+        for world in (1, 2, 3, 4, 8):
+            if world > B:
+                continue
+            parts = [shard.sample_slice(B, world, q) for q in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == B
+            assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+            sizes = [b - a for a, b in parts]
+            assert max(sizes) - min(sizes) <= 1 and min(sizes) >= 1
+    cfg = I.config("c5")
+    s = shard.shard_cfg(cfg, 4, 3)
+    assert s["batch"] == 16 and s["samples"]["E"] == cfg["samples"]["E"][48:64]
+    with pytest.raises(ValueError):
+        shard.shard_cfg(I.config("c3"), 2, 0)
+
+
+def _c5_small(n_steps=6, r=24):
+    """c5 geometry and samples with seeded stand-in operators of rank r (cheap; the sharding is what is tested)."""
+    from paper_2511_20687_b200 import problem
+    cfg = I.config("c5")
+    cfg["rom"] = dict(cfg["rom"], r=r)
+    cfg["n_steps"] = n_steps
+    ops = {}
+    for i in range(2):
+        n_free, n_s = problem.dof_split(cfg, i)
+        o = I.synthetic_rom_operators(n_free, n_s, r, 6, cfg["dt"], 11 + i)
+        ops[i] = o
+    return cfg, ops
+
+
+def _oracle_samples(cfg, ops):
+    from oracle import schwarz
+    e = np.asarray(cfg["samples"]["E"]) / cfg["E"]
+    models = schwarz.build_models(cfg, rom_ops=ops, e_scale=e)
+    states, iters = schwarz.run(models, [I.initial_displacements(cfg, s) for s in cfg["subdomains"]], cfg["dt"],
+                                cfg["n_steps"], cfg["tol"])
+    return np.concatenate([states[0]["uh"], states[0]["vh"], states[1]["uh"], states[1]["vh"]], axis=1), iters.T
+
+
+def _shard_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path.insert(0, ROOT)
+    from paper_2511_20687_b200 import shard
+    cfg, ops = _c5_small()
+    mine = shard.shard_cfg(cfg, world, rank)
+    st, it = _oracle_samples(mine, ops)
+    allst = shard.gather_samples(st, dist, cfg["batch"], world)
+    allit = shard.gather_samples(it.astype(np.int64), dist, cfg["batch"], world)
+    if rank == 0:
+        q.put((allst, allit))
+    dist.destroy_process_group()
+
+
+def test_c5_sample_shards_gloo_world2_equal_the_full_batch():
+    """Each rank advances its own slice of the 64 samples (no data-path collective), the per-sample results
+    gathered after the run equal the single-process run of the whole batch (oracle on both sides: the library
+    needs a GPU; tests/test_gpu_shard.py runs the same split through libosam.so)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    allst, allit = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=60)
+    cfg, ops = _c5_small()
+    st, it = _oracle_samples(cfg, ops)
+    assert allst.shape == st.shape == (64, 4 * 24)
+    assert np.array_equal(allit, it)
+    assert np.abs(allst - st).max() <= 1e-13 * np.abs(st).max()
