@@ -282,10 +282,6 @@ struct Prod {
 
 __device__ __forceinline__ void prod_issue(const FomLaunch& L, const TileGrid& G, Prod& pr, unsigned char* ring,
                                            unsigned long long* full, const Maps& M) {
-#ifdef OSAM_NOLOAD  // probe: only the first ring fill is loaded; later planes reuse stale (finite) data
-  if (pr.issued >= NSTAGE) mbar_arrive(&full[pr.issued % NSTAGE]);
-  else
-#endif
   issue_plane(pr.P, pr.wp != 0, pr.it, pr.issued % NSTAGE, ring, full, M);
   ++pr.issued;
   if (++pr.it == pr.P.nplanes) {
@@ -327,13 +323,9 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
     double* A = acc[SA];
     double* B = acc[SB];
     double* C = acc[SC];
-#ifdef OSAM_NOCOMPUTE
-    if (false) {
-#else
     if (T.cy() == 1 && m >= 2 && m <= nz - 2) {
       plane_fast<true, true, true>(A, B, C, xs, pos_base(), S);
     } else {
-#endif
       const Contrib3 r = plane_slow(xs, pos_base(), T.cy(), axis_class(m + 1, g.nn[2]), axis_class(m, g.nn[2]),
                                     axis_class(kf, g.nn[2]), L.rowc);
 #pragma unroll
@@ -367,14 +359,8 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
           const double x = xo[c * PLANE], w0 = wo[c * WPL];
           const double an = -C[c] * inv_m;
           const double wn = fma(L.cw, an, w0);
-#ifdef OSAM_NOSTORE  // probe: the arithmetic stays, the global stores go (results wrong by design)
-          if (wn == 1.2345e300) {
-#else
-          {
-#endif
-            qo[c * np] = fma(L.cq, wn, x);
-            wp[c * np] = wn;
-          }
+          qo[c * np] = fma(L.cq, wn, x);
+          wp[c * np] = wn;
           if (L.with_norm) {  // outside the band q = w' itself: d == 0 exactly (R38)
             const double w = fma(L.dt, fma(L.cv, an, w0), x);
             const double q = T.prev() ? qw[c * WPL] : (ZN ? w : wn);
@@ -418,6 +404,8 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
 #pragma unroll
   for (int c = 0; c < 3; ++c) acc[SC][c] = 0.0;
 }
+
+
 
 __device__ __noinline__ void xface_body(const FomLaunch& L, int side_mask, int blk, int tid, int slot);
 
@@ -472,6 +460,7 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
   double acc[3][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
   double num = 0.0, den = 0.0;
   int gi = 0;
+
   for (int tile = blockIdx.x; tile < G.count(); tile += L.n_tile_ctas) {
     const TileGeo P = tile_geo(g, G, tile);
     Tile T;
