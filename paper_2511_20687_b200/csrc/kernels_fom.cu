@@ -361,14 +361,25 @@ __device__ __forceinline__ void small_step_begin(const Ctl& C) {
   *C.step_dev += 1;
 }
 
+// CLUSTER: the whole group runs as one thread-block cluster (<= 16 CTAs, each looping over its node blocks)
+// and the phases are separated by cluster barriers (barrier.cluster arrive.release / wait.acquire: global
+// writes of the phase are visible after it) instead of grid-wide cooperative barriers
+template <bool CLUSTER>
+__device__ __forceinline__ void phase_sync() {
+  if (CLUSTER)
+    cg::this_cluster().sync();
+  else
+    cg::this_grid().sync();
+}
+
+template <bool CLUSTER>
 __global__ void __launch_bounds__(GB) small_persistent_kernel(const __grid_constant__ SmallArgs A) {
-  cg::grid_group grid = cg::this_grid();
   __shared__ double red[2][GB / 32];
   const Ctl& C = A.ctl;
   int total_vb = 0;
   for (int i = 0; i < A.n_sd; ++i) total_vb += A.s[i].nvb;
   if (blockIdx.x == 0 && threadIdx.x == 0) small_step_begin(C);  // later steps begin inside K3 below
-  grid.sync();
+  phase_sync<CLUSTER>();
   for (int k = 0; k < A.n_steps; ++k) {
     auto cb = [&](int i) { return (k & 1) ? 1 - A.s[i].cur0 : A.s[i].cur0; };
     for (int n = 1; n <= A.max_iters; ++n) {
@@ -377,7 +388,7 @@ __global__ void __launch_bounds__(GB) small_persistent_kernel(const __grid_const
       // reads another destination's output, measured slower on c1: 13.9k vs 18.3k steps/s)
       for (int i = 0; i < A.n_sd; ++i) {
         for (int mi = 0; mi < A.s[i].n_maps; ++mi) small_xfer(A, i, mi, first, k);
-        if (A.s[i].n_maps) grid.sync();
+        if (A.s[i].n_maps) phase_sync<CLUSTER>();
       }
       // K1S of every subdomain (no transfer reads a FOM advance's output, R30)
       for (int vb = blockIdx.x; vb < total_vb; vb += gridDim.x) {
@@ -395,7 +406,7 @@ __global__ void __launch_bounds__(GB) small_persistent_kernel(const __grid_const
         gather_body(L, b);
         __syncthreads();  // block_partial's scratch is reused by the next node block
       }
-      grid.sync();
+      phase_sync<CLUSTER>();
       // K3 and the controller flags (block 0; fixed-order sums); the continue decision goes through A.go so
       // that the next step's begin can be written here too
       if (blockIdx.x == 0) {
@@ -446,7 +457,7 @@ __global__ void __launch_bounds__(GB) small_persistent_kernel(const __grid_const
           if (!go && k + 1 < A.n_steps) small_step_begin(C);
         }
       }
-      grid.sync();
+      phase_sync<CLUSTER>();
       if (!*(volatile int*)A.go) break;
     }
   }
@@ -880,18 +891,57 @@ int small_persistent_grid() {
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_persistent_kernel, GB, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_persistent_kernel<false>, GB, 0);
     g = std::max(1, sms * std::max(1, per_sm));
   }
   return g;
 }
 
+// One thread-block cluster of up to 16 CTAs (non-portable size; cluster barriers between the phases) when the
+// group is small enough that its node blocks fit a few per CTA (OSAM_SMALL_CLUSTER=0: the grid-wide
+// cooperative launch); otherwise every co-resident CTA with grid-wide barriers.
 cudaError_t launch_small_persistent(const SmallArgs& A, cudaStream_t s) {
   int total_vb = 0;
   for (int i = 0; i < A.n_sd; ++i) total_vb += A.s[i].nvb;
+  const bool cl_env = !(getenv("OSAM_SMALL_CLUSTER") && getenv("OSAM_SMALL_CLUSTER")[0] == '0');
+  static int cl_max = -1;
+  if (cl_max < 0) {
+    cl_max = 0;
+    if (cudaFuncSetAttribute(small_persistent_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+        cudaSuccess) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(16);
+      q.blockDim = dim3(GB);
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 16;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      q.attrs = at;
+      q.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxPotentialClusterSize(&n, small_persistent_kernel<true>, &q) == cudaSuccess) cl_max = n;
+    }
+    cudaGetLastError();
+  }
+  if (cl_env && cl_max >= 2 && total_vb <= 8 * cl_max) {
+    cudaLaunchConfig_t cfg = {};
+    const int n = std::min(cl_max, total_vb);
+    cfg.gridDim = dim3(n);
+    cfg.blockDim = dim3(GB);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = n;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, small_persistent_kernel<true>, A);
+  }
   const int grid = std::max(1, std::min(small_persistent_grid(), total_vb));
   void* args[] = {const_cast<SmallArgs*>(&A)};
-  return cudaLaunchCooperativeKernel((void*)small_persistent_kernel, dim3(grid), dim3(GB), args, 0, s);
+  return cudaLaunchCooperativeKernel((void*)small_persistent_kernel<false>, dim3(grid), dim3(GB), args, 0, s);
 }
 
 void launch_fom_advance_nl(const FomLaunch& L, cudaStream_t s, int* launches) {

@@ -10,12 +10,13 @@ from test_gpu_parity import _substeps, run_both  # noqa: F401  (shared GPU-vs-or
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["persistent", "graph"])
+@pytest.fixture(autouse=True, params=["persistent", "persistent_grid", "graph"])
 def gather_path(monkeypatch, request):
-    """K1S everywhere; small all-FOM groups run either the cooperative persistent controller (default) or the
-    per-step CUDA graph (OSAM_SMALL_PERSIST=0)."""
+    """K1S everywhere; small all-FOM groups run the persistent controller as one thread-block cluster (default),
+    as a grid-wide cooperative launch (OSAM_SMALL_CLUSTER=0), or the per-step CUDA graph (OSAM_SMALL_PERSIST=0)."""
     monkeypatch.setenv("OSAM_GATHER_MAX", str(1 << 30))
-    monkeypatch.setenv("OSAM_SMALL_PERSIST", "1" if request.param == "persistent" else "0")
+    monkeypatch.setenv("OSAM_SMALL_PERSIST", "0" if request.param == "graph" else "1")
+    monkeypatch.setenv("OSAM_SMALL_CLUSTER", "0" if request.param == "persistent_grid" else "1")
 
 
 @pytest.fixture(scope="module")
