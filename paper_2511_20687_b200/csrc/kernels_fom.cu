@@ -138,24 +138,6 @@ __device__ __forceinline__ bool mbar_try(unsigned long long* bar, unsigned phase
   return ok != 0;
 }
 
-// the same operations on a precomputed shared-memory address (hoisted out of the plane loop)
-__device__ __forceinline__ bool mbar_try_u32(unsigned bar, unsigned phase) {
-  unsigned ok;
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
-      "selp.u32 %0, 1, 0, P1;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(bar), "r"(phase)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_arrive_u32(unsigned bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
 #ifndef OSAM_BACKOFF
 #define OSAM_BACKOFF 64  // ns between polls of a pending mbarrier phase (frees issue slots; measured +3.6%)

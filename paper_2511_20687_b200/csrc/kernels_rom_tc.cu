@@ -11,6 +11,9 @@
 // shared memory once.  The split-K partials are summed in split order by the consumer kernel: every C
 // element accumulates in a fixed order and results are bitwise repeatable.  Tensor cores only here; the FOM path is HBM-bound and stays on the FP64 pipe.
 #include <algorithm>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "osam_internal.h"
 
@@ -205,6 +208,249 @@ __global__ void tc_lift_reduce_kernel(long long nl, int B, int S, const double* 
   out[(long long)b * nl + q] = v;
 }
 
+
+// ---- persistent controller for batched tensor-core ROM groups (osam_internal.h RomPArgs) -------------------
+__device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// One C tile (TM x TN over K split z) by the 128 threads t of one half of the CTA (named barrier bid): the body
+// of dmma_gemm_kernel.
+__device__ void gemm_tile_dev(const GemmArgs& g, int mt, int nt, int z, double (*As)[TM + 1], double (*Bs)[TN + 1],
+                              int t, int bid) {
+  const int lane = t & 31, warp = t >> 5;
+  const int m0 = mt * TM, n0 = nt * TN, k0 = z * g.kc;
+  const int kn = min(g.kc, g.K - k0);
+  bar_named(bid, 128);  // the previous tile of this half is done with As, Bs
+  for (int q = t; q < g.kc * TM; q += 128) {
+    const int kk = q / TM, mm = q % TM;
+    const int m = m0 + mm;
+    As[kk][mm] = (m < g.M && kk < kn) ? g.A[m * g.sam + (k0 + kk) * g.sak] : 0.0;
+  }
+  for (int q = t; q < g.kc * TN; q += 128) {
+    const int kk = q / TN, nn = q % TN;
+    const int n = n0 + nn;
+    Bs[kk][nn] = (n < g.N && kk < kn) ? g.B[(k0 + kk) * g.sbk + n * g.sbn] : 0.0;
+  }
+  bar_named(bid, 128);
+  const int wm = (warp & 1) * 16, wn = (warp >> 1) * 16;
+  double acc[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
+  for (int ks = 0; ks < g.kc; ks += 4) {
+    double a[2], b[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) a[i] = As[ks + (lane & 3)][wm + 8 * i + (lane >> 2)];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) b[j] = Bs[ks + (lane & 3)][wn + 8 * j + (lane >> 2)];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+  double* C = g.C + (size_t)z * g.M * g.N;
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = m0 + wm + 8 * i + (lane >> 2);
+        const int n = n0 + wn + 8 * j + 2 * (lane & 3) + h;
+        if (m < g.M && n < g.N) C[m + (long long)g.M * n] = acc[i][j][h];
+      }
+}
+
+constexpr int RP_T = 256;  // threads of the persistent CTA (two 128-thread GEMM halves)
+
+// Grid-wide barrier of the co-resident CTAs (cooperative launch): one arrival counter and a generation word in
+// global memory; thread 0 of each CTA arrives with a release fence and waits with acquire loads (nanosleep
+// backoff), the last arrival resets the counter and publishes the next generation.  bar[0] count, bar[1] gen.
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = ld_acquire_gpu(bar + 1);
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      st_release_gpu(bar + 1, g + 1);
+    } else {
+      while (ld_acquire_gpu(bar + 1) == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+
+
+__device__ __forceinline__ void rom_step_begin(const Ctl& C, int B) {
+  for (int b = 0; b < B; ++b) {
+    C.active[b] = 1;
+    C.iters[b] = 0;
+  }
+  C.flags[0] = 1;
+  C.flags[1] = 0;
+  *C.n_dev = 0;
+  *C.step_dev += 1;
+}
+
+__global__ void __launch_bounds__(RP_T) rom_persistent_kernel(const __grid_constant__ RomPArgs A) {
+  extern __shared__ __align__(16) unsigned char rp_smem[];
+  auto As = reinterpret_cast<double (*)[KMAX][TM + 1]>(rp_smem);
+  auto Bs = reinterpret_cast<double (*)[KMAX][TN + 1]>(rp_smem + 2 * sizeof(double) * KMAX * (TM + 1));
+  __shared__ double red[2][RP_T / 32];
+  const Ctl& C = A.ctl;
+  const int B = A.B;
+  const int t = threadIdx.x, lane = t & 31;
+  for (int k = 0; k < A.n_steps; ++k) {
+    if (blockIdx.x == 0 && t == 0) rom_step_begin(C, B);
+    grid_barrier(A.bar);
+    for (int n = 1; n <= A.max_iters; ++n) {
+      const bool first = n == 1;
+      for (int i = 0; i < A.n_sd; ++i) {
+        const RomPSub& d = A.s[i];
+        const RomPSub& src = A.s[d.src];
+        const int c = (k & 1) ? 1 - d.cur0 : d.cur0;
+        const int cs = (k & 1) ? 1 - src.cur0 : src.cur0;
+        const bool newest = (d.src < i) || !first;  // iterate n of an earlier source, else n - 1 (n = 1: checkpoint)
+        // phase 1: predictor u~ -> Z[0:r] (as tc_predict_kernel) and the folded boundary input g^ = G u^_src
+        // -> Z[r:r+rb], one warp per (row, sample): lane l sums k = l, l + 32, ... in order, then a butterfly
+        for (int q = blockIdx.x * RP_T + t; q < d.r * B; q += gridDim.x * RP_T) {
+          const int ii = q % d.r, b = q / d.r;
+          d.Z[ii + (long long)d.rz * b] = fma(A.c2, d.rst[c][2][q], fma(A.dt, d.rst[c][1][q], d.rst[c][0][q]));
+        }
+        {
+          const double* Gu = src.rst[newest ? 1 - cs : cs][0];
+          for (int q = (blockIdx.x * RP_T + t) >> 5; q < d.rb * B; q += (gridDim.x * RP_T) >> 5) {
+            const int m = q % d.rb, b = q / d.rb;
+            const double* gr = d.G + m;
+            const double* ub = Gu + (long long)d.Gr * b;
+            double v = 0.0;
+#pragma unroll 4
+            for (int kk = lane; kk < d.Gr; kk += 32) v = fma(gr[(long long)d.rb * kk], ub[kk], v);
+            v = warp_sum(v);
+            if (lane == 0) d.Z[d.r + m + (long long)d.rz * b] = v;
+          }
+        }
+        grid_barrier(A.bar);
+        // phase 2: araw = [-Kbar | Bbar] [u~; g^], split-K DMMA tiles (the plan of gemm()), two per CTA at a time
+        {
+          GemmArgs g{d.r, B, d.rz, d.KB, 1, d.r, d.Z, 1, d.rz, d.part, d.kc_u};
+          const int mt_n = (d.r + TM - 1) / TM, nt_n = (B + TN - 1) / TN;
+          const int tasks = mt_n * nt_n * d.S_u;
+          const int half = t >> 7, th = t & 127;
+          for (int q = 2 * blockIdx.x + half; q < tasks; q += 2 * gridDim.x) {
+            const int z = q % d.S_u, tile = q / d.S_u;
+            gemm_tile_dev(g, tile % mt_n, tile / mt_n, z, As[half], Bs[half], th, 1 + half);
+          }
+        }
+        grid_barrier(A.bar);
+        // phase 3: epilogue (tc_epilogue_kernel, mode 0): a^', v^', u^', norm partials of the active samples
+        const int nblk = (d.r + RP_T - 1) / RP_T;
+        for (int u = blockIdx.x; u < nblk * B; u += gridDim.x) {
+          const int blk = u % nblk, b = u / nblk;
+          const int ii = blk * RP_T + t;
+          double num = 0.0, den = 0.0;
+          if (ii < d.r && C.active[b]) {
+            const long long id = ii + (long long)d.r * b;
+            double araw = 0.0;
+            for (int z = 0; z < d.S_u; ++z) araw += __ldcg(d.part + (size_t)z * d.r * B + id);
+            const double an = d.e[b] * araw;
+            const double un = d.Z[ii + (long long)d.rz * b];
+            const double vn = fma(0.5 * A.dt, d.rst[c][2][id] + an, d.rst[c][1][id]);
+            if (!first) {
+              const double dd = (un - d.rst[1 - c][0][id]) + A.dt * (vn - d.rst[1 - c][1][id]);
+              const double w = un + A.dt * vn;
+              num = dd * dd;
+              den = w * w;
+            }
+            d.rst[1 - c][0][id] = un;
+            d.rst[1 - c][1][id] = vn;
+            d.rst[1 - c][2][id] = an;
+          }
+          num = warp_sum(num);
+          den = warp_sum(den);
+          if (lane == 0) {
+            red[0][t >> 5] = num;
+            red[1][t >> 5] = den;
+          }
+          __syncthreads();
+          if (t == 0) {
+            double a = 0.0, cc = 0.0;
+            for (int w = 0; w < RP_T / 32; ++w) {
+              a += red[0][w];
+              cc += red[1][w];
+            }
+            A.partial[(long long)(d.slot0 + blk) * B + b] = make_double2(a, cc);
+          }
+          __syncthreads();
+        }
+        grid_barrier(A.bar);
+      }
+      // K3, per sample (CTA b, warp 0): finalize_kernel's fixed-order sum (1024 virtual threads: thread v holds
+      // slot v, a warp butterfly per 32, the warp sums added in order; virtual warps beyond the slots add +0.0 and
+      // are skipped, exactly), the test and the sample's flags
+      for (int b = blockIdx.x; b < B; b += gridDim.x) {
+        if (t < 32) {
+          double num = 0.0, den = 0.0;
+          if (n >= A.min_iters)
+            for (int w = 0; 32 * w < A.n_slots; ++w) {
+              const int v = 32 * w + lane;
+              double x = 0.0, y = 0.0;
+              if (v < A.n_slots) {
+                const double2 pv = __ldcg(A.partial + (long long)v * B + b);
+                x = pv.x;
+                y = pv.y;
+              }
+              num += warp_sum(x);
+              den += warp_sum(y);
+            }
+          if (lane == 0 && C.active[b]) {
+            C.iters[b] = n;
+            if (C.iters_all) C.iters_all[(long long)(*C.step_dev - 1) * B + b] = n;
+            if (n >= A.min_iters) {
+              C.numden[2 * b] = num;
+              C.numden[2 * b + 1] = den;
+              if (C.trace && n <= C.trace_T) {
+                double* tr = C.trace + 2 * (((long long)(*C.step_dev - 1) * C.trace_T + (n - 1)) * B + b);
+                tr[0] = num;
+                tr[1] = den;
+              }
+              if (!isfinite(num) || !isfinite(den)) {
+                C.flags[1] = 1;
+                C.sticky[0] = 1;
+              }
+              bool conv = (num == 0.0) || (num < A.tol_rel * A.tol_rel * den);
+              if (A.tol_abs > 0.0) conv = conv || (num < A.tol_abs * A.tol_abs);
+              if (conv) C.active[b] = 0;
+            }
+          }
+        }
+      }
+      grid_barrier(A.bar);
+      // the continue decision, in every CTA from the same flags (nothing writes them until the next barrier)
+      int any = 0;
+      for (int b = t; b < B; b += RP_T) any |= __ldcg(C.active + b);
+      any = __syncthreads_or(any);
+      const bool unstable = __ldcg(C.flags + 1) != 0;
+      const bool go = any && !unstable && n < A.max_iters;
+      if (blockIdx.x == 0 && t == 0) {  // any_active_body's bookkeeping
+        *C.n_dev = n;
+        C.flags[0] = any;
+        if (any && n >= A.max_iters) C.sticky[1] = 1;
+      }
+      if (!go) break;
+    }
+    grid_barrier(A.bar);  // every CTA has read this step's flags before block 0 begins the next step
+  }
+}
+
 }  // namespace
 
 // Batched ROM advance (B >= 2) on the tensor cores; scratch Z ((r + r_b) x B) and `part` (split-K
@@ -280,6 +526,37 @@ void launch_rom_lift_tc(int r, int B, long long nl, const double* Phi_lift, cons
   launch_k(tc_lift_reduce_kernel, dim3(dim3(cdiv(nl, 256), B)), dim3(256), 0, st, nl, B, S, part, code, sv, ns, out);
   debug_check("tc_lift_reduce_kernel", st);
   *launches += 2;
+}
+
+
+void rom_persist_plan(int r, int rb, int Gr, int B, RomPSub* p) {
+  auto plan = [](int M, int N, int K, int* S, int* kc) {
+    const int s = gemm_splits(M, N, K);
+    *kc = (int)(cdiv(cdiv(K, s), 4) * 4);
+    *S = (int)cdiv(K, *kc);
+  };
+  plan(r, B, r + rb, &p->S_u, &p->kc_u);
+  (void)Gr;
+}
+
+int rom_persist_slots(int r) { return (int)cdiv(r, TM); }
+int rom_persist_tiles(int r, int B) { return (int)(cdiv(r, TM) * cdiv(B, TN)); }
+
+cudaError_t launch_rom_persistent(const RomPArgs& A, cudaStream_t s) {
+  const size_t smem = 2 * sizeof(double) * KMAX * (TM + 1) + 2 * sizeof(double) * KMAX * (TN + 1);
+  static int grid = 0;
+  if (grid == 0) {
+    cudaFuncSetAttribute(rom_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rom_persistent_kernel, RP_T, smem);
+    grid = std::max(1, sms * std::min(1, std::max(1, per_sm)));  // one CTA per SM (two GEMM tiles at a time)
+  }
+  int g = grid;
+  if (const char* e = getenv("OSAM_ROM_PERSIST_GRID")) g = std::max(1, std::min(grid, atoi(e)));
+  void* args[] = {const_cast<RomPArgs*>(&A)};
+  return cudaLaunchCooperativeKernel((void*)rom_persistent_kernel, dim3(g), dim3(RP_T), args, smem, s);
 }
 
 }  // namespace osam

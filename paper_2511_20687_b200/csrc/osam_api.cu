@@ -212,6 +212,7 @@ void release_binding(Sub& s) {
   dfree(s.F);
   dfree(s.Z);
   dfree(s.part);
+  dfree(s.rp_cnt);
   s.bound = false;
   s.group.clear();
 }
@@ -240,6 +241,8 @@ struct Group {
   long long iters_cap = 0;
   unsigned long long* stamps = nullptr;  // K1 timeline stamps [n_sd][2] (Ctl::stamps)
   double* busy = nullptr;                // [5] K1 timeline accumulators (Ctl::busy)
+  double2* ppartial = nullptr;           // norm partials of the persistent batched-ROM controller
+  unsigned* rbar = nullptr;              // its grid barrier (count, generation)
   double* ctrace = nullptr;  // [steps][trace_T][B][2] convergence trace of the last osam_step call
   long long trace_cap = 0;
   int trace_T = 0, trace_steps = 0;
@@ -271,6 +274,8 @@ struct Group {
     dfree(ctrace);
     dfree(stamps);
     dfree(busy);
+    dfree(ppartial);
+    dfree(rbar);
     if (h_ctl) cudaFreeHost(h_ctl);
     for (auto e : ev) cudaEventDestroy(e);
   }
@@ -1673,7 +1678,68 @@ int osam_step(osam_subdomain* const* sds, int32_t n_sd, const osam_schwarz_cfg* 
     persist = d.kind == OSAM_FOM && d.material == OSAM_LINEAR && d.n_sub == 1 && fom_small(d.g) &&
               d.maps.size() <= 6 && d.ux == 1 - d.cur;
   }
-  if (persist) {
+  // groups of batched tensor-core ROMs with the folded exchange (c5): one cooperative persistent launch when
+  // OSAM_ROM_PERSIST=1 (measured 6.2k vs 6.8k steps/s for the per-step graph on c5: its phases are latency-bound
+  // chains of L2 round trips that kernel boundaries do not add much to, so the graph stays the default)
+  bool rpersist = n_steps > 0 && !g_prof && !nograph && B > 1 && n_sd <= ROMP_MAX_SD && !G->trace &&
+                  getenv("OSAM_ROM_PERSIST") && getenv("OSAM_ROM_PERSIST")[0] == '1';
+  for (int i = 0; i < n_sd && rpersist; ++i) {
+    const Sub& d = sds[i]->s;
+    rpersist = d.kind == OSAM_ROM && d.use_tc && d.fold && d.maps.size() == 1 && d.n_sub == 1 && d.beta == 0.0 &&
+               d.nf == 0 && d.batch == B && d.r_b > 0;
+  }
+  if (rpersist) {
+    RomPArgs A{};
+    A.n_sd = n_sd;
+    A.B = B;
+    int slot = 0;
+    for (int i = 0; i < n_sd; ++i) {
+      Sub& d = sds[i]->s;
+      const XferMap& m = d.maps[0];
+      RomPSub& p = A.s[i];
+      p.r = d.r;
+      p.rb = d.r_b;
+      p.rz = d.r + d.r_b;
+      p.src = m.src;
+      p.Gr = sds[m.src]->s.r;
+      p.KB = d.KB;
+      p.G = m.G;
+      p.e = d.e;
+      p.Z = d.Z;
+      p.part = d.part;
+      if (!d.rp_cnt) {
+        TRY(dalloc(&d.rp_cnt, (size_t)rom_persist_tiles(d.r, B)));
+        CK(cudaMemset(d.rp_cnt, 0, sizeof(int) * rom_persist_tiles(d.r, B)));
+      }
+      p.cnt = d.rp_cnt;
+      for (int b = 0; b < 2; ++b)
+        for (int q = 0; q < 4; ++q) p.rst[b][q] = d.rst[b][q];
+      p.slot0 = slot;
+      slot += rom_persist_slots(d.r);
+      p.cur0 = d.cur;
+      rom_persist_plan(d.r, d.r_b, p.Gr, B, &p);
+    }
+    A.n_steps = n_steps;
+    A.min_iters = cfg->min_iters;
+    A.max_iters = cfg->max_iters;
+    A.n_slots = slot;
+    A.dt = cfg->dt;
+    A.c2 = 0.5 * cfg->dt * cfg->dt;
+    A.tol_rel = cfg->tol_rel;
+    A.tol_abs = cfg->tol_abs;
+    if (!G->ppartial) TRY(dalloc(&G->ppartial, (size_t)slot * B));
+    A.partial = G->ppartial;
+    A.ctl = G->ctl(cfg->max_iters);
+    if (!G->go) TRY(dalloc(&G->go, 1));
+    A.go = G->go;
+    if (!G->rbar) TRY(dalloc(&G->rbar, 2));
+    CK(cudaMemsetAsync(G->rbar, 0, 2 * sizeof(unsigned), st));
+    A.bar = G->rbar;
+    CK(launch_rom_persistent(A, st));
+    ++g_launches;
+    if (n_steps & 1)
+      for (int i = 0; i < n_sd; ++i) commit_step(sds[i]->s);
+  } else if (persist) {
     SmallArgs A{};
     A.n_sd = n_sd;
     int slot = 0;
@@ -1733,7 +1799,7 @@ int osam_step(osam_subdomain* const* sds, int32_t n_sd, const osam_schwarz_cfg* 
   CK(cudaGetLastError());
   if (n_steps > 0) {
     if (iters_out) std::memcpy(iters_out, its.data(), sizeof(int32_t) * its.size());
-    if (!(g_prof || nograph) && !persist) {  // kernels the graphs ran: step_begin + the sweeps (max over samples)
+    if (!(g_prof || nograph) && !persist && !rpersist) {  // kernels the graphs ran: step_begin + the sweeps (max over samples)
       for (int k = 0; k < n_steps; ++k) {
         int nmax = 0;
         for (int b = 0; b < B; ++b) nmax = std::max(nmax, its[(size_t)k * B + b]);

@@ -148,6 +148,7 @@ struct Sub {
   double* KBr = nullptr;   // the same, row-major (CUDA-core path)
   double* Z = nullptr;     // (r + r_b) x B
   double* part = nullptr;  // split-K partial products (tc_part_size doubles)
+  int* rp_cnt = nullptr;  // persistent batched-ROM controller: arrival counters of the update GEMM's C tiles
 
   // Phi given on a subset of its rows (osam.h phi_rows): the free-row index of each row of h_Phi,
   // ascending; empty = all n_free rows.  desc_n_free = the descriptor's n_free.
@@ -379,6 +380,36 @@ bool fom_small(const Geom& g);  // the K1S (gather) path applies (g.small)
 // Decide the FOM kernel path of a subdomain once (OSAM_GATHER_MAX -> g.small, OSAM_K1_SHAPE or the lane
 // occupancy -> f.shape); called at create and at bind, before the TMA descriptors are encoded.
 void choose_fom_path(Geom& g, Faces& f);
+
+// Persistent controller for groups of batched tensor-core ROMs with the folded exchange (c5; kernels_rom_tc.cu
+// rom_persistent_kernel): one cooperative launch runs every controller step of an osam_step call -- per ROM in
+// sweep order (1) the predictor and the folded boundary input g^ = G u^_src, (2) the update GEMM [-Kbar | Bbar]
+// [u~; g^] as split-K DMMA tiles whose last split runs the tile's epilogue (a^', v^', u^', norm partials), then K3
+// and the controller flags for every sample -- two grid-wide barriers per ROM and one for K3 per sweep.
+struct RomPSub {
+  int r, rb, rz, Gr, src;
+  const double *KB, *G, *e;
+  double *Z, *part;
+  int* cnt;                  // per C tile of the update GEMM: splits done (the last one runs the epilogue)
+  double* rst[2][4];
+  int slot0, cur0;
+  int S_u, kc_u;             // split-K plan of the update GEMM (as gemm())
+};
+constexpr int ROMP_MAX_SD = 4;
+struct RomPArgs {
+  int n_sd, B;
+  RomPSub s[ROMP_MAX_SD];
+  int n_steps, min_iters, max_iters, n_slots;
+  double dt, c2, tol_rel, tol_abs;
+  double2* partial;
+  Ctl ctl;
+  int* go;
+  unsigned* bar;  // [2] grid barrier (count, generation), zeroed before the launch
+};
+void rom_persist_plan(int r, int rb, int Gr, int B, RomPSub* p);  // split plan of the update GEMM (as gemm())
+int rom_persist_slots(int r);           // norm partial slots of one ROM (one per 32-row tile)
+int rom_persist_tiles(int r, int B);    // C tiles of the update GEMM (arrival counters)
+cudaError_t launch_rom_persistent(const RomPArgs& A, cudaStream_t s);
 
 // Convergence test of the sweep that just ran (iteration n = *n_dev + 1): K3 + flags/conditional.
 // Returns the number of kernels launched (1 for a single sample: K3 and the flag update fused).
