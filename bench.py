@@ -352,12 +352,24 @@ def run_ours(args):
         cfg["material"] = args.material
     desc, fom_dofs = workload_desc(cfg)
     stream = torch.cuda.current_stream(dev)
-    ops = workload_ops(cfg)
+    trained = c4_trained_ops() if args.workload == "c4" else None
+    ops = trained if trained is not None else workload_ops(cfg)
     subs = problem.build(cfg, ops, stream=stream.cuda_stream)
     fields = problem.initial_fields(cfg)
-    gpu_fields = [torch.from_numpy(f).to(dev) for f in fields]
-    for sub, f in zip(subs, gpu_fields):
-        sub.set_ic(f)
+    if trained is not None:  # c4's trained ROMs take the oracle's reduced IC (Phi given on the lift rows only)
+        for i, s_ in enumerate(cfg["subdomains"]):
+            if s_["kind"] == "rom":
+                fields[i] = None
+    gpu_fields = [None if f is None else torch.from_numpy(f).to(dev) for f in fields]
+
+    def upload_ic(src):
+        for i, (sub, f) in enumerate(zip(subs, src)):
+            if f is None:
+                sub.set_ic_reduced(np.ascontiguousarray(ops[i]["uh0"]), None, np.ascontiguousarray(ops[i]["s0"]))
+            else:
+                sub.set_ic(f)
+
+    upload_ic(gpu_fields)
     # warm-up (first call binds the Schwarz maps)
     problem.run(cfg, subs, n_steps=args.warmup)
 
@@ -399,20 +411,22 @@ def run_ours(args):
     # end to end through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
-        host_in = [torch.from_numpy(f).pin_memory() for f in fields]
-        host_out = [torch.empty(2 * f.size, dtype=torch.float64).pin_memory() for f in fields]
+        host_in = [None if f is None else torch.from_numpy(f).pin_memory() for f in fields]
+        # state read-back: FOM u, v (3n each); ROM u^, v^ (r x batch each)
+        host_out = [torch.empty(2 * (3 * sub.n_nodes if sub.kind == osam.OSAM_FOM else sub.r * sub.batch),
+                                dtype=torch.float64).pin_memory() for sub in subs]
         barrier()
         t0 = time.perf_counter()
-        for sub, h in zip(subs, host_in):
-            sub.set_ic(h)
+        upload_ic(host_in)
         _, it2 = problem.run(cfg, subs, n_steps=args.steps)
         for sub, h in zip(subs, host_out):
             n = h.numel() // 2
             sub.get_state(h[:n], h[n:])
         barrier()
         el = max_over_ranks(time.perf_counter() - t0, dist, dev)
-        h2d = sum(f.nbytes for f in fields)
-        d2h = sum(2 * f.nbytes for f in fields) + 4 * (2 + 2) * int(it2.sum())
+        h2d = sum(f.nbytes for f in fields if f is not None) + sum(
+            8 * (ops[i]["uh0"].size + ops[i]["s0"].size) for i, f in enumerate(fields) if f is None)
+        d2h = sum(8 * h.numel() for h in host_out) + 4 * int(it2.size)
         e2e = {"value": sum_over_ranks(int(it2.max(axis=1).sum()) * (rom_units if rom_only else fom_dofs), dist,
                                        dev) / el,
                "unit": "reduced updates/s" if rom_only else UNIT,
@@ -434,6 +448,9 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.workload}: {desc} ({fom_dofs} FOM DOFs)",
                        "l2": "inputs larger than L2 (two state buffers x (q, w) x 8 B x FOM DOFs, > 126 MB)",
+                       **({"rom_operators": "oracle-trained (tools/gen_c4_rom.py, cache/c4_rom_ops.npz)" if trained
+                           is not None else "seeded stand-ins of the trained sizes (osam_inputs.synthetic_rom_operators)"}
+                          if any(s_["kind"] == "rom" for s_ in cfg["subdomains"]) else {}),
                        "parallelism": (f"samples sharded {I.config(args.workload)['batch']}/{world} per rank, no "
                                        "data-path collective" if sharded else "replicas") if world > 1 else "1 GPU"},
             "schwarz_steps_per_s": world * steps_per_s,

@@ -593,26 +593,16 @@ long long tile_count(const Geom& g, const Faces& f) {
   return (long long)tile_cols(g, f) * cdiv(g.nn[1], TY) * cdiv(g.nn[2], ZC);
 }
 
-// CTAs of the tiled kernel: one per tile, or (OSAM_PERSISTENT=1) as many as fit on the device at
-// once, each looping over tiles
+// CTAs of the tiled kernel: one per tile (a persistent variant, each resident CTA looping over tiles with one
+// continuous TMA stream, measured equal in round 1 and was removed)
 int tiled_ctas(const Geom& g, const Faces& f) {
-  static const bool persistent = getenv("OSAM_PERSISTENT") && getenv("OSAM_PERSISTENT")[0] == '1';
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(fom_tiled_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TILED);
     cudaFuncSetAttribute(fom_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_TILED);
     attr = true;
   }
-  if (!persistent) return (int)tile_count(g, f);
-  static int resident = 0;
-  if (resident == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fom_tiled_kernel<false>, NT, SMEM_TILED);
-    resident = std::max(1, sms * std::max(1, per_sm));
-  }
-  return (int)std::min<long long>(resident, tile_count(g, f));
+  return (int)tile_count(g, f);
 }
 
 unsigned xface_blocks(const Geom& g, const Faces& f) {
