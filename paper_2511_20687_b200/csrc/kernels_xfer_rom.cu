@@ -33,20 +33,31 @@ __global__ void transfer_kernel(int n, const int* __restrict__ idx, const double
                                 const int* __restrict__ out, const double* __restrict__ src, long long cs,
                                 long long bs_src, double* __restrict__ dst, long long bs_dst,
                                 const int* __restrict__ active, int compact) {
-  pdl_enter();
+  // The map (out, xi, idx) is fixed at bind, so it is read before waiting for the predecessor (programmatic
+  // dependent launch): only the source field and the store depend on earlier kernels of the sweep.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.y;
-  if (t >= 3 * n || (active != nullptr && !active[b])) return;
-  const int p = t / 3, c = t - 3 * p;
-  const int o = out[3 * p + c];
-  if (o < 0) return;
-  const double x = xi[3 * p], y = xi[3 * p + 1], z = xi[3 * p + 2];
+  const bool in = t < 3 * n;
+  const int p = in ? t / 3 : 0, c = in ? t - 3 * p : 0;
+  const int o = in ? out[3 * p + c] : -1;
+  double x = 0.0, y = 0.0, z = 0.0;
+  int id[8];
+  if (o >= 0) {
+    x = xi[3 * p];
+    y = xi[3 * p + 1];
+    z = xi[3 * p + 2];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) id[q] = idx[8 * p + q];
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (o < 0 || (active != nullptr && !active[b])) return;
   const double* sb = src + b * bs_src + c * cs;
   double acc = 0.0;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const double w = ((q & 1) ? x : 1.0 - x) * ((q & 2) ? y : 1.0 - y) * ((q & 4) ? z : 1.0 - z);
-    acc = fma(w, sb[idx[8 * p + q]], acc);
+    acc = fma(w, sb[id[q]], acc);
   }
   dst[b * bs_dst + (compact ? 3 * p + c : o)] = acc;
 }
@@ -199,6 +210,11 @@ __global__ void __launch_bounds__(FIN_T) finalize_kernel(Ctl c, const double2* _
 }
 
 
+// Programmatic dependent launch, split: a kernel lets its dependents launch, reads what its predecessors do
+// not write (operators and maps fixed at bind) and only then waits for them (pdl_enter does both at once).
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Fixed-order block sum of one value per thread (blockDim.x = 256).
 __device__ __forceinline__ double block_sum256(double v) {
   __shared__ double red[8];
@@ -218,13 +234,25 @@ __global__ void __launch_bounds__(256) rom_project_bnd_kernel(int r_b, int B, lo
                                                               const double* __restrict__ Phi_s,
                                                               const double* __restrict__ s,
                                                               double* __restrict__ gpart) {
-  pdl_enter();
+  pdl_launch();
   const int k = blockIdx.x, z = blockIdx.y, b = blockIdx.z;
   const double* col = Phi_s + (long long)k * ns;
   const double* sb = s + (long long)b * ns;
   const long long q0 = (long long)z * GCHUNK, q1 = q0 + GCHUNK < ns ? q0 + GCHUNK : ns;
+  constexpr int PER = GCHUNK / 256;
+  double phi[PER];  // this thread's Phi_s entries, read before the wait (fixed at bind)
+#pragma unroll
+  for (int m = 0; m < PER; ++m) {
+    const long long q = q0 + threadIdx.x + 256LL * m;
+    phi[m] = q < q1 ? col[q] : 0.0;
+  }
+  pdl_wait();
   double acc = 0.0;
-  for (long long q = q0 + threadIdx.x; q < q1; q += 256) acc = fma(col[q], sb[q], acc);
+#pragma unroll
+  for (int m = 0; m < PER; ++m) {
+    const long long q = q0 + threadIdx.x + 256LL * m;
+    if (q < q1) acc = fma(phi[m], sb[q], acc);
+  }
   acc = block_sum256(acc);
   if (threadIdx.x == 0) gpart[((long long)z * B + b) * r_b + k] = acc;
 }
@@ -244,13 +272,25 @@ __global__ void rom_predict_kernel(int r, int B, const double* __restrict__ uh, 
 // mode 1: acceleration only (initial condition); mode 2 (implicit): the right-hand side
 // e_b (-Kbar u~ + Bbar g^ ...) into ah1, finished by rom_implicit_kernel.
 constexpr int UPD_GS_MAX = 1024;  // r_b staged in shared memory up to this (else per row, same order)
+constexpr int UPD_PRE_K = 8, UPD_PRE_B = 2;  // row entries per lane read before the wait (r <= 256, r_b <= 64)
 __global__ void __launch_bounds__(256) rom_update_kernel(const RomLaunch L, int mode) {
-  pdl_enter();
+  pdl_launch();
   __shared__ double red[2][8];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int i = blockIdx.x * 8 + w;
   const int b = blockIdx.y;
   const int r = L.r, rz = L.r + L.r_b + L.nf;
+  // the operator row [-Kbar | Bbar] of this warp is fixed at bind: read it before waiting for the predecessors
+  const bool pre = r <= 32 * UPD_PRE_K && L.r_b <= 32 * UPD_PRE_B && L.nf == 0 && i < r;
+  double rk[UPD_PRE_K], rb_[UPD_PRE_B];
+  if (pre) {
+    const double* row = L.KBr + (long long)i * rz;
+#pragma unroll
+    for (int m = 0; m < UPD_PRE_K; ++m) rk[m] = lane + 32 * m < r ? row[lane + 32 * m] : 0.0;
+#pragma unroll
+    for (int m = 0; m < UPD_PRE_B; ++m) rb_[m] = lane + 32 * m < L.r_b ? row[r + lane + 32 * m] : 0.0;
+  }
+  pdl_wait();
   const bool on = i < r && (mode == 1 || L.active[b]);
   // g^[., b] = chunk partials summed in order, once per block (every row of the block reads it)
   __shared__ double gs[UPD_GS_MAX];
@@ -268,15 +308,33 @@ __global__ void __launch_bounds__(256) rom_update_kernel(const RomLaunch L, int 
     const double* row = L.KBr + (long long)i * rz;
     const double* us = L.ustar + (long long)r * b;
     double acc = 0.0;
+    if (pre) {  // the same terms in the same order from the preloaded row
+#pragma unroll
+      for (int m = 0; m < UPD_PRE_K; ++m)
+        if (lane + 32 * m < r) acc = fma(rk[m], us[lane + 32 * m], acc);
+#pragma unroll
+      for (int m = 0; m < UPD_PRE_B; ++m) {
+        const int k = lane + 32 * m;
+        if (k < L.r_b) {
+          double g = 0.0;
+          if (gsm)
+            g = gs[k];
+          else
+            for (int z = 0; z < L.gchunks; ++z) g += L.gh[((long long)z * L.B + b) * L.r_b + k];
+          acc = fma(rb_[m], g, acc);
+        }
+      }
+    } else {
 #pragma unroll 4
-    for (int j = lane; j < r; j += 32) acc = fma(row[j], us[j], acc);
-    for (int k = lane; k < L.r_b; k += 32) {
-      double g = 0.0;  // g^[k, b]: chunk partials in order
-      if (gsm)
-        g = gs[k];
-      else
-        for (int z = 0; z < L.gchunks; ++z) g += L.gh[((long long)z * L.B + b) * L.r_b + k];
-      acc = fma(row[r + k], g, acc);
+      for (int j = lane; j < r; j += 32) acc = fma(row[j], us[j], acc);
+      for (int k = lane; k < L.r_b; k += 32) {
+        double g = 0.0;  // g^[k, b]: chunk partials in order
+        if (gsm)
+          g = gs[k];
+        else
+          for (int z = 0; z < L.gchunks; ++z) g += L.gh[((long long)z * L.B + b) * L.r_b + k];
+        acc = fma(row[r + k], g, acc);
+      }
     }
     const double* fb = L.F + (long long)L.nf * b;  // polynomial OpInf features
     for (int q = lane; q < L.nf; q += 32) acc = fma(row[r + L.r_b + q], fb[q], acc);
@@ -325,11 +383,14 @@ constexpr int LIFT_ROWS = 4;
 __global__ void rom_lift_kernel(int r, int B, long long nl, const double* __restrict__ Phi_lift,
                                 const int* __restrict__ code, const double* __restrict__ uh,
                                 const double* __restrict__ s, long long ns, double* __restrict__ out) {
-  pdl_enter();
+  pdl_launch();
   const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const long long nw = (nl + LIFT_ROWS - 1) / LIFT_ROWS;  // warps per sample
-  if (w >= nw * B) return;
+  if (w >= nw * B) {
+    pdl_wait();
+    return;
+  }
   const int b = (int)(w / nw);
   const long long ld0 = (w % nw) * LIFT_ROWS;
   int cd[LIFT_ROWS];
@@ -342,7 +403,30 @@ __global__ void rom_lift_kernel(int r, int B, long long nl, const double* __rest
     acc[q] = 0.0;
   }
   const double* u = uh + (long long)r * b;
-  if ((r & 1) == 0) {
+  if ((r & 1) == 0 && r <= 256) {  // Phi_lift rows (fixed at bind) read before waiting for the predecessors
+    double2 a[LIFT_ROWS][4];
+#pragma unroll
+    for (int q = 0; q < LIFT_ROWS; ++q)
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        a[q][m] = (cd[q] >= 0 && lane + 32 * m < r / 2) ? reinterpret_cast<const double2*>(row[q])[lane + 32 * m]
+                                                        : make_double2(0.0, 0.0);
+    pdl_wait();
+    const double2* u2 = reinterpret_cast<const double2*>(u);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int j = lane + 32 * m;
+      if (j >= r / 2) break;
+      const double2 x = u2[j];
+#pragma unroll
+      for (int q = 0; q < LIFT_ROWS; ++q)
+        if (cd[q] >= 0) {
+          acc[q] = fma(a[q][m].x, x.x, acc[q]);
+          acc[q] = fma(a[q][m].y, x.y, acc[q]);
+        }
+    }
+  } else if ((r & 1) == 0) {
+    pdl_wait();
     const double2* u2 = reinterpret_cast<const double2*>(u);
 #pragma unroll 2
     for (int j = lane; j < r / 2; j += 32) {
@@ -356,6 +440,7 @@ __global__ void rom_lift_kernel(int r, int B, long long nl, const double* __rest
         }
     }
   } else {
+    pdl_wait();
     for (int j = lane; j < r; j += 32) {
       const double x = u[j];
 #pragma unroll
