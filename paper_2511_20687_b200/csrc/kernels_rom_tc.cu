@@ -44,17 +44,20 @@ struct GemmArgs {
 // One block: a 32 x 32 tile of C over the K range [z kc, (z+1) kc): A and B staged once in shared
 // memory, then 2 x 2 m8n8k4 fragments per warp accumulate over k in increasing order.
 __global__ void __launch_bounds__(128) dmma_gemm_kernel(const GemmArgs g) {
-  pdl_enter();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ double As[KMAX][TM + 1];  // As[k][m]
   __shared__ double Bs[KMAX][TN + 1];  // Bs[k][n]
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int m0 = blockIdx.x * TM, n0 = blockIdx.y * TN, k0 = blockIdx.z * g.kc;
   const int kn = min(g.kc, g.K - k0);
+  // A is an operator fixed at bind ([-Kbar | Bbar], the folded G, Phi_dS^T, Phi_lift): staged before waiting for
+  // the predecessors (programmatic dependent launch); B is this sweep's data
   for (int q = t; q < g.kc * TM; q += 128) {
     const int kk = q / TM, mm = q % TM;
     const int m = m0 + mm;
     As[kk][mm] = (m < g.M && kk < kn) ? g.A[m * g.sam + (k0 + kk) * g.sak] : 0.0;
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int q = t; q < g.kc * TN; q += 128) {
     const int kk = q / TN, nn = q % TN;
     const int n = n0 + nn;
@@ -103,8 +106,14 @@ int gemm(GemmArgs g, double* part, cudaStream_t s) {
   const int S = gemm_splits(g.M, g.N, g.K);
   g.kc = (int)(cdiv(cdiv(g.K, S), 4) * 4);
   g.C = part;
-  // no programmatic early launch for the GEMM: its many CTAs would sit on SMs the predecessors need
-  dmma_gemm_kernel<<<dim3(dim3(cdiv(g.M, TM), cdiv(g.N, TN), cdiv(g.K, g.kc))), 128, 0, s>>>(g);
+  // programmatic early launch (OSAM_GEMM_PDL=1): the CTAs stage A while the predecessors finish; measured
+  // against the plain launch (its many CTAs may sit on SMs the predecessors need)
+  static const bool gemm_pdl = getenv("OSAM_GEMM_PDL") && getenv("OSAM_GEMM_PDL")[0] == '1';
+  const dim3 grid(cdiv(g.M, TM), cdiv(g.N, TN), cdiv(g.K, g.kc));
+  if (gemm_pdl)
+    launch_k(dmma_gemm_kernel, grid, dim3(128), 0, s, g);
+  else
+    dmma_gemm_kernel<<<grid, 128, 0, s>>>(g);
   debug_check("dmma_gemm_kernel", s);
   return (int)cdiv(g.K, g.kc);
 }
