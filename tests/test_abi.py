@@ -92,3 +92,44 @@ def test_descriptor_validation_before_any_gpu_work(case):
     rc = osam.lib().osam_create_subdomain(ctypes.byref(d), None, ctypes.byref(h))
     assert rc == -1, (case, rc, osam.lib().osam_last_error())
     assert not h.value
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="libosam.so not built")
+@pytest.mark.parametrize("rows", [[3, 1, 5], [0, 2, 9], [0, -1, 2], [0, 1]])
+def test_phi_row_subset_validation_before_any_gpu_work(rows):
+    """phi_rows (Phi given on the rows the transfer lifts) must be strictly ascending free-row indices in
+    [0, n_free) with at least r rows: anything else is OSAM_EINVAL from host-side validation (GPU or not)."""
+    import numpy as np
+    from paper_2511_20687_b200 import osam
+    r, n_free = 3, 9
+    d = osam.osam_subdomain_desc()
+    d.kind = osam.OSAM_ROM
+    d.lo[:] = [0.0, 0.0, 0.0]
+    d.hi[:] = [1.0, 1.0, 1.0]
+    d.nel[:] = [2, 2, 2]
+    d.E, d.nu, d.rho = 1e9, 0.25, 1000.0
+    d.batch = 1
+    ids = np.asarray(rows, dtype=np.int64)
+    Phi = np.asfortranarray(np.ones((len(rows), r)))
+    K = np.asfortranarray(np.eye(r))
+    d.r, d.r_b, d.n_free, d.n_s = r, 0, n_free, 0
+    d.Phi, d.Kbar = osam._dptr(Phi), osam._dptr(K)
+    d.phi_rows = ids.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    d.n_phi_rows = len(rows)
+    h = ctypes.c_void_p()
+    rc = osam.lib().osam_create_subdomain(ctypes.byref(d), None, ctypes.byref(h))
+    assert rc == -1, (rows, rc, osam.lib().osam_last_error())
+    assert not h.value
+
+
+def test_binding_rejects_wrong_buffers():
+    """The binding checks dtype, contiguity and element count before handing a pointer to the library."""
+    import numpy as np
+    from paper_2511_20687_b200 import osam
+    with pytest.raises(ValueError):
+        osam._ptr(np.zeros(4, dtype=np.float32))
+    with pytest.raises(ValueError):
+        osam._ptr(np.zeros(4), numel=5)
+    with pytest.raises(ValueError):
+        osam._ptr(np.zeros((4, 4))[:, 1])
+    assert osam._ptr(np.zeros(4), numel=4) is not None
