@@ -19,13 +19,16 @@ constexpr int PLANE = PX * PY;                             // positions per stag
 #ifndef OSAM_NSTAGE
 #define OSAM_NSTAGE 4
 #endif
-constexpr int NSTAGE = OSAM_NSTAGE;  // ring: NSTAGE-2 planes in flight, current, previous
+constexpr int NSTAGE = OSAM_NSTAGE;
+#ifndef OSAM_PROD
+#define OSAM_PROD 2  // TMA producer: 0 thread 0 with a shared cursor, 1 thread 0 stateless, 2 rotated over the warps
+#endif  // ring: NSTAGE-2 planes in flight, current, previous
 constexpr int ARR_BYTES = 3 * PLANE * 8;                   // X (x,y,z comps) of one plane, with halo
 constexpr int ARR_STRIDE = (ARR_BYTES + 127) / 128 * 128;  // 128-B aligned TMA destinations
 constexpr int WPL = TX * TY;                               // tile positions of W (no halo)
 constexpr int W_BYTES = 3 * WPL * 8;
 constexpr int STAGE_BYTES = ARR_STRIDE + 2 * W_BYTES;  // X, W, W'_prev
-constexpr int SMEM_TILED = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8 + 64;  // ring, barriers, producer cursor
+constexpr int SMEM_TILED = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8;  // ring, barriers
 
 // ---- interior rows: parity-reduced stencil ---------------------------------------------
 // On a uniform box every interior block K_cd(ox, oy, oz) is even or odd in ox and in oy (the 1D
@@ -270,30 +273,6 @@ __device__ __forceinline__ void issue_plane(const TileGeo& P, bool wp, int it, i
   if (wp) tma_load_4d(st + ARR_STRIDE + W_BYTES, M.wp, P.x0 + 2, P.y0 + 1, m, 0, &full[s]);
 }
 
-// Producer cursor (thread 0 only, in shared memory): the next plane to load, possibly in a later
-// tile of this CTA.  Plane p of the CTA's stream lives in stage p % NSTAGE.
-struct Prod {
-  int t;       // tile (>= ntiles: done)
-  int it;      // plane within the tile
-  int issued;  // planes issued so far (all tiles)
-  int wp;      // the tile stages the previous iterate (needs_prev)
-  TileGeo P;
-};
-
-__device__ __forceinline__ void prod_issue(const FomLaunch& L, const TileGrid& G, Prod& pr, unsigned char* ring,
-                                           unsigned long long* full, const Maps& M) {
-  issue_plane(pr.P, pr.wp != 0, pr.it, pr.issued % NSTAGE, ring, full, M);
-  ++pr.issued;
-  if (++pr.it == pr.P.nplanes) {
-    pr.it = 0;
-    pr.t += L.n_tile_ctas;
-    if (pr.t < G.count()) {
-      pr.P = tile_geo(L.g, G, pr.t);
-      pr.wp = needs_prev(L, pr.P);
-    }
-  }
-}
-
 // One staged plane (iteration it of the tile, plane gi of the CTA's stream, staged plane
 // m = kbeg - 1 + it).  Accumulator slots rotate by role: A = acc[SA] (node plane m+1), B = acc[SB]
 // (plane m), C = acc[SC] (plane m-1, finished here if it lies in [kbeg, kend], then zeroed to become
@@ -302,19 +281,25 @@ __device__ __forceinline__ void prod_issue(const FomLaunch& L, const TileGrid& G
 template <bool ZN, int SA, int SB, int SC>
 __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStencil& S, const Tile& T, int it, int gi,
                                         double (&acc)[3][3], double& num, double& den, unsigned char* ring,
-                                        unsigned long long* full, unsigned long long* empty, const Maps& M, Prod* pr,
-                                        const TileGrid& G) {
+                                        unsigned long long* full, unsigned long long* empty, const Maps& M) {
   const Geom& g = L.g;
   const int nz = g.nn[2] - 1;
   const long long np = g.npad;
   const int m = T.kbeg - 1 + it;
   const int kf = m - 1;
   const bool fin = T.writer() && kf >= T.kbeg && kf <= T.kend;
-  // producer: plane gi + NSTAGE - 2 into the stage released by plane gi - 2
-  if (threadIdx.x + threadIdx.y == 0 && pr->t < G.count()) {
-    const int p = pr->issued;
+  // producer (thread 0): plane it + NSTAGE - 2 into the stage released by plane it - 2.  One tile per CTA, so
+  // the plane and its coordinates follow from the iteration and the thread's own tile constants (no cursor
+  // in shared memory: c3 932 -> 953 steps/s; the role rotated over the warps, a non-blocking producer and an
+  // issue at the end of the iteration were measured slower, profiles/r3_k1_experiments.md)
+  if (threadIdx.x + threadIdx.y == 0 && it + NSTAGE - 2 < T.nplanes) {
+    const int p = it + NSTAGE - 2;
     if (p >= NSTAGE) mbar_wait(&empty[p % NSTAGE], (unsigned)(((p - NSTAGE) / NSTAGE) & 1));
-    prod_issue(L, G, *pr, ring, full, M);
+    TileGeo Pq;
+    Pq.x0 = T.i - 2;
+    Pq.y0 = T.j - 1;
+    Pq.kbeg = T.kbeg;
+    issue_plane(Pq, T.prev(), p, p % NSTAGE, ring, full, M);
   }
   const int s = gi % NSTAGE;
   mbar_wait(&full[s], (unsigned)((gi / NSTAGE) & 1));
@@ -412,6 +397,7 @@ __device__ __noinline__ void xface_body(const FomLaunch& L, int side_mask, int b
 #ifndef OSAM_MINB
 #define OSAM_MINB 4
 #endif
+
 #ifndef OSAM_K1_ROT
 // 0 (default): one copy of k1_iter per plane, the accumulator roles moved through the slots (9 moves per
 // plane); 1: k1_iter unrolled by the period 3 of the roles (no moves).  The single copy keeps the loop in
@@ -427,7 +413,6 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
   unsigned char* ring = smem;
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + NSTAGE * STAGE_BYTES);
   unsigned long long* empty = full + NSTAGE;
-  Prod* pr = reinterpret_cast<Prod*>(empty + NSTAGE);
   if (L.stamp && threadIdx.x + threadIdx.y == 0) atomicMin(L.stamp, global_ns());  // in-schedule timeline
   if ((int)blockIdx.x >= L.n_tile_ctas) {  // x-face CTAs (after the tile CTAs)
     xface_body(L, xface_sides(L.f), blockIdx.x - L.n_tile_ctas, threadIdx.x + TX * threadIdx.y, blockIdx.x);
@@ -438,74 +423,56 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
   const int nx = g.nn[0] - 1, ny = g.nn[1] - 1;
   const Maps M{&tmx, &tmw, &tmwp};
   const TileGrid G = tile_grid(g, L.f);
-  const bool lead = threadIdx.x + threadIdx.y == 0;
+  // one CTA per tile (the grid's first n_tile_ctas CTAs)
+  const TileGeo P = tile_geo(g, G, blockIdx.x);
+  Tile T;
+  T.i = P.x0 + 2 + (int)threadIdx.x;
+  T.j = P.y0 + 1 + (int)threadIdx.y;
+  const bool active = (T.i <= nx) && (T.j <= ny);
+  const bool xface = (T.i == 0) || (T.i == nx);
+  const int xsd = T.i == 0 ? 0 : 1;
+  const bool writer = active && (!xface || L.f.dir[xsd] == 7 || L.f.sw[xsd]);
+  T.flags = (active ? 1u : 0u) | (xface ? 2u : 0u) | (writer ? 4u : 0u) | ((unsigned)axis_class(T.j, g.nn[1]) << 3) |
+            (needs_prev(L, P) ? 32u : 0u);
+  T.kbeg = P.kbeg;
+  T.kend = P.kend;
+  T.nplanes = P.nplanes;
+  T.id0 = T.i + (long long)g.px * T.j;
 
-  if (lead) {
+  if (threadIdx.x + threadIdx.y == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NWARP);
     }
     mbar_fence_init();
-    pr->t = blockIdx.x;
-    pr->it = 0;
-    pr->issued = 0;
-    if (pr->t < G.count()) {
-      pr->P = tile_geo(g, G, pr->t);
-      pr->wp = needs_prev(L, pr->P);
-      for (int p = 0; p < NSTAGE - 2 && pr->t < G.count(); ++p) prod_issue(L, G, *pr, ring, full, M);
-    }
+    for (int p = 0; p < NSTAGE - 2 && p < T.nplanes; ++p) issue_plane(P, T.prev(), p, p, ring, full, M);
   }
   __syncthreads();
 
   double acc[3][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
   double num = 0.0, den = 0.0;
-  int gi = 0;
-
-  for (int tile = blockIdx.x; tile < G.count(); tile += L.n_tile_ctas) {
-    const TileGeo P = tile_geo(g, G, tile);
-    Tile T;
-    T.i = P.x0 + 2 + (int)threadIdx.x;
-    T.j = P.y0 + 1 + (int)threadIdx.y;
-    const bool active = (T.i <= nx) && (T.j <= ny);
-    const bool xface = (T.i == 0) || (T.i == nx);
-    const int xsd = T.i == 0 ? 0 : 1;
-    const bool writer = active && (!xface || L.f.dir[xsd] == 7 || L.f.sw[xsd]);
-    T.flags = (active ? 1u : 0u) | (xface ? 2u : 0u) | (writer ? 4u : 0u) | ((unsigned)axis_class(T.j, g.nn[1]) << 3) |
-              (needs_prev(L, P) ? 32u : 0u);
-    T.kbeg = P.kbeg;
-    T.kend = P.kend;
-    T.nplanes = P.nplanes;
-    T.id0 = T.i + (long long)g.px * T.j;
 #if OSAM_K1_ROT
-    for (int it = 0; it < T.nplanes;) {  // unrolled by the period 3 of the slot rotation
-      k1_iter<ZN, 0, 1, 2>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
-      ++gi;
-      if (++it >= T.nplanes) break;
-      k1_iter<ZN, 2, 0, 1>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
-      ++gi;
-      if (++it >= T.nplanes) break;
-      k1_iter<ZN, 1, 2, 0>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
-      ++gi;
-      ++it;
-    }
-#else
-    // one copy of the iteration; the roles move through the slots (C, zeroed by k1_iter, becomes A)
-#pragma unroll 1
-    for (int it = 0; it < T.nplanes; ++it, ++gi) {
-      k1_iter<ZN, 0, 1, 2>(L, S, T, it, gi, acc, num, den, ring, full, empty, M, pr, G);
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        acc[2][c] = acc[1][c];
-        acc[1][c] = acc[0][c];
-        acc[0][c] = 0.0;
-      }
-    }
-#endif
-#pragma unroll
-    for (int q = 0; q < 3; ++q)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) acc[q][c] = 0.0;
+  for (int it = 0; it < T.nplanes;) {  // unrolled by the period 3 of the slot rotation
+    k1_iter<ZN, 0, 1, 2>(L, S, T, it, it, acc, num, den, ring, full, empty, M);
+    if (++it >= T.nplanes) break;
+    k1_iter<ZN, 2, 0, 1>(L, S, T, it, it, acc, num, den, ring, full, empty, M);
+    if (++it >= T.nplanes) break;
+    k1_iter<ZN, 1, 2, 0>(L, S, T, it, it, acc, num, den, ring, full, empty, M);
+    ++it;
   }
+#else
+  // one copy of the iteration; the roles move through the slots (C, zeroed by k1_iter, becomes A)
+#pragma unroll 1
+  for (int it = 0; it < T.nplanes; ++it) {
+    k1_iter<ZN, 0, 1, 2>(L, S, T, it, it, acc, num, den, ring, full, empty, M);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      acc[2][c] = acc[1][c];
+      acc[1][c] = acc[0][c];
+      acc[0][c] = 0.0;
+    }
+  }
+#endif
   block_partial<NT>(num, den, L.partial, blockIdx.x);
   if (L.stamp && threadIdx.x + threadIdx.y == 0) atomicMax(L.stamp + 1, global_ns());
 }

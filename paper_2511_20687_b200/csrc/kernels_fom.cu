@@ -926,6 +926,334 @@ cudaError_t launch_small_persistent(const SmallArgs& A, cudaStream_t s) {
   return cudaLaunchCooperativeKernel((void*)small_persistent_kernel<false>, dim3(grid), dim3(GB), args, 0, s);
 }
 
+// ---- cluster-resident controller for small all-FOM groups (c1) ---------------------------------------------
+// The persistent controller above keeps the state in global memory, so each of its phases is a chain of L2 round
+// trips.  Here the whole group lives on chip, in one thread-block cluster: every CTA holds a replica of every
+// subdomain's stencil input X (the checkpoint q with the current Schwarz values) and of the checkpoint u (the
+// previous step's X) in its shared memory, computes every transfer itself into its own replica (a few hundred
+// nodes: cheaper than exchanging them), and advances a contiguous range of nodes of every subdomain (its own W,
+// W' and Q' in shared memory).  The cluster exchanges only (a) the CTAs' norm partials once per sweep (DSMEM, one
+// cluster barrier) and (b) once per controller step the new checkpoint q of every CTA's nodes into every replica
+// (DSMEM stores, one cluster barrier).  The two X replicas alternate by step parity, the three W buffers by role.
+// Per node the arithmetic is gather_body's (class-table stencil, the same FMA order, the same finish) and per
+// destination DOF small_xfer's, so the states are bitwise those of the graph path; only the summation order of
+// the convergence norm differs (every CTA sums the partials in rank order, so all take the same decision).
+constexpr int RB = 512;  // threads per CTA (4 lanes per node: 128 nodes per pass)
+
+__device__ __forceinline__ int res_chunk(int n, int nc) { return (n + nc - 1) / nc; }
+
+template <int NTH>
+__device__ __forceinline__ double2 cta_sum2(double num, double den, double* red) {
+  num = warp_sum(num);
+  den = warp_sum(den);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[2 * w] = num;
+    red[2 * w + 1] = den;
+  }
+  __syncthreads();
+  double a = 0.0, b = 0.0;
+  if (threadIdx.x == 0)
+    for (int q = 0; q < NTH / 32; ++q) {
+      a += red[2 * q];
+      b += red[2 * q + 1];
+    }
+  return make_double2(a, b);
+}
+
+__global__ void __launch_bounds__(RB, 1) small_resident_kernel(const __grid_constant__ SmallArgs A) {
+  extern __shared__ __align__(16) double rsm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int NC = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  const int tid = threadIdx.x;
+  const Ctl& C = A.ctl;
+  // shared memory: X replicas [2][xtot] | per subdomain owned arrays W[3][3][chunk], QN[3][chunk] | partials
+  // [2][NC] (x num, y den) | block scratch | flags
+  int xoff[SMALL_MAX_SD], woff[SMALL_MAX_SD], chunk[SMALL_MAX_SD], cum[SMALL_MAX_SD + 1];
+  int xtot = 0, wtot = 0;
+  cum[0] = 0;
+  for (int i = 0; i < A.n_sd; ++i) {
+    xoff[i] = xtot;
+    xtot += (int)A.s[i].L.g.total;
+    const Geom& g = A.s[i].L.g;
+    chunk[i] = res_chunk(g.nn[0] * g.nn[1] * g.nn[2], NC);
+    woff[i] = wtot;
+    wtot += 12 * chunk[i];
+    cum[i + 1] = cum[i] + chunk[i];
+  }
+  double* Xb[2] = {rsm, rsm + xtot};
+  double* Wb = rsm + 2 * xtot;
+  double2* cpart = reinterpret_cast<double2*>(Wb + wtot);  // [2][NC]
+  double* red = reinterpret_cast<double*>(cpart + 2 * NC);  // [2 * RB / 32]
+  int* flag = reinterpret_cast<int*>(red + 2 * (RB / 32));
+
+  // load the replicas (X = q of the checkpoint, U = u of the checkpoint) and this CTA's W
+  for (int i = 0; i < A.n_sd; ++i) {
+    const SmallSub& d = A.s[i];
+    const long long tot = d.L.g.total;
+    const double* q0 = d.st[d.cur0][0];
+    const double* u0 = d.st[1 - d.cur0][0];
+    for (long long t = tid; t < tot; t += RB) {
+      Xb[0][xoff[i] + t] = q0[t];
+      Xb[1][xoff[i] + t] = u0[t];
+    }
+    const Geom& g = d.L.g;
+    const int n = g.nn[0] * g.nn[1] * g.nn[2];
+    for (int l = tid; l < chunk[i]; l += RB) {
+      const int t = rank * chunk[i] + l;
+      if (t >= n) continue;
+      const int ii = t % g.nn[0], jj = (t / g.nn[0]) % g.nn[1], kk = t / (g.nn[0] * g.nn[1]);
+      const long long id = gidx(g, ii, jj, kk);
+#pragma unroll
+      for (int c = 0; c < 3; ++c) Wb[woff[i] + c * chunk[i] + l] = d.st[d.cur0][1][c * g.npad + id];
+    }
+  }
+  if (rank == 0 && tid == 0) small_step_begin(C);
+  int ck = 0;     // W buffer of the checkpoint (buffers 0..2, each [3][chunk])
+  int kpar = 0;   // X replica of the current step (the other one holds u of the checkpoint)
+  cl.sync();
+  for (int k = 0; k < A.n_steps; ++k) {
+    double* Xc = Xb[kpar];
+    const double* Xu = Xb[1 - kpar];
+    int wo = ck;
+    for (int n = 1; n <= A.max_iters; ++n) {
+      const bool first = n == 1;
+      const int wp = wo;                       // W' of iterate n - 1 (unused at n = 1)
+      wo = (ck + 1 + (n & 1)) % 3;             // W' of iterate n: alternates between the two non-checkpoint buffers
+      // K2 in sweep order into this CTA's replica (a later destination reads iterate n of an earlier source)
+      for (int i = 0; i < A.n_sd; ++i) {
+        const SmallSub& d = A.s[i];
+        for (int mi = 0; mi < d.n_maps; ++mi) {
+          const SmallMap& m = d.maps[mi];
+          const bool newest = (m.src < i) || !first;
+          const double* field = (newest ? Xc : Xu) + xoff[m.src];
+          const long long cs = A.s[m.src].L.g.npad;
+          for (int t = tid; t < 3 * m.n; t += RB) {
+            const int p = t / 3, cc = t - 3 * p;
+            const int o = __ldg(m.out + 3 * p + cc);
+            if (o < 0) continue;
+            const double xx = __ldg(m.xi + 3 * p), yy = __ldg(m.xi + 3 * p + 1), zz = __ldg(m.xi + 3 * p + 2);
+            const double* sb = field + cc * cs;
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const double w = ((q & 1) ? xx : 1.0 - xx) * ((q & 2) ? yy : 1.0 - yy) * ((q & 4) ? zz : 1.0 - zz);
+              acc = fma(w, sb[__ldg(m.idx + 8 * p + q)], acc);
+            }
+            Xc[xoff[i] + o] = acc;
+          }
+        }
+        if (d.n_maps) __syncthreads();
+      }
+      // K1S on this CTA's nodes of every subdomain: 4 lanes per node (oz = sub - 1), gather_body's arithmetic
+      double num = 0.0, den = 0.0;
+      for (int u0 = 0; u0 < cum[A.n_sd]; u0 += RB / 4) {
+        const int u = u0 + (tid >> 2), sub = tid & 3;
+        int i = 0;
+        while (i + 1 < A.n_sd && u >= cum[i + 1]) ++i;
+        const SmallSub& d = A.s[i];
+        const Geom& g = d.L.g;
+        const int l = u - cum[i];
+        const int t = rank * chunk[i] + l;
+        const bool valid = u < cum[A.n_sd] && l < chunk[i] && t < g.nn[0] * g.nn[1] * g.nn[2];
+        const int ii = valid ? t % g.nn[0] : 0;
+        const int jj = valid ? (t / g.nn[0]) % g.nn[1] : 0;
+        const int kk = valid ? t / (g.nn[0] * g.nn[1]) : 0;
+        const int cx = axis_class(ii, g.nn[0]), cy = axis_class(jj, g.nn[1]), cz = axis_class(kk, g.nn[2]);
+        const double* X = Xc + xoff[i];
+        const long long np = g.npad;
+        double f[3] = {0.0, 0.0, 0.0};
+        const int oz = sub - 1;
+        if (valid && sub < 3 && kk + oz >= 0 && kk + oz <= g.nn[2] - 1) {
+          const double* coef = d.L.coef + (size_t)(cx + 3 * (cy + 3 * cz)) * 27 * 9;
+#pragma unroll
+          for (int oy = -1; oy <= 1; ++oy) {
+            if (jj + oy < 0 || jj + oy > g.nn[1] - 1) continue;
+#pragma unroll
+            for (int ox = -1; ox <= 1; ++ox) {
+              if (ii + ox < 0 || ii + ox > g.nn[0] - 1) continue;
+              const long long q = gidx(g, ii + ox, jj + oy, kk + oz);
+              const double x[3] = {X[q], X[np + q], X[2 * np + q]};
+              const double* cb = coef + ((ox + 1) + 3 * ((oy + 1) + 3 * (oz + 1))) * 9;
+#pragma unroll
+              for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int dd = 0; dd < 3; ++dd) f[c] = fma(__ldg(cb + c * 3 + dd), x[dd], f[c]);
+            }
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double f1 = __shfl_down_sync(0xffffffffu, f[c], 1, 4);
+          const double f2 = __shfl_down_sync(0xffffffffu, f[c], 2, 4);
+          f[c] = (f[c] + f1) + f2;
+        }
+        if (valid && sub == 0) {
+          const long long id = gidx(g, ii, jj, kk);
+          const unsigned fm = free_mask(g, d.L.f, ii, jj, kk);
+          const double inv_m = d.L.inv_mass[(cx == 1 ? 1 : 0) + (cy == 1 ? 2 : 0) + (cz == 1 ? 4 : 0)];
+          const FomLaunch& L = d.L;
+          double* W = Wb + woff[i];
+          const int ch = chunk[i];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const double x = X[c * np + id];
+            double wn = 0.0, qn = x;
+            if ((fm >> c) & 1) {
+              const double w0 = W[(ck * 3 + c) * ch + l];
+              const double an = -f[c] * inv_m;
+              wn = fma(L.cw, an, w0);
+              qn = fma(L.cq, wn, x);
+              const double w = fma(L.dt, fma(L.cv, an, w0), x);
+              if (!first) {
+                const double dl = 0.5 * L.dt * (wn - W[(wp * 3 + c) * ch + l]);
+                num = fma(dl, dl, num);
+                den = fma(w, w, den);
+              }
+            }
+            W[(wo * 3 + c) * ch + l] = wn;
+            W[(9 + c) * ch + l] = qn;
+          }
+        }
+      }
+      // the CTA's (num, den), then the cluster's, summed in rank order by every CTA (the same decision everywhere)
+      const double2 mine = cta_sum2<RB>(num, den, red);
+      if (tid == 0) cpart[(n & 1) * NC] = mine;  // slot 0 of this CTA's own copy; read remotely below
+      cl.sync();
+      if (tid == 0) {
+        double sn = 0.0, sd = 0.0;
+        for (int r = 0; r < NC; ++r) {
+          const double2 v = *cl.map_shared_rank(cpart + (n & 1) * NC, r);
+          sn += v.x;
+          sd += v.y;
+        }
+        int go;
+        if (rank == 0) {  // controller state (as small_persistent_kernel's K3)
+          if (C.active[0]) {
+            C.iters[0] = n;
+            if (n >= A.min_iters) {
+              C.numden[0] = sn;
+              C.numden[1] = sd;
+              if (!isfinite(sn) || !isfinite(sd)) {
+                C.flags[1] = 1;
+                C.sticky[0] = 1;
+              }
+            }
+          }
+        }
+        bool conv = false, bad = false;
+        if (n >= A.min_iters) {
+          bad = !isfinite(sn) || !isfinite(sd);
+          conv = (sn == 0.0) || (sn < A.tol_rel * A.tol_rel * sd);
+          if (A.tol_abs > 0.0) conv = conv || (sn < A.tol_abs * A.tol_abs);
+        }
+        go = !conv && !bad && n < A.max_iters;
+        if (rank == 0) {
+          if (conv) C.active[0] = 0;
+          *C.n_dev = n;
+          C.flags[0] = C.active[0];
+          if (C.iters_all) C.iters_all[*C.step_dev - 1] = C.iters[0];
+          if (C.active[0] && n >= A.max_iters) C.sticky[1] = 1;
+          if (!go && k + 1 < A.n_steps) small_step_begin(C);
+        }
+        flag[0] = go;
+      }
+      __syncthreads();
+      if (!flag[0]) break;
+    }
+    // commit: the new checkpoint q (Q' of the last iterate) of this CTA's nodes into every replica's other buffer
+    // (which held u of the old checkpoint, no longer read); the last iterate's W' becomes the checkpoint w
+    double* Xn = Xb[1 - kpar];
+    for (int i = 0; i < A.n_sd; ++i) {
+      const Geom& g = A.s[i].L.g;
+      const int n = g.nn[0] * g.nn[1] * g.nn[2];
+      const int ch = chunk[i];
+      const double* QN = Wb + woff[i] + 9 * ch;
+      for (int e = tid; e < 3 * ch * NC; e += RB) {
+        const int r = e / (3 * ch), rem = e - r * 3 * ch, c = rem / ch, l = rem - c * ch;
+        const int t = rank * ch + l;
+        if (t >= n) continue;
+        const int ii = t % g.nn[0], jj = (t / g.nn[0]) % g.nn[1], kk = t / (g.nn[0] * g.nn[1]);
+        *cl.map_shared_rank(Xn + xoff[i] + c * g.npad + gidx(g, ii, jj, kk), r) = QN[c * ch + l];
+      }
+    }
+    ck = wo;
+    kpar ^= 1;
+    cl.sync();
+  }
+  // write back: the checkpoint buffer gets q (this CTA's nodes) and w, the spare buffer's q slot u (R30)
+  for (int i = 0; i < A.n_sd; ++i) {
+    const SmallSub& d = A.s[i];
+    const int cbf = (A.n_steps & 1) ? 1 - d.cur0 : d.cur0;
+    const Geom& g = d.L.g;
+    const int n = g.nn[0] * g.nn[1] * g.nn[2];
+    const int ch = chunk[i];
+    for (int e = tid; e < 3 * ch; e += RB) {
+      const int c = e / ch, l = e - c * ch;
+      const int t = rank * ch + l;
+      if (t >= n) continue;
+      const int ii = t % g.nn[0], jj = (t / g.nn[0]) % g.nn[1], kk = t / (g.nn[0] * g.nn[1]);
+      const long long o = c * g.npad + gidx(g, ii, jj, kk);
+      d.st[cbf][0][o] = Xb[kpar][xoff[i] + o];
+      d.st[1 - cbf][0][o] = Xb[1 - kpar][xoff[i] + o];
+      d.st[cbf][1][o] = Wb[woff[i] + (ck * 3 + c) * ch + l];
+    }
+  }
+}
+
+// Launch of the cluster-resident controller; cudaErrorNotSupported when the group does not fit one cluster's
+// shared memory (or clusters of >= 2 CTAs are unavailable): the caller then uses small_persistent_kernel.
+cudaError_t launch_small_resident(const SmallArgs& A, cudaStream_t s) {
+  if (getenv("OSAM_SMALL_RESIDENT") && getenv("OSAM_SMALL_RESIDENT")[0] == '0') return cudaErrorNotSupported;
+  static int cl_max = -1;
+  constexpr int SMEM_MAX = 227 * 1024;
+  if (cl_max < 0) {
+    cl_max = 0;
+    if (cudaFuncSetAttribute(small_resident_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+            cudaSuccess &&
+        cudaFuncSetAttribute(small_resident_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX) ==
+            cudaSuccess) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(16);
+      q.blockDim = dim3(RB);
+      q.dynamicSmemBytes = SMEM_MAX;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 16;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      q.attrs = at;
+      q.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxPotentialClusterSize(&n, small_resident_kernel, &q) == cudaSuccess) cl_max = n;
+    }
+    cudaGetLastError();
+  }
+  if (cl_max < 2) return cudaErrorNotSupported;
+  const int NC = std::min(cl_max, 16);
+  long long xtot = 0, wtot = 0;
+  for (int i = 0; i < A.n_sd; ++i) {
+    const Geom& g = A.s[i].L.g;
+    xtot += g.total;
+    wtot += 12LL * (((long long)g.nn[0] * g.nn[1] * g.nn[2] + NC - 1) / NC);
+  }
+  const long long smem = 8 * (2 * xtot + wtot) + 16LL * 2 * NC + 8LL * 2 * (RB / 32) + 16;
+  if (smem > SMEM_MAX) return cudaErrorNotSupported;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(NC);
+  cfg.blockDim = dim3(RB);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = NC;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, small_resident_kernel, A);
+}
+
 void launch_fom_advance_nl(const FomLaunch& L, cudaStream_t s, int* launches) {
   static bool attr = false;
   if (!attr) {
