@@ -961,124 +961,180 @@ __device__ __forceinline__ double2 cta_sum2(double num, double den, double* red)
   return make_double2(a, b);
 }
 
+__device__ __forceinline__ void res_step_begin(const Ctl& C, int step) {
+  C.active[0] = 1;
+  C.iters[0] = 0;
+  C.flags[0] = 1;
+  C.flags[1] = 0;
+  *C.n_dev = 0;
+  *C.step_dev = step;
+}
+
+// in-range test of a neighbour offset o in {-1, 0, 1} for a node of axis class c (0 low face, 2 high face)
+__device__ __forceinline__ bool res_in(int c, int o) { return !((c == 0 && o < 0) || (c == 2 && o > 0)); }
+
 __global__ void __launch_bounds__(RB, 1) small_resident_kernel(const __grid_constant__ SmallArgs A) {
   extern __shared__ __align__(16) double rsm[];
   cg::cluster_group cl = cg::this_cluster();
   const int NC = (int)cl.num_blocks(), rank = (int)cl.block_rank();
   const int tid = threadIdx.x;
   const Ctl& C = A.ctl;
-  // shared memory: X replicas [2][xtot] | per subdomain owned arrays W[3][3][chunk], QN[3][chunk] | partials
-  // [2][NC] (x num, y den) | block scratch | flags
+  // shared memory: X replicas [2][xtot] | per subdomain W[3 buffers][3][chunk], Q'[3][chunk] | per owned slot
+  // (offset, class | free mask << 5 | mass index << 8) | partials [2] | block scratch | flag | class tables |
+  // transfer maps (idx [8n], out [3n], xi [3n])
   int xoff[SMALL_MAX_SD], woff[SMALL_MAX_SD], chunk[SMALL_MAX_SD], cum[SMALL_MAX_SD + 1];
   int xtot = 0, wtot = 0;
   cum[0] = 0;
   for (int i = 0; i < A.n_sd; ++i) {
-    xoff[i] = xtot;
-    xtot += (int)A.s[i].L.g.total;
     const Geom& g = A.s[i].L.g;
+    xoff[i] = xtot;
+    xtot += (int)g.total;
     chunk[i] = res_chunk(g.nn[0] * g.nn[1] * g.nn[2], NC);
     woff[i] = wtot;
     wtot += 12 * chunk[i];
     cum[i + 1] = cum[i] + chunk[i];
   }
+  const int nslot = cum[A.n_sd];
   double* Xb[2] = {rsm, rsm + xtot};
   double* Wb = rsm + 2 * xtot;
-  double2* cpart = reinterpret_cast<double2*>(Wb + wtot);  // [2][NC]
-  double* red = reinterpret_cast<double*>(cpart + 2 * NC);  // [2 * RB / 32]
-  int* flag = reinterpret_cast<int*>(red + 2 * (RB / 32));
+  int2* meta = reinterpret_cast<int2*>(Wb + wtot);
+  double2* cpart = reinterpret_cast<double2*>(meta + (nslot + 1) / 2 * 2);  // [2] (16-byte aligned)
+  double* red = reinterpret_cast<double*>(cpart + 2);          // [2 * RB / 32]
+  int* flag = reinterpret_cast<int*>(red + 2 * (RB / 32));     // [4]
+  double* csm = reinterpret_cast<double*>(flag + 4);
+  const double* coefp[SMALL_MAX_SD];
+  for (int i = 0; i < A.n_sd; ++i) {
+    coefp[i] = A.s[i].L.coef;
+    if (A.res_coef_smem) {
+      double* dst = csm + (size_t)i * NCLASS * 27 * 9;
+      for (int t = tid; t < NCLASS * 27 * 9; t += RB) dst[t] = A.s[i].L.coef[t];
+      coefp[i] = dst;
+    }
+  }
+  // the transfer maps (read every sweep) in shared memory
+  unsigned char* mp = reinterpret_cast<unsigned char*>(csm + (A.res_coef_smem ? (size_t)A.n_sd * NCLASS * 27 * 9 : 0));
+  SmallMap maps[SMALL_MAX_SD][6];
+  for (int i = 0; i < A.n_sd; ++i)
+    for (int mi = 0; mi < A.s[i].n_maps; ++mi) {
+      const SmallMap& m = A.s[i].maps[mi];
+      double* xi = reinterpret_cast<double*>(mp);
+      int* idx = reinterpret_cast<int*>(xi + 3 * m.n);
+      int* out = idx + 8 * m.n;
+      for (int t = tid; t < 3 * m.n; t += RB) {
+        xi[t] = m.xi[t];
+        out[t] = m.out[t];
+      }
+      for (int t = tid; t < 8 * m.n; t += RB) idx[t] = m.idx[t];
+      maps[i][mi] = SmallMap{m.n, m.src, idx, out, xi};
+      mp += ((size_t)3 * m.n * 8 + (size_t)11 * m.n * 4 + 15) / 16 * 16;
+    }
 
-  // load the replicas (X = q of the checkpoint, U = u of the checkpoint) and this CTA's W
+  // load the replicas (X = q of the checkpoint, U = u of the checkpoint), this CTA's W and its slots' metadata
   for (int i = 0; i < A.n_sd; ++i) {
     const SmallSub& d = A.s[i];
-    const long long tot = d.L.g.total;
+    const Geom& g = d.L.g;
     const double* q0 = d.st[d.cur0][0];
     const double* u0 = d.st[1 - d.cur0][0];
-    for (long long t = tid; t < tot; t += RB) {
+    for (long long t = tid; t < g.total; t += RB) {
       Xb[0][xoff[i] + t] = q0[t];
       Xb[1][xoff[i] + t] = u0[t];
     }
-    const Geom& g = d.L.g;
     const int n = g.nn[0] * g.nn[1] * g.nn[2];
     for (int l = tid; l < chunk[i]; l += RB) {
       const int t = rank * chunk[i] + l;
-      if (t >= n) continue;
-      const int ii = t % g.nn[0], jj = (t / g.nn[0]) % g.nn[1], kk = t / (g.nn[0] * g.nn[1]);
-      const long long id = gidx(g, ii, jj, kk);
+      int2 mt = make_int2(-1, 0);
+      if (t < n) {
+        const int ii = t % g.nn[0], jj = (t / g.nn[0]) % g.nn[1], kk = t / (g.nn[0] * g.nn[1]);
+        const int cx = axis_class(ii, g.nn[0]), cy = axis_class(jj, g.nn[1]), cz = axis_class(kk, g.nn[2]);
+        const int im = (cx == 1 ? 1 : 0) + (cy == 1 ? 2 : 0) + (cz == 1 ? 4 : 0);
+        mt = make_int2((int)gidx(g, ii, jj, kk), (cx + 3 * (cy + 3 * cz)) | ((int)free_mask(g, d.L.f, ii, jj, kk) << 5) |
+                                                     (im << 8));
 #pragma unroll
-      for (int c = 0; c < 3; ++c) Wb[woff[i] + c * chunk[i] + l] = d.st[d.cur0][1][c * g.npad + id];
+        for (int c = 0; c < 3; ++c) Wb[woff[i] + c * chunk[i] + l] = d.st[d.cur0][1][c * g.npad + mt.x];
+      }
+      meta[cum[i] + l] = mt;
     }
   }
-  if (rank == 0 && tid == 0) small_step_begin(C);
-  int ck = 0;     // W buffer of the checkpoint (buffers 0..2, each [3][chunk])
-  int kpar = 0;   // X replica of the current step (the other one holds u of the checkpoint)
+  // controller state lives in rank 0's registers; the global copies are only written
+  int step = 0, active = 1;
+  if (rank == 0 && tid == 0) {
+    step = *C.step_dev + 1;
+    res_step_begin(C, step);
+  }
+  int ck = 0;    // W buffer of the checkpoint (buffers 0..2, each [3][chunk])
+  int kpar = 0;  // X replica of the current step (the other one holds u of the checkpoint)
   cl.sync();
+#ifdef OSAM_RES_PROF
+  long long tp[8] = {0, 0, 0, 0, 0, 0, 0, 0}, t_0 = clock64();
+#define RES_T(q) if (tid == 0 && rank == 0) { const long long t_ = clock64(); tp[q] += t_ - t_0; t_0 = t_; }
+#else
+#define RES_T(q)
+#endif
   for (int k = 0; k < A.n_steps; ++k) {
     double* Xc = Xb[kpar];
     const double* Xu = Xb[1 - kpar];
     int wo = ck;
     for (int n = 1; n <= A.max_iters; ++n) {
       const bool first = n == 1;
-      const int wp = wo;                       // W' of iterate n - 1 (unused at n = 1)
-      wo = (ck + 1 + (n & 1)) % 3;             // W' of iterate n: alternates between the two non-checkpoint buffers
+      const int wp = wo;            // W' of iterate n - 1 (unused at n = 1)
+      wo = (ck + 1 + (n & 1)) % 3;  // W' of iterate n: alternates between the two non-checkpoint buffers
       // K2 in sweep order into this CTA's replica (a later destination reads iterate n of an earlier source)
       for (int i = 0; i < A.n_sd; ++i) {
-        const SmallSub& d = A.s[i];
-        for (int mi = 0; mi < d.n_maps; ++mi) {
-          const SmallMap& m = d.maps[mi];
+        const int nm = A.s[i].n_maps;
+        for (int mi = 0; mi < nm; ++mi) {
+          const SmallMap& m = maps[i][mi];
           const bool newest = (m.src < i) || !first;
           const double* field = (newest ? Xc : Xu) + xoff[m.src];
-          const long long cs = A.s[m.src].L.g.npad;
+          const int cs = (int)A.s[m.src].L.g.npad;
           for (int t = tid; t < 3 * m.n; t += RB) {
             const int p = t / 3, cc = t - 3 * p;
-            const int o = __ldg(m.out + 3 * p + cc);
+            const int o = m.out[t];
             if (o < 0) continue;
-            const double xx = __ldg(m.xi + 3 * p), yy = __ldg(m.xi + 3 * p + 1), zz = __ldg(m.xi + 3 * p + 2);
+            const double xx = m.xi[3 * p], yy = m.xi[3 * p + 1], zz = m.xi[3 * p + 2];
             const double* sb = field + cc * cs;
+            const int* ix = m.idx + 8 * p;
             double acc = 0.0;
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
               const double w = ((q & 1) ? xx : 1.0 - xx) * ((q & 2) ? yy : 1.0 - yy) * ((q & 4) ? zz : 1.0 - zz);
-              acc = fma(w, sb[__ldg(m.idx + 8 * p + q)], acc);
+              acc = fma(w, sb[ix[q]], acc);
             }
             Xc[xoff[i] + o] = acc;
           }
         }
-        if (d.n_maps) __syncthreads();
+        if (nm) __syncthreads();
       }
+      RES_T(0);
       // K1S on this CTA's nodes of every subdomain: 4 lanes per node (oz = sub - 1), gather_body's arithmetic
       double num = 0.0, den = 0.0;
-      for (int u0 = 0; u0 < cum[A.n_sd]; u0 += RB / 4) {
+      for (int u0 = 0; u0 < nslot; u0 += RB / 4) {
         const int u = u0 + (tid >> 2), sub = tid & 3;
         int i = 0;
         while (i + 1 < A.n_sd && u >= cum[i + 1]) ++i;
+        const int2 mt = u < nslot ? meta[u] : make_int2(-1, 0);
+        const bool valid = mt.x >= 0;
+        const int cls = mt.y & 31, cx = cls % 3, cy = (cls / 3) % 3, cz = cls / 9;
         const SmallSub& d = A.s[i];
         const Geom& g = d.L.g;
-        const int l = u - cum[i];
-        const int t = rank * chunk[i] + l;
-        const bool valid = u < cum[A.n_sd] && l < chunk[i] && t < g.nn[0] * g.nn[1] * g.nn[2];
-        const int ii = valid ? t % g.nn[0] : 0;
-        const int jj = valid ? (t / g.nn[0]) % g.nn[1] : 0;
-        const int kk = valid ? t / (g.nn[0] * g.nn[1]) : 0;
-        const int cx = axis_class(ii, g.nn[0]), cy = axis_class(jj, g.nn[1]), cz = axis_class(kk, g.nn[2]);
         const double* X = Xc + xoff[i];
-        const long long np = g.npad;
+        const int np = (int)g.npad, px = g.px, pl = (int)g.plane;
         double f[3] = {0.0, 0.0, 0.0};
         const int oz = sub - 1;
-        if (valid && sub < 3 && kk + oz >= 0 && kk + oz <= g.nn[2] - 1) {
-          const double* coef = d.L.coef + (size_t)(cx + 3 * (cy + 3 * cz)) * 27 * 9;
+        if (valid && sub < 3 && res_in(cz, oz)) {
+          const double* coef = coefp[i] + (size_t)cls * 27 * 9;
 #pragma unroll
           for (int oy = -1; oy <= 1; ++oy) {
-            if (jj + oy < 0 || jj + oy > g.nn[1] - 1) continue;
+            if (!res_in(cy, oy)) continue;
 #pragma unroll
             for (int ox = -1; ox <= 1; ++ox) {
-              if (ii + ox < 0 || ii + ox > g.nn[0] - 1) continue;
-              const long long q = gidx(g, ii + ox, jj + oy, kk + oz);
+              if (!res_in(cx, ox)) continue;
+              const int q = mt.x + ox + px * oy + pl * oz;
               const double x[3] = {X[q], X[np + q], X[2 * np + q]};
               const double* cb = coef + ((ox + 1) + 3 * ((oy + 1) + 3 * (oz + 1))) * 9;
 #pragma unroll
               for (int c = 0; c < 3; ++c)
 #pragma unroll
-                for (int dd = 0; dd < 3; ++dd) f[c] = fma(__ldg(cb + c * 3 + dd), x[dd], f[c]);
+                for (int dd = 0; dd < 3; ++dd) f[c] = fma(cb[c * 3 + dd], x[dd], f[c]);
             }
           }
         }
@@ -1089,15 +1145,14 @@ __global__ void __launch_bounds__(RB, 1) small_resident_kernel(const __grid_cons
           f[c] = (f[c] + f1) + f2;
         }
         if (valid && sub == 0) {
-          const long long id = gidx(g, ii, jj, kk);
-          const unsigned fm = free_mask(g, d.L.f, ii, jj, kk);
-          const double inv_m = d.L.inv_mass[(cx == 1 ? 1 : 0) + (cy == 1 ? 2 : 0) + (cz == 1 ? 4 : 0)];
+          const unsigned fm = (unsigned)(mt.y >> 5) & 7u;
           const FomLaunch& L = d.L;
+          const double inv_m = L.inv_mass[(mt.y >> 8) & 7];
           double* W = Wb + woff[i];
-          const int ch = chunk[i];
+          const int ch = chunk[i], l = u - cum[i];
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            const double x = X[c * np + id];
+            const double x = X[c * np + mt.x];
             double wn = 0.0, qn = x;
             if ((fm >> c) & 1) {
               const double w0 = W[(ck * 3 + c) * ch + l];
@@ -1116,30 +1171,22 @@ __global__ void __launch_bounds__(RB, 1) small_resident_kernel(const __grid_cons
           }
         }
       }
-      // the CTA's (num, den), then the cluster's, summed in rank order by every CTA (the same decision everywhere)
+      RES_T(1);
+      // the CTA's (num, den), then the cluster's, summed by the same butterfly in every CTA (the same decision
+      // everywhere)
       const double2 mine = cta_sum2<RB>(num, den, red);
-      if (tid == 0) cpart[(n & 1) * NC] = mine;  // slot 0 of this CTA's own copy; read remotely below
+      if (tid == 0) cpart[n & 1] = mine;
+      RES_T(2);
       cl.sync();
-      if (tid == 0) {
-        double sn = 0.0, sd = 0.0;
-        for (int r = 0; r < NC; ++r) {
-          const double2 v = *cl.map_shared_rank(cpart + (n & 1) * NC, r);
-          sn += v.x;
-          sd += v.y;
-        }
-        int go;
-        if (rank == 0) {  // controller state (as small_persistent_kernel's K3)
-          if (C.active[0]) {
-            C.iters[0] = n;
-            if (n >= A.min_iters) {
-              C.numden[0] = sn;
-              C.numden[1] = sd;
-              if (!isfinite(sn) || !isfinite(sd)) {
-                C.flags[1] = 1;
-                C.sticky[0] = 1;
-              }
-            }
-          }
+      RES_T(3);
+      if (tid < 32) {
+        double2 v = make_double2(0.0, 0.0);
+        if (tid < NC) v = *cl.map_shared_rank(cpart + (n & 1), tid);
+        double sn = v.x, sd = v.y;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          sn += __shfl_xor_sync(0xffffffffu, sn, o);
+          sd += __shfl_xor_sync(0xffffffffu, sd, o);
         }
         bool conv = false, bad = false;
         if (n >= A.min_iters) {
@@ -1147,53 +1194,72 @@ __global__ void __launch_bounds__(RB, 1) small_resident_kernel(const __grid_cons
           conv = (sn == 0.0) || (sn < A.tol_rel * A.tol_rel * sd);
           if (A.tol_abs > 0.0) conv = conv || (sn < A.tol_abs * A.tol_abs);
         }
-        go = !conv && !bad && n < A.max_iters;
-        if (rank == 0) {
-          if (conv) C.active[0] = 0;
+        const int go = !conv && !bad && n < A.max_iters;
+        if (rank == 0 && tid == 0) {  // controller state (as small_persistent_kernel's K3), stores only
+          C.iters[0] = n;
+          if (n >= A.min_iters) {
+            C.numden[0] = sn;
+            C.numden[1] = sd;
+            if (bad) {
+              C.flags[1] = 1;
+              C.sticky[0] = 1;
+            }
+          }
+          if (conv) active = 0;
+          C.active[0] = active;
           *C.n_dev = n;
-          C.flags[0] = C.active[0];
-          if (C.iters_all) C.iters_all[*C.step_dev - 1] = C.iters[0];
-          if (C.active[0] && n >= A.max_iters) C.sticky[1] = 1;
-          if (!go && k + 1 < A.n_steps) small_step_begin(C);
+          C.flags[0] = active;
+          if (C.iters_all) C.iters_all[step - 1] = n;
+          if (active && n >= A.max_iters) C.sticky[1] = 1;
+          if (!go && k + 1 < A.n_steps) {
+            ++step;
+            active = 1;
+            res_step_begin(C, step);
+          }
         }
-        flag[0] = go;
+        if (tid == 0) flag[0] = go;
       }
       __syncthreads();
+      RES_T(4);
       if (!flag[0]) break;
     }
     // commit: the new checkpoint q (Q' of the last iterate) of this CTA's nodes into every replica's other buffer
     // (which held u of the old checkpoint, no longer read); the last iterate's W' becomes the checkpoint w
     double* Xn = Xb[1 - kpar];
     for (int i = 0; i < A.n_sd; ++i) {
-      const Geom& g = A.s[i].L.g;
-      const int n = g.nn[0] * g.nn[1] * g.nn[2];
-      const int ch = chunk[i];
+      const int ch = chunk[i], np = (int)A.s[i].L.g.npad;
       const double* QN = Wb + woff[i] + 9 * ch;
-      for (int e = tid; e < 3 * ch * NC; e += RB) {
-        const int r = e / (3 * ch), rem = e - r * 3 * ch, c = rem / ch, l = rem - c * ch;
-        const int t = rank * ch + l;
-        if (t >= n) continue;
-        const int ii = t % g.nn[0], jj = (t / g.nn[0]) % g.nn[1], kk = t / (g.nn[0] * g.nn[1]);
-        *cl.map_shared_rank(Xn + xoff[i] + c * g.npad + gidx(g, ii, jj, kk), r) = QN[c * ch + l];
+      for (int e = tid; e < 3 * ch; e += RB) {
+        const int c = e / ch, l = e - c * ch;
+        const int ofs = meta[cum[i] + l].x;
+        if (ofs < 0) continue;
+        const double v = QN[e];
+        double* dst = Xn + xoff[i] + c * np + ofs;
+        for (int r = 0; r < NC; ++r) *cl.map_shared_rank(dst, r) = v;
       }
     }
     ck = wo;
     kpar ^= 1;
+    RES_T(5);
     cl.sync();
+    RES_T(6);
   }
+#ifdef OSAM_RES_PROF
+  if (tid == 0 && rank == 0)
+    printf("RESPROF NC %d steps %d cycles: xfer %lld stencil %lld ctasum %lld clsync %lld decide %lld commit %lld commitsync %lld\n",
+           NC, A.n_steps, tp[0], tp[1], tp[2], tp[3], tp[4], tp[5], tp[6]);
+#endif
   // write back: the checkpoint buffer gets q (this CTA's nodes) and w, the spare buffer's q slot u (R30)
   for (int i = 0; i < A.n_sd; ++i) {
     const SmallSub& d = A.s[i];
     const int cbf = (A.n_steps & 1) ? 1 - d.cur0 : d.cur0;
     const Geom& g = d.L.g;
-    const int n = g.nn[0] * g.nn[1] * g.nn[2];
     const int ch = chunk[i];
     for (int e = tid; e < 3 * ch; e += RB) {
       const int c = e / ch, l = e - c * ch;
-      const int t = rank * ch + l;
-      if (t >= n) continue;
-      const int ii = t % g.nn[0], jj = (t / g.nn[0]) % g.nn[1], kk = t / (g.nn[0] * g.nn[1]);
-      const long long o = c * g.npad + gidx(g, ii, jj, kk);
+      const int ofs = meta[cum[i] + l].x;
+      if (ofs < 0) continue;
+      const long long o = c * g.npad + ofs;
       d.st[cbf][0][o] = Xb[kpar][xoff[i] + o];
       d.st[1 - cbf][0][o] = Xb[1 - kpar][xoff[i] + o];
       d.st[cbf][1][o] = Wb[woff[i] + (ck * 3 + c) * ch + l];
@@ -1230,15 +1296,26 @@ cudaError_t launch_small_resident(const SmallArgs& A, cudaStream_t s) {
     cudaGetLastError();
   }
   if (cl_max < 2) return cudaErrorNotSupported;
-  const int NC = std::min(cl_max, 16);
+  int NC = std::min(cl_max, 16);
+  if (const char* e = getenv("OSAM_RESIDENT_NC")) NC = std::max(2, std::min(NC, atoi(e)));  // A/B of the cluster size
   long long xtot = 0, wtot = 0;
   for (int i = 0; i < A.n_sd; ++i) {
     const Geom& g = A.s[i].L.g;
     xtot += g.total;
     wtot += 12LL * (((long long)g.nn[0] * g.nn[1] * g.nn[2] + NC - 1) / NC);
   }
-  const long long smem = 8 * (2 * xtot + wtot) + 16LL * 2 * NC + 8LL * 2 * (RB / 32) + 16;
+  long long nslot = 0, msize = 0;
+  for (int i = 0; i < A.n_sd; ++i) {
+    const Geom& g = A.s[i].L.g;
+    nslot += ((long long)g.nn[0] * g.nn[1] * g.nn[2] + NC - 1) / NC;
+    for (int mi = 0; mi < A.s[i].n_maps; ++mi) msize += (24LL * A.s[i].maps[mi].n + 44LL * A.s[i].maps[mi].n + 15) / 16 * 16;
+  }
+  long long smem = 8 * (2 * xtot + wtot) + 8 * ((nslot + 1) / 2 * 2) + 16LL * 2 + 8LL * 2 * (RB / 32) + 16 + msize;
   if (smem > SMEM_MAX) return cudaErrorNotSupported;
+  SmallArgs B = A;
+  const long long csize = 8LL * NCLASS * 27 * 9 * A.n_sd;
+  B.res_coef_smem = smem + csize <= SMEM_MAX && !(getenv("OSAM_RESIDENT_COEF") && getenv("OSAM_RESIDENT_COEF")[0] == '0');
+  if (B.res_coef_smem) smem += csize;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(NC);
   cfg.blockDim = dim3(RB);
@@ -1251,7 +1328,7 @@ cudaError_t launch_small_resident(const SmallArgs& A, cudaStream_t s) {
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, small_resident_kernel, A);
+  return cudaLaunchKernelEx(&cfg, small_resident_kernel, B);
 }
 
 void launch_fom_advance_nl(const FomLaunch& L, cudaStream_t s, int* launches) {

@@ -1770,7 +1770,13 @@ int osam_step(osam_subdomain* const* sds, int32_t n_sd, const osam_schwarz_cfg* 
     A.ctl = G->ctl(cfg->max_iters);
     if (!G->go) TRY(dalloc(&G->go, 1));
     A.go = G->go;
-    CK(launch_small_persistent(A, st));
+    const cudaError_t re = launch_small_resident(A, st);
+    if (re == cudaErrorNotSupported) {
+      cudaGetLastError();
+      CK(launch_small_persistent(A, st));
+    } else {
+      CK(re);
+    }
     ++g_launches;
     if (n_steps & 1)
       for (int i = 0; i < n_sd; ++i) commit_step(sds[i]->s);  // the roles alternate every step

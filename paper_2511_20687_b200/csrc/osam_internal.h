@@ -373,8 +373,12 @@ struct SmallArgs {
   double2* partial;
   Ctl ctl;
   int* go;             // device int: the sweep loop continues (written by K3, read after the barrier)
+  int res_coef_smem;   // small_resident_kernel: the class tables are staged in shared memory (set by its launcher)
 };
 cudaError_t launch_small_persistent(const SmallArgs& A, cudaStream_t s);
+// The same group on one thread-block cluster with every subdomain's state in shared memory (kernels_fom.cu
+// small_resident_kernel); cudaErrorNotSupported if it does not fit (OSAM_SMALL_RESIDENT=0: never).
+cudaError_t launch_small_resident(const SmallArgs& A, cudaStream_t s);
 int small_persistent_grid();  // CTAs that can be co-resident (cooperative launch bound)
 bool fom_small(const Geom& g);  // the K1S (gather) path applies (g.small)
 // Decide the FOM kernel path of a subdomain once (OSAM_GATHER_MAX -> g.small, OSAM_K1_SHAPE or the lane

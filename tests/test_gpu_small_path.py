@@ -10,13 +10,16 @@ from test_gpu_parity import _substeps, run_both  # noqa: F401  (shared GPU-vs-or
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["persistent", "persistent_grid", "graph"])
+@pytest.fixture(autouse=True, params=["resident", "persistent", "persistent_grid", "graph"])
 def gather_path(monkeypatch, request):
-    """K1S everywhere; small all-FOM groups run the persistent controller as one thread-block cluster (default),
-    as a grid-wide cooperative launch (OSAM_SMALL_CLUSTER=0), or the per-step CUDA graph (OSAM_SMALL_PERSIST=0)."""
+    """K1S everywhere; small all-FOM groups run the cluster-resident controller (default, state in shared
+    memory, when it fits), the persistent controller as one thread-block cluster (OSAM_SMALL_RESIDENT=0), as a
+    grid-wide cooperative launch (OSAM_SMALL_CLUSTER=0), or the per-step CUDA graph (OSAM_SMALL_PERSIST=0)."""
     monkeypatch.setenv("OSAM_GATHER_MAX", str(1 << 30))
     monkeypatch.setenv("OSAM_SMALL_PERSIST", "0" if request.param == "graph" else "1")
+    monkeypatch.setenv("OSAM_SMALL_RESIDENT", "1" if request.param == "resident" else "0")
     monkeypatch.setenv("OSAM_SMALL_CLUSTER", "0" if request.param == "persistent_grid" else "1")
+    return request.param
 
 
 @pytest.fixture(scope="module")
@@ -105,3 +108,28 @@ def test_unstable_gather(gpu):
     with pytest.raises(osam.OsamError) as e:
         gpu.run(cfg, subs, n_steps=200)
     assert e.value.code == -5
+
+
+def test_controllers_bitwise_c1(gpu, monkeypatch, gather_path):
+    """c1 over an odd number of steps: every small-group controller (resident, persistent cluster, persistent
+    grid) leaves states bitwise equal to the per-step graph's (same per-node arithmetic) and the same counts."""
+    if gather_path != "resident":
+        pytest.skip("runs every controller itself")
+    cfg = I.config("c1")
+    out = {}
+    for name, env in (("graph", dict(OSAM_SMALL_PERSIST="0")),
+                      ("resident", dict(OSAM_SMALL_PERSIST="1", OSAM_SMALL_RESIDENT="1")),
+                      ("persistent", dict(OSAM_SMALL_PERSIST="1", OSAM_SMALL_RESIDENT="0", OSAM_SMALL_CLUSTER="1")),
+                      ("grid", dict(OSAM_SMALL_PERSIST="1", OSAM_SMALL_RESIDENT="0", OSAM_SMALL_CLUSTER="0"))):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        subs = gpu.build(cfg)
+        gpu.set_ics(cfg, subs, device="cuda:0")
+        _, it = gpu.run(cfg, subs, n_steps=37)
+        _, it2 = gpu.run(cfg, subs, n_steps=4)  # a second call continues from the written-back state
+        out[name] = (np.concatenate([it.ravel(), it2.ravel()]), [gpu.fom_state(s) for s in subs])
+    ref = out["graph"]
+    for name, (it, st) in out.items():
+        assert np.array_equal(it, ref[0]), name
+        for a, b in zip(st, ref[1]):
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), name
