@@ -14,21 +14,26 @@ constexpr int XF_BLOCK = NT;  // x-face work runs in extra CTAs of the tiled ker
 // boundary in the innermost dimension (an odd fp64 start coordinate raises an illegal
 // instruction on sm_100a), so the left halo is two columns wide (the first is unused).
 constexpr int PX = TX + 4;
-constexpr int PY = TY + 2;
+#ifndef OSAM_K1_WARP
+#define OSAM_K1_WARP 0
+#endif
+// OSAM_K1_WARP = 1: every warp streams its own rows (its own TMA boxes, ring and full barriers; no empty
+// barriers), so no warp waits for another; the staged box is the warp's WR rows plus the y halo.
+constexpr int WR = 32 / TX;                          // node rows per warp
+constexpr int SR = OSAM_K1_WARP ? WR : TY;           // node rows of one staged box
+constexpr int NRING = OSAM_K1_WARP ? NWARP : 1;      // rings per CTA
+constexpr int PY = SR + 2;
 constexpr int PLANE = PX * PY;                             // positions per staged plane
 #ifndef OSAM_NSTAGE
 #define OSAM_NSTAGE 4
 #endif
-constexpr int NSTAGE = OSAM_NSTAGE;
-#ifndef OSAM_PROD
-#define OSAM_PROD 2  // TMA producer: 0 thread 0 with a shared cursor, 1 thread 0 stateless, 2 rotated over the warps
-#endif  // ring: NSTAGE-2 planes in flight, current, previous
+constexpr int NSTAGE = OSAM_NSTAGE;  // ring: NSTAGE-2 planes in flight, current, previous
 constexpr int ARR_BYTES = 3 * PLANE * 8;                   // X (x,y,z comps) of one plane, with halo
 constexpr int ARR_STRIDE = (ARR_BYTES + 127) / 128 * 128;  // 128-B aligned TMA destinations
-constexpr int WPL = TX * TY;                               // tile positions of W (no halo)
+constexpr int WPL = TX * SR;                               // staged positions of W (no halo)
 constexpr int W_BYTES = 3 * WPL * 8;
 constexpr int STAGE_BYTES = ARR_STRIDE + 2 * W_BYTES;  // X, W, W'_prev
-constexpr int SMEM_TILED = NSTAGE * STAGE_BYTES + 2 * NSTAGE * 8;  // ring, barriers
+constexpr int SMEM_TILED = NRING * NSTAGE * STAGE_BYTES + NRING * 2 * NSTAGE * 8;  // rings, barriers
 
 // ---- interior rows: parity-reduced stencil ---------------------------------------------
 // On a uniform box every interior block K_cd(ox, oy, oz) is even or odd in ox and in oy (the 1D
@@ -234,9 +239,10 @@ struct Tile {
 };
 
 // staged positions of this thread: own node, (-1,-1) neighbour, W tile position
-__device__ __forceinline__ int pos_own() { return ((int)threadIdx.y + 1) * PX + ((int)threadIdx.x + 2); }
-__device__ __forceinline__ int pos_base() { return (int)threadIdx.y * PX + (int)threadIdx.x + 1; }
-__device__ __forceinline__ int pos_w() { return (int)threadIdx.y * TX + (int)threadIdx.x; }
+__device__ __forceinline__ int srow() { return OSAM_K1_WARP ? (int)threadIdx.y % WR : (int)threadIdx.y; }
+__device__ __forceinline__ int pos_own() { return (srow() + 1) * PX + ((int)threadIdx.x + 2); }
+__device__ __forceinline__ int pos_base() { return srow() * PX + (int)threadIdx.x + 1; }
+__device__ __forceinline__ int pos_w() { return srow() * TX + (int)threadIdx.x; }
 
 struct Maps {
   const CUtensorMap *x, *w, *wp;
@@ -288,13 +294,29 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
   const int m = T.kbeg - 1 + it;
   const int kf = m - 1;
   const bool fin = T.writer() && kf >= T.kbeg && kf <= T.kend;
+#ifdef OSAM_K1_PROF
+  __shared__ long long k1prof[NWARP][4];
+  const int kpw = ((int)threadIdx.x + TX * (int)threadIdx.y) >> 5;
+  const bool kpl = (((int)threadIdx.x + TX * (int)threadIdx.y) & 31) == 0;
+  if (it == 0 && kpl) k1prof[kpw][0] = k1prof[kpw][1] = k1prof[kpw][2] = k1prof[kpw][3] = 0;
+  const long long kt0 = clock64();
+#endif
   // producer (thread 0): plane it + NSTAGE - 2 into the stage released by plane it - 2.  One tile per CTA, so
   // the plane and its coordinates follow from the iteration and the thread's own tile constants (no cursor
   // in shared memory: c3 932 -> 953 steps/s; the role rotated over the warps, a non-blocking producer and an
   // issue at the end of the iteration were measured slower, profiles/r3_k1_experiments.md)
-  if (threadIdx.x + threadIdx.y == 0 && it + NSTAGE - 2 < T.nplanes) {
+#if OSAM_K1_WARP
+  // per-warp rings: lane 0 refills the stage its own warp released at the end of the previous iteration
+  const bool issuer = (((int)threadIdx.x + TX * (int)threadIdx.y) & 31) == 0;
+  if (issuer && it >= 2) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // its reads, then TMA
+#else
+  const bool issuer = threadIdx.x + threadIdx.y == 0;
+#endif
+  if (issuer && it + NSTAGE - 2 < T.nplanes) {
     const int p = it + NSTAGE - 2;
+#if !defined(OSAM_K1_NOEMPTY) && !OSAM_K1_WARP  // NOEMPTY: probe only (wrong results)
     if (p >= NSTAGE) mbar_wait(&empty[p % NSTAGE], (unsigned)(((p - NSTAGE) / NSTAGE) & 1));
+#endif
     TileGeo Pq;
     Pq.x0 = T.i - 2;
     Pq.y0 = T.j - 1;
@@ -302,7 +324,13 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
     issue_plane(Pq, T.prev(), p, p % NSTAGE, ring, full, M);
   }
   const int s = gi % NSTAGE;
+#ifdef OSAM_K1_PROF
+  const long long kt1 = clock64();
+#endif
   mbar_wait(&full[s], (unsigned)((gi / NSTAGE) & 1));
+#ifdef OSAM_K1_PROF
+  const long long kt2 = clock64();
+#endif
   const double* xs = reinterpret_cast<const double*>(ring + (size_t)s * STAGE_BYTES);
   if (T.active()) {
     double* A = acc[SA];
@@ -385,7 +413,19 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
   }
   // this warp is done with the previous plane of the stream (own values above, stencil before)
   __syncwarp();
-  if (gi >= 1 && (((int)threadIdx.x + TX * (int)threadIdx.y) & 31) == 0) mbar_arrive(&empty[(gi + NSTAGE - 1) % NSTAGE]);
+  if (!OSAM_K1_WARP && gi >= 1 && (((int)threadIdx.x + TX * (int)threadIdx.y) & 31) == 0)
+    mbar_arrive(&empty[(gi + NSTAGE - 1) % NSTAGE]);
+#ifdef OSAM_K1_PROF
+  if (kpl) {
+    const long long kt3 = clock64();
+    k1prof[kpw][0] += kt1 - kt0;
+    k1prof[kpw][1] += kt2 - kt1;
+    k1prof[kpw][2] += kt3 - kt2;
+    if (it == T.nplanes - 1 && (blockIdx.x % 401) == 17)
+      printf("K1PROF nx %d blk %d warp %d planes %d prod %lld wait %lld work %lld\n", L.g.nn[0], (int)blockIdx.x, kpw,
+             T.nplanes, k1prof[kpw][0], k1prof[kpw][1], k1prof[kpw][2]);
+  }
+#endif
 #pragma unroll
   for (int c = 0; c < 3; ++c) acc[SC][c] = 0.0;
 }
@@ -411,8 +451,8 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
                      const __grid_constant__ CUtensorMap tmwp) {
   extern __shared__ __align__(128) unsigned char smem[];
   unsigned char* ring = smem;
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + NSTAGE * STAGE_BYTES);
-  unsigned long long* empty = full + NSTAGE;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + NRING * NSTAGE * STAGE_BYTES);
+  unsigned long long* empty = full + NRING * NSTAGE;
   if (L.stamp && threadIdx.x + threadIdx.y == 0) atomicMin(L.stamp, global_ns());  // in-schedule timeline
   if ((int)blockIdx.x >= L.n_tile_ctas) {  // x-face CTAs (after the tile CTAs)
     xface_body(L, xface_sides(L.f), blockIdx.x - L.n_tile_ctas, threadIdx.x + TX * threadIdx.y, blockIdx.x);
@@ -439,6 +479,23 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
   T.nplanes = P.nplanes;
   T.id0 = T.i + (long long)g.px * T.j;
 
+#if OSAM_K1_WARP
+  if (threadIdx.x + threadIdx.y == 0) {
+    for (int s = 0; s < NRING * NSTAGE; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  {
+    const int w = ((int)threadIdx.x + TX * (int)threadIdx.y) >> 5;
+    ring += (size_t)w * NSTAGE * STAGE_BYTES;
+    full += w * NSTAGE;
+    if ((((int)threadIdx.x + TX * (int)threadIdx.y) & 31) == 0) {
+      TileGeo Pq = P;
+      Pq.y0 = T.j - 1;  // the warp's first row - 1
+      for (int p = 0; p < NSTAGE - 2 && p < T.nplanes; ++p) issue_plane(Pq, T.prev(), p, p, ring, full, M);
+    }
+  }
+#else
   if (threadIdx.x + threadIdx.y == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&full[s], 1);
@@ -448,6 +505,7 @@ __global__ void __launch_bounds__(NT, OSAM_MINB)
     for (int p = 0; p < NSTAGE - 2 && p < T.nplanes; ++p) issue_plane(P, T.prev(), p, p, ring, full, M);
   }
   __syncthreads();
+#endif
 
   double acc[3][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
   double num = 0.0, den = 0.0;
@@ -606,7 +664,7 @@ int make_tmap(const Geom& g, double* array, bool halo, CUtensorMap* out) {
   }
   const cuuint64_t dims[4] = {(cuuint64_t)g.px, (cuuint64_t)g.nn[1], (cuuint64_t)g.nn[2], 3};
   const cuuint64_t strides[3] = {(cuuint64_t)g.px * 8, (cuuint64_t)g.plane * 8, (cuuint64_t)g.npad * 8};
-  const cuuint32_t box[4] = {halo ? (cuuint32_t)PX : (cuuint32_t)TX, halo ? (cuuint32_t)PY : (cuuint32_t)TY, 1, 3};
+  const cuuint32_t box[4] = {halo ? (cuuint32_t)PX : (cuuint32_t)TX, halo ? (cuuint32_t)PY : (cuuint32_t)SR, 1, 3};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   const CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, array, dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

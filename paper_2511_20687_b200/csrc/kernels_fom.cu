@@ -1200,6 +1200,11 @@ __global__ void __launch_bounds__(RB, 1) small_resident_kernel(const __grid_cons
           if (n >= A.min_iters) {
             C.numden[0] = sn;
             C.numden[1] = sd;
+            if (C.trace && n <= C.trace_T) {  // convergence trace (osam_set_conv_trace), B = 1
+              double* tr = C.trace + 2 * ((long long)(step - 1) * C.trace_T + (n - 1));
+              tr[0] = sn;
+              tr[1] = sd;
+            }
             if (bad) {
               C.flags[1] = 1;
               C.sticky[0] = 1;

@@ -39,6 +39,9 @@ struct GemmArgs {
   long long sbk, sbn;  // B(k, n) = B[k sbk + n sbn]
   double* C;           // partial products: C[z][m + M n] for K split z (dense, M x N per split)
   int kc;              // K range of one split (multiple of 4, <= KMAX)
+  const double* B2;    // rows k >= kb of B come from B2: B(k, n) = B2[(k - kb) sbk2 + n sbn2] (null: none)
+  long long sbk2, sbn2;
+  int kb;
 };
 
 // One block: a 32 x 32 tile of C over the K range [z kc, (z+1) kc): A and B staged once in shared
@@ -61,7 +64,10 @@ __global__ void __launch_bounds__(128) dmma_gemm_kernel(const GemmArgs g) {
   for (int q = t; q < g.kc * TN; q += 128) {
     const int kk = q / TN, nn = q % TN;
     const int n = n0 + nn;
-    Bs[kk][nn] = (n < g.N && kk < kn) ? g.B[(k0 + kk) * g.sbk + n * g.sbn] : 0.0;
+    const int k = k0 + kk;
+    Bs[kk][nn] = (n < g.N && kk < kn)
+                     ? ((g.B2 && k >= g.kb) ? g.B2[(k - g.kb) * g.sbk2 + n * g.sbn2] : g.B[k * g.sbk + n * g.sbn])
+                     : 0.0;
   }
   __syncthreads();
   const int wm = (warp & 1) * 16, wn = (warp >> 1) * 16;  // warp sub-tile
@@ -237,7 +243,10 @@ __device__ void gemm_tile_dev(const GemmArgs& g, int mt, int nt, int z, double (
   for (int q = t; q < g.kc * TN; q += 128) {
     const int kk = q / TN, nn = q % TN;
     const int n = n0 + nn;
-    Bs[kk][nn] = (n < g.N && kk < kn) ? g.B[(k0 + kk) * g.sbk + n * g.sbn] : 0.0;
+    const int k = k0 + kk;
+    Bs[kk][nn] = (n < g.N && kk < kn)
+                     ? ((g.B2 && k >= g.kb) ? g.B2[(k - g.kb) * g.sbk2 + n * g.sbn2] : g.B[k * g.sbk + n * g.sbn])
+                     : 0.0;
   }
   bar_named(bid, 128);
   const int wm = (warp & 1) * 16, wn = (warp >> 1) * 16;
@@ -464,6 +473,8 @@ __global__ void __launch_bounds__(RP_T) rom_persistent_kernel(const __grid_const
 
 // Batched ROM advance (B >= 2) on the tensor cores; scratch Z ((r + r_b) x B) and `part` (split-K
 // partials, tc_part_size doubles).
+long long tc_gemm_part(int M, int N, int K) { return (long long)gemm_splits(M, N, K) * M * N; }
+
 long long tc_part_size(int r, int r_b, int nf, int B, long long n_s, long long n_lift3) {
   const long long a = (long long)gemm_splits(r, B, r + r_b + nf) * r * B;
   const long long g = r_b > 0 ? (long long)gemm_splits(r_b, B, (int)n_s) * r_b * B : 0;
@@ -471,15 +482,31 @@ long long tc_part_size(int r, int r_b, int nf, int B, long long n_s, long long n
   return std::max(std::max(a, g), std::max<long long>(l, 1));
 }
 
-void launch_rom_advance_tc(const RomLaunch& L, const double* KB, double* Z, double* part, cudaStream_t s,
-                           int* launches) {
+void launch_rom_predict_tc(const RomLaunch& L, double* Z, cudaStream_t s, int* launches) {
   const int r = L.r, rb = L.r_b, rz = L.r + L.r_b + L.nf, B = L.B;
   launch_k(tc_predict_kernel, dim3(cdiv((long long)r * B, 256)), dim3(256), 0, s, r, rz, B, L.uh0, L.vh0, L.ah0, L.dt, L.c2, Z);
   debug_check("tc_predict_kernel", s);
   launch_rom_features(L.nf, B, L.feat_idx, Z, rz, Z + r + rb, rz, s);  // polynomial OpInf rows of Z
-  *launches += L.nf > 0;
+  *launches += 1 + (L.nf > 0);
+}
+
+void launch_rom_advance_tc(const RomLaunch& L, const double* KB, double* Z, double* part, cudaStream_t s,
+                           int* launches) {
+  const int r = L.r, rb = L.r_b, rz = L.r + L.r_b + L.nf, B = L.B;
+  if (!L.pre) {
+    launch_rom_predict_tc(L, Z, s, launches);
+    --*launches;  // counted with the advance below
+  }
+  if (L.pre && L.KBG) {  // araw = [-Kbar | Bbar G] [u~; u^_src]: the exchange folded into the update (one GEMM)
+    GemmArgs ga{r, B, r + L.Gr, L.KBG, 1, r, Z, 1, rz, nullptr, 0, L.Gu, 1, L.Gld ? L.Gld : L.Gr, r};
+    const int S = gemm(ga, part, s);
+    launch_k(tc_epilogue_kernel, dim3(dim3(cdiv(r, 256), B)), dim3(256), 0, s, L, part, S, Z, rz, 0);
+    debug_check("tc_epilogue_kernel", s);
+    *launches += 2;
+    return;
+  }
   if (rb > 0 && L.G) {  // folded exchange: g^ = G u^_src -> Z[r:, :]
-    const int S = gemm(GemmArgs{rb, B, L.Gr, L.G, 1, rb, L.Gu, 1, L.Gr, nullptr, 0}, part, s);
+    const int S = gemm(GemmArgs{rb, B, L.Gr, L.G, 1, rb, L.Gu, 1, L.Gld ? L.Gld : L.Gr, nullptr, 0}, part, s);
     launch_k(reduce_splits_kernel, dim3(cdiv((long long)rb * B, 256)), dim3(256), 0, s, rb, B, S, part, Z + r, 1, rz);
     debug_check("reduce_splits_kernel", s);
     *launches += 2;
@@ -498,7 +525,7 @@ void launch_rom_advance_tc(const RomLaunch& L, const double* KB, double* Z, doub
   const int S = gemm(GemmArgs{r, B, rz, KB, 1, r, Z, 1, rz, nullptr, 0}, part, s);
   launch_k(tc_epilogue_kernel, dim3(dim3(cdiv(r, 256), B)), dim3(256), 0, s, L, part, S, Z, rz, L.beta > 0.0 ? 2 : 0);
   debug_check("tc_epilogue_kernel", s);
-  *launches += 3;
+  *launches += L.pre ? 2 : 3;
   if (L.beta > 0.0) {
     launch_rom_implicit(L, Z, rz, rom_partial_slots(r, true), s);
     ++*launches;

@@ -207,6 +207,7 @@ void release_binding(Sub& s) {
   dfree(s.Phi_lift);
   dfree(s.lift_code);
   dfree(s.KB);
+  dfree(s.KBG);
   dfree(s.KBr);
   dfree(s.feat_idx);
   dfree(s.F);
@@ -674,6 +675,26 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
       }
       TRY(upload(&m.G, G, d.stream));
       d.fold = true;
+      if (d.nf == 0 && d.beta == 0.0) {  // [-Kbar | Bbar G]: the whole reduced update of a linear explicit ROM
+        const long long r = d.r, rs = src.r, rb = d.r_b;
+        std::vector<double> kbg((size_t)(r * (r + rs)));
+        for (long long j = 0; j < r; ++j)
+          for (long long q = 0; q < r; ++q) kbg[(size_t)(j * r + q)] = -d.h_Kbar[(size_t)(j * r + q)];
+        for (long long j = 0; j < rs; ++j)
+          for (long long q = 0; q < r; ++q) {
+            double a = 0.0;
+            for (long long k = 0; k < rb; ++k) a += d.h_Bbar[(size_t)(k * r + q)] * G[(size_t)(k + rb * j)];
+            kbg[(size_t)((r + j) * r + q)] = a;
+          }
+        TRY(upload(&d.KBG, kbg, d.stream));
+        const long long need = tc_gemm_part(d.r, d.batch, d.r + src.r);
+        long long rmx = 0;
+        for (int q = 0; q < n; ++q) rmx = std::max<long long>(rmx, subs[q]->r);
+        if (need > tc_part_size(d.r, d.r_b, d.nf, d.batch, std::max<long long>(d.n_sdof, rmx), 3 * d.n_lift)) {
+          dfree(d.part);
+          TRY(dalloc(&d.part, (size_t)need));
+        }
+      }
     }
     d.maps.push_back(m);
   }
@@ -923,6 +944,24 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
   const int set = first ? 0 : n_sd;
   if (par && (int)G.side.size() < 2 * n_sd) return fail(OSAM_ECUDA, "internal: side streams not created");
   std::vector<int> joins;
+  // Groups of explicit batched tensor-core ROMs with the folded exchange (c5): an explicit ROM iterate's
+  // displacement is its predictor u~ (u^' = u~), which depends on the checkpoint only, so u~ is formed once per
+  // controller step (before sweep 1, into Z[0:r]) and a destination's folded input G u^_src reads the source's
+  // Z[0:r] (its checkpoint u^ at n = 1 when the source comes later).  No ROM advance then reads another's output
+  // within a sweep: each forks onto a side stream and joins before the test (parallel graph branches), as the FOM
+  // advances do.  OSAM_ROM_PAR=0 keeps the serial chain.
+  static const bool rom_par_env = !(getenv("OSAM_ROM_PAR") && getenv("OSAM_ROM_PAR")[0] == '0');
+  bool rom_pre = rom_par_env && n_sd >= 2;
+  for (int i = 0; i < n_sd && rom_pre; ++i) {
+    const Sub& d = *subs[i];
+    rom_pre = d.kind == OSAM_ROM && d.use_tc && d.fold && d.beta == 0.0 && d.n_sub == 1 && d.maps.size() == 1;
+  }
+  if (rom_pre && first)
+    for (int i = 0; i < n_sd; ++i) {
+      Sub& d = *subs[i];
+      const RomLaunch L = rom_launch(d, d.rst[d.cur], d.rst[1 - d.cur], ctl.active, cfg.dt, 0, nullptr);
+      launch_rom_predict_tc(L, d.Z, st, launches);
+    }
   for (int i = 0; i < n_sd; ++i) {
     Sub& d = *subs[i];
     for (const XferMap& m : d.maps) {
@@ -991,9 +1030,26 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
         L.G = m.G;
         L.Gu = src.rst[newest ? 1 - src.cur : src.cur][0];
         L.Gr = src.r;
+        if (rom_pre && newest) {  // = the source's predictor (explicit ROM), formed at the step's start
+          L.Gu = src.Z;
+          L.Gld = src.r + src.r_b + src.nf;
+        }
+      }
+      cudaStream_t rs = st;
+      static const bool kbg_env = !(getenv("OSAM_ROM_KBG") && getenv("OSAM_ROM_KBG")[0] == '0');
+      if (rom_pre && kbg_env) L.KBG = d.KBG;
+      if (rom_pre && par) {
+        L.pre = 1;
+        CK(cudaEventRecord(G.fork_ev[set + i], st));
+        CK(cudaStreamWaitEvent(G.side[set + i], G.fork_ev[set + i], 0));
+        rs = G.side[set + i];
+        joins.push_back(set + i);
+      } else if (rom_pre) {
+        L.pre = 1;
       }
       if (d.use_tc) {
-        launch_rom_advance_tc(L, d.KB, d.Z, d.part, st, launches);
+        launch_rom_advance_tc(L, d.KB, d.Z, d.part, rs, launches);
+        if (rs != st) CK(cudaEventRecord(G.join_ev[set + i], rs));
         if (!d.fold)  // in a folded group no map reads a lift
           launch_rom_lift_tc(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, d.rst[1 - c][0], d.rst[1 - c][3],
                              d.n_sdof, d.lift[1 - c], d.part, st, launches);

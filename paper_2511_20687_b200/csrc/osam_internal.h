@@ -145,6 +145,7 @@ struct Sub {
   // batched ROM on the tensor cores (kernels_rom_tc.cu): [-Kbar | Bbar] and scratch
   bool use_tc = false;
   double* KB = nullptr;    // r x (r + r_b) column-major
+  double* KBG = nullptr;   // folded exchange, linear explicit ROM: [-Kbar | Bbar G] (r x (r + r_src), column-major)
   double* KBr = nullptr;   // the same, row-major (CUDA-core path)
   double* Z = nullptr;     // (r + r_b) x B
   double* part = nullptr;  // split-K partial products (tc_part_size doubles)
@@ -237,8 +238,11 @@ struct RomLaunch {
   double beta;         // 0: explicit; > 0: implicit average acceleration through Minv (R32)
   const double* Minv;  // [B][r][r] row-major
   const double* G;     // folded exchange: g^ = G Gu (r_b x Gr), null: g^ = Phi_dS^T s
-  const double* Gu;    // the source's reduced state (Gr x B)
+  const double* Gu;    // the source's reduced state (Gr x B, column stride Gld; 0: Gr)
   int Gr;
+  long long Gld;
+  int pre;             // TC path: Z[0:r] (the predictor u~, and its features) was written at the step's start
+  const double* KBG;   // TC path, pre: the update is [-Kbar | Bbar G] [u~; Gu] in one GEMM (null: G Gu first)
   int with_norm;
   double2* partial;
 };
@@ -259,11 +263,14 @@ void launch_rom_newton(const RomLaunch& L, const double* ut, long long uts, cons
 // implicit ROM finish (R32): a^' = Minv f (f in L.ah1), u^', v^', norm partials; u~ at ut (stride uts)
 void launch_rom_implicit(const RomLaunch& L, const double* ut, long long uts, int n_slots, cudaStream_t s);
 long long tc_part_size(int r, int r_b, int nf, int B, long long n_s, long long n_lift3);
+long long tc_gemm_part(int M, int N, int K);  // split-K partial doubles of one M x N x K product
 // F[q, b] = prod of u[idx[q][.], b]  (compressed Khatri-Rao monomials of the reduced state)
 void launch_rom_features(int nf, int B, const int* idx, const double* u, long long ustride, double* F, long long fstride,
                          cudaStream_t s);
 void launch_rom_advance_tc(const RomLaunch& L, const double* KB, double* Z, double* part, cudaStream_t s,
                            int* launches);
+// Z[0:r] = u~ = u^ + dt v^ + c2 a^ of the checkpoint (and the polynomial features of u~), once per controller step
+void launch_rom_predict_tc(const RomLaunch& L, double* Z, cudaStream_t s, int* launches);
 void launch_rom_accel_tc(const RomLaunch& L, const double* uh, double* ah, const double* KB, double* Z, double* part,
                          cudaStream_t s, int* launches);
 void launch_rom_lift_tc(int r, int B, long long nl, const double* Phi_lift, const int* code, const double* uh,
