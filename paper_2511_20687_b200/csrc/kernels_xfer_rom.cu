@@ -148,6 +148,7 @@ __device__ __forceinline__ void any_active_body(const Ctl& c, int B) {
   if (c.has_cond) cudaGraphSetConditional(c.cond, more ? 1u : 0u);
 }
 
+
 __global__ void any_active_kernel(Ctl c, int B) {
   pdl_enter();
   any_active_body(c, B);
@@ -794,6 +795,8 @@ void launch_step_begin(Ctl c, int B, cudaStream_t s) { launch_k(step_begin_kerne
 
 int launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int min_iters, double tol_rel,
                     double tol_abs, cudaStream_t s) {
+  // B > 1: the controller update in a launch of its own (doing it in the last block to finish, through an arrival
+  // counter, measured slower on c5: 10.24k vs 10.70k steps/s)
   launch_k(finalize_kernel, dim3(B), dim3(FIN_T), 0, s, c, partial, n_slots, B, min_iters, tol_rel, tol_abs,
            B == 1 ? 1 : 0);
   debug_check("finalize_kernel", s);
@@ -827,12 +830,81 @@ int rom_gchunks(long long n_s) { return (int)std::max<long long>(1, cdiv(n_s, GC
 
 int rom_partial_slots(int r, bool tc) { return (int)(tc ? cdiv(r, 256) : cdiv(r, 8)); }
 
+// a^'[i] = e (sum_j KBF[i, j] z[j]) with z = [u~; x_d], x_d[t] = src[xd_idx[t]] (the FOM values the folded
+// exchange reads), then rom_update_kernel's finish (v^', u^' = u~, norm partials).  B = 1.  One block per row:
+// its 256 threads read the row and z with every load in flight at once (a warp-per-row loop is a chain of L2
+// round trips), then a fixed-order block sum; the row is fixed at bind and read before the wait.  One norm
+// partial slot per row (K3 sums the slots in order).
+constexpr int FU_T = 256, FU_PER = 8;  // threads, row entries per thread held in registers (rows <= 2048)
+__global__ void __launch_bounds__(FU_T) rom_fold_update_kernel(const RomLaunch L, const double* __restrict__ KBF,
+                                                               const int* __restrict__ xd_idx, int n_xd,
+                                                               const double* __restrict__ src) {
+  pdl_launch();
+  const int i = blockIdx.x, t = threadIdx.x;
+  const int r = L.r, nz = L.r + n_xd;
+  const double* row = KBF + (long long)i * nz;
+  double k[FU_PER];
+  int xi[FU_PER];
+#pragma unroll
+  for (int m = 0; m < FU_PER; ++m) {
+    const int j = t + FU_T * m;
+    k[m] = j < nz ? row[j] : 0.0;
+    xi[m] = (j >= r && j < nz) ? xd_idx[j - r] : 0;
+  }
+  pdl_wait();
+  double z[FU_PER];
+#pragma unroll
+  for (int m = 0; m < FU_PER; ++m) {
+    const int j = t + FU_T * m;
+    z[m] = j < r ? L.ustar[j] : (j < nz ? src[xi[m]] : 0.0);
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int m = 0; m < FU_PER; ++m) acc = fma(k[m], z[m], acc);
+  for (int j = t + FU_T * FU_PER; j < nz; j += FU_T)  // rows longer than FU_T * FU_PER
+    acc = fma(row[j], j < r ? L.ustar[j] : src[xd_idx[j - r]], acc);
+  acc = block_sum256(acc);
+  if (t == 0) {
+    double num = 0.0, den = 0.0;
+    if (L.active[0]) {
+      const double an = L.e[0] * acc;
+      const double vn = fma(0.5 * L.dt, L.ah0[i] + an, L.vh0[i]);
+      const double un = L.ustar[i];
+      if (L.with_norm) {
+        const double d = (un - L.uh1[i]) + L.dt * (vn - L.vh1[i]);
+        const double wv = un + L.dt * vn;
+        num = d * d;
+        den = wv * wv;
+      }
+      L.uh1[i] = un;
+      L.vh1[i] = vn;
+      L.ah1[i] = an;
+    }
+    L.partial[i] = make_double2(num, den);
+  }
+}
+
+void launch_rom_fold_update(const RomLaunch& L, const double* KBF, const int* xd_idx, int n_xd, const double* src_field,
+                            cudaStream_t s, int* launches) {
+  launch_k(rom_fold_update_kernel, dim3(L.r), dim3(FU_T), 0, s, L, KBF, xd_idx, n_xd, src_field);
+  debug_check("rom_fold_update_kernel", s);
+  ++*launches;
+}
+
+void launch_rom_predict(const RomLaunch& L, cudaStream_t s, int* launches) {
+  launch_k(rom_predict_kernel, dim3(cdiv((long long)L.r * L.B, 256)), dim3(256), 0, s, L.r, L.B, L.uh0, L.vh0, L.ah0, L.dt, L.c2,
+           L.ustar);
+  debug_check("rom_predict_kernel", s);
+  ++*launches;
+}
+
 void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches) {
   if (L.r_b > 0)
     launch_k(rom_project_bnd_kernel, dim3(dim3(L.r_b, rom_gchunks(L.n_sdof), L.B)), dim3(256), 0, s, L.r_b, L.B, L.n_sdof, L.Phi_s,
                                                                                    L.s, L.gh);
-  launch_k(rom_predict_kernel, dim3(cdiv((long long)L.r * L.B, 256)), dim3(256), 0, s, L.r, L.B, L.uh0, L.vh0, L.ah0, L.dt, L.c2,
-                                                                     L.ustar);
+  if (!L.pre)
+    launch_k(rom_predict_kernel, dim3(cdiv((long long)L.r * L.B, 256)), dim3(256), 0, s, L.r, L.B, L.uh0, L.vh0, L.ah0,
+             L.dt, L.c2, L.ustar);
   launch_rom_features(L.nf, L.B, L.feat_idx, L.ustar, L.r, L.F, L.nf, s);
   *launches += L.nf > 0;
   debug_check("rom_predict_kernel", s);
@@ -843,7 +915,7 @@ void launch_rom_advance(const RomLaunch& L, cudaStream_t s, int* launches) {
   }
   launch_k(rom_update_kernel, dim3(dim3(cdiv(L.r, 8), L.B)), dim3(256), 0, s, L, L.beta > 0.0 ? 2 : 0);
   debug_check("rom_update_kernel", s);
-  *launches += (L.r_b > 0) + 2;
+  *launches += (L.r_b > 0) + (L.pre ? 1 : 2);
   if (L.beta > 0.0) {
     launch_rom_implicit(L, L.ustar, L.r, rom_partial_slots(L.r, false), s);
     ++*launches;

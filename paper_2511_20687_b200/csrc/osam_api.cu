@@ -169,6 +169,12 @@ int fom_slots(const Sub& s) {
   return s.material == OSAM_LINEAR ? fom_partial_slots(s.g, s.faces) : fom_nl_partial_slots(s.g);
 }
 
+// partial slots of a subdomain's advance: FOM blocks, ROM row groups (the folded FOM exchange: one per row)
+int sub_slots(const Sub& s) {
+  if (s.kind == OSAM_FOM) return fom_slots(s);
+  return s.KBF ? s.r : rom_partial_slots(s.r, s.use_tc);
+}
+
 // ---- binding ------------------------------------------------------------------------------
 void release_maps(Sub& s) {
   for (auto& m : s.maps) {
@@ -208,6 +214,9 @@ void release_binding(Sub& s) {
   dfree(s.lift_code);
   dfree(s.KB);
   dfree(s.KBG);
+  dfree(s.KBF);
+  dfree(s.xd_idx);
+  s.n_xd = 0;
   dfree(s.KBr);
   dfree(s.feat_idx);
   dfree(s.F);
@@ -698,6 +707,82 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
     }
     d.maps.push_back(m);
   }
+  // B = 1 ROM fed by one FOM map that reads no source Schwarz DOF (c2): g^ = Phi_dS^T Pi x = G_F x_d exactly up
+  // to rounding, x_d = the source DOFs the map reads; with the ROM's own update [-Kbar | Bbar G_F] acts on
+  // [u~; x_d] (one small kernel per sweep instead of transfer + projection + update).  Needs the ROM's lift to
+  // read no ROM Schwarz DOF (its s is then never formed) and an explicit single-substep linear ROM; groups with a
+  // multi-substep subdomain keep the trace path.  OSAM_NO_FOLD disables it.
+  bool any_sub = false, any_tc = false;
+  for (int i = 0; i < n; ++i) {
+    any_sub = any_sub || subs[i]->n_sub > 1;
+    any_tc = any_tc || (subs[i]->kind == OSAM_ROM && subs[i]->use_tc);
+  }
+  for (int i = 0; i < n; ++i) {
+    Sub& d = *subs[i];
+    d.pre1 = false;
+    if (any_sub || any_tc || getenv("OSAM_NO_PRE1") || d.kind != OSAM_ROM || d.batch != 1 || d.nf != 0 ||
+        d.beta != 0.0)
+      continue;
+    bool ok = true;
+    for (auto& mm : d.maps) ok = ok && !mm.reads_src_schwarz;
+    for (int q = 0; q < n && ok; ++q)
+      for (auto& mm : subs[q]->maps)
+        if (mm.src == i && mm.reads_src_schwarz) ok = false;
+    d.pre1 = ok;
+  }
+  for (auto& P : pend) {
+    Sub& d = *subs[P.dst];
+    const Sub& src = *subs[P.src];
+    int maps_d = 0;
+    for (auto& Q : pend) maps_d += Q.dst == P.dst;
+    const bool ok = !getenv("OSAM_NO_FOLD") && d.pre1 && d.r_b > 0 && maps_d == 1 && src.kind == OSAM_FOM;
+    if (!ok) continue;
+    std::map<long long, int> col;  // source DOF offset -> column of x_d
+    std::vector<int> xd;
+    for (size_t t = 0; t < P.out.size(); ++t) {
+      if (P.out[t] < 0) continue;
+      const int c = (int)(t % 3);
+      const long long p = (long long)(t / 3);
+      for (int q = 0; q < 8; ++q) {
+        const long long node = P.corner[8 * p + q];
+        const long long i0 = node % src.g.nn[0], j0 = (node / src.g.nn[0]) % src.g.nn[1],
+                        k0 = node / ((long long)src.g.nn[0] * src.g.nn[1]);
+        const long long off = c * src.g.npad + i0 + src.g.px * j0 + src.g.plane * k0;
+        if (col.emplace(off, (int)xd.size()).second) xd.push_back((int)off);
+      }
+    }
+    const long long r = d.r, rb = d.r_b, nx = (long long)xd.size();
+    if (r * (r + nx) > (4LL << 20)) continue;
+    std::vector<double> G((size_t)(rb * nx), 0.0);  // G[k + rb t]
+    for (size_t t = 0; t < P.out.size(); ++t) {
+      const int sd = P.out[t];
+      if (sd < 0) continue;
+      const int c = (int)(t % 3);
+      const long long p = (long long)(t / 3);
+      const double x = P.xi[3 * p], y = P.xi[3 * p + 1], z = P.xi[3 * p + 2];
+      for (int q = 0; q < 8; ++q) {
+        const double w = ((q & 1) ? x : 1.0 - x) * ((q & 2) ? y : 1.0 - y) * ((q & 4) ? z : 1.0 - z);
+        const long long node = P.corner[8 * p + q];
+        const long long i0 = node % src.g.nn[0], j0 = (node / src.g.nn[0]) % src.g.nn[1],
+                        k0 = node / ((long long)src.g.nn[0] * src.g.nn[1]);
+        const int tc = col[c * src.g.npad + i0 + src.g.px * j0 + src.g.plane * k0];
+        for (long long k = 0; k < rb; ++k) G[(size_t)(k + rb * tc)] += d.h_Phi_s[(size_t)sd + (size_t)d.n_sdof * k] * w;
+      }
+    }
+    std::vector<double> kbf((size_t)(r * (r + nx)));  // row-major
+    for (long long i = 0; i < r; ++i) {
+      double* row = kbf.data() + (size_t)(i * (r + nx));
+      for (long long j = 0; j < r; ++j) row[j] = -d.h_Kbar[(size_t)(j * r + i)];
+      for (long long t = 0; t < nx; ++t) {
+        double a = 0.0;
+        for (long long k = 0; k < rb; ++k) a += d.h_Bbar[(size_t)(k * r + i)] * G[(size_t)(k + rb * t)];
+        row[r + t] = a;
+      }
+    }
+    TRY(upload(&d.KBF, kbf, d.stream));
+    TRY(upload(&d.xd_idx, xd, d.stream));
+    d.n_xd = (int)nx;
+  }
   // multi-substep group: a trace of n_src_sub + 1 slots per map (R31)
   bool trace = false;
   int Bg = 1;
@@ -794,7 +879,7 @@ int get_group(osam_subdomain* const* sds, int n_sd, Group** out) {
     for (auto s : subs) G->B = std::max(G->B, s->batch);
     for (auto s : subs) G->trace = G->trace || s->n_sub > 1;
     G->n_slots = 0;
-    for (auto s : subs) G->n_slots += s->kind == OSAM_FOM ? fom_slots(*s) : rom_partial_slots(s->r, s->use_tc);
+    for (auto s : subs) G->n_slots += sub_slots(*s);
     TRY(dalloc(&G->partial, (size_t)std::max(1, G->n_slots) * G->B));
     TRY(dalloc(&G->ctl_i, (size_t)G->ctl_len()));
     CK(cudaMemset(G->ctl_i, 0, sizeof(int) * G->ctl_len()));
@@ -956,6 +1041,20 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
     const Sub& d = *subs[i];
     rom_pre = d.kind == OSAM_ROM && d.use_tc && d.fold && d.beta == 0.0 && d.n_sub == 1 && d.maps.size() == 1;
   }
+  // B = 1 ROMs with the folded FOM exchange (KBF, c2): the explicit iterate's displacement is u~, formed once per
+  // controller step with its lift (what the FOM's transfer reads from sweep 2 on); the ROM's update reads the
+  // source FOM's field (its stencil input, fixed within the step at the DOFs the map reads) and no other
+  // advance's output, so it runs as a parallel branch too
+  if (first)
+    for (int i = 0; i < n_sd; ++i) {
+      Sub& d = *subs[i];
+      if (!d.pre1) continue;
+      const RomLaunch L = rom_launch(d, d.rst[d.cur], d.rst[1 - d.cur], ctl.active, cfg.dt, 0, nullptr);
+      launch_rom_predict(L, st, launches);
+      launch_rom_lift(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, d.ustar, d.rst[1 - d.cur][3], d.n_sdof,
+                      d.lift[1 - d.cur], st);
+      *launches += d.n_lift > 0;
+    }
   if (rom_pre && first)
     for (int i = 0; i < n_sd; ++i) {
       Sub& d = *subs[i];
@@ -965,7 +1064,7 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
   for (int i = 0; i < n_sd; ++i) {
     Sub& d = *subs[i];
     for (const XferMap& m : d.maps) {
-      if (d.fold) continue;  // folded ROM-ROM exchange: g^ = G u^_src inside the ROM advance
+      if (d.fold || d.pre1) continue;  // folded exchange: inside the ROM advance; pre1: on its branch below
       const Sub& src = *subs[m.src];
       const bool newest = (m.src < i) || !first;
       const double* field;
@@ -1034,6 +1133,51 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
           L.Gu = src.Z;
           L.Gld = src.r + src.r_b + src.nf;
         }
+      }
+      if (d.KBF) {  // folded FOM exchange (B = 1): one kernel, a parallel branch
+        const Sub& src = *subs[d.maps[0].src];
+        cudaStream_t rs2 = st;
+        if (par) {
+          CK(cudaEventRecord(G.fork_ev[set + i], st));
+          CK(cudaStreamWaitEvent(G.side[set + i], G.fork_ev[set + i], 0));
+          rs2 = G.side[set + i];
+          joins.push_back(set + i);
+        }
+        launch_rom_fold_update(L, d.KBF, d.xd_idx, d.n_xd, src.st[src.cur][0], rs2, launches);
+        if (par) CK(cudaEventRecord(G.join_ev[set + i], rs2));
+        slot += sub_slots(d);
+        continue;
+      }
+      if (d.pre1) {  // transfers into it, then its advance (the predictor formed at the step's start): a branch
+        cudaStream_t rs2 = st;
+        if (par) {
+          CK(cudaEventRecord(G.fork_ev[set + i], st));
+          CK(cudaStreamWaitEvent(G.side[set + i], G.fork_ev[set + i], 0));
+          rs2 = G.side[set + i];
+          joins.push_back(set + i);
+        }
+        for (const XferMap& m : d.maps) {
+          const Sub& src = *subs[m.src];
+          const bool newest = (m.src < i) || !first;
+          const double* field;
+          long long cs, bs;
+          if (src.kind == OSAM_FOM) {
+            field = newest ? src.st[src.cur][0] : src.st[src.ux][0];
+            cs = src.g.npad;
+            bs = 0;
+          } else {
+            field = src.lift[newest ? 1 - src.cur : src.cur];
+            cs = src.n_lift;
+            bs = 3 * src.n_lift;
+          }
+          launch_transfer(m, field, cs, bs, d.rst[1 - d.cur][3], d.n_sdof, B, nullptr, rs2);
+          ++*launches;
+        }
+        L.pre = 1;
+        launch_rom_advance(L, rs2, launches);
+        if (par) CK(cudaEventRecord(G.join_ev[set + i], rs2));
+        slot += sub_slots(d);
+        continue;
       }
       cudaStream_t rs = st;
       static const bool kbg_env = !(getenv("OSAM_ROM_KBG") && getenv("OSAM_ROM_KBG")[0] == '0');
@@ -1179,7 +1323,7 @@ int enqueue_sweep_trace(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, b
           ++*launches;
         }
     }
-    slot += d.kind == OSAM_FOM ? fom_slots(d) : rom_partial_slots(d.r, d.use_tc);
+    slot += sub_slots(d);
   }
   *launches += launch_finalize(ctl, G.partial, G.n_slots, B, cfg.min_iters, cfg.tol_rel, cfg.tol_abs, st);
   return OSAM_OK;
@@ -1292,7 +1436,7 @@ int step_graph_capture(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t st, c
 }
 
 // CUDA graph of one controller step: step_begin, sweep 1, then a conditional while node whose
-// body is one sweep n >= 2; K3 (any_active_kernel) sets the loop condition on the device, so a step
+// body is one sweep n >= 2; K3 (finalize_kernel) sets the loop condition on the device, so a step
 // needs no host round trip.  One graph per (configuration, buffer parity), cached in the group.
 int step_graph_capture(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t st, cudaGraph_t* graph_out,
                        int* launches_out);

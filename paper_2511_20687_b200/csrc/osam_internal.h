@@ -146,6 +146,15 @@ struct Sub {
   bool use_tc = false;
   double* KB = nullptr;    // r x (r + r_b) column-major
   double* KBG = nullptr;   // folded exchange, linear explicit ROM: [-Kbar | Bbar G] (r x (r + r_src), column-major)
+  // B = 1 ROM fed by one FOM map (c2): [-Kbar | Bbar G_F] row-major (r x (r + n_xd)), G_F = Phi_dS^T Pi restricted
+  // to the n_xd source DOFs the map reads (xd_idx: their offsets in the source field); null: not folded
+  double* KBF = nullptr;
+  int* xd_idx = nullptr;
+  int n_xd = 0;
+  // explicit B = 1 ROM (CUDA-core path) whose exchange reads checkpoint-fixed data only (no map into it reads a
+  // source Schwarz DOF, no map reading its lift reads its Schwarz DOFs): u~ and its lift are formed once per
+  // controller step and its advance is a parallel graph branch (bind_group; implied by KBF)
+  bool pre1 = false;
   double* KBr = nullptr;   // the same, row-major (CUDA-core path)
   double* Z = nullptr;     // (r + r_b) x B
   double* part = nullptr;  // split-K partial products (tc_part_size doubles)
@@ -271,6 +280,11 @@ void launch_rom_advance_tc(const RomLaunch& L, const double* KB, double* Z, doub
                            int* launches);
 // Z[0:r] = u~ = u^ + dt v^ + c2 a^ of the checkpoint (and the polynomial features of u~), once per controller step
 void launch_rom_predict_tc(const RomLaunch& L, double* Z, cudaStream_t s, int* launches);
+// B = 1 ROM with the FOM exchange folded (KBF): a^' = e (-Kbar u~ + Bbar G_F x_d), x_d gathered from the source
+// FOM field, u~ = L.ustar formed at the step's start; v^', u^', norm partials (one launch)
+void launch_rom_fold_update(const RomLaunch& L, const double* KBF, const int* xd_idx, int n_xd, const double* src_field,
+                            cudaStream_t s, int* launches);
+void launch_rom_predict(const RomLaunch& L, cudaStream_t s, int* launches);  // L.ustar = u~ (CUDA-core path)
 void launch_rom_accel_tc(const RomLaunch& L, const double* uh, double* ah, const double* KB, double* Z, double* part,
                          cudaStream_t s, int* launches);
 void launch_rom_lift_tc(int r, int B, long long nl, const double* Phi_lift, const int* code, const double* uh,

@@ -51,3 +51,35 @@ def test_process_wide_switches_keep_parity(gpu, env):
     out = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
     assert out.stdout.strip().splitlines()[-1].startswith("ok")
+
+
+ROM_SCRIPT = r'''
+import sys, numpy as np
+sys.path.insert(0, {root!r}); sys.path.insert(0, {tests!r})
+import torch
+assert torch.cuda.is_available()
+import osam_inputs as I
+from oracle import opinf
+from test_gpu_parity import run_both
+from paper_2511_20687_b200 import problem
+cfg = I.config("c2")
+_, it, worst = run_both(problem, cfg, 120, rom_ops=opinf.train(cfg, I), checkpoints=(1,))
+assert (it == 3).all()
+cfg = I.config("c5")
+_, it2, worst2 = run_both(problem, cfg, 150, rom_ops=opinf.train(cfg, I), checkpoints=(1,))
+assert (it2 == 3).all()
+print("ok", worst, worst2)
+'''
+
+
+@pytest.mark.parametrize("env", [{}, {"OSAM_NO_FOLD": "1"}, {"OSAM_ROM_PAR": "0"}, {"OSAM_ROM_KBG": "0"}])
+def test_rom_exchange_switches_keep_parity(gpu, env):
+    """c2 (FOM-ROM, B = 1: the FOM exchange folded into the ROM update by default) and c5 (batched ROM-ROM: the
+    predictor once per step, parallel ROM branches, [-Kbar | Bbar G] by default) against the oracle, with every
+    ROM-exchange switch: OSAM_NO_FOLD=1 (transfer + projection + update), OSAM_ROM_PAR=0 (serial ROM chain, the
+    predictor per sweep), OSAM_ROM_KBG=0 (g^ = G u^ before the update GEMM)."""
+    e = dict(os.environ, **env)
+    code = ROM_SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
+    out = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
+    assert out.stdout.strip().splitlines()[-1].startswith("ok")
