@@ -1045,10 +1045,18 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
   // controller step with its lift (what the FOM's transfer reads from sweep 2 on); the ROM's update reads the
   // source FOM's field (its stencil input, fixed within the step at the DOFs the map reads) and no other
   // advance's output, so it runs as a parallel branch too
+  // a pre1 ROM whose lift a later subdomain reads in sweep 1 (iterate 1 of an earlier source) forms u~ and the lift
+  // here; the others do it on their own branch (the lift overlaps the FOM advance)
+  auto lift_early = [&](int i) {
+    for (int q = i + 1; q < n_sd; ++q)
+      for (const XferMap& mm : subs[q]->maps)
+        if (mm.src == i) return true;
+    return false;
+  };
   if (first)
     for (int i = 0; i < n_sd; ++i) {
       Sub& d = *subs[i];
-      if (!d.pre1) continue;
+      if (!d.pre1 || !lift_early(i)) continue;
       const RomLaunch L = rom_launch(d, d.rst[d.cur], d.rst[1 - d.cur], ctl.active, cfg.dt, 0, nullptr);
       launch_rom_predict(L, st, launches);
       launch_rom_lift(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, d.ustar, d.rst[1 - d.cur][3], d.n_sdof,
@@ -1143,7 +1151,14 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
           rs2 = G.side[set + i];
           joins.push_back(set + i);
         }
+        const bool late = first && !lift_early(i);
+        if (late) launch_rom_predict(L, rs2, launches);
         launch_rom_fold_update(L, d.KBF, d.xd_idx, d.n_xd, src.st[src.cur][0], rs2, launches);
+        if (late) {
+          launch_rom_lift(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, d.ustar, d.rst[1 - d.cur][3], d.n_sdof,
+                          d.lift[1 - d.cur], rs2);
+          *launches += d.n_lift > 0;
+        }
         if (par) CK(cudaEventRecord(G.join_ev[set + i], rs2));
         slot += sub_slots(d);
         continue;
@@ -1174,7 +1189,14 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
           ++*launches;
         }
         L.pre = 1;
+        const bool late = first && !lift_early(i);
+        if (late) launch_rom_predict(L, rs2, launches);
         launch_rom_advance(L, rs2, launches);
+        if (late) {
+          launch_rom_lift(d.r, d.batch, 3 * d.n_lift, d.Phi_lift, d.lift_code, d.ustar, d.rst[1 - d.cur][3], d.n_sdof,
+                          d.lift[1 - d.cur], rs2);
+          *launches += d.n_lift > 0;
+        }
         if (par) CK(cudaEventRecord(G.join_ev[set + i], rs2));
         slot += sub_slots(d);
         continue;
