@@ -17,9 +17,6 @@ constexpr int PX = TX + 4;
 #ifndef OSAM_K1_WARP
 #define OSAM_K1_WARP 0
 #endif
-#ifndef OSAM_PROD_AFTER
-#define OSAM_PROD_AFTER 0
-#endif
 // OSAM_K1_WARP = 1: every warp streams its own rows (its own TMA boxes, ring and full barriers; no empty
 // barriers), so no warp waits for another; the staged box is the warp's WR rows plus the y halo.
 constexpr int WR = 32 / TX;                          // node rows per warp
@@ -308,7 +305,6 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
   // the plane and its coordinates follow from the iteration and the thread's own tile constants (no cursor
   // in shared memory: c3 932 -> 953 steps/s; the role rotated over the warps, a non-blocking producer and an
   // issue at the end of the iteration were measured slower, profiles/r3_k1_experiments.md)
-#if !OSAM_PROD_AFTER
 #if OSAM_K1_WARP
   // per-warp rings: lane 0 refills the stage its own warp released at the end of the previous iteration
   const bool issuer = (((int)threadIdx.x + TX * (int)threadIdx.y) & 31) == 0;
@@ -327,7 +323,6 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
     Pq.kbeg = T.kbeg;
     issue_plane(Pq, T.prev(), p, p % NSTAGE, ring, full, M);
   }
-#endif
   const int s = gi % NSTAGE;
 #ifdef OSAM_K1_PROF
   const long long kt1 = clock64();
@@ -354,26 +349,6 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
       }
     }
   }
-#if OSAM_PROD_AFTER  // the producer after its own stencil work: the other warps have longer to release the stage
-#if OSAM_K1_WARP
-  // per-warp rings: lane 0 refills the stage its own warp released at the end of the previous iteration
-  const bool issuer = (((int)threadIdx.x + TX * (int)threadIdx.y) & 31) == 0;
-  if (issuer && it >= 2) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // its reads, then TMA
-#else
-  const bool issuer = threadIdx.x + threadIdx.y == 0;
-#endif
-  if (issuer && it + NSTAGE - 2 < T.nplanes) {
-    const int p = it + NSTAGE - 2;
-#if !defined(OSAM_K1_NOEMPTY) && !OSAM_K1_WARP  // NOEMPTY: probe only (wrong results)
-    if (p >= NSTAGE) mbar_wait(&empty[p % NSTAGE], (unsigned)(((p - NSTAGE) / NSTAGE) & 1));
-#endif
-    TileGeo Pq;
-    Pq.x0 = T.i - 2;
-    Pq.y0 = T.j - 1;
-    Pq.kbeg = T.kbeg;
-    issue_plane(Pq, T.prev(), p, p % NSTAGE, ring, full, M);
-  }
-#endif
   if (T.active()) {
     const double* C = acc[SC];
     if (fin) {
