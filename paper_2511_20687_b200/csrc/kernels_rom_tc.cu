@@ -482,6 +482,13 @@ long long tc_part_size(int r, int r_b, int nf, int B, long long n_s, long long n
   return std::max(std::max(a, g), std::max<long long>(l, 1));
 }
 
+int launch_rom_update_gemm_tc(const RomLaunch& L, double* Z, double* part, cudaStream_t s, int* launches) {
+  const int r = L.r, rz = L.r + L.r_b + L.nf, B = L.B;
+  GemmArgs ga{r, B, r + L.Gr, L.KBG, 1, r, Z, 1, rz, nullptr, 0, L.Gu, 1, L.Gld ? L.Gld : L.Gr, r};
+  ++*launches;
+  return gemm(ga, part, s);
+}
+
 void launch_rom_predict_tc(const RomLaunch& L, double* Z, cudaStream_t s, int* launches) {
   const int r = L.r, rb = L.r_b, rz = L.r + L.r_b + L.nf, B = L.B;
   launch_k(tc_predict_kernel, dim3(cdiv((long long)r * B, 256)), dim3(256), 0, s, r, rz, B, L.uh0, L.vh0, L.ah0, L.dt, L.c2, Z);

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(FIN_T) finalize_kernel(Ctl c, const double2* _
   double num = 0.0, den = 0.0;
   if (n >= min_iters) {
 #pragma unroll 4
-    for (int s = t; s < n_slots; s += FIN_T) {
+    for (int s = t; s < n_slots; s += blockDim.x) {
       const double2 v = part[(long long)s * B + b];
       num += v.x;
       den += v.y;
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(FIN_T) finalize_kernel(Ctl c, const double2* _
   if (t == 0) {
     num = 0.0;
     den = 0.0;
-    for (int w = 0; w < FIN_T / 32; ++w) {
+    for (int w = 0; w < (int)blockDim.x / 32; ++w) {
       num += red[0][w];
       den += red[1][w];
     }
@@ -793,11 +793,99 @@ void launch_rom_implicit(const RomLaunch& L, const double* ut, long long uts, in
 
 void launch_step_begin(Ctl c, int B, cudaStream_t s) { launch_k(step_begin_kernel, dim3(1), dim3(256), 0, s, c, B); }
 
+// The epilogues of a folded batched-ROM group and K3, one block per sample b: for every ROM in group order and
+// every row (thread-strided), a^' = e_b sum_z part[z][i + r b] (splits in order), v^' = v^ + dt/2 (a^ + a^'),
+// u^' = u~, and the norm terms; the block sums them in a fixed order and runs K3's test for b (finalize_kernel's
+// body).  Frozen samples (converged, R29) keep their state.
+constexpr int EF_T = 1024;
+__global__ void __launch_bounds__(EF_T) rom_epi_finalize_kernel(const EpiArgs A, Ctl c) {
+  pdl_enter();
+  __shared__ double red[2][EF_T / 32];
+  const int b = blockIdx.x, t = threadIdx.x;
+  const int n = *c.n_dev + 1;
+  const bool on = c.active[b] != 0;
+  double num = 0.0, den = 0.0;
+  if (on)
+    for (int q = 0; q < A.n_sd; ++q) {
+      const EpiSub& d = A.s[q];
+      const long long col = (long long)d.r * b;
+      for (int i = t; i < d.r; i += EF_T) {
+        const long long id = col + i;
+        const double* pp = d.part + id;
+        const size_t zs = (size_t)d.r * A.B;
+        double pv[16];  // the split partials in flight together (S <= 16 for these products), summed in order
+#pragma unroll
+        for (int z = 0; z < 16; ++z) pv[z] = z < d.S ? pp[z * zs] : 0.0;
+        double araw = 0.0;
+#pragma unroll
+        for (int z = 0; z < 16; ++z)
+          if (z < d.S) araw += pv[z];
+        for (int z = 16; z < d.S; ++z) araw += pp[z * zs];
+        const double an = d.e[b] * araw;
+        const double un = d.Z[i + (long long)d.rz * b];
+        const double vn = fma(0.5 * A.dt, d.ah0[id] + an, d.vh0[id]);
+        if (A.with_norm) {
+          const double dd = (un - d.uh1[id]) + A.dt * (vn - d.vh1[id]);
+          const double w = un + A.dt * vn;
+          num = fma(dd, dd, num);
+          den = fma(w, w, den);
+        }
+        d.uh1[id] = un;
+        d.vh1[id] = vn;
+        d.ah1[id] = an;
+      }
+    }
+  num = warp_sum(num);
+  den = warp_sum(den);
+  if ((t & 31) == 0) {
+    red[0][t >> 5] = num;
+    red[1][t >> 5] = den;
+  }
+  __syncthreads();
+  if (t == 0) {
+    num = 0.0;
+    den = 0.0;
+    for (int w = 0; w < EF_T / 32; ++w) {
+      num += red[0][w];
+      den += red[1][w];
+    }
+    if (on) {
+      c.iters[b] = n;
+      if (n >= A.min_iters) {
+        c.numden[2 * b] = num;
+        c.numden[2 * b + 1] = den;
+        if (c.trace && n <= c.trace_T) {
+          double* tr = c.trace + 2 * (((long long)(*c.step_dev - 1) * c.trace_T + (n - 1)) * A.B + b);
+          tr[0] = num;
+          tr[1] = den;
+        }
+        if (!isfinite(num) || !isfinite(den)) {
+          c.flags[1] = 1;
+          c.sticky[0] = 1;
+        }
+        bool conv = (num == 0.0) || (num < A.tol_rel * A.tol_rel * den);
+        if (A.tol_abs > 0.0) conv = conv || (num < A.tol_abs * A.tol_abs);
+        if (conv) c.active[b] = 0;
+      }
+    }
+  }
+}
+
+int launch_rom_epi_finalize(const EpiArgs& A, Ctl c, cudaStream_t s) {
+  launch_k(rom_epi_finalize_kernel, dim3(A.B), dim3(EF_T), 0, s, A, c);
+  debug_check("rom_epi_finalize_kernel", s);
+  launch_k(any_active_kernel, dim3(1), dim3(1), 0, s, c, A.B);
+  debug_check("any_active_kernel", s);
+  return 2;
+}
+
 int launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int min_iters, double tol_rel,
                     double tol_abs, cudaStream_t s) {
   // B > 1: the controller update in a launch of its own (doing it in the last block to finish, through an arrival
   // counter, measured slower on c5: 10.24k vs 10.70k steps/s)
-  launch_k(finalize_kernel, dim3(B), dim3(FIN_T), 0, s, c, partial, n_slots, B, min_iters, tol_rel, tol_abs,
+  // block size: enough warps for the slots (fewer idle warps per sample when there are few slots, e.g. c5)
+  const int nt = std::min(FIN_T, std::max(32, (n_slots + 31) / 32 * 32));
+  launch_k(finalize_kernel, dim3(B), dim3(nt), 0, s, c, partial, n_slots, B, min_iters, tol_rel, tol_abs,
            B == 1 ? 1 : 0);
   debug_check("finalize_kernel", s);
   if (B == 1) return 1;

@@ -1069,6 +1069,13 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
       const RomLaunch L = rom_launch(d, d.rst[d.cur], d.rst[1 - d.cur], ctl.active, cfg.dt, 0, nullptr);
       launch_rom_predict_tc(L, d.Z, st, launches);
     }
+  // ... and with every update folded ([-Kbar | Bbar G]), the epilogues run with K3 in one launch per sweep
+  // (rom_epi_finalize_kernel; OSAM_EPI_FUSED=0: an epilogue per ROM, then K3)
+  static const bool epi_env = !(getenv("OSAM_EPI_FUSED") && getenv("OSAM_EPI_FUSED")[0] == '0');
+  static const bool kbg_env0 = !(getenv("OSAM_ROM_KBG") && getenv("OSAM_ROM_KBG")[0] == '0');
+  bool epi_fused = rom_pre && kbg_env0 && epi_env && n_sd <= 4;
+  for (int i = 0; i < n_sd && epi_fused; ++i) epi_fused = subs[i]->KBG != nullptr;
+  EpiArgs epi{};
   for (int i = 0; i < n_sd; ++i) {
     Sub& d = *subs[i];
     for (const XferMap& m : d.maps) {
@@ -1213,7 +1220,22 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
       } else if (rom_pre) {
         L.pre = 1;
       }
-      if (d.use_tc) {
+      if (d.use_tc && epi_fused) {  // the update GEMM only; its epilogue runs with K3 below
+        const int S = launch_rom_update_gemm_tc(L, d.Z, d.part, rs, launches);
+        if (rs != st) CK(cudaEventRecord(G.join_ev[set + i], rs));
+        EpiSub& es = epi.s[epi.n_sd++];
+        es.part = d.part;
+        es.S = S;
+        es.r = d.r;
+        es.rz = d.r + d.r_b + d.nf;
+        es.Z = d.Z;
+        es.e = d.e;
+        es.ah0 = L.ah0;
+        es.vh0 = L.vh0;
+        es.uh1 = L.uh1;
+        es.vh1 = L.vh1;
+        es.ah1 = L.ah1;
+      } else if (d.use_tc) {
         launch_rom_advance_tc(L, d.KB, d.Z, d.part, rs, launches);
         if (rs != st) CK(cudaEventRecord(G.join_ev[set + i], rs));
         if (!d.fold)  // in a folded group no map reads a lift
@@ -1229,6 +1251,16 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
     }
   }
   for (int i : joins) CK(cudaStreamWaitEvent(st, G.join_ev[i], 0));  // every FOM advance before the test
+  if (epi_fused) {
+    epi.B = B;
+    epi.dt = cfg.dt;
+    epi.with_norm = first ? 0 : 1;
+    epi.min_iters = cfg.min_iters;
+    epi.tol_rel = cfg.tol_rel;
+    epi.tol_abs = cfg.tol_abs;
+    *launches += launch_rom_epi_finalize(epi, ctl, st);
+    return OSAM_OK;
+  }
   *launches += launch_finalize(ctl, G.partial, G.n_slots, B, cfg.min_iters, cfg.tol_rel, cfg.tol_abs, st);
   return OSAM_OK;
 }

@@ -440,5 +440,25 @@ cudaError_t launch_rom_persistent(const RomPArgs& A, cudaStream_t s);
 // Returns the number of kernels launched (1 for a single sample: K3 and the flag update fused).
 int launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int min_iters, double tol_rel,
                     double tol_abs, cudaStream_t s);
+// Groups of explicit batched tensor-core ROMs on the folded update (c5): the update GEMMs' epilogues (a^' from
+// the split-K partials, v^', u^' = u~, the norm terms) and K3 in one launch, one block per sample; then the
+// controller update.  Returns the launches.
+struct EpiSub {
+  const double* part;  // split-K partials of [-Kbar | Bbar G] [u~; u^_src]: part[z][i + r b]
+  int S, r, rz;
+  const double* Z;     // u~ in Z[0:r, b]
+  const double *e, *ah0, *vh0;
+  double *uh1, *vh1, *ah1;
+};
+struct EpiArgs {
+  int n_sd, B;
+  EpiSub s[4];
+  double dt;
+  int with_norm, min_iters;
+  double tol_rel, tol_abs;
+};
+int launch_rom_epi_finalize(const EpiArgs& A, Ctl c, cudaStream_t s);
+// the folded update GEMM alone (no epilogue); returns its number of K splits
+int launch_rom_update_gemm_tc(const RomLaunch& L, double* Z, double* part, cudaStream_t s, int* launches);
 
 }  // namespace osam

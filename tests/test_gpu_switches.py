@@ -72,7 +72,8 @@ print("ok", worst, worst2)
 '''
 
 
-@pytest.mark.parametrize("env", [{}, {"OSAM_NO_FOLD": "1"}, {"OSAM_ROM_PAR": "0"}, {"OSAM_ROM_KBG": "0"}])
+@pytest.mark.parametrize("env", [{}, {"OSAM_NO_FOLD": "1"}, {"OSAM_ROM_PAR": "0"}, {"OSAM_ROM_KBG": "0"},
+                                 {"OSAM_EPI_FUSED": "0"}])
 def test_rom_exchange_switches_keep_parity(gpu, env):
     """c2 (FOM-ROM, B = 1: the FOM exchange folded into the ROM update by default) and c5 (batched ROM-ROM: the
     predictor once per step, parallel ROM branches, [-Kbar | Bbar G] by default) against the oracle, with every
