@@ -232,24 +232,33 @@ constexpr int NL_UNROLL = OSAM_NL_UNROLL;  // NL1: unroll of the Gauss-point loo
 
 
 // Small subdomains (K1S): the TMA-streamed tiled kernel pays a load round trip per z-plane inside each
-// CTA, which dominates for boxes of a few thousand nodes (c1, c2).  Here every node is one group of 4
-// lanes (lane sub = 0, 1, 2 gathers the plane oz = sub - 1 with the class-table stencil, the partial
-// forces are summed in the order sub = 0, 1, 2), all planes at once; the field is L2-resident.
-constexpr int GB = 256;
+// CTA, which dominates for boxes of a few thousand nodes (c1, c2).  Here every node gathers its three planes
+// at once (class-table stencil) from the L2-resident field.
+// Groups of 32 nodes, 3 warps each: warp 3 g + o gathers the plane oz = o - 1 for group g's 32 nodes, so the lanes
+// of a warp read the same coefficient offsets (one class-table address per load for a warp of interior nodes
+// instead of up to 24 with 4 lanes per node); the three plane contributions meet in shared memory and the group's
+// first warp sums them in the order (oz = -1 + oz = 0) + oz = +1 -- every force component is the same FMA chain as
+// with 4 lanes per node, bitwise (and as small_resident_kernel's).  2 groups = 64 nodes per block (measured: c2 18.3k /
+// 21.2k / 19.6k steps/s with 1 / 2 / 4 groups; the persistent small controller 11.1k / 17.4k / 19.4k).
+constexpr int GGRP = 2;
+constexpr int GB = 96 * GGRP;
+constexpr int GNODES = 32 * GGRP;
 __device__ __forceinline__ void gather_body(const FomLaunch& L, int blk) {
+  __shared__ double sf[GGRP][3][3][32];
   const Geom& g = L.g;
   const long long np = g.npad;
   const long long n = (long long)g.nn[0] * g.nn[1] * g.nn[2];
-  const long long t = (blk * (long long)GB + threadIdx.x) >> 2;
-  const int sub = threadIdx.x & 3;
+  const int lane = threadIdx.x & 31, wz = threadIdx.x >> 5;
+  const int grp = wz / 3, o = wz % 3;
+  const long long t = (long long)blk * GNODES + grp * 32 + lane;
   const bool valid = t < n;
   const int i = valid ? (int)(t % g.nn[0]) : 0;
   const int j = valid ? (int)((t / g.nn[0]) % g.nn[1]) : 0;
   const int k = valid ? (int)(t / ((long long)g.nn[0] * g.nn[1])) : 0;
   const int cx = axis_class(i, g.nn[0]), cy = axis_class(j, g.nn[1]), cz = axis_class(k, g.nn[2]);
   double f[3] = {0.0, 0.0, 0.0};
-  const int oz = sub - 1;
-  if (valid && sub < 3 && k + oz >= 0 && k + oz <= g.nn[2] - 1) {
+  const int oz = o - 1;
+  if (valid && k + oz >= 0 && k + oz <= g.nn[2] - 1) {
     const double* coef = L.coef + (size_t)(cx + 3 * (cy + 3 * cz)) * 27 * 9;
 #pragma unroll
     for (int oy = -1; oy <= 1; ++oy) {
@@ -268,11 +277,12 @@ __device__ __forceinline__ void gather_body(const FomLaunch& L, int blk) {
     }
   }
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    const double f1 = __shfl_down_sync(0xffffffffu, f[c], 1, 4);
-    const double f2 = __shfl_down_sync(0xffffffffu, f[c], 2, 4);
-    f[c] = (f[c] + f1) + f2;
-  }
+  for (int c = 0; c < 3; ++c) sf[grp][o][c][lane] = f[c];
+  __syncthreads();
+  if (o == 0)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) f[c] = (sf[grp][0][c][lane] + sf[grp][1][c][lane]) + sf[grp][2][c][lane];
+  const int sub = o;  // the group's first warp finishes its nodes
   double num = 0.0, den = 0.0;
   if (valid && sub == 0) {
     const long long id = gidx(g, i, j, k);
@@ -858,7 +868,7 @@ int nl_ctas(const Geom& g) {
 }  // namespace
 
 int fom_partial_slots(const Geom& g, const Faces& f) {
-  if (small_fom(g)) return (int)cdiv(4LL * g.nn[0] * g.nn[1] * g.nn[2], GB);
+  if (small_fom(g)) return (int)cdiv((long long)g.nn[0] * g.nn[1] * g.nn[2], GNODES);
   return k1_shape(g, f) ? k1b::partial_slots(g, f) : k1a::partial_slots(g, f);
 }
 
@@ -1368,7 +1378,7 @@ void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUt
     return;
   }
   if (small_fom(L.g)) {  // K1S: one gather pass over every node
-    launch_k(fom_gather_kernel, dim3(cdiv(4LL * L.g.nn[0] * L.g.nn[1] * L.g.nn[2], GB)), dim3(GB), 0, s, L);
+    launch_k(fom_gather_kernel, dim3(cdiv((long long)L.g.nn[0] * L.g.nn[1] * L.g.nn[2], GNODES)), dim3(GB), 0, s, L);
     debug_check("fom_gather_kernel", s);
     ++*launches;
     return;
