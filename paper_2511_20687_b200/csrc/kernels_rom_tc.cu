@@ -54,20 +54,67 @@ __global__ void __launch_bounds__(128) dmma_gemm_kernel(const GemmArgs g) {
   const int m0 = blockIdx.x * TM, n0 = blockIdx.y * TN, k0 = blockIdx.z * g.kc;
   const int kn = min(g.kc, g.K - k0);
   // A is an operator fixed at bind ([-Kbar | Bbar], the folded G, Phi_dS^T, Phi_lift): staged before waiting for
-  // the predecessors (programmatic dependent launch); B is this sweep's data
-  for (int q = t; q < g.kc * TM; q += 128) {
-    const int kk = q / TM, mm = q % TM;
-    const int m = m0 + mm;
-    As[kk][mm] = (m < g.M && kk < kn) ? g.A[m * g.sam + (k0 + kk) * g.sak] : 0.0;
+  // the predecessors (programmatic dependent launch); B is this sweep's data.  Each thread first loads all its
+  // elements into registers (every load in flight at once; a load-then-store loop is a chain of L2 round trips),
+  // consecutive threads along the operand's contiguous dimension, then stores them to shared memory.
+  constexpr int PT = KMAX * TM / 128;
+  static_assert(KMAX * TN / 128 == PT, "tile shapes");
+  const bool a_mfast = g.sam == 1 || g.sak != 1;  // A contiguous in m (else in k)
+  const bool b_kfast = g.sbk == 1 || g.sbn != 1;  // B contiguous in k (else in n)
+  auto split = [&](int q, bool first_fast, int w, int& kk, int& x) {  // q -> (kk, m or n)
+    if (first_fast) {
+      kk = q / w;
+      x = q - kk * w;
+    } else {
+      x = q / g.kc;
+      kk = q - x * g.kc;
+    }
+  };
+  double va[PT];
+#pragma unroll
+  for (int u = 0; u < PT; ++u) {
+    const int q = t + 128 * u;
+    double v = 0.0;
+    if (q < g.kc * TM) {
+      int kk, mm;
+      split(q, a_mfast, TM, kk, mm);
+      const int m = m0 + mm;
+      if (m < g.M && kk < kn) v = g.A[m * g.sam + (k0 + kk) * g.sak];
+    }
+    va[u] = v;
+  }
+#pragma unroll
+  for (int u = 0; u < PT; ++u) {
+    const int q = t + 128 * u;
+    if (q < g.kc * TM) {
+      int kk, mm;
+      split(q, a_mfast, TM, kk, mm);
+      As[kk][mm] = va[u];
+    }
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  for (int q = t; q < g.kc * TN; q += 128) {
-    const int kk = q / TN, nn = q % TN;
-    const int n = n0 + nn;
-    const int k = k0 + kk;
-    Bs[kk][nn] = (n < g.N && kk < kn)
-                     ? ((g.B2 && k >= g.kb) ? g.B2[(k - g.kb) * g.sbk2 + n * g.sbn2] : g.B[k * g.sbk + n * g.sbn])
-                     : 0.0;
+#pragma unroll
+  for (int u = 0; u < PT; ++u) {
+    const int q = t + 128 * u;
+    double v = 0.0;
+    if (q < g.kc * TN) {
+      int kk, nn;
+      split(q, !b_kfast, TN, kk, nn);
+      const int n = n0 + nn;
+      const int k = k0 + kk;
+      if (n < g.N && kk < kn)
+        v = (g.B2 && k >= g.kb) ? g.B2[(k - g.kb) * g.sbk2 + n * g.sbn2] : g.B[k * g.sbk + n * g.sbn];
+    }
+    va[u] = v;
+  }
+#pragma unroll
+  for (int u = 0; u < PT; ++u) {
+    const int q = t + 128 * u;
+    if (q < g.kc * TN) {
+      int kk, nn;
+      split(q, !b_kfast, TN, kk, nn);
+      Bs[kk][nn] = va[u];
+    }
   }
   __syncthreads();
   const int wm = (warp & 1) * 16, wn = (warp >> 1) * 16;  // warp sub-tile

@@ -98,60 +98,92 @@ __global__ void step_begin_kernel(Ctl c, int B) {
 
 // after finalize (single thread): n_dev += 1, flags[0] = any sample active, per-step iteration
 // counts, max_iters flag, and (graph mode) the condition of the sweep while-loop
-__device__ __forceinline__ void any_active_body(const Ctl& c, int B) {
-  const int n = *c.n_dev + 1;
-  *c.n_dev = n;
-  if (c.stamps) {  // K1 timeline of this sweep (every K1 of the sweep joined before K3)
-    unsigned long long s[8], e[8];
-    int m = 0;
-    for (int i = 0; i < c.n_stamp && m < 8; ++i) {
-      const unsigned long long a = c.stamps[2 * i], b = c.stamps[2 * i + 1];
-      c.stamps[2 * i] = ~0ULL;
-      c.stamps[2 * i + 1] = 0ULL;
-      if (a == ~0ULL || b < a) continue;  // no K1 of subdomain i in this sweep
-      int q = m++;
-      for (; q > 0 && s[q - 1] > a; --q) {  // insertion sort by start
-        s[q] = s[q - 1];
-        e[q] = e[q - 1];
-      }
-      s[q] = a;
-      e[q] = b;
-    }
-    double uni = 0.0, sum = 0.0;
-    unsigned long long lo = 0, hi = 0;
-    for (int q = 0; q < m; ++q) {
-      sum += (double)(e[q] - s[q]);
-      if (q == 0 || s[q] > hi) {
-        if (q > 0) uni += (double)(hi - lo);
-        lo = s[q];
-        hi = e[q];
-      } else if (e[q] > hi) {
-        hi = e[q];
-      }
-    }
-    if (m > 0) uni += (double)(hi - lo);
-    c.busy[0] += uni;
-    c.busy[1] += sum;
-    c.busy[2] += m;
-    c.busy[3] += 1.0;
-    c.busy[4] += n >= 2 ? 1.0 : 0.0;
-  }
-  int a = 0;
-  for (int b = 0; b < B; ++b) a |= c.active[b];
+__device__ __forceinline__ void any_active_finish(const Ctl& c, int n, int a) {
   c.flags[0] = a;
-  if (c.iters_all) {
-    const long long k = *c.step_dev - 1;
-    for (int b = 0; b < B; ++b) c.iters_all[k * B + b] = c.iters[b];
-  }
   const bool more = a && n < c.max_iters && !c.flags[1];
   if (a && n >= c.max_iters) c.sticky[1] = 1;
   if (c.has_cond) cudaGraphSetConditional(c.cond, more ? 1u : 0u);
 }
 
+__device__ void any_active_stamps(const Ctl& c, int n);
 
+// thread 0 of any_active_kernel after the block has folded the samples: n_dev, the K1 timeline, flags
+__device__ __forceinline__ void any_active_tail(const Ctl& c, int a) {
+  const int n = *c.n_dev + 1;
+  *c.n_dev = n;
+  if (c.stamps) any_active_stamps(c, n);
+  any_active_finish(c, n, a);
+}
+
+__device__ __forceinline__ void any_active_body(const Ctl& c, int B) {
+  const int n = *c.n_dev + 1;
+  *c.n_dev = n;
+  if (c.stamps) any_active_stamps(c, n);
+  int a = 0;
+  for (int b = 0; b < B; ++b) a |= c.active[b];
+  if (c.iters_all) {
+    const long long k = *c.step_dev - 1;
+    for (int b = 0; b < B; ++b) c.iters_all[k * B + b] = c.iters[b];
+  }
+  any_active_finish(c, n, a);
+}
+// K1 timeline of the sweep that just ran (every K1 of the sweep joined before K3): union, sum and count of the
+// subdomains' K1 intervals into busy[], stamps reset
+__device__ void any_active_stamps(const Ctl& c, int n) {
+  unsigned long long s[8], e[8];
+  int m = 0;
+  for (int i = 0; i < c.n_stamp && m < 8; ++i) {
+    const unsigned long long a = c.stamps[2 * i], b = c.stamps[2 * i + 1];
+    c.stamps[2 * i] = ~0ULL;
+    c.stamps[2 * i + 1] = 0ULL;
+    if (a == ~0ULL || b < a) continue;  // no K1 of subdomain i in this sweep
+    int q = m++;
+    for (; q > 0 && s[q - 1] > a; --q) {  // insertion sort by start
+      s[q] = s[q - 1];
+      e[q] = e[q - 1];
+    }
+    s[q] = a;
+    e[q] = b;
+  }
+  double uni = 0.0, sum = 0.0;
+  unsigned long long lo = 0, hi = 0;
+  for (int q = 0; q < m; ++q) {
+    sum += (double)(e[q] - s[q]);
+    if (q == 0 || s[q] > hi) {
+      if (q > 0) uni += (double)(hi - lo);
+      lo = s[q];
+      hi = e[q];
+    } else if (e[q] > hi) {
+      hi = e[q];
+    }
+  }
+  if (m > 0) uni += (double)(hi - lo);
+  c.busy[0] += uni;
+  c.busy[1] += sum;
+  c.busy[2] += m;
+  c.busy[3] += 1.0;
+  c.busy[4] += n >= 2 ? 1.0 : 0.0;
+}
+
+
+
+// B > 1: the per-sample parts of any_active_body spread over the block (a single thread walking B samples is a
+// chain of L2 round trips: 9 us for c5's 64), then thread 0 finishes
 __global__ void any_active_kernel(Ctl c, int B) {
   pdl_enter();
-  any_active_body(c, B);
+  __shared__ int any;
+  const int t = threadIdx.x;
+  if (t == 0) any = 0;
+  __syncthreads();
+  int a = 0;
+  for (int b = t; b < B; b += blockDim.x) a |= c.active[b];
+  if (a) any = 1;  // benign: every writer stores 1
+  if (c.iters_all) {
+    const long long k = *c.step_dev - 1;
+    for (int b = t; b < B; b += blockDim.x) c.iters_all[k * B + b] = c.iters[b];
+  }
+  __syncthreads();
+  if (t == 0) any_active_tail(c, any);
 }
 
 // one block of FIN_T threads per sample; the sweep that just ran is iteration n = *n_dev + 1.  fused
@@ -874,7 +906,7 @@ __global__ void __launch_bounds__(EF_T) rom_epi_finalize_kernel(const EpiArgs A,
 int launch_rom_epi_finalize(const EpiArgs& A, Ctl c, cudaStream_t s) {
   launch_k(rom_epi_finalize_kernel, dim3(A.B), dim3(EF_T), 0, s, A, c);
   debug_check("rom_epi_finalize_kernel", s);
-  launch_k(any_active_kernel, dim3(1), dim3(1), 0, s, c, A.B);
+  launch_k(any_active_kernel, dim3(1), dim3(std::min(1024, (A.B + 31) / 32 * 32)), 0, s, c, A.B);
   debug_check("any_active_kernel", s);
   return 2;
 }
@@ -889,7 +921,7 @@ int launch_finalize(Ctl c, const double2* partial, int n_slots, int B, int min_i
            B == 1 ? 1 : 0);
   debug_check("finalize_kernel", s);
   if (B == 1) return 1;
-  launch_k(any_active_kernel, dim3(1), dim3(1), 0, s, c, B);
+  launch_k(any_active_kernel, dim3(1), dim3(std::min(1024, (B + 31) / 32 * 32)), 0, s, c, B);
   debug_check("any_active_kernel", s);
   return 2;
 }
