@@ -983,8 +983,10 @@ __device__ __forceinline__ void res_step_begin(const Ctl& C, int step) {
 // in-range test of a neighbour offset o in {-1, 0, 1} for a node of axis class c (0 low face, 2 high face)
 __device__ __forceinline__ bool res_in(int c, int o) { return !((c == 0 && o < 0) || (c == 2 && o > 0)); }
 
+constexpr int RGRP = RB / 96;  // node groups of 3 warps per pass (5: 160 nodes; the 16th warp idles)
 __global__ void __launch_bounds__(RB, 1) small_resident_kernel(const __grid_constant__ SmallArgs A) {
   extern __shared__ __align__(16) double rsm[];
+  __shared__ double sfr[RGRP][3][3][32];  // the planes' forces of a pass (11.5 KB static)
   cg::cluster_group cl = cg::this_cluster();
   const int NC = (int)cl.num_blocks(), rank = (int)cl.block_rank();
   const int tid = threadIdx.x;
@@ -1115,13 +1117,16 @@ __global__ void __launch_bounds__(RB, 1) small_resident_kernel(const __grid_cons
         if (nm) __syncthreads();
       }
       RES_T(0);
-      // K1S on this CTA's nodes of every subdomain: 4 lanes per node (oz = sub - 1), gather_body's arithmetic
+      // K1S on this CTA's nodes of every subdomain, gather_body's arithmetic and layout: groups of 32 nodes, warp
+      // 3 g + o gathers the plane oz = o - 1 of group g (one class-table offset per warp), the planes meet in
+      // shared memory and the group's first warp sums them in the order (-1 + 0) + 1 and finishes
       double num = 0.0, den = 0.0;
-      for (int u0 = 0; u0 < nslot; u0 += RB / 4) {
-        const int u = u0 + (tid >> 2), sub = tid & 3;
+      const int lane = tid & 31, grp = (tid >> 5) / 3, o = (tid >> 5) % 3;
+      for (int u0 = 0; u0 < nslot; u0 += RGRP * 32) {
+        const int u = u0 + grp * 32 + lane;
         int i = 0;
         while (i + 1 < A.n_sd && u >= cum[i + 1]) ++i;
-        const int2 mt = u < nslot ? meta[u] : make_int2(-1, 0);
+        const int2 mt = (grp < RGRP && u < nslot) ? meta[u] : make_int2(-1, 0);
         const bool valid = mt.x >= 0;
         const int cls = mt.y & 31, cx = cls % 3, cy = (cls / 3) % 3, cz = cls / 9;
         const SmallSub& d = A.s[i];
@@ -1129,8 +1134,8 @@ __global__ void __launch_bounds__(RB, 1) small_resident_kernel(const __grid_cons
         const double* X = Xc + xoff[i];
         const int np = (int)g.npad, px = g.px, pl = (int)g.plane;
         double f[3] = {0.0, 0.0, 0.0};
-        const int oz = sub - 1;
-        if (valid && sub < 3 && res_in(cz, oz)) {
+        const int oz = o - 1;
+        if (valid && res_in(cz, oz)) {
           const double* coef = coefp[i] + (size_t)cls * 27 * 9;
 #pragma unroll
           for (int oy = -1; oy <= 1; ++oy) {
@@ -1148,12 +1153,14 @@ __global__ void __launch_bounds__(RB, 1) small_resident_kernel(const __grid_cons
             }
           }
         }
+        if (grp < RGRP)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          const double f1 = __shfl_down_sync(0xffffffffu, f[c], 1, 4);
-          const double f2 = __shfl_down_sync(0xffffffffu, f[c], 2, 4);
-          f[c] = (f[c] + f1) + f2;
-        }
+          for (int c = 0; c < 3; ++c) sfr[grp][o][c][lane] = f[c];
+        __syncthreads();
+        if (grp < RGRP && o == 0)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) f[c] = (sfr[grp][0][c][lane] + sfr[grp][1][c][lane]) + sfr[grp][2][c][lane];
+        const int sub = o;
         if (valid && sub == 0) {
           const unsigned fm = (unsigned)(mt.y >> 5) & 7u;
           const FomLaunch& L = d.L;
@@ -1180,6 +1187,7 @@ __global__ void __launch_bounds__(RB, 1) small_resident_kernel(const __grid_cons
             W[(9 + c) * ch + l] = qn;
           }
         }
+        __syncthreads();  // sfr is reused by the next pass
       }
       RES_T(1);
       // the CTA's (num, den), then the cluster's, summed by the same butterfly in every CTA (the same decision
@@ -1287,7 +1295,7 @@ __global__ void __launch_bounds__(RB, 1) small_resident_kernel(const __grid_cons
 cudaError_t launch_small_resident(const SmallArgs& A, cudaStream_t s) {
   if (getenv("OSAM_SMALL_RESIDENT") && getenv("OSAM_SMALL_RESIDENT")[0] == '0') return cudaErrorNotSupported;
   static int cl_max = -1;
-  constexpr int SMEM_MAX = 227 * 1024;
+  constexpr int SMEM_MAX = 227 * 1024 - (int)sizeof(double) * RGRP * 9 * 32;  // dynamic; the pass buffer is static
   if (cl_max < 0) {
     cl_max = 0;
     if (cudaFuncSetAttribute(small_resident_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
