@@ -440,6 +440,9 @@ __device__ __noinline__ void xface_body(const FomLaunch& L, int side_mask, int b
 #ifndef OSAM_MINB
 #define OSAM_MINB 4
 #endif
+#ifndef K1_MINB
+#define K1_MINB OSAM_MINB
+#endif
 
 #ifndef OSAM_K1_ROT
 // 0 (default): one copy of k1_iter per plane, the accumulator roles moved through the slots (9 moves per
@@ -448,7 +451,7 @@ __device__ __noinline__ void xface_body(const FomLaunch& L, int side_mask, int b
 #define OSAM_K1_ROT 0
 #endif
 template <bool ZN>
-__global__ void __launch_bounds__(NT, OSAM_MINB)
+__global__ void __launch_bounds__(NT, K1_MINB)
     fom_tiled_kernel(const __grid_constant__ FomLaunch L, const __grid_constant__ InteriorStencil S,
                      const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
                      const __grid_constant__ CUtensorMap tmwp) {
@@ -674,3 +677,4 @@ int make_tmap(const Geom& g, double* array, bool halo, CUtensorMap* out) {
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : (int)r;
 }
+#undef K1_MINB

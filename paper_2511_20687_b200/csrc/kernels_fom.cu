@@ -206,6 +206,19 @@ namespace k1b {
 #undef K1_TY
 #undef K1_ZC
 }  // namespace k1b
+#ifndef OSAM_ZC_C
+#define OSAM_ZC_C 24
+#endif
+namespace k1c {  // 48 x 2: three warps per tile, 5 CTAs per SM; long TMA rows (416-byte X, 384-byte W)
+#define K1_TX 48
+#define K1_TY 2
+#define K1_ZC OSAM_ZC_C
+#define K1_MINB 5
+#include "k1_tiled.cuh"
+#undef K1_TX
+#undef K1_TY
+#undef K1_ZC
+}  // namespace k1c
 
 // Tile shape of a subdomain's K1 (0: k1a, 1: k1b): the fraction of lanes that own a node, over x (the
 // tile columns, the excluded last column not counted) and y; k1b only when it is clearly better (it
@@ -214,13 +227,18 @@ namespace k1b {
 // launch, so the shape, the descriptors and the partial-slot counts always agree.
 static int k1_shape_choice(const Geom& g, const Faces& f) {
   const char* e = getenv("OSAM_K1_SHAPE");
-  if (e && (e[0] == '0' || e[0] == '1')) return e[0] - '0';
+  if (e && (e[0] == '0' || e[0] == '1' || e[0] == '2')) return e[0] - '0';
   auto occ = [&](int tx, int ty, int cols, bool xl) {
     const double nx = (double)(xl ? g.nn[0] - 1 : g.nn[0]);
     return nx / ((double)cols * tx) * (double)g.nn[1] / ((double)((g.nn[1] + ty - 1) / ty) * ty);
   };
   const double a = occ(k1a::TX, k1a::TY, k1a::tile_cols(g, f), k1a::xlast_excluded(g, f));
   const double b = occ(k1b::TX, k1b::TY, k1b::tile_cols(g, f), k1b::xlast_excluded(g, f));
+  const double c = occ(k1c::TX, k1c::TY, k1c::tile_cols(g, f), k1c::xlast_excluded(g, f));
+  // 48 x 2 for a box whose x extent it fits clearly better (opt-in: on c3's Omega1 the launch alone is 2.5% faster,
+  // the concurrent step with Omega2's 16 x 8 CTAs 1.3% slower, profiles/r3_k1_experiments.md)
+  static const bool use_c = getenv("OSAM_K1_C") && getenv("OSAM_K1_C")[0] == '1';
+  if (use_c && c > 1.03 * a && c >= b) return 2;
   return b > 1.03 * a ? 1 : 0;
 }
 int k1_shape(const Geom&, const Faces& f) { return f.shape; }
@@ -869,7 +887,11 @@ int nl_ctas(const Geom& g) {
 
 int fom_partial_slots(const Geom& g, const Faces& f) {
   if (small_fom(g)) return (int)cdiv((long long)g.nn[0] * g.nn[1] * g.nn[2], GNODES);
-  return k1_shape(g, f) ? k1b::partial_slots(g, f) : k1a::partial_slots(g, f);
+  switch (k1_shape(g, f)) {
+    case 1: return k1b::partial_slots(g, f);
+    case 2: return k1c::partial_slots(g, f);
+    default: return k1a::partial_slots(g, f);
+  }
 }
 
 int fom_nl_partial_slots(const Geom& g) { return nl_ctas(g); }
@@ -1372,7 +1394,9 @@ void launch_fom_advance_nl(const FomLaunch& L, cudaStream_t s, int* launches) {
 
 void launch_fom_xlast(const FomLaunch& L, cudaStream_t s, int* launches) {
   if (L.material != OSAM_LINEAR || small_fom(L.g)) return;
-  if (!(k1_shape(L.g, L.f) ? k1b::xlast_excluded(L.g, L.f) : k1a::xlast_excluded(L.g, L.f))) return;
+  const int sh = k1_shape(L.g, L.f);
+  if (!(sh == 1 ? k1b::xlast_excluded(L.g, L.f) : sh == 2 ? k1c::xlast_excluded(L.g, L.f) : k1a::xlast_excluded(L.g, L.f)))
+    return;
   xlast_copy_kernel<<<cdiv((long long)L.g.nn[1] * L.g.nn[2], 128 * XL_PER), 128, 0, s>>>(L);
   debug_check("xlast_copy_kernel", s);
   ++*launches;
@@ -1391,16 +1415,21 @@ void launch_fom_advance(const FomLaunch& L, const InteriorStencil& st, const CUt
     ++*launches;
     return;
   }
-  if (k1_shape(L.g, L.f))
-    k1b::launch_tiled(L, st, tmx, tmw, tmwp, s);
-  else
-    k1a::launch_tiled(L, st, tmx, tmw, tmwp, s);
+  switch (k1_shape(L.g, L.f)) {
+    case 1: k1b::launch_tiled(L, st, tmx, tmw, tmwp, s); break;
+    case 2: k1c::launch_tiled(L, st, tmx, tmw, tmwp, s); break;
+    default: k1a::launch_tiled(L, st, tmx, tmw, tmwp, s);
+  }
   ++*launches;
   if (with_xlast) launch_fom_xlast(L, s, launches);
 }
 
 int make_field_tmap(const Geom& g, const Faces& f, double* array, bool halo, CUtensorMap* out) {
-  return k1_shape(g, f) ? k1b::make_tmap(g, array, halo, out) : k1a::make_tmap(g, array, halo, out);
+  switch (k1_shape(g, f)) {
+    case 1: return k1b::make_tmap(g, array, halo, out);
+    case 2: return k1c::make_tmap(g, array, halo, out);
+    default: return k1a::make_tmap(g, array, halo, out);
+  }
 }
 
 void launch_fom_pack(const Geom& g, const double* src, double* dst, long long n, cudaStream_t s) {

@@ -1,5 +1,5 @@
-"""Both tile shapes of the tiled K1 (kernels_fom.cu k1_shape: k1a 32 x 4, a warp per x-row; k1b 16 x 8, a
-warp per two 16-node rows, picked for x-ragged boxes such as c3's) on the tiled-K1 parity cases of
+"""The tile shapes of the tiled K1 (kernels_fom.cu k1_shape: k1a 32 x 4, a warp per x-row; k1b 16 x 8, a
+warp per two 16-node rows, picked for x-ragged boxes such as c3's; k1c 48 x 2, three warps over two rows) on the tiled-K1 parity cases of
 tests/test_gpu_parity.py, each forced with OSAM_K1_SHAPE: against the oracle, and bitwise between the
 controllers."""
 import pytest
@@ -13,14 +13,14 @@ from test_gpu_parity import (  # noqa: F401  (re-collected here under both shape
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["k1a", "k1b"])
+@pytest.fixture(autouse=True, params=["k1a", "k1b", "k1c"])
 def k1_shape(monkeypatch, request):
     monkeypatch.setenv("OSAM_GATHER_MAX", "0")          # the tiled K1 at every size
-    monkeypatch.setenv("OSAM_K1_SHAPE", "0" if request.param == "k1a" else "1")
+    monkeypatch.setenv("OSAM_K1_SHAPE", {"k1a": "0", "k1b": "1", "k1c": "2"}[request.param])
 
 
 @pytest.mark.timeout(300, method="thread")
-@pytest.mark.parametrize("created,stepped", [("1", "0"), ("0", "1")])
+@pytest.mark.parametrize("created,stepped", [("1", "0"), ("0", "1"), ("2", "1")])
 def test_tmaps_follow_the_shape_at_bind(gpu, monkeypatch, created, stepped):
     """The TMA boxes follow the tile shape, which is fixed only at bind (it depends on the Schwarz faces):
     subdomains created (and given their IC) under one shape and stepped under the other still match the
