@@ -268,6 +268,130 @@ __device__ __forceinline__ bool needs_prev(const FomLaunch& L, const TileGeo& P)
   return false;
 }
 
+// ---- the transfer in the K1 grid -------------------------------------------------
+// Tile columns whose staged X box [bx TX - 2, bx TX + TX + 1] holds a node of a Schwarz x-face: lo columns at
+// x = 0 (only column 0: column 1 starts at TX - 2 > 0), hi columns at x = nx.  These tiles are dispatched last and
+// wait for the transfer CTAs; every other tile reads no Schwarz value.
+__host__ __device__ __forceinline__ void wait_cols(const Geom& g, const Faces& f, int tx, int& lo, int& hi) {
+  const int nx = g.nn[0] - 1;
+  lo = f.sw[0] ? 1 : 0;
+  hi = 0;
+  if (f.sw[1])
+    for (int bx = tx - 1; bx >= lo && bx * TX + TX + 1 >= nx; --bx) ++hi;
+  if (lo > tx) lo = tx;
+}
+
+// rank r of a tile CTA (dispatch order) -> natural tile index bx + tx (by + ty bz): the tx - lo - hi middle
+// columns first, then the waiting columns
+__device__ __forceinline__ int tile_of_rank(const TileGrid& G, int lo, int hi, int r) {
+  const int mid = G.tx - lo - hi;
+  const int nmid = mid * G.ty * G.tz;
+  if (r < nmid) {
+    const int rest = r / mid;
+    return lo + (r - rest * mid) + G.tx * rest;
+  }
+  r -= nmid;
+  const int w = lo + hi;
+  const int rest = r / w, col = r - rest * w;
+  return (col < lo ? col : G.tx - hi + (col - lo)) + G.tx * rest;
+}
+
+// The transfer CTAs occupy K1-sized slots (shared memory, registers) while they wait on memory, so there are few of
+// them (at most XF_CTAS) and each thread loops over destination nodes, XF_U nodes per round: the map of the round's
+// nodes (out, idx, xi) in one round of loads, then their 24 XF_U source loads at once.
+constexpr int XF_CTAS = 48, XF_U = 2;
+__host__ __device__ __forceinline__ int xfer_ctas(const FomLaunch& L) {
+  long long n = 0;
+  for (int m = 0; m < L.n_xf; ++m) n += L.xf[m].n;
+  const long long c = (n + NT * XF_U - 1) / (NT * XF_U);
+  return (int)(c < XF_CTAS ? c : XF_CTAS);
+}
+
+// K2 of the maps into this subdomain, s[p, c] = sum_{b<8} w_pb src[c cs + idx_pb] into X at out[3p + c] (P:L475-487,
+// reading R11; the same arithmetic and order as transfer_kernel).  The sources' values it reads are fixed within the
+// controller step (no donor corner on a source Schwarz DOF, or a ROM lift formed once per step, R39), so it runs
+// beside the source's own K1.  Then the CTA signals xsync[0] (release).
+__device__ __noinline__ void xfer_body(const FomLaunch& L, int blk, int tid) {
+  const int n0 = L.xf[0].n;
+  const int ntot = n0 + (L.n_xf > 1 ? L.xf[1].n : 0);
+  const int stride = L.n_xf_ctas * NT;
+  double* dst = const_cast<double*>(L.x);
+  for (int t0 = blk * NT + tid; t0 < ntot; t0 += XF_U * stride) {
+    int o[XF_U][3], id[XF_U][8];
+    double xs[XF_U][3];
+    const double* sb[XF_U];
+    long long cs[XF_U];
+#pragma unroll
+    for (int u = 0; u < XF_U; ++u) {
+      const int t = t0 + u * stride;
+      const bool m0 = t < n0;
+      const int p = m0 ? t : t - n0;
+      o[u][0] = o[u][1] = o[u][2] = -1;
+      sb[u] = m0 ? L.xf[0].src : L.xf[1].src;
+      cs[u] = m0 ? L.xf[0].cs : L.xf[1].cs;
+      if (t < ntot) {
+        const int* out = (m0 ? L.xf[0].out : L.xf[1].out) + 3 * p;
+        const int4* ix = reinterpret_cast<const int4*>((m0 ? L.xf[0].idx : L.xf[1].idx) + 8 * p);
+        const double* xi = (m0 ? L.xf[0].xi : L.xf[1].xi) + 3 * p;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          o[u][c] = __ldg(out + c);
+          xs[u][c] = __ldg(xi + c);
+        }
+        const int4 ia = __ldg(ix), ib = __ldg(ix + 1);
+        id[u][0] = ia.x, id[u][1] = ia.y, id[u][2] = ia.z, id[u][3] = ia.w;
+        id[u][4] = ib.x, id[u][5] = ib.y, id[u][6] = ib.z, id[u][7] = ib.w;
+      }
+    }
+    double v[XF_U][3][8];
+#pragma unroll
+    for (int u = 0; u < XF_U; ++u)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[u][c][q] = o[u][c] >= 0 ? __ldg(sb[u] + c * cs[u] + id[u][q]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < XF_U; ++u)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double x = xs[u][0], y = xs[u][1], z = xs[u][2];
+        double a = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double w = ((q & 1) ? x : 1.0 - x) * ((q & 2) ? y : 1.0 - y) * ((q & 4) ? z : 1.0 - z);
+          a = fma(w, v[u][c][q], a);
+        }
+        if (o[u][c] >= 0) dst[o[u][c]] = a;
+      }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(L.xsync) : "memory");
+  }
+}
+
+// thread 0 of a waiting tile, before its first TMA issue: every transfer CTA of this launch is done (acquire; then
+// the generic-proxy stores are ordered before the TMA reads).  The last of the n_wait waiters resets the handshake
+// for the next launch.  A transfer CTA cannot be starved: CTAs are dispatched in index order and the transfer CTAs
+// come first.  200 ms without them means a broken GPU: trap instead of hanging.
+__device__ __noinline__ void xfer_wait(const FomLaunch& L, unsigned n_wait) {
+  const unsigned long long t0 = global_ns();
+  unsigned v;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(L.xsync) : "memory");
+    if (v >= (unsigned)L.n_xf_ctas) break;
+    if (global_ns() - t0 > 200000000ULL) __trap();
+    __nanosleep(128);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (atomicAdd(L.xsync + 1, 1u) == n_wait - 1) {
+    L.xsync[0] = 0u;
+    L.xsync[1] = 0u;
+  }
+}
+
 // stage layout: X plane (halo box) | W plane (tile box) | W'_prev plane (tile box)
 __device__ __forceinline__ void issue_plane(const TileGeo& P, bool wp, int it, int s, unsigned char* ring,
                                             unsigned long long* full, const Maps& M) {
@@ -460,8 +584,14 @@ __global__ void __launch_bounds__(NT, K1_MINB)
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + NRING * NSTAGE * STAGE_BYTES);
   unsigned long long* empty = full + NRING * NSTAGE;
   if (L.stamp && threadIdx.x + threadIdx.y == 0) atomicMin(L.stamp, global_ns());  // in-schedule timeline
-  if ((int)blockIdx.x >= L.n_tile_ctas) {  // x-face CTAs (after the tile CTAs)
-    xface_body(L, xface_sides(L.f), blockIdx.x - L.n_tile_ctas, threadIdx.x + TX * threadIdx.y, blockIdx.x);
+  if ((int)blockIdx.x < L.n_xf_ctas) {  // transfer CTAs (first)
+    xfer_body(L, blockIdx.x, threadIdx.x + TX * threadIdx.y);
+    if (L.stamp && threadIdx.x + threadIdx.y == 0) atomicMax(L.stamp + 1, global_ns());
+    return;
+  }
+  const int b = (int)blockIdx.x - L.n_xf_ctas;  // = the partial slot of a tile (natural order) or x-face CTA
+  if (b >= L.n_tile_ctas) {  // x-face CTAs (after the tile CTAs)
+    xface_body(L, xface_sides(L.f), b - L.n_tile_ctas, threadIdx.x + TX * threadIdx.y, b);
     if (L.stamp && threadIdx.x + threadIdx.y == 0) atomicMax(L.stamp + 1, global_ns());
     return;
   }
@@ -469,8 +599,16 @@ __global__ void __launch_bounds__(NT, K1_MINB)
   const int nx = g.nn[0] - 1, ny = g.nn[1] - 1;
   const Maps M{&tmx, &tmw, &tmwp};
   const TileGrid G = tile_grid(g, L.f);
-  // one CTA per tile (the grid's first n_tile_ctas CTAs)
-  const TileGeo P = tile_geo(g, G, blockIdx.x);
+  // one CTA per tile; with the transfer in the grid the tiles that stage a Schwarz node come last and wait
+  int t = b, wlo = 0, whi = 0;
+  bool waits = false;
+  if (L.n_xf_ctas) {
+    wait_cols(g, L.f, G.tx, wlo, whi);
+    t = tile_of_rank(G, wlo, whi, b);
+    const int bx = t % G.tx;
+    waits = bx < wlo || bx >= G.tx - whi;
+  }
+  const TileGeo P = tile_geo(g, G, t);
   Tile T;
   T.i = P.x0 + 2 + (int)threadIdx.x;
   T.j = P.y0 + 1 + (int)threadIdx.y;
@@ -487,6 +625,7 @@ __global__ void __launch_bounds__(NT, K1_MINB)
 
 #if OSAM_K1_WARP
   if (threadIdx.x + threadIdx.y == 0) {
+    if (waits) xfer_wait(L, (unsigned)((wlo + whi) * G.ty * G.tz));
     for (int s = 0; s < NRING * NSTAGE; ++s) mbar_init(&full[s], 1);
     mbar_fence_init();
   }
@@ -503,6 +642,7 @@ __global__ void __launch_bounds__(NT, K1_MINB)
   }
 #else
   if (threadIdx.x + threadIdx.y == 0) {
+    if (waits) xfer_wait(L, (unsigned)((wlo + whi) * G.ty * G.tz));
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NWARP);
@@ -537,7 +677,7 @@ __global__ void __launch_bounds__(NT, K1_MINB)
     }
   }
 #endif
-  block_partial<NT>(num, den, L.partial, blockIdx.x);
+  block_partial<NT>(num, den, L.partial, t);
   if (L.stamp && threadIdx.x + threadIdx.y == 0) atomicMax(L.stamp + 1, global_ns());
 }
 
@@ -647,7 +787,9 @@ void launch_tiled(const FomLaunch& L, const InteriorStencil& st, const CUtensorM
                   const CUtensorMap* tmwp, cudaStream_t s) {
   FomLaunch Lt = L;
   Lt.n_tile_ctas = tiled_ctas(L.g, L.f);
-  const int grid = Lt.n_tile_ctas + (int)xface_blocks(L.g, L.f);  // tile CTAs, then x-face CTAs
+  Lt.n_xf_ctas = L.n_xf > 0 ? xfer_ctas(L) : 0;
+  // transfer CTAs, tile CTAs, then x-face CTAs
+  const int grid = Lt.n_xf_ctas + Lt.n_tile_ctas + (int)xface_blocks(L.g, L.f);
   if (L.z_out)  // last substep of a multi-substep interval: z = u + dt v out, norm from z - z_prev (R33)
     fom_tiled_kernel<true><<<grid, dim3(TX, TY), SMEM_TILED, s>>>(Lt, st, *tmx, *tmw, *tmwp);
   else

@@ -896,6 +896,13 @@ int fom_partial_slots(const Geom& g, const Faces& f) {
 
 int fom_nl_partial_slots(const Geom& g) { return nl_ctas(g); }
 
+bool fom_ingrid_xfer_ok(const Geom& g, const Faces& f, int material) {
+  if (material != OSAM_LINEAR || small_fom(g) || g.nn[0] < 4) return false;
+  for (int q = 2; q < 6; ++q)
+    if (f.sw[q]) return false;
+  return f.sw[0] || f.sw[1];
+}
+
 bool fom_small(const Geom& g) { return small_fom(g); }
 void choose_fom_path(Geom& g, Faces& f) { choose_fom_path_impl(g, f); }
 

@@ -191,6 +191,7 @@ void release_maps(Sub& s) {
 void release_binding(Sub& s) {
   release_maps(s);
   dfree(s.scratch_partial);
+  dfree(s.xsync);
   dfree(s.Phi);
   dfree(s.Phi_s);
   dfree(s.Kbar);
@@ -420,6 +421,8 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
         inner *= std::max(0, s.g.nn[a] - 2 * (int)s.faces.sw[2 * a] - 2 * (int)s.faces.sw[2 * a + 1]);
       s.n_band = s.n_nodes - inner;
       TRY(dalloc(&s.scratch_partial, (size_t)fom_slots(s)));
+      TRY(dalloc(&s.xsync, 2));
+      CK(cudaMemset(s.xsync, 0, 2 * sizeof(unsigned)));
       if (const int r = encode_tmaps(s)) return fail(OSAM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", r);
       continue;
     }
@@ -729,6 +732,28 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
       for (auto& mm : subs[q]->maps)
         if (mm.src == i && mm.reads_src_schwarz) ok = false;
     d.pre1 = ok;
+  }
+  // The transfers into a FOM run as the first CTAs of its tiled K1 ("the transfer in the K1 grid")
+  // when every value they read is fixed within the controller step -- a FOM source's stencil input off its
+  // Schwarz DOFs (R30), a pre1 ROM source's lift (R39) -- and no map reads this FOM's Schwarz DOFs (which the
+  // in-grid transfer writes while other advances run).  Opt-in (OSAM_XFER_INGRID=1): measured slower than the
+  // separate launches (c3 903 vs 970 steps/s), so the default keeps those.
+  static const bool xin_env = getenv("OSAM_XFER_INGRID") && getenv("OSAM_XFER_INGRID")[0] == '1';
+  for (int i = 0; i < n; ++i) {
+    Sub& d = *subs[i];
+    d.xin = false;
+    if (!xin_env || any_sub || d.kind != OSAM_FOM || d.batch != 1 || d.maps.empty() ||
+        (int)d.maps.size() > FOM_XF_MAX || !fom_ingrid_xfer_ok(d.g, d.faces, d.material))
+      continue;
+    bool ok = true;
+    for (auto& mm : d.maps) {
+      const Sub& src = *subs[mm.src];
+      ok = ok && !mm.reads_src_schwarz && (src.kind == OSAM_FOM ? src.batch == 1 : src.pre1);
+    }
+    for (int q = 0; q < n && ok; ++q)
+      for (auto& mm : subs[q]->maps)
+        if (mm.src == i && mm.reads_src_schwarz) ok = false;
+    d.xin = ok;
   }
   for (auto& P : pend) {
     Sub& d = *subs[P.dst];
@@ -1078,8 +1103,13 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
   EpiArgs epi{};
   for (int i = 0; i < n_sd; ++i) {
     Sub& d = *subs[i];
+    // the transfers into d as the first CTAs of its K1 (bind: d.xin); in sweep 1 a later FOM source's iterate 0 is
+    // its checkpoint u, the buffer its own K1 overwrites concurrently: separate launches before that K1 forks
+    bool xin_now = d.xin;
+    for (const XferMap& m : d.maps)
+      if (first && m.src > i && subs[m.src]->kind == OSAM_FOM) xin_now = false;
     for (const XferMap& m : d.maps) {
-      if (d.fold || d.pre1) continue;  // folded exchange: inside the ROM advance; pre1: on its branch below
+      if (d.fold || d.pre1 || xin_now) continue;  // folded exchange: inside the ROM advance; pre1: on its branch below
       const Sub& src = *subs[m.src];
       const bool newest = (m.src < i) || !first;
       const double* field;
@@ -1113,6 +1143,27 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
       FomLaunch L = fom_launch(d, d.st[c][0], d.st[c][1], d.st[x][0], d.st[x][1], cfg.dt, cfg.dt,
                                0.5 * cfg.dt, cfg.dt, with_norm, G.partial + (size_t)slot * B, nullptr);
       L.stamp = G.stamps + 2 * i;  // in-schedule K1 timeline (tiled K1; folded by K3)
+      if (xin_now) {
+        for (size_t q = 0; q < d.maps.size(); ++q) {
+          const XferMap& m = d.maps[q];
+          const Sub& src = *subs[m.src];
+          const bool newest = (m.src < i) || !first;
+          XferPart& xp = L.xf[q];
+          xp.idx = m.idx;
+          xp.xi = m.xi;
+          xp.out = m.out;
+          xp.n = m.n;
+          if (src.kind == OSAM_FOM) {
+            xp.src = newest ? src.st[src.cur][0] : src.st[src.ux][0];
+            xp.cs = src.g.npad;
+          } else {
+            xp.src = src.lift[newest ? 1 - src.cur : src.cur];
+            xp.cs = src.n_lift;
+          }
+        }
+        L.n_xf = (int)d.maps.size();
+        L.xsync = d.xsync;
+      }
       cudaStream_t ks = st;
       if (par) {
         CK(cudaEventRecord(G.fork_ev[set + i], st));
@@ -1121,11 +1172,12 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
         joins.push_back(set + i);
       }
       if (fom_k && g_prof) CK(cudaEventRecord(G.ev[2 * *fom_k], st));
-      launch_fom_advance(L, d.stencil, &d.tmap[c], &d.tmapw[c], &d.tmapw[x], ks, launches, !par);
+      // the excluded last x column copies X there, Schwarz values included: after an in-grid transfer it follows K1
+      launch_fom_advance(L, d.stencil, &d.tmap[c], &d.tmapw[c], &d.tmapw[x], ks, launches, !par || xin_now);
       if (fom_k && g_prof) CK(cudaEventRecord(G.ev[2 * *fom_k + 1], st));
       if (par) {
         CK(cudaEventRecord(G.join_ev[set + i], ks));
-        launch_fom_xlast(L, st, launches);  // concurrently with the tiled kernel on the side stream
+        if (!xin_now) launch_fom_xlast(L, st, launches);  // concurrently with the tiled kernel on the side stream
       }
       if (fom_k) ++*fom_k;
       // algorithmic bytes: read q, w and write q', w' (32 B/DOF) + the previous w' of the DOFs within one

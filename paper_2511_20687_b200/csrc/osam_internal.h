@@ -116,6 +116,8 @@ struct Sub {
   double* scratch_v = nullptr;         // 3 * npad: v for osam_get_state
   double* scratch_a = nullptr;         // 3 * npad: acceleration for osam_get_accel
   double2* scratch_partial = nullptr;  // partial slots of non-sweep K1 launches
+  unsigned* xsync = nullptr;           // [2] in-grid transfer handshake of the tiled K1 (FomLaunch::xsync)
+  bool xin = false;                    // the transfers into it run as the first CTAs of its tiled K1 (bind)
 
   // ROM device data
   double *Phi = nullptr, *Phi_s = nullptr, *Kbar = nullptr, *Bbar = nullptr, *e = nullptr;
@@ -174,6 +176,18 @@ struct Sub {
 };
 
 // ---- kernel launchers (defined in the .cu files) ---------------------------------------
+// One Schwarz transfer evaluated by the first CTAs of the destination's tiled K1 grid ("the
+// transfer in the K1 grid"): s[p, c] = sum_b w_pb src[c cs + idx_pb] into the destination's X at out[3p + c].
+struct XferPart {
+  const int* idx;
+  const double* xi;
+  const int* out;
+  const double* src;
+  long long cs;
+  int n;
+};
+constexpr int FOM_XF_MAX = 2;
+
 struct FomLaunch {
   Geom g;
   Faces f;
@@ -197,9 +211,18 @@ struct FomLaunch {
   unsigned long long* stamp;  // K1 in-schedule timeline (may be null): [0] earliest CTA start, [1] latest
                               // CTA end, %globaltimer ns (atomicMin / atomicMax); folded by K3, see Ctl
   double mat_lam, mat_mu, mat_kappa;
+  // in-grid transfer (tiled K1 in a sweep, 0 otherwise): the first n_xf_ctas CTAs evaluate xf[0 .. n_xf) into x; the
+  // tile CTAs whose staged box holds a Schwarz node run last and wait for them on xsync[0] (transfer CTAs done);
+  // xsync[1] counts the waiters that passed, and the last one resets both
+  XferPart xf[FOM_XF_MAX];
+  int n_xf, n_xf_ctas;
+  unsigned* xsync;
 };
 // Number of partial slots a K1 launch writes (tiled blocks + x-face blocks).
 int fom_partial_slots(const Geom& g, const Faces& f);
+// Can the transfers into this subdomain run as the first CTAs of its tiled K1 (Schwarz faces on x only, tiled
+// linear path, and some tile column stages a Schwarz node)?
+bool fom_ingrid_xfer_ok(const Geom& g, const Faces& f, int material);
 int fom_nl_partial_slots(const Geom& g);  // NL1 (nonlinear materials): one slot per CTA
 // with_xlast = false: the caller launches the excluded last x column (launch_fom_xlast) itself, e.g. on
 // another stream concurrently with the tiled kernel (it reads only X and writes only that column).

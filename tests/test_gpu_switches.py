@@ -44,7 +44,8 @@ def gpu():
         pytest.skip("no CUDA device")
 
 
-@pytest.mark.parametrize("env", [{"OSAM_SERIAL_K1": "1"}, {"OSAM_PDL": "0"}, {"OSAM_NOGRAPH": "1"}])
+@pytest.mark.parametrize("env", [{"OSAM_SERIAL_K1": "1"}, {"OSAM_PDL": "0"}, {"OSAM_NOGRAPH": "1"},
+                                 {"OSAM_XFER_INGRID": "1"}])
 def test_process_wide_switches_keep_parity(gpu, env):
     e = dict(os.environ, OSAM_GATHER_MAX="0", **env)
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
