@@ -9,6 +9,14 @@ constexpr int NT = TX * TY;
 constexpr int NWARP = NT / 32;
 constexpr int ZC = K1_ZC;  // target z-planes per block (balanced split)
 constexpr int XF_BLOCK = NT;  // x-face work runs in extra CTAs of the tiled kernel (same block)
+#ifndef OSAM_K1_PW
+#define OSAM_K1_PW 0
+#endif
+// OSAM_K1_PW = 1: a dedicated producer warp (one more warp per CTA, the rows threadIdx.y >= TY) issues every TMA
+// load, so no consumer warp carries the ~400 cycles of issue per plane and the CTA no longer runs at warp 0's pace.
+constexpr int PW = (OSAM_K1_PW && 32 % K1_TX == 0) ? 1 : 0;
+constexpr int NTB = NT + 32 * PW;                    // threads per CTA
+constexpr int BY = TY + PW * (32 / (K1_TX > 32 ? 32 : K1_TX));  // blockDim.y
 
 // Staged x-range [x0, x0 + PX) with x0 = 32 bx - 2: the TMA box must start on a 16-byte
 // boundary in the innermost dimension (an odd fp64 start coordinate raises an illegal
@@ -436,7 +444,7 @@ __device__ __forceinline__ void k1_iter(const FomLaunch& L, const InteriorStenci
 #else
   const bool issuer = threadIdx.x + threadIdx.y == 0;
 #endif
-  if (issuer && it + NSTAGE - 2 < T.nplanes) {
+  if (!PW && issuer && it + NSTAGE - 2 < T.nplanes) {
     const int p = it + NSTAGE - 2;
 #if !defined(OSAM_K1_NOEMPTY) && !OSAM_K1_WARP  // NOEMPTY: probe only (wrong results)
     if (p >= NSTAGE) mbar_wait(&empty[p % NSTAGE], (unsigned)(((p - NSTAGE) / NSTAGE) & 1));
@@ -575,7 +583,7 @@ __device__ __noinline__ void xface_body(const FomLaunch& L, int side_mask, int b
 #define OSAM_K1_ROT 0
 #endif
 template <bool ZN>
-__global__ void __launch_bounds__(NT, K1_MINB)
+__global__ void __launch_bounds__(NTB, K1_MINB)
     fom_tiled_kernel(const __grid_constant__ FomLaunch L, const __grid_constant__ InteriorStencil S,
                      const __grid_constant__ CUtensorMap tmx, const __grid_constant__ CUtensorMap tmw,
                      const __grid_constant__ CUtensorMap tmwp) {
@@ -584,6 +592,8 @@ __global__ void __launch_bounds__(NT, K1_MINB)
   unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + NRING * NSTAGE * STAGE_BYTES);
   unsigned long long* empty = full + NRING * NSTAGE;
   if (L.stamp && threadIdx.x + threadIdx.y == 0) atomicMin(L.stamp, global_ns());  // in-schedule timeline
+  const bool is_prod = PW && (int)threadIdx.y >= TY;  // the producer warp (whole warp: it may exit early)
+  if (is_prod && ((int)blockIdx.x < L.n_xf_ctas || (int)blockIdx.x - L.n_xf_ctas >= L.n_tile_ctas)) return;
   if ((int)blockIdx.x < L.n_xf_ctas) {  // transfer CTAs (first)
     xfer_body(L, blockIdx.x, threadIdx.x + TX * threadIdx.y);
     if (L.stamp && threadIdx.x + threadIdx.y == 0) atomicMax(L.stamp + 1, global_ns());
@@ -642,15 +652,30 @@ __global__ void __launch_bounds__(NT, K1_MINB)
   }
 #else
   if (threadIdx.x + threadIdx.y == 0) {
-    if (waits) xfer_wait(L, (unsigned)((wlo + whi) * G.ty * G.tz));
+    if (!PW && waits) xfer_wait(L, (unsigned)((wlo + whi) * G.ty * G.tz));
     for (int s = 0; s < NSTAGE; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NWARP);
     }
     mbar_fence_init();
-    for (int p = 0; p < NSTAGE - 2 && p < T.nplanes; ++p) issue_plane(P, T.prev(), p, p, ring, full, M);
+    if (!PW)
+      for (int p = 0; p < NSTAGE - 2 && p < T.nplanes; ++p) issue_plane(P, T.prev(), p, p, ring, full, M);
   }
   __syncthreads();
+  if (is_prod) {
+    // the whole TMA stream of the tile: plane p goes into the stage plane p - NSTAGE left, released by the NWARP
+    // consumer warps at the end of their iteration p - NSTAGE + 1 (the finish reads the previous stage)
+    if (threadIdx.x == 0 && (int)threadIdx.y == TY) {
+      if (waits) xfer_wait(L, (unsigned)((wlo + whi) * G.ty * G.tz));
+      const bool wp = needs_prev(L, P);
+#pragma unroll 1
+      for (int p = 0; p < P.nplanes; ++p) {
+        if (p >= NSTAGE) mbar_wait(&empty[p % NSTAGE], (unsigned)(((p - NSTAGE) / NSTAGE) & 1));
+        issue_plane(P, wp, p, p % NSTAGE, ring, full, M);
+      }
+    }
+    return;
+  }
 #endif
 
   double acc[3][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
@@ -791,9 +816,9 @@ void launch_tiled(const FomLaunch& L, const InteriorStencil& st, const CUtensorM
   // transfer CTAs, tile CTAs, then x-face CTAs
   const int grid = Lt.n_xf_ctas + Lt.n_tile_ctas + (int)xface_blocks(L.g, L.f);
   if (L.z_out)  // last substep of a multi-substep interval: z = u + dt v out, norm from z - z_prev (R33)
-    fom_tiled_kernel<true><<<grid, dim3(TX, TY), SMEM_TILED, s>>>(Lt, st, *tmx, *tmw, *tmwp);
+    fom_tiled_kernel<true><<<grid, dim3(TX, BY), SMEM_TILED, s>>>(Lt, st, *tmx, *tmw, *tmwp);
   else
-    fom_tiled_kernel<false><<<grid, dim3(TX, TY), SMEM_TILED, s>>>(Lt, st, *tmx, *tmw, *tmwp);
+    fom_tiled_kernel<false><<<grid, dim3(TX, BY), SMEM_TILED, s>>>(Lt, st, *tmx, *tmw, *tmwp);
   debug_check("fom_tiled_kernel", s);
 }
 
