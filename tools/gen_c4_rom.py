@@ -47,6 +47,17 @@ def load_full_ops():
     return ops
 
 
+def rom_ops_id(ops):
+    """Identity of one training run: sha256 over Kbar and Bbar of both ROMs (the noise modes beyond the snapshot
+    rank differ from run to run, so golden data belongs to exactly one set of operators)."""
+    import hashlib
+    h = hashlib.sha256()
+    for i in (0, 2):
+        h.update(np.ascontiguousarray(ops[i]["Kbar"], dtype=np.float64).tobytes())
+        h.update(np.ascontiguousarray(ops[i]["Bbar"], dtype=np.float64).tobytes())
+    return h.hexdigest()
+
+
 def load_online_ops(path=ONLINE):
     """{i: dict(phi_rows, Phi (rows subset), Phi_s, Kbar, Bbar, uh0, s0, n_free, r, r_b)} or None if absent."""
     if not os.path.exists(path):

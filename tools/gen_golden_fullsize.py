@@ -78,7 +78,20 @@ def main():
     ap.add_argument("--record", type=str, default=None, help="comma-separated steps with node samples")
     ap.add_argument("--out", type=str, default=None)
     ap.add_argument("--resume", action="store_true", help="continue from var/<out>_ckpt.pkl")
+    ap.add_argument("--stamp-ops", action="store_true",
+                    help="c4: only (re)write rom_ops_id of var/c4_ops into the provenance .json")
     args = ap.parse_args()
+    if args.stamp_ops:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import gen_c4_rom
+        jp = os.path.join(GOLDEN, (args.out or "c4_long") + ".json")
+        with open(jp) as fh:
+            prov = json.load(fh)
+        prov["rom_ops_id"] = gen_c4_rom.rom_ops_id(gen_c4_rom.load_full_ops())
+        with open(jp, "w") as fh:
+            json.dump(prov, fh, indent=1)
+        print("rom_ops_id", prov["rom_ops_id"])
+        return
     cfg = I.config(args.config)
     n_steps = args.steps or cfg["n_steps"]
     record = sorted({int(x) for x in args.record.split(",")}) if args.record else \
@@ -88,6 +101,7 @@ def main():
         sys.path.insert(0, os.path.join(ROOT, "tools"))
         import gen_c4_rom
         rom_ops = gen_c4_rom.load_full_ops()
+        args.rom_ops_id = gen_c4_rom.rom_ops_id(rom_ops)
     models = schwarz.build_models(cfg, rom_ops)
     u0s = [I.initial_displacements(cfg, s) for s in cfg["subdomains"]]
     states = [m.init_state(u0) for m, u0 in zip(models, u0s)]
@@ -170,6 +184,8 @@ def _write(args, cfg, n_steps, k_done, record, iters, trace_step, trace_n, trace
                 oracle_seconds=round(elapsed, 1), sample_seed=20251120,
                 sha256=hashlib.sha256(open(path, "rb").read()).hexdigest(),
                 source="oracle only (oracle.schwarz.controller_step); no value from the CUDA path")
+    if getattr(args, "rom_ops_id", None):
+        prov["rom_ops_id"] = args.rom_ops_id     # the trained operators this run used (tools/gen_c4_rom.py)
     with open(os.path.join(GOLDEN, name + ".json"), "w") as fh:
         json.dump(prov, fh, indent=1)
 
