@@ -221,13 +221,29 @@ struct TileGeo {
   int nplanes;       // staged planes kbeg-1 .. kend+1
 };
 
+// First node plane of z-chunk b of tz.  CTAs are dispatched chunk layer by chunk layer (bz slowest), so the chunks
+// taper: their sizes fall linearly from (1 + p/100) to (1 - p/100) of the mean, the long CTAs start first and the
+// launch drains through short ones (the tail of a launch is one CTA duration at falling occupancy).  The number of
+// chunks, and with it the halo planes re-read, is unchanged.  p = OSAM_ZTAPER (0: balanced split).  Measured
+// (profiles/r7c_ab_k1_ztaper.log): K1 alone 0.178 -> 0.164 ms per launch (c3), the concurrent c3 step 946 -> 976
+// steps/s at p = 55 (25: 964, 40: 972, 70: 968, 85: 952).
+#ifndef OSAM_ZTAPER
+#define OSAM_ZTAPER 55
+#endif
+__device__ __forceinline__ int zsplit(int nz, int tz, int b) {
+  constexpr long long p = OSAM_ZTAPER;
+  if (p == 0 || tz < 2) return (int)((long long)b * nz / tz);
+  const long long c = (long long)b * (100 + p) * (tz - 1) - p * (long long)b * (b - 1);
+  return (int)((long long)nz * c / (100LL * tz * (tz - 1)));
+}
+
 __device__ __forceinline__ TileGeo tile_geo(const Geom& g, const TileGrid& G, int t) {
   const int bx = t % G.tx, by = (t / G.tx) % G.ty, bz = t / (G.tx * G.ty);
   TileGeo o;
   o.x0 = bx * TX - 2;
   o.y0 = by * TY - 1;
-  o.kbeg = (int)((long long)bz * g.nn[2] / G.tz);
-  o.kend = (int)((long long)(bz + 1) * g.nn[2] / G.tz) - 1;
+  o.kbeg = zsplit(g.nn[2], G.tz, bz);
+  o.kend = zsplit(g.nn[2], G.tz, bz + 1) - 1;
   o.nplanes = o.kend - o.kbeg + 3;
   return o;
 }
