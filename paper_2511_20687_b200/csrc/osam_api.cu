@@ -267,6 +267,7 @@ struct Group {
   // step graph's capture is still open, and a stream that joined one capture cannot join another)
   std::vector<cudaStream_t> side;
   std::vector<cudaEvent_t> fork_ev, join_ev;
+  std::vector<cudaEvent_t> join2_ev, xl_ev;  // pipelined transfers: their end; the last-column copy's end
   int launches_begin = 1;      // kernels before sweep 1 (step_begin [+ trace slot 0])
   bool trace = false;          // some subdomain takes several substeps: transfers through traces + Xi
   int ctl_len() const { return 2 + 2 * B + 4; }
@@ -275,6 +276,8 @@ struct Group {
     for (auto x : side) cudaStreamDestroy(x);
     for (auto e : fork_ev) cudaEventDestroy(e);
     for (auto e : join_ev) cudaEventDestroy(e);
+    for (auto e : join2_ev) cudaEventDestroy(e);
+    for (auto e : xl_ev) cudaEventDestroy(e);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (cap_main) cudaStreamDestroy(cap_main);
     dfree(partial);
@@ -755,6 +758,37 @@ int bind_group(const std::vector<Sub*>& subs, const std::vector<osam_subdomain*>
         if (mm.src == i && mm.reads_src_schwarz) ok = false;
     d.xin = ok;
   }
+  // Pipelined transfers: under the same conditions the transfers into a FOM for sweep n + 1 are
+  // launched on its own branch right after its advance of sweep n (they write its Schwarz entries, which only that
+  // advance reads), beside the other advances and K3 instead of ahead of the next sweep.  Every sweep still runs
+  // every transfer; the one issued after the last sweep of a step rewrites the same bits (the values it reads are
+  // fixed within the step from sweep 2 on).  OSAM_XFER_PIPE=0 keeps them at the head of their sweep.
+  static const bool xpipe_env = !(getenv("OSAM_XFER_PIPE") && getenv("OSAM_XFER_PIPE")[0] == '0');
+  for (int i = 0; i < n; ++i) {
+    Sub& d = *subs[i];
+    d.xpipe = false;
+    if (!xpipe_env || d.xin || any_sub || d.kind != OSAM_FOM || d.batch != 1 || d.maps.empty()) continue;
+    bool ok = true;
+    for (auto& mm : d.maps) {
+      const Sub& src = *subs[mm.src];
+      ok = ok && !mm.reads_src_schwarz && (src.kind == OSAM_FOM ? src.batch == 1 : src.pre1);
+    }
+    for (int q = 0; q < n && ok; ++q)
+      for (auto& mm : subs[q]->maps)
+        if (mm.src == i && mm.reads_src_schwarz) ok = false;
+    d.xpipe = ok;
+  }
+  // ... only in groups with one FOM (c2, c4: +1.4% on c4).  With two FOM advances in a sweep (c3) the second one's
+  // transfers already run beside the first advance, and pipelining both (the two K1s start together: 965 vs 992
+  // steps/s) or only the first (988 vs 996: the non-K1 time falls by 14 us per step but the K1s' union grows by
+  // 22 us) measured slower (profiles/r7d_ab_xfer_pipe.log).  OSAM_XFER_PIPE=2 pipelines the first FOM of any group.
+  static const bool xpipe_any = getenv("OSAM_XFER_PIPE") && getenv("OSAM_XFER_PIPE")[0] == '2';
+  int n_fom = 0;
+  for (int i = 0; i < n; ++i) n_fom += subs[i]->kind == OSAM_FOM;
+  for (int i = 0, seen = 0; i < n; ++i)
+    if (subs[i]->kind == OSAM_FOM) {
+      if (seen++ || (n_fom > 1 && !xpipe_any)) subs[i]->xpipe = false;
+    }
   for (auto& P : pend) {
     Sub& d = *subs[P.dst];
     const Sub& src = *subs[P.src];
@@ -1026,13 +1060,17 @@ int ensure_side(Group& G) {
   const int n = 2 * (int)G.sds.size();
   while ((int)G.side.size() < n) {
     cudaStream_t x;
-    cudaEvent_t a, b;
+    cudaEvent_t a, b, c, e;
     CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     G.side.push_back(x);
     G.fork_ev.push_back(a);
     G.join_ev.push_back(b);
+    G.join2_ev.push_back(c);
+    G.xl_ev.push_back(e);
   }
   return OSAM_OK;
 }
@@ -1108,8 +1146,10 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
     bool xin_now = d.xin;
     for (const XferMap& m : d.maps)
       if (first && m.src > i && subs[m.src]->kind == OSAM_FOM) xin_now = false;
+    // pipelined transfers (bind: d.xpipe): from sweep 2 on the previous sweep issued them after this FOM's advance
+    const bool xp = par && cfg.max_iters >= 2 && d.xpipe && !xin_now;
     for (const XferMap& m : d.maps) {
-      if (d.fold || d.pre1 || xin_now) continue;  // folded exchange: inside the ROM advance; pre1: on its branch below
+      if (d.fold || d.pre1 || xin_now || (xp && !first)) continue;  // folded: inside the ROM advance; pre1: below
       const Sub& src = *subs[m.src];
       const bool newest = (m.src < i) || !first;
       const double* field;
@@ -1178,6 +1218,7 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
       if (par) {
         CK(cudaEventRecord(G.join_ev[set + i], ks));
         if (!xin_now) launch_fom_xlast(L, st, launches);  // concurrently with the tiled kernel on the side stream
+        if (xp) CK(cudaEventRecord(G.xl_ev[set + i], st));  // it reads X's last column, Schwarz values included
       }
       if (fom_k) ++*fom_k;
       // algorithmic bytes: read q, w and write q', w' (32 B/DOF) + the previous w' of the DOFs within one
@@ -1302,6 +1343,35 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
       slot += rom_partial_slots(d.r, d.use_tc);
     }
   }
+  // pipelined transfers: the next sweep's Schwarz values of FOM i, on its branch after its advance (which alone
+  // reads them); a ROM source's lift formed on that ROM's branch in sweep 1 is waited for
+  std::vector<int> joins2;
+  for (int i = 0; i < n_sd; ++i) {
+    Sub& d = *subs[i];
+    if (!(par && cfg.max_iters >= 2 && d.xpipe) || d.kind != OSAM_FOM) continue;
+    cudaStream_t ks = G.side[set + i];
+    CK(cudaStreamWaitEvent(ks, G.xl_ev[set + i], 0));
+    for (const XferMap& m : d.maps) {
+      const Sub& src = *subs[m.src];
+      const double* field;
+      long long cs, bs;
+      if (src.kind == OSAM_FOM) {
+        field = src.st[src.cur][0];
+        cs = src.g.npad;
+        bs = 0;
+      } else {
+        if (first && std::find(joins.begin(), joins.end(), set + m.src) != joins.end())
+          CK(cudaStreamWaitEvent(ks, G.join_ev[set + m.src], 0));
+        field = src.lift[1 - src.cur];
+        cs = src.n_lift;
+        bs = 3 * src.n_lift;
+      }
+      launch_transfer(m, field, cs, bs, d.st[d.cur][0], 0, B, nullptr, ks);
+      ++*launches;
+    }
+    CK(cudaEventRecord(G.join2_ev[set + i], ks));
+    joins2.push_back(set + i);
+  }
   for (int i : joins) CK(cudaStreamWaitEvent(st, G.join_ev[i], 0));  // every FOM advance before the test
   if (epi_fused) {
     epi.B = B;
@@ -1314,6 +1384,7 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
     return OSAM_OK;
   }
   *launches += launch_finalize(ctl, G.partial, G.n_slots, B, cfg.min_iters, cfg.tol_rel, cfg.tol_abs, st);
+  for (int i : joins2) CK(cudaStreamWaitEvent(st, G.join2_ev[i], 0));  // the branches rejoin after K3
   return OSAM_OK;
 }
 

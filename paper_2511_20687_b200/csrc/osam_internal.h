@@ -118,6 +118,7 @@ struct Sub {
   double2* scratch_partial = nullptr;  // partial slots of non-sweep K1 launches
   unsigned* xsync = nullptr;           // [2] in-grid transfer handshake of the tiled K1 (FomLaunch::xsync)
   bool xin = false;                    // the transfers into it run as the first CTAs of its tiled K1 (bind)
+  bool xpipe = false;                  // the transfers into it for sweep n + 1 follow its own advance of sweep n (bind)
 
   // ROM device data
   double *Phi = nullptr, *Phi_s = nullptr, *Kbar = nullptr, *Bbar = nullptr, *e = nullptr;

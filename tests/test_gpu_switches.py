@@ -45,7 +45,7 @@ def gpu():
 
 
 @pytest.mark.parametrize("env", [{"OSAM_SERIAL_K1": "1"}, {"OSAM_PDL": "0"}, {"OSAM_NOGRAPH": "1"},
-                                 {"OSAM_XFER_INGRID": "1"}])
+                                 {"OSAM_XFER_INGRID": "1"}, {"OSAM_XFER_PIPE": "0"}])
 def test_process_wide_switches_keep_parity(gpu, env):
     e = dict(os.environ, OSAM_GATHER_MAX="0", **env)
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))

@@ -57,3 +57,20 @@ def test_ingrid_transfer_bitwise_equals_separate_launches(tmp_path):
     for k in a:
         assert np.array_equal(a[k], b[k]), k
     assert (a["c3_iters"] == 3).all()
+
+
+def test_pipelined_transfers_bitwise_equal_head_of_sweep_transfers(tmp_path):
+    """Default: the transfers into a FOM for sweep n + 1 follow its own advance of sweep n on its branch (DESIGN.md
+    §6, "pipelined transfers"); OSAM_XFER_PIPE=0 launches them at the head of their sweep.  Same kernels, same
+    values: bitwise equal states and identical counts, in graph mode and with host-driven sweeps."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    a = _run({}, str(tmp_path / "pipe.npz"))
+    b = _run({"OSAM_XFER_PIPE": "0"}, str(tmp_path / "head.npz"))
+    c = _run({"OSAM_NOGRAPH": "1"}, str(tmp_path / "pipe_host.npz"))
+    assert a.keys() == b.keys() == c.keys()
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+        assert np.array_equal(a[k], c[k]), k
+    assert (a["c3_iters"] == 3).all()
