@@ -603,6 +603,17 @@ __global__ void __launch_bounds__(128) xlast_copy_kernel(const FomLaunch L) {
 // (no spills at <= 255 registers).
 namespace nl {
 constexpr int TXN = 16, TYN = 14, ZCN = 32;
+// First node plane of z-chunk b of tz: the chunk sizes taper over the chunk layers (dispatched in order, bz slowest)
+// from (1 + p/100) to (1 - p/100) of the mean, so the launch drains through short CTAs (as K1's zsplit, k1_tiled.cuh)
+#ifndef OSAM_NL_ZTAPER
+#define OSAM_NL_ZTAPER 60  // measured (profiles/r8d_ab_nl_ztaper.log): SVK 154.6 -> 159.2, Neohookean 106.0 -> 109.0 steps/s on c3
+#endif
+__device__ __forceinline__ int nl_zsplit(int nz, int tz, int b) {
+  constexpr long long p = OSAM_NL_ZTAPER;
+  if (p == 0 || tz < 2) return (int)((long long)b * nz / tz);
+  const long long c = (long long)b * (100 + p) * (tz - 1) - p * (long long)b * (b - 1);
+  return (int)((long long)nz * c / (100LL * tz * (tz - 1)));
+}
 constexpr int EX = TXN + 1, EY = TYN + 1, NE = EX * EY;
 constexpr int PXN = TXN + 2, PYN = TYN + 2, PLN = PXN * PYN;
 constexpr int NTN = 256;
@@ -762,7 +773,7 @@ __global__ void __launch_bounds__(nl::NTN, 1) fom_nl_kernel(const __grid_constan
   const int nzc = (g.nn[2] + ZCN - 1) / ZCN;
   const int bx = blockIdx.x % ntx, by = (blockIdx.x / ntx) % nty, bz = blockIdx.x / (ntx * nty);
   const int x0 = bx * TXN, y0 = by * TYN;
-  const int kbeg = (int)((long long)bz * g.nn[2] / nzc), kend = (int)((long long)(bz + 1) * g.nn[2] / nzc) - 1;
+  const int kbeg = nl_zsplit(g.nn[2], nzc, bz), kend = nl_zsplit(g.nn[2], nzc, bz + 1) - 1;
   const int nelx = g.nn[0] - 1, nely = g.nn[1] - 1, nelz = g.nn[2] - 1;
   const bool need_prev = L.with_norm != 0;
   const double* prev = L.z_out ? L.z_out : L.w_out;  // previous iterate for the norm (read before written)
