@@ -447,7 +447,10 @@ def run_ours(args):
             "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.workload}: {desc} ({fom_dofs} FOM DOFs)",
-                       "l2": "inputs larger than L2 (two state buffers x (q, w) x 8 B x FOM DOFs, > 126 MB)",
+                       "l2": ("inputs larger than L2 (two state buffers x (q, w) x 8 B x FOM DOFs, > 126 MB)"
+                              if 32 * fom_dofs > 126e6 else
+                              "state and operators fit the 126 MB L2 and are not flushed: a latency-bound config, "
+                              "L2-resident by design (no HBM roofline claim)"),
                        **({"rom_operators": "oracle-trained (tools/gen_c4_rom.py, cache/c4_rom_ops.npz)" if trained
                            is not None else "seeded stand-ins of the trained sizes (osam_inputs.synthetic_rom_operators)"}
                           if any(s_["kind"] == "rom" for s_ in cfg["subdomains"]) else {}),
