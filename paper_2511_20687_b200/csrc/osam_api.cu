@@ -269,6 +269,7 @@ struct Group {
   std::vector<cudaEvent_t> fork_ev, join_ev;
   std::vector<cudaEvent_t> join2_ev, xl_ev;  // pipelined transfers: their end; the last-column copy's end
   int launches_begin = 1;      // kernels before sweep 1 (step_begin [+ trace slot 0])
+  int unrolled = 0;            // sweeps 2 .. min_iters captured into the step graph itself (step_graph_capture)
   bool trace = false;          // some subdomain takes several substeps: transfers through traces + Xi
   int ctl_len() const { return 2 + 2 * B + 4; }
   ~Group() {
@@ -1076,7 +1077,7 @@ int ensure_side(Group& G) {
 }
 
 int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool first, cudaStream_t st, int* launches,
-                  int* fom_k) {
+                  int* fom_k, bool main_set = false) {
   if (G.trace) return enqueue_sweep_trace(G, cfg, ctl, first, st, launches, fom_k);
   std::vector<Sub*> subs;
   for (auto h : G.sds) subs.push_back(&h->s);
@@ -1089,7 +1090,9 @@ int enqueue_sweep(Group& G, const osam_schwarz_cfg& cfg, const Ctl& ctl, bool fi
   // mode (per-launch K1 events) and OSAM_SERIAL_K1=1 keep them on the main stream.
   static const bool serial_env = getenv("OSAM_SERIAL_K1") && getenv("OSAM_SERIAL_K1")[0] == '1';
   const bool par = !g_prof && !serial_env;
-  const int set = first ? 0 : n_sd;
+  // side-stream set: 0 for sweeps captured into the step graph itself (sweep 1 and the unconditional sweeps up to
+  // min_iters), n_sd for the while-loop body (captured while the step graph's capture is still open)
+  const int set = (first || main_set) ? 0 : n_sd;
   if (par && (int)G.side.size() < 2 * n_sd) return fail(OSAM_ECUDA, "internal: side streams not created");
   std::vector<int> joins;
   // Groups of explicit batched tensor-core ROMs with the folded exchange (c5): an explicit ROM iterate's
@@ -1579,11 +1582,6 @@ int step_graph_capture(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t st, c
   Ctl ctl = G.ctl(cfg.max_iters);
   int launches = 0;
   CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-  launch_step_begin(ctl, G.B, st);
-  int begin = 1;
-  if (G.trace) TRY(enqueue_trace_begin(G, st, &begin));
-  G.launches_begin = begin;
-  TRY(enqueue_sweep(G, cfg, ctl, true, st, &launches, nullptr));
   cudaStreamCaptureStatus status;
   const cudaGraphNode_t* deps = nullptr;
   size_t ndeps = 0;
@@ -1592,6 +1590,29 @@ int step_graph_capture(Group& G, const osam_schwarz_cfg& cfg, cudaStream_t st, c
   CK(cudaStreamGetCaptureInfo(st, &status, &cap_id, &cap, &deps, &ndeps));
   cudaGraphConditionalHandle h;
   CK(cudaGraphConditionalHandleCreate(&h, cap, cfg.max_iters >= 2 ? 1u : 0u, cudaGraphCondAssignDefault));
+  launch_step_begin(ctl, G.B, st);
+  int begin = 1;
+  if (G.trace) TRY(enqueue_trace_begin(G, st, &begin));
+  G.launches_begin = begin;
+  TRY(enqueue_sweep(G, cfg, ctl, true, st, &launches, nullptr));
+  // Sweeps 2 .. min_iters always run (the test starts at n = min_iters, R6/R7): they are captured into the step
+  // graph itself, so a step pays the while-node's iteration overhead only from sweep min_iters + 1 on; their K3
+  // sets the loop condition like the body's (no sample freezes and no error flag is raised before the first test at
+  // n = min_iters, so the loop would have run them anyway).  Single-substep groups; OSAM_UNROLL_MIN=0 keeps every
+  // sweep n >= 2 in the loop.
+  static const bool unroll_env = !(getenv("OSAM_UNROLL_MIN") && getenv("OSAM_UNROLL_MIN")[0] == '0');
+  G.unrolled = 0;
+  if (unroll_env && !G.trace) {
+    Ctl cu = ctl;
+    cu.has_cond = 1;
+    cu.cond = h;
+    for (int n = 2; n <= cfg.min_iters && n <= cfg.max_iters; ++n) {
+      int l2 = 0;
+      TRY(enqueue_sweep(G, cfg, cu, false, st, &l2, nullptr, true));
+      ++G.unrolled;
+    }
+  }
+  CK(cudaStreamGetCaptureInfo(st, &status, &cap_id, &cap, &deps, &ndeps));
   cudaGraphNodeParams cp = {};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = h;

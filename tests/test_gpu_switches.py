@@ -45,7 +45,7 @@ def gpu():
 
 
 @pytest.mark.parametrize("env", [{"OSAM_SERIAL_K1": "1"}, {"OSAM_PDL": "0"}, {"OSAM_NOGRAPH": "1"},
-                                 {"OSAM_XFER_INGRID": "1"}, {"OSAM_XFER_PIPE": "0"}])
+                                 {"OSAM_XFER_INGRID": "1"}, {"OSAM_XFER_PIPE": "0"}, {"OSAM_UNROLL_MIN": "0"}])
 def test_process_wide_switches_keep_parity(gpu, env):
     e = dict(os.environ, OSAM_GATHER_MAX="0", **env)
     code = SCRIPT.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
@@ -74,7 +74,7 @@ print("ok", worst, worst2)
 
 
 @pytest.mark.parametrize("env", [{}, {"OSAM_NO_FOLD": "1"}, {"OSAM_ROM_PAR": "0"}, {"OSAM_ROM_KBG": "0"},
-                                 {"OSAM_EPI_FUSED": "0"}])
+                                 {"OSAM_EPI_FUSED": "0"}, {"OSAM_UNROLL_MIN": "0"}])
 def test_rom_exchange_switches_keep_parity(gpu, env):
     """c2 (FOM-ROM, B = 1: the FOM exchange folded into the ROM update by default) and c5 (batched ROM-ROM: the
     predictor once per step, parallel ROM branches, [-Kbar | Bbar G] by default) against the oracle, with every
